@@ -1,0 +1,143 @@
+/*
+ * bmps.h -- C ABI of the B200-native MPS hot path (libbmps.so, sm_100a).
+ *
+ * The reference (mpsqvm, /root/reference/pkg) has no FFI: its "operator API"
+ * is the Python class MpsState + TruncationPolicy (src/mpsqvm/mps.py:24-237),
+ * driven per gate by backends.mps_run (src/mpsqvm/backends.py:47-60). This
+ * header is the boundary a drop-in binds to: every entry
+ * point names the reference method it replaces.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only. All pointers are DEVICE pointers unless
+ *     the name ends in _host. complex128 is two consecutive doubles (re, im).
+ *   - A "state batch" holds S independent n-qubit states at bond capacity cap:
+ *       gamma : complex128 [S][n][cap*2*cap]; site (s,k) element (l,p,r) at
+ *               ((l*2 + p)*cap + r)  -- the reference's C-order (chi_l, 2, chi_r)
+ *               tensor (mps.py:60-62) with row stride cap.
+ *       lam   : float64 [S][n+1][cap]; bond b is the left bond of site b.
+ *               Bonds 0 and n are the boundary vector [1.0]; internal bond b
+ *               is the reference's bond_vectors[b-1] (mps.py:63).
+ *       dims  : int32 [S][n+1]; dims[0] = dims[n] = 1.
+ *       stats : float64 trunc_err[S], int64 entries[S], int64 peak[S],
+ *               int32 max_bond_seen[S], int32 status[S], int32 status_bond[S]
+ *               (RunRecord / MpsState bookkeeping, mps.py:64-84).
+ *   - Every call is asynchronous on the given cudaStream_t (passed as void*),
+ *     never allocates, never synchronises (except bmps_apply_2q mode 2, which
+ *     polls Jacobi convergence once per sweep), and returns 0 or a negative
+ *     BMPS_E_* launch/argument error. Numerical failures are reported through
+ *     the per-state status words (BMPS_S_*) and read at the next host sync.
+ *   - Work lists ("items") are int32 pairs (state index, site q), in program
+ *     order per state; gates are complex128 row-major 2x2 / 4x4 matrices, one
+ *     per item, 4x4 indexed [2a+b][2s+t] with a,s on site q (gates.py:3-4).
+ */
+#ifndef BMPS_H
+#define BMPS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* launch / argument errors (return values) */
+#define BMPS_OK 0
+#define BMPS_E_ARG -1
+#define BMPS_E_LAUNCH -2
+#define BMPS_E_WORKSPACE -3
+/* per-state numerical status (status[] words) */
+#define BMPS_S_OK 0
+#define BMPS_S_SVD_FAILED 1        /* mps.py:117-118 "SVD failed on bond q" */
+#define BMPS_S_ALL_TRUNCATED 2     /* mps.py:125-126 "all singular values truncated" */
+#define BMPS_S_CAPACITY 3          /* kept bond would exceed the allocated capacity */
+
+typedef struct bmps_policy {
+  double cutoff;     /* TruncationPolicy.cutoff   (mps.py:33) */
+  int32_t max_bond;  /* TruncationPolicy.max_bond, <= 0 means None (mps.py:34) */
+  int32_t relative;  /* TruncationPolicy.relative (mps.py:35) */
+} bmps_policy;
+
+/* ABI version and a human-readable message for a return/status code. */
+int32_t bmps_version(void);
+const char* bmps_status_string(int32_t code);
+
+/* MpsState.__init__ (mps.py:55-66): |0...0>, unit boundary bonds, stats reset. */
+int32_t bmps_init_product(double* gamma, double* lam, int32_t* dims, double* trunc_err,
+                          int64_t* entries, int64_t* peak, int32_t* max_bond_seen,
+                          int32_t* status, int32_t* status_bond, int32_t S, int32_t n,
+                          int32_t cap, void* stream);
+
+/* MpsState.apply_one_qubit (mps.py:88-92) over a batch of (state, site) items. */
+int32_t bmps_apply_1q(double* gamma, const int32_t* dims, int32_t S, int32_t n, int32_t cap,
+                      const int32_t* items, const double* gates, int32_t nitems, void* stream);
+
+/* Per-update record written by bmps_apply_2q (32 bytes): discarded weight
+ * sum(sigma[keep:]^2) (mps.py:121-122), bond dims before the update, kept
+ * dimension, status (BMPS_S_*) and the site q. */
+typedef struct bmps_update_record {
+  double err;
+  int32_t dl, dm, dr, keep, status, site;
+} bmps_update_record;
+
+/* Workspace bytes for bmps_apply_2q with nitems items at capacity cap. */
+size_t bmps_apply_2q_workspace_bytes(int32_t cap, int32_t nitems);
+
+/* MpsState.apply_two_qubit_adjacent (mps.py:94-136) over a batch of
+ * independent items (no two items may share a site): contract (theta) ->
+ * one-sided Jacobi SVD -> truncate (policy) -> split. Item i's record is
+ * written to log[log_index[i]]; bookkeeping is applied by bmps_stats_replay in
+ * program order. dim_bound (<= cap, 0 = cap) is an upper bound on the left /
+ * right bond dims of every item, used only to size grids. mode: 0 auto,
+ * 1 persistent (one CTA per item), 2 round-parallel (one launch per Jacobi
+ * round; polls convergence with one stream sync per sweep). */
+int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int32_t n,
+                      int32_t cap, const int32_t* items, const double* gates, int32_t nitems,
+                      bmps_policy policy, bmps_update_record* log, const int32_t* log_index,
+                      void* workspace, size_t workspace_bytes, int32_t dim_bound, int32_t mode,
+                      void* stream);
+
+/* Bookkeeping of MpsState._note_sizes / trunc_error_sq (mps.py:82-84, 122)
+ * replayed over update records in PROGRAM order: ranges holds nranges int32
+ * triples (state, first record, count). Sets the first failing record's
+ * status and site into status / status_bond. */
+int32_t bmps_stats_replay(const bmps_update_record* log, const int32_t* ranges, int32_t nranges,
+                          double* trunc_err, int64_t* entries, int64_t* peak,
+                          int32_t* max_bond_seen, int32_t* status, int32_t* status_bond,
+                          void* stream);
+
+/* Diagnostics of the last bmps_apply_2q on this workspace: per-item Jacobi
+ * sweeps (int32), copied into a device buffer of length nitems. */
+int32_t bmps_apply_2q_sweeps(const void* workspace, int32_t nitems, int32_t* sweeps,
+                             void* stream);
+
+/* MpsState.amplitude (mps.py:172-179) for a batch of (state, bitstring):
+ * bits is uint8 [count][n] (0/1), out is complex128 [count]. */
+int32_t bmps_amplitudes(const double* gamma, const double* lam, const int32_t* dims, int32_t S,
+                        int32_t n, int32_t cap, const int32_t* state_idx, const uint8_t* bits,
+                        int32_t count, double* out, void* stream);
+
+/* One environment transfer step for a batch of (state, site, pauli) items,
+ * the building block of MpsState.expectation_pauli / norm_sq
+ * (mps.py:181-204): direction 0 (left, E_{k+1} from E_k, mps.py:200) or
+ * 1 (right, R_k from R_{k+1}). Environments are cap x cap complex128
+ * matrices (row stride cap); item i's input starts at env_in + i*in_stride
+ * and its output at env_out + i*out_stride (strides in complex elements).
+ * pauli codes I=0 X=1 Y=2 Z=3. scratch: complex128 [2][count][2*cap*cap]. */
+int32_t bmps_env_transfer(const double* gamma, const double* lam, const int32_t* dims, int32_t S,
+                          int32_t n, int32_t cap, const int32_t* state_idx, const int32_t* site,
+                          const uint8_t* pauli, int32_t direction, const double* env_in,
+                          int64_t in_stride, double* env_out, int64_t out_stride, double* scratch,
+                          int32_t count, void* stream);
+
+/* <E_left, R_right> contraction: out[i] = sum_{r,q} L_i[r,q] * R_i[r,q] over
+ * the dims[s][b_i] x dims[s][b_i] leading block (complex128 out); L_i at
+ * env_l + i*l_stride, R_i at env_r + i*r_stride (complex elements). */
+int32_t bmps_env_close(const int32_t* dims, int32_t n, int32_t cap, const int32_t* state_idx,
+                       const int32_t* bond, const double* env_l, int64_t l_stride,
+                       const double* env_r, int64_t r_stride, int32_t count, double* out,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BMPS_H */

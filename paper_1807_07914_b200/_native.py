@@ -1,0 +1,77 @@
+"""ctypes binding of ``libbmps.so`` (the C ABI declared in ``include/bmps.h``).
+
+The library is built in-tree by ``paper_1807_07914_b200/build.py`` (or
+``__graft_entry__.build()``). There is no CPU fallback: importing a compute
+entry point without the library, or without a CUDA device, raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libbmps.so"
+
+BMPS_S_OK = 0
+BMPS_S_SVD_FAILED = 1
+BMPS_S_ALL_TRUNCATED = 2
+BMPS_S_CAPACITY = 3
+
+
+class BmpsPolicy(ctypes.Structure):
+    _fields_ = [("cutoff", ctypes.c_double), ("max_bond", ctypes.c_int32), ("relative", ctypes.c_int32)]
+
+
+RECORD_BYTES = 32  # sizeof(bmps_update_record)
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int32
+_SZ = ctypes.c_size_t
+_L = ctypes.c_int64
+
+_SIGNATURES = {
+    "bmps_version": ([], _I),
+    "bmps_status_string": ([_I], ctypes.c_char_p),
+    "bmps_init_product": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P], _I),
+    "bmps_apply_1q": ([_P, _P, _I, _I, _I, _P, _P, _I, _P], _I),
+    "bmps_apply_2q_workspace_bytes": ([_I, _I], _SZ),
+    "bmps_apply_2q": ([_P, _P, _P, _I, _I, _I, _P, _P, _I, BmpsPolicy, _P, _P, _P, _SZ, _I, _I, _P], _I),
+    "bmps_stats_replay": ([_P, _P, _I, _P, _P, _P, _P, _P, _P, _P], _I),
+    "bmps_apply_2q_sweeps": ([_P, _I, _P, _P], _I),
+    "bmps_amplitudes": ([_P, _P, _P, _I, _I, _I, _P, _P, _I, _P, _P], _I),
+    "bmps_env_transfer": ([_P, _P, _P, _I, _I, _I, _P, _P, _P, _I, _P, _L, _P, _L, _P, _I, _P], _I),
+    "bmps_env_close": ([_P, _I, _I, _P, _P, _P, _L, _P, _L, _I, _P, _P], _I),
+}
+
+EXPORTED = tuple(_SIGNATURES)
+
+_lib = None
+
+
+def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
+    """Load libbmps.so and declare every exported signature (no device needed)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path is not None else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(
+            f"libbmps.so not found at {p}; build it with `python -m paper_1807_07914_b200.build` "
+            "(there is no CPU fallback)"
+        )
+    lib = ctypes.CDLL(str(p))
+    for name, (args, res) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load().bmps_status_string(rc).decode()
+        raise RuntimeError(f"{what} failed: {msg} (code {rc})")

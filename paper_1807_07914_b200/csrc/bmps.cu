@@ -1,0 +1,596 @@
+// libbmps: B200-native (sm_100a) MPS hot path behind the C ABI of include/bmps.h.
+//
+// Kernels: K1 apply_1q, K2 theta, K3 block Jacobi SVD,
+// K4 finalize + split, K5 environment transfers, K6 amplitudes, plus init and
+// in-order stats. All complex128/float64; GEMM-shaped work (theta, Gram,
+// rotation apply, split, transfers) runs on FP64 tensor cores (DMMA).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "bmps.h"
+#include "bmps_update.cuh"
+
+using namespace bmps;
+
+namespace {
+
+constexpr int kNumSMs = 148;
+
+// ---------------------------------------------------------------------------
+// init: product state |0...0> (mps.py:55-66)
+// ---------------------------------------------------------------------------
+__global__ void init_kernel(StateView sv, int S, double* trunc_err, long long* entries,
+                            long long* peak, int* mbs, int* status, int* status_bond) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = sv.n;
+  if (g < S * (n + 1)) {
+    const int s = g / (n + 1), b = g % (n + 1);
+    sv.dimv(s)[b] = 1;
+    sv.bond(s, b)[0] = 1.0;
+    if (b < n) {
+      double2* t = sv.site(s, b);
+      t[0] = make_double2(1.0, 0.0);        // (l=0, p=0, r=0)
+      t[sv.cap] = make_double2(0.0, 0.0);   // (l=0, p=1, r=0)
+    }
+  }
+  if (g < S) {
+    trunc_err[g] = 0.0;
+    entries[g] = 2LL * n;
+    peak[g] = 2LL * n;
+    mbs[g] = 1;
+    status[g] = 0;
+    status_bond[g] = -1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1: Gamma[l,s,r] <- sum_t G[s,t] Gamma[l,t,r] (mps.py:88-92), coalesced over r.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) apply1q_kernel(StateView sv, const int* items,
+                                                      const double2* gates) {
+  const int item = blockIdx.y;
+  const int s = items[2 * item], q = items[2 * item + 1];
+  const int* d = sv.dimv(s);
+  const int dl = d[q], dr = d[q + 1], cap = sv.cap;
+  const double2 g00 = gates[4 * (size_t)item + 0], g01 = gates[4 * (size_t)item + 1];
+  const double2 g10 = gates[4 * (size_t)item + 2], g11 = gates[4 * (size_t)item + 3];
+  double2* t = sv.site(s, q);
+  const int total = dl * dr;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const int l = idx / dr, r = idx % dr;
+    double2* p0 = t + (size_t)(2 * l) * cap + r;
+    double2* p1 = p0 + cap;
+    const double2 a = *p0, b = *p1;
+    *p0 = cadd(cmul(g00, a), cmul(g01, b));
+    *p1 = cadd(cmul(g10, a), cmul(g11, b));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K6: <bits|psi> = [1] T_0[:, b_0, :] ... T_{n-1}[:, b_{n-1}, :] (mps.py:172-179),
+// T_k = Gamma_k lam_{k+1}. One CTA per bitstring, vector in shared memory.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) amplitude_kernel(StateView sv, const int* state_idx,
+                                                        const unsigned char* bits, double2* out) {
+  extern __shared__ __align__(16) double2 vbuf[];  // 2 * cap
+  const int it = blockIdx.x, s = state_idx[it], n = sv.n, cap = sv.cap;
+  const int* d = sv.dimv(s);
+  const unsigned char* bb = bits + (size_t)it * n;
+  double2* cur = vbuf;
+  double2* nxt = vbuf + cap;
+  if (threadIdx.x == 0) cur[0] = make_double2(1.0, 0.0);
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    const int dl = d[k], dr = d[k + 1], b = bb[k];
+    const double2* t = sv.site(s, k) + (size_t)b * cap;
+    const double* lam = sv.bond(s, k + 1);
+    for (int r = threadIdx.x; r < dr; r += blockDim.x) {
+      double2 acc = make_double2(0.0, 0.0);
+      for (int l = 0; l < dl; ++l) acc = cfma(cur[l], t[(size_t)(2 * l) * cap + r], acc);
+      nxt[r] = cscale(acc, lam[r]);
+    }
+    __syncthreads();
+    double2* tmp = cur;
+    cur = nxt;
+    nxt = tmp;
+  }
+  if (threadIdx.x == 0) out[it] = cur[0];
+}
+
+// ---------------------------------------------------------------------------
+// K5: environment transfers (mps.py:196-204 reassociated into two GEMMs).
+//   prep : OT[b,s,q] = sum_t O[s,t] Gamma[b,t,q] lam[q]   (Pauli O)
+//   left : F = E_k @ OT (dl x 2dr);   E_{k+1} = T^H F  (T as (2dl x dr))
+//   right: F = OT @ R^T (2dl x dr);   R_k = conj(T) F^T (T, F as (dl x 2dr))
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) env_prep_kernel(StateView sv, const int* state_idx,
+                                                       const int* site, const unsigned char* pauli,
+                                                       double2* ot, size_t ot_stride) {
+  const int it = blockIdx.y;
+  const int s = state_idx[it], k = site[it], op = pauli[it], cap = sv.cap;
+  const int* d = sv.dimv(s);
+  const int dl = d[k], dr = d[k + 1];
+  const double2* g = sv.site(s, k);
+  const double* lam = sv.bond(s, k + 1);
+  double2* o = ot + (size_t)it * ot_stride;
+  const int total = dl * dr;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const int b = idx / dr, q = idx % dr;
+    const double2 t0 = cscale(g[(size_t)(2 * b) * cap + q], lam[q]);
+    const double2 t1 = cscale(g[(size_t)(2 * b + 1) * cap + q], lam[q]);
+    double2 o0, o1;
+    switch (op) {
+      case 1: o0 = t1; o1 = t0; break;                                   // X
+      case 2: o0 = make_double2(t1.y, -t1.x); o1 = make_double2(-t0.y, t0.x); break;  // Y: -i t1, i t0
+      case 3: o0 = t0; o1 = make_double2(-t1.x, -t1.y); break;           // Z
+      default: o0 = t0; o1 = t1; break;                                  // I
+    }
+    o[(size_t)(2 * b) * cap + q] = o0;
+    o[(size_t)(2 * b + 1) * cap + q] = o1;
+  }
+}
+
+struct EnvOpBase {
+  StateView sv;
+  const int* state_idx;
+  const int* site;
+  int dl, dr, cap;
+  BMPS_DEV void dims_of(int item) {
+    const int s = state_idx[item], k = site[item];
+    const int* d = sv.dimv(s);
+    dl = d[k];
+    dr = d[k + 1];
+    cap = sv.cap;
+  }
+};
+
+// left GEMM1: F[a, (s,q)] = sum_b E[a,b] OT[b,s,q];  F stored as (2a+s)*cap + q
+struct EnvL1 : EnvOpBase {
+  static constexpr bool kAKMajor = true, kBKMajor = false;
+  const double2* env;
+  const double2* ot;
+  double2* f;
+  size_t env_stride, ot_stride;
+  const double2 *e_, *o_;
+  double2* f_;
+  BMPS_DEV bool begin(int item, int& M, int& N, int& K) {
+    dims_of(item);
+    e_ = env + (size_t)item * env_stride;
+    o_ = ot + (size_t)item * ot_stride;
+    f_ = f + (size_t)item * ot_stride;
+    M = dl;
+    N = 2 * dr;
+    K = dl;
+    return true;
+  }
+  BMPS_DEV double2 a(int i, int k) const { return e_[(size_t)i * cap + k]; }
+  BMPS_DEV double2 b(int k, int j) const {
+    const int s = j / dr, q = j % dr;
+    return o_[(size_t)(2 * k + s) * cap + q];
+  }
+  BMPS_DEV void store(int i, int j, double2 v) const {
+    const int s = j / dr, q = j % dr;
+    f_[(size_t)(2 * i + s) * cap + q] = v;
+  }
+};
+
+// left GEMM2: E'[r,q] = sum_{(a,s)} conj(Gamma[(a,s),r] lam[r]) F[(a,s),q]
+struct EnvL2 : EnvOpBase {
+  static constexpr bool kAKMajor = false, kBKMajor = false;
+  const double2* f;
+  double2* out;
+  size_t ot_stride, env_stride;
+  const double2* g_;
+  const double* lam_;
+  const double2* f_;
+  double2* o_;
+  BMPS_DEV bool begin(int item, int& M, int& N, int& K) {
+    dims_of(item);
+    const int s = state_idx[item], k = site[item];
+    g_ = sv.site(s, k);
+    lam_ = sv.bond(s, k + 1);
+    f_ = f + (size_t)item * ot_stride;
+    o_ = out + (size_t)item * env_stride;
+    M = dr;
+    N = dr;
+    K = 2 * dl;
+    return true;
+  }
+  BMPS_DEV double2 a(int i, int k) const { return cconj(cscale(g_[(size_t)k * cap + i], lam_[i])); }
+  BMPS_DEV double2 b(int k, int j) const { return f_[(size_t)k * cap + j]; }
+  BMPS_DEV void store(int i, int j, double2 v) const { o_[(size_t)i * cap + j] = v; }
+};
+
+// right GEMM1: F[(b,s), r] = sum_q OT[(b,s),q] R[r,q]
+struct EnvR1 : EnvOpBase {
+  static constexpr bool kAKMajor = true, kBKMajor = true;
+  const double2* env;
+  const double2* ot;
+  double2* f;
+  size_t env_stride, ot_stride;
+  const double2 *e_, *o_;
+  double2* f_;
+  BMPS_DEV bool begin(int item, int& M, int& N, int& K) {
+    dims_of(item);
+    e_ = env + (size_t)item * env_stride;
+    o_ = ot + (size_t)item * ot_stride;
+    f_ = f + (size_t)item * ot_stride;
+    M = 2 * dl;
+    N = dr;
+    K = dr;
+    return true;
+  }
+  BMPS_DEV double2 a(int i, int k) const { return o_[(size_t)i * cap + k]; }
+  BMPS_DEV double2 b(int k, int j) const { return e_[(size_t)j * cap + k]; }
+  BMPS_DEV void store(int i, int j, double2 v) const { f_[(size_t)i * cap + j] = v; }
+};
+
+// right GEMM2: R'[a,b] = sum_{(s,r)} conj(Gamma[a,s,r] lam[r]) F[(b,s), r]
+struct EnvR2 : EnvOpBase {
+  static constexpr bool kAKMajor = true, kBKMajor = true;
+  const double2* f;
+  double2* out;
+  size_t ot_stride, env_stride;
+  const double2* g_;
+  const double* lam_;
+  const double2* f_;
+  double2* o_;
+  BMPS_DEV bool begin(int item, int& M, int& N, int& K) {
+    dims_of(item);
+    const int s = state_idx[item], k = site[item];
+    g_ = sv.site(s, k);
+    lam_ = sv.bond(s, k + 1);
+    f_ = f + (size_t)item * ot_stride;
+    o_ = out + (size_t)item * env_stride;
+    M = dl;
+    N = dl;
+    K = 2 * dr;
+    return true;
+  }
+  BMPS_DEV double2 a(int i, int k) const {
+    const int s = k / dr, r = k % dr;
+    return cconj(cscale(g_[(size_t)(2 * i + s) * cap + r], lam_[r]));
+  }
+  BMPS_DEV double2 b(int k, int j) const {
+    const int s = k / dr, r = k % dr;
+    return f_[(size_t)(2 * j + s) * cap + r];
+  }
+  BMPS_DEV void store(int i, int j, double2 v) const { o_[(size_t)i * cap + j] = v; }
+};
+
+__global__ void __launch_bounds__(256) env_close_kernel(const int* dims, int n, int cap,
+                                                        const int* state_idx, const int* bond,
+                                                        const double2* el, size_t l_stride,
+                                                        const double2* er, size_t r_stride,
+                                                        double2* out) {
+  const int it = blockIdx.x;
+  const int D = dims[(size_t)state_idx[it] * (n + 1) + bond[it]];
+  const double2* a = el + (size_t)it * l_stride;
+  const double2* b = er + (size_t)it * r_stride;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int idx = threadIdx.x; idx < D * D; idx += blockDim.x) {
+    const int i = idx / D, j = idx % D;
+    acc = cfma(a[(size_t)i * cap + j], b[(size_t)i * cap + j], acc);
+  }
+  __shared__ double2 red[256];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = cadd(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[it] = red[0];
+}
+
+__global__ void item_info_kernel(const ItemMeta* meta, int nitems, int* sweeps, int* keep) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nitems) return;
+  if (sweeps) sweeps[i] = meta[i].sweeps;
+  if (keep) keep[i] = meta[i].keep;
+}
+
+// workspace layout for bmps_apply_2q
+struct Ws {
+  ItemMeta* meta;
+  double* sig;
+  int* perm;
+  int* counter;
+  double2* M0;
+  double2* X;
+  size_t mat_stride;
+  int sig_stride;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t ws_layout(int cap, int nitems, char* base, Ws* ws) {
+  const size_t mat_stride = (size_t)4 * cap * cap;
+  const int sig_stride = 2 * cap;
+  size_t off = 0;
+  const size_t o_meta = off;
+  off = align256(off + sizeof(ItemMeta) * (size_t)nitems);
+  const size_t o_sig = off;
+  off = align256(off + sizeof(double) * (size_t)sig_stride * nitems);
+  const size_t o_perm = off;
+  off = align256(off + sizeof(int) * (size_t)sig_stride * nitems);
+  const size_t o_cnt = off;
+  off = align256(off + 256);
+  const size_t o_m0 = off;
+  off = align256(off + sizeof(double2) * mat_stride * nitems);
+  const size_t o_x = off;
+  off = align256(off + sizeof(double2) * mat_stride * nitems);
+  if (ws && base) {
+    ws->meta = (ItemMeta*)(base + o_meta);
+    ws->sig = (double*)(base + o_sig);
+    ws->perm = (int*)(base + o_perm);
+    ws->counter = (int*)(base + o_cnt);
+    ws->M0 = (double2*)(base + o_m0);
+    ws->X = (double2*)(base + o_x);
+    ws->mat_stride = mat_stride;
+    ws->sig_stride = sig_stride;
+  }
+  return off;
+}
+
+bool g_attrs_set = false;
+void set_attrs() {
+  if (g_attrs_set) return;
+  cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
+  cudaFuncSetAttribute(jacobi_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)JacCfg<32>::kSmem);
+  cudaFuncSetAttribute(jacobi_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)JacCfg<64>::kSmem);
+  g_attrs_set = true;
+}
+
+int32_t launch_status() {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "libbmps: launch failed: %s\n", cudaGetErrorString(e));
+    return BMPS_E_LAUNCH;
+  }
+  return BMPS_OK;
+}
+
+StateView make_view(double* gamma, double* lam, int32_t* dims, int n, int cap) {
+  StateView sv;
+  sv.gamma = (double2*)gamma;
+  sv.lam = lam;
+  sv.dims = dims;
+  sv.n = n;
+  sv.cap = cap;
+  return sv;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t bmps_version(void) { return 1; }
+
+const char* bmps_status_string(int32_t code) {
+  switch (code) {
+    case BMPS_OK: return "ok";
+    case BMPS_E_ARG: return "invalid argument";
+    case BMPS_E_LAUNCH: return "kernel launch failed";
+    case BMPS_E_WORKSPACE: return "workspace too small";
+    case BMPS_S_SVD_FAILED: return "SVD failed (Jacobi did not converge)";
+    case BMPS_S_ALL_TRUNCATED: return "all singular values truncated";
+    case BMPS_S_CAPACITY: return "bond dimension exceeds allocated capacity";
+    default: return "unknown status";
+  }
+}
+
+int32_t bmps_init_product(double* gamma, double* lam, int32_t* dims, double* trunc_err,
+                          int64_t* entries, int64_t* peak, int32_t* max_bond_seen,
+                          int32_t* status, int32_t* status_bond, int32_t S, int32_t n,
+                          int32_t cap, void* stream) {
+  if (S < 1 || n < 1 || cap < 1 || !gamma || !lam || !dims) return BMPS_E_ARG;
+  StateView sv = make_view(gamma, lam, dims, n, cap);
+  const int total = std::max(S * (n + 1), S);
+  init_kernel<<<(total + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+      sv, S, trunc_err, (long long*)entries, (long long*)peak, max_bond_seen, status, status_bond);
+  return launch_status();
+}
+
+int32_t bmps_apply_1q(double* gamma, const int32_t* dims, int32_t S, int32_t n, int32_t cap,
+                      const int32_t* items, const double* gates, int32_t nitems, void* stream) {
+  if (nitems == 0) return BMPS_OK;
+  if (nitems < 0 || S < 1 || n < 1 || cap < 1) return BMPS_E_ARG;
+  StateView sv = make_view(gamma, nullptr, (int32_t*)dims, n, cap);
+  const int per_item = std::min(std::max((cap * cap + 255) / 256, 1), 64);
+  dim3 grid(per_item, nitems);
+  apply1q_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(sv, items, (const double2*)gates);
+  return launch_status();
+}
+
+size_t bmps_apply_2q_workspace_bytes(int32_t cap, int32_t nitems) {
+  return ws_layout(cap, nitems, nullptr, nullptr);
+}
+
+int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int32_t n,
+                      int32_t cap, const int32_t* items, const double* gates, int32_t nitems,
+                      bmps_policy policy, bmps_update_record* log, const int32_t* log_index,
+                      void* workspace, size_t workspace_bytes, int32_t dim_bound, int32_t mode,
+                      void* stream) {
+  if (nitems == 0) return BMPS_OK;
+  if (nitems < 0 || S < 1 || n < 2 || cap < 1 || cap > 1024 || !log || !log_index)
+    return BMPS_E_ARG;
+  if (workspace_bytes < ws_layout(cap, nitems, nullptr, nullptr)) return BMPS_E_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  set_attrs();
+  Ws ws;
+  ws_layout(cap, nitems, (char*)workspace, &ws);
+  StateView sv = make_view(gamma, lam, dims, n, cap);
+  if (dim_bound <= 0 || dim_bound > cap) dim_bound = cap;
+
+  // K2 theta
+  const int tpd = (dim_bound + 31) / 32;
+  theta_kernel<<<dim3(tpd * tpd, nitems), 256, kThetaSmem, st>>>(
+      sv, items, (const double2*)gates, ws.meta, ws.M0, ws.X, ws.mat_stride, tpd);
+  int32_t rc = launch_status();
+  if (rc) return rc;
+
+  // K3 Jacobi SVD
+  const int cmax = 2 * dim_bound;
+  const int max_sweeps = 60;
+  const double tol_factor = 4.0;
+  JacArgs ja;
+  ja.meta = ws.meta;
+  ja.X = ws.X;
+  ja.mat_stride = ws.mat_stride;
+  ja.round = 0;
+  ja.max_sweeps = max_sweeps;
+  ja.max_inner = 1;
+  ja.tol_factor = tol_factor;
+  const int explicit_mode = mode & 3;
+  if (cmax <= 64) {
+    ja.persistent = 1;
+    if (cmax <= 32)
+      jacobi_kernel<32><<<dim3(1, nitems), 256, JacCfg<32>::kSmem, st>>>(ja);
+    else
+      jacobi_kernel<64><<<dim3(1, nitems), 256, JacCfg<64>::kSmem, st>>>(ja);
+    if ((rc = launch_status())) return rc;
+  } else {
+    const int nbmax = (cmax + 15) / 16 + ((cmax + 15) / 16 & 1);
+    const bool persistent =
+        explicit_mode == 1 || (explicit_mode == 0 && (long)nitems * 2 >= 2L * kNumSMs * 2);
+    if (persistent) {
+      ja.persistent = 1;
+      jacobi_kernel<32><<<dim3(1, nitems), 256, JacCfg<32>::kSmem, st>>>(ja);
+      if ((rc = launch_status())) return rc;
+    } else {
+      ja.persistent = 0;
+      static int* h_cnt = nullptr;
+      if (!h_cnt) cudaMallocHost(&h_cnt, sizeof(int));
+      for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+        cudaMemsetAsync(ws.counter, 0, sizeof(int), st);
+        for (int rho = 0; rho < nbmax - 1; ++rho) {
+          ja.round = rho;
+          jacobi_kernel<32><<<dim3(nbmax / 2, nitems), 256, JacCfg<32>::kSmem, st>>>(ja);
+        }
+        sweep_end_kernel<<<(nitems + 127) / 128, 128, 0, st>>>(ws.meta, nitems, max_sweeps,
+                                                               ws.counter);
+        if ((rc = launch_status())) return rc;
+        if (sweep >= 3) {
+          cudaMemcpyAsync(h_cnt, ws.counter, sizeof(int), cudaMemcpyDeviceToHost, st);
+          cudaStreamSynchronize(st);
+          if (*h_cnt == 0) break;
+        }
+      }
+    }
+  }
+
+  // K4 finalize + split
+  finalize_kernel<<<nitems, 512, 0, st>>>(sv, items, ws.meta, ws.X, ws.mat_stride, ws.sig,
+                                          ws.perm, ws.sig_stride, policy.cutoff, policy.max_bond,
+                                          policy.relative, log, log_index);
+  if ((rc = launch_status())) return rc;
+  SplitOp sop;
+  sop.sv = sv;
+  sop.items = items;
+  sop.meta = ws.meta;
+  sop.M0 = ws.M0;
+  sop.X = ws.X;
+  sop.mat_stride = ws.mat_stride;
+  sop.sig_ws = ws.sig;
+  sop.perm_ws = ws.perm;
+  sop.sig_stride = ws.sig_stride;
+  const int kb = policy.max_bond > 0 ? std::min(policy.max_bond, cap) : cap;
+  dim3 sgrid((cmax + 63) / 64, (std::min(kb, cmax) + 63) / 64, nitems);
+  gemm_kernel<SplitOp><<<sgrid, 256, 0, st>>>(sop);
+  if ((rc = launch_status())) return rc;
+  return launch_status();
+}
+
+int32_t bmps_stats_replay(const bmps_update_record* log, const int32_t* ranges, int32_t nranges,
+                          double* trunc_err, int64_t* entries, int64_t* peak,
+                          int32_t* max_bond_seen, int32_t* status, int32_t* status_bond,
+                          void* stream) {
+  if (nranges == 0) return BMPS_OK;
+  if (nranges < 0 || !log || !ranges) return BMPS_E_ARG;
+  stats_replay_kernel<<<(nranges + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
+      log, ranges, nranges, trunc_err, (long long*)entries, (long long*)peak, max_bond_seen,
+      status, status_bond);
+  return launch_status();
+}
+
+int32_t bmps_apply_2q_sweeps(const void* workspace, int32_t nitems, int32_t* sweeps,
+                             void* stream) {
+  if (nitems <= 0) return BMPS_OK;
+  const ItemMeta* meta = (const ItemMeta*)workspace;  // meta sits at offset 0
+  item_info_kernel<<<(nitems + 127) / 128, 128, 0, (cudaStream_t)stream>>>(meta, nitems, sweeps,
+                                                                           nullptr);
+  return launch_status();
+}
+
+int32_t bmps_amplitudes(const double* gamma, const double* lam, const int32_t* dims, int32_t S,
+                        int32_t n, int32_t cap, const int32_t* state_idx, const uint8_t* bits,
+                        int32_t count, double* out, void* stream) {
+  if (count == 0) return BMPS_OK;
+  if (count < 0 || S < 1 || n < 1 || cap < 1) return BMPS_E_ARG;
+  StateView sv = make_view((double*)gamma, (double*)lam, (int32_t*)dims, n, cap);
+  amplitude_kernel<<<count, 256, 2 * cap * sizeof(double2), (cudaStream_t)stream>>>(
+      sv, state_idx, bits, (double2*)out);
+  return launch_status();
+}
+
+int32_t bmps_env_transfer(const double* gamma, const double* lam, const int32_t* dims, int32_t S,
+                          int32_t n, int32_t cap, const int32_t* state_idx, const int32_t* site,
+                          const uint8_t* pauli, int32_t direction, const double* env_in,
+                          int64_t in_stride, double* env_out, int64_t out_stride, double* scratch,
+                          int32_t count, void* stream) {
+  if (count == 0) return BMPS_OK;
+  if (count < 0 || S < 1 || n < 1 || cap < 1 || (direction != 0 && direction != 1))
+    return BMPS_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  StateView sv = make_view((double*)gamma, (double*)lam, (int32_t*)dims, n, cap);
+  const size_t ot_stride = (size_t)2 * cap * cap;
+  double2* ot = (double2*)scratch;
+  double2* f = ot + ot_stride * count;
+  const int per_item = std::min(std::max((cap * cap + 255) / 256, 1), 64);
+  env_prep_kernel<<<dim3(per_item, count), 256, 0, st>>>(sv, state_idx, site, pauli, ot, ot_stride);
+  int32_t rc = launch_status();
+  if (rc) return rc;
+  const int t1 = (cap + 63) / 64, t2 = (2 * cap + 63) / 64;
+  if (direction == 0) {
+    EnvL1 g1;
+    g1.sv = sv; g1.state_idx = state_idx; g1.site = site;
+    g1.env = (const double2*)env_in; g1.ot = ot; g1.f = f;
+    g1.env_stride = (size_t)in_stride; g1.ot_stride = ot_stride;
+    gemm_kernel<EnvL1><<<dim3(t1, t2, count), 256, 0, st>>>(g1);
+    if ((rc = launch_status())) return rc;
+    EnvL2 g2;
+    g2.sv = sv; g2.state_idx = state_idx; g2.site = site;
+    g2.f = f; g2.out = (double2*)env_out; g2.ot_stride = ot_stride; g2.env_stride = (size_t)out_stride;
+    gemm_kernel<EnvL2><<<dim3(t1, t1, count), 256, 0, st>>>(g2);
+  } else {
+    EnvR1 g1;
+    g1.sv = sv; g1.state_idx = state_idx; g1.site = site;
+    g1.env = (const double2*)env_in; g1.ot = ot; g1.f = f;
+    g1.env_stride = (size_t)in_stride; g1.ot_stride = ot_stride;
+    gemm_kernel<EnvR1><<<dim3(t2, t1, count), 256, 0, st>>>(g1);
+    if ((rc = launch_status())) return rc;
+    EnvR2 g2;
+    g2.sv = sv; g2.state_idx = state_idx; g2.site = site;
+    g2.f = f; g2.out = (double2*)env_out; g2.ot_stride = ot_stride; g2.env_stride = (size_t)out_stride;
+    gemm_kernel<EnvR2><<<dim3(t1, t1, count), 256, 0, st>>>(g2);
+  }
+  return launch_status();
+}
+
+int32_t bmps_env_close(const int32_t* dims, int32_t n, int32_t cap, const int32_t* state_idx,
+                       const int32_t* bond, const double* env_l, int64_t l_stride,
+                       const double* env_r, int64_t r_stride, int32_t count, double* out,
+                       void* stream) {
+  if (count == 0) return BMPS_OK;
+  if (count < 0 || n < 1 || cap < 1) return BMPS_E_ARG;
+  env_close_kernel<<<count, 256, 0, (cudaStream_t)stream>>>(
+      dims, n, cap, state_idx, bond, (const double2*)env_l, (size_t)l_stride,
+      (const double2*)env_r, (size_t)r_stride, (double2*)out);
+  return launch_status();
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// Shared device helpers for libbmps: complex128 arithmetic, FP64 tensor-core
+// (DMMA, mma.sync m8n8k4 f64) complex tile products, state indexing.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bmps.h"
+
+#define BMPS_DEV __device__ __forceinline__
+
+namespace bmps {
+
+constexpr double kEps = 1.1102230246251565e-16;   // unit roundoff of float64
+constexpr double kPinvFloor = 1e-12;              // mps.py:21 _PINV_FLOOR
+
+BMPS_DEV double2 cmake(double x, double y) { return make_double2(x, y); }
+BMPS_DEV double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+BMPS_DEV double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+BMPS_DEV double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+BMPS_DEV double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+BMPS_DEV double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+// a*b + c
+BMPS_DEV double2 cfma(double2 a, double2 b, double2 c) {
+  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
+BMPS_DEV double cabs2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
+
+// Reference pseudo-inverse of a bond entry: 1/x if x > 1e-12 else 0 (mps.py:129-130).
+BMPS_DEV double pinv(double x) { return x > kPinvFloor ? 1.0 / x : 0.0; }
+
+// d += a * b for one 8x8x4 FP64 tensor-core step (DMMA.8x8x4 on sm_100a).
+// Fragment layout: A(8x4) row = lane>>2, col = lane&3; B(4x8) row = lane&3,
+// col = lane>>2; D(8x8) row = lane>>2, cols 2*(lane&3) + {0,1}.
+BMPS_DEV void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+// complex accumulate: c[0..1] real part, c[2..3] imaginary part.
+BMPS_DEV void zmma(double (&c)[4], double2 a, double2 b) {
+  dmma(c[0], c[1], a.x, b.x);
+  dmma(c[0], c[1], -a.y, b.y);
+  dmma(c[2], c[3], a.x, b.y);
+  dmma(c[2], c[3], a.y, b.x);
+}
+
+// Circle-method round robin over N (even) players: pair p of round rho.
+BMPS_DEV void tourney_pair(int N, int rho, int p, int& i, int& j) {
+  int a, b;
+  if (p == 0) {
+    a = rho;
+    b = N - 1;
+  } else {
+    a = (rho + p) % (N - 1);
+    b = (rho - p + N - 1) % (N - 1);
+  }
+  i = a < b ? a : b;
+  j = a < b ? b : a;
+}
+
+// Complex Jacobi rotation zeroing the (i,j) entry of the 2x2 Hermitian Gram
+// [[a, g], [conj(g), b]]. Column transform [x_i, x_j] <- [x_i, x_j] J with
+// J = [[c, s], [-s*conj(e), c*conj(e)]], e = g/|g| (Rutishauser's tangent).
+BMPS_DEV bool jacobi_rotation(double a, double b, double2 g, double tol, double& c, double& s,
+                              double2& e) {
+  const double ag = hypot(g.x, g.y);
+  if (!(ag > tol * sqrt(a * b))) return false;
+  const double zeta = (b - a) / (2.0 * ag);
+  double t;
+  if (fabs(zeta) > 1e150) {
+    t = 0.5 / zeta;
+  } else {
+    t = 1.0 / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+    if (zeta < 0) t = -t;
+  }
+  c = 1.0 / sqrt(fma(t, t, 1.0));
+  s = c * t;
+  e = make_double2(g.x / ag, g.y / ag);
+  return true;
+}
+
+struct StateView {
+  double2* gamma;
+  double* lam;
+  int* dims;
+  int n;
+  int cap;
+  BMPS_DEV double2* site(int s, int k) const {
+    return gamma + ((size_t)s * n + k) * (size_t)(2 * (size_t)cap * cap);
+  }
+  BMPS_DEV double* bond(int s, int b) const { return lam + ((size_t)s * (n + 1) + b) * cap; }
+  BMPS_DEV int* dimv(int s) const { return dims + (size_t)s * (n + 1); }
+};
+
+// Per-item bookkeeping of one two-site update (lives in the caller's workspace).
+struct ItemMeta {
+  int r, c, orient, dl, dm, dr;   // X rows/cols, orientation, bond dims before update
+  int keep, status, sweeps, conv, flag, pad;
+  double err, norm;
+};
+
+}  // namespace bmps

@@ -1,0 +1,738 @@
+// Two-site update kernels: theta contraction (K2), block one-sided Jacobi SVD
+// (K3), truncation + split (K4) and in-order stats (mps.py:94-136, 82-84).
+#pragma once
+#include "bmps_gemm.cuh"
+
+namespace bmps {
+
+// ---------------------------------------------------------------------------
+// K2 theta: M[(l,a),(b,r)] = sum_{s,t} G[2a+b][2s+t] * C[(l,s),(t,r)] with
+// C = (lam_l * Gamma_q * lam_m) (2dl x dm) @ (Gamma_{q+1} * lam_r) (dm x 2dr)
+// (mps.py:101-114). The GEMM runs on DMMA with GEMM columns interleaved as
+// j = 2r + t so each 64x64 tile holds all four (s,t) entries of its 32x32
+// (l,r) block; the 4x4 gate is applied in the epilogue. The result is written
+// column-major as X0 = M (orient 0, dl >= dr) or X0 = M^H (orient 1) so the
+// SVD always sees rows >= cols, into both the preserved copy M0 and the
+// Jacobi working copy X.
+// ---------------------------------------------------------------------------
+struct ThetaOp {
+  static constexpr bool kAKMajor = true;
+  static constexpr bool kBKMajor = false;
+  StateView sv;
+  const int* items;
+  const double2* ga;
+  const double2* gb;
+  const double* ll;
+  const double* lm;
+  const double* lr;
+  int cap, dl, dm, dr;
+  BMPS_DEV bool begin(int item, int& M, int& N, int& K) {
+    const int s = items[2 * item], q = items[2 * item + 1];
+    const int* d = sv.dimv(s);
+    dl = d[q];
+    dm = d[q + 1];
+    dr = d[q + 2];
+    cap = sv.cap;
+    ga = sv.site(s, q);
+    gb = sv.site(s, q + 1);
+    ll = sv.bond(s, q);
+    lm = sv.bond(s, q + 1);
+    lr = sv.bond(s, q + 2);
+    M = 2 * dl;
+    N = 2 * dr;
+    K = dm;
+    return true;
+  }
+  BMPS_DEV double2 a(int i, int k) const {
+    return cscale(ga[(size_t)i * cap + k], ll[i >> 1] * lm[k]);
+  }
+  BMPS_DEV double2 b(int k, int j) const {
+    const int r = j >> 1, t = j & 1;
+    return cscale(gb[(size_t)(2 * k + t) * cap + r], lr[r]);
+  }
+};
+
+constexpr int kThetaLdc = 65;
+constexpr size_t kThetaSmem = (size_t)kTile * kThetaLdc * sizeof(double2);
+
+__global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* items,
+                                                    const double2* gates, ItemMeta* meta,
+                                                    double2* M0, double2* X, size_t mat_stride,
+                                                    int tiles_per_dim) {
+  __shared__ __align__(16) double2 sA[kKC][kLds];
+  __shared__ __align__(16) double2 sB[kKC][kLds];
+  __shared__ double2 sG[16];
+  extern __shared__ __align__(16) double2 sC[];  // 64 x kThetaLdc
+  const int item = blockIdx.y;
+  ThetaOp op;
+  op.sv = sv;
+  op.items = items;
+  int M, N, K;
+  op.begin(item, M, N, K);
+  const int dl = op.dl, dm = op.dm, dr = op.dr;
+  const int orient = dl >= dr ? 0 : 1;
+  const int R = orient == 0 ? 2 * dl : 2 * dr;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ItemMeta* m = meta + item;
+    m->r = R;
+    m->c = orient == 0 ? 2 * dr : 2 * dl;
+    m->orient = orient;
+    m->dl = dl;
+    m->dm = dm;
+    m->dr = dr;
+    m->keep = 0;
+    m->status = 0;
+    m->sweeps = 0;
+    m->conv = 0;
+    m->flag = 0;
+    m->err = 0.0;
+    m->norm = 0.0;
+  }
+  const int tm = blockIdx.x / tiles_per_dim, tn = blockIdx.x % tiles_per_dim;
+  const int m0 = tm * kTile, n0 = tn * kTile;
+  if (m0 >= M || n0 >= N) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;
+  if (tid < 16) sG[tid] = gates[(size_t)item * 16 + tid];
+  double acc[4][2][4];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[mi][ni][q] = 0.0;
+  for (int k0 = 0; k0 < K; k0 += kKC) {
+    gemm_load_chunk(op, sA, sB, M, N, K, m0, n0, k0, tid);
+    __syncthreads();
+    gemm_mma_chunk(acc, sA, sB, wm, wn, lane);
+    __syncthreads();
+  }
+  {
+    const int rr = lane >> 2, cc = (lane & 3) * 2;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = wm * 32 + mi * 8 + rr, j = wn * 16 + ni * 8 + cc + h;
+          sC[i * kThetaLdc + j] = make_double2(acc[mi][ni][h], acc[mi][ni][2 + h]);
+        }
+  }
+  __syncthreads();
+  double2* m0p = M0 + (size_t)item * mat_stride;
+  double2* xp = X + (size_t)item * mat_stride;
+  for (int idx = tid; idx < 32 * 32; idx += 256) {
+    // orient 0 writes (2l+a) contiguous -> l fastest; orient 1 writes (b*dr+r) -> r fastest
+    const int lloc = orient == 0 ? (idx & 31) : (idx >> 5);
+    const int rloc = orient == 0 ? (idx >> 5) : (idx & 31);
+    const int l = (m0 >> 1) + lloc, r = (n0 >> 1) + rloc;
+    if (l >= dl || r >= dr) continue;
+    double2 c4[4];
+#pragma unroll
+    for (int st = 0; st < 4; ++st) c4[st] = sC[(2 * lloc + (st >> 1)) * kThetaLdc + 2 * rloc + (st & 1)];
+#pragma unroll
+    for (int ab = 0; ab < 4; ++ab) {
+      double2 v = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int st = 0; st < 4; ++st) v = cfma(sG[ab * 4 + st], c4[st], v);
+      const int a = ab >> 1, b = ab & 1;
+      size_t off;
+      if (orient == 0) {
+        off = (size_t)(2 * l + a) + (size_t)(b * dr + r) * R;
+      } else {
+        off = (size_t)(b * dr + r) + (size_t)(2 * l + a) * R;
+        v = cconj(v);
+      }
+      m0p[off] = v;
+      xp[off] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3 block one-sided (Hestenes) Jacobi SVD, Gram-based, on DMMA.
+//
+// X (r x c, column-major, r >= c) is orthogonalised in place by unitary column
+// rotations: X <- X V. Columns are grouped into blocks of w = W2/2; a visit of
+// block pair (I, J) forms the W2 x W2 Gram of the panel [X_I X_J] on FP64
+// tensor cores, runs cyclic two-sided Jacobi sweeps on the Gram in shared
+// memory (accumulating Q), and applies X_panel <- X_panel Q on tensor cores.
+// Block pairs follow a round-robin tournament; an item converges when a full
+// sweep finds every fresh panel Gram off-diagonal below tol*sqrt(G_ii G_jj).
+// V is not accumulated: the split recovers the other singular vectors from the
+// preserved M0 by a GEMM (V = M0^H U Sigma^-1, see split_kernel).
+// ---------------------------------------------------------------------------
+template <int W2>
+struct JacCfg {
+  static constexpr int RC = (W2 == 32) ? 128 : 64;
+  static constexpr int RCP = RC + 4;
+  static constexpr int LDG = W2 + 4;
+  static constexpr int NT = W2 / 8;
+  static constexpr int GT = NT * NT / 8;
+  static constexpr int AT = (RC / 8) * NT / 8;
+  static constexpr int RPW = AT / NT;
+  static constexpr size_t kSmem = (size_t)(2 * W2 * LDG + RCP * W2) * sizeof(double2);
+};
+
+struct JacArgs {
+  ItemMeta* meta;
+  double2* X;
+  size_t mat_stride;
+  int round;
+  int persistent;
+  int max_sweeps;
+  int max_inner;
+  double tol_factor;
+};
+
+template <int W2>
+BMPS_DEV int panel_col(int p, int I, int J) {
+  constexpr int w = W2 / 2;
+  return p < w ? I * w + p : J * w + (p - w);
+}
+
+template <int W2>
+BMPS_DEV void jac_load_chunk(double2* sP, const double2* X, int r, int c, int row0, int I, int J) {
+  using C = JacCfg<W2>;
+  for (int idx = threadIdx.x; idx < C::RC * W2; idx += blockDim.x) {
+    const int m = idx % C::RC, p = idx / C::RC;
+    const int row = row0 + m, col = panel_col<W2>(p, I, J);
+    sP[m + p * C::RCP] =
+        (row < r && col < c) ? X[(size_t)row + (size_t)col * r] : make_double2(0.0, 0.0);
+  }
+}
+
+template <int W2>
+BMPS_DEV void jac_store_chunk(const double2* sP, double2* X, int r, int c, int row0, int I, int J) {
+  using C = JacCfg<W2>;
+  for (int idx = threadIdx.x; idx < C::RC * W2; idx += blockDim.x) {
+    const int m = idx % C::RC, p = idx / C::RC;
+    const int row = row0 + m, col = panel_col<W2>(p, I, J);
+    if (row < r && col < c) X[(size_t)row + (size_t)col * r] = sP[m + p * C::RCP];
+  }
+}
+
+// Accumulate G += P^H P over one staged chunk (rows < nrows are meaningful).
+template <int W2>
+BMPS_DEV void jac_gram_chunk(double (&acc)[JacCfg<W2>::GT][4], const double2* sP, int nrows) {
+  using C = JacCfg<W2>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tile0 = warp * C::GT, ti = tile0 / C::NT, tj0 = tile0 % C::NT;
+  const int kr = lane & 3, rc = lane >> 2;
+  const int nk4 = (nrows + 3) >> 2;
+  for (int k4 = 0; k4 < nk4; ++k4) {
+    const int k = k4 * 4 + kr;
+    const double2 a = cconj(sP[k + (ti * 8 + rc) * C::RCP]);
+#pragma unroll
+    for (int u = 0; u < C::GT; ++u) {
+      const double2 b = sP[k + ((tj0 + u) * 8 + rc) * C::RCP];
+      zmma(acc[u], a, b);
+    }
+  }
+}
+
+// Out(chunk) = P_chunk (RC x W2) * Q (W2 x W2), written back into sP.
+template <int W2>
+BMPS_DEV void jac_apply_chunk(double2* sP, const double2* sQ) {
+  using C = JacCfg<W2>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int kr = lane & 3, rc = lane >> 2;
+  const int mi0 = warp * C::RPW;
+  double acc[C::AT][4];
+#pragma unroll
+  for (int u = 0; u < C::AT; ++u)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
+#pragma unroll 2
+  for (int k4 = 0; k4 < W2 / 4; ++k4) {
+    const int k = k4 * 4 + kr;
+    double2 b[C::NT];
+#pragma unroll
+    for (int nj = 0; nj < C::NT; ++nj) b[nj] = sQ[k + (nj * 8 + rc) * C::LDG];
+#pragma unroll
+    for (int rr = 0; rr < C::RPW; ++rr) {
+      const double2 a = sP[(mi0 + rr) * 8 + rc + k * C::RCP];
+#pragma unroll
+      for (int nj = 0; nj < C::NT; ++nj) zmma(acc[rr * C::NT + nj], a, b[nj]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int rr = 0; rr < C::RPW; ++rr)
+#pragma unroll
+    for (int nj = 0; nj < C::NT; ++nj)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = (mi0 + rr) * 8 + rc, nn = nj * 8 + kr * 2 + h;
+        sP[m + nn * C::RCP] = make_double2(acc[rr * C::NT + nj][h], acc[rr * C::NT + nj][2 + h]);
+      }
+  __syncthreads();
+}
+
+struct RotShared {
+  double c[32], s[32];
+  double2 e[32];
+  int i[32], j[32], act[32];
+};
+
+// Cyclic two-sided Jacobi on the W2 x W2 Hermitian Gram, accumulating Q.
+template <int W2>
+BMPS_DEV void jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, int max_inner) {
+  using C = JacCfg<W2>;
+  constexpr int w = W2 / 2;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < W2 * W2; idx += blockDim.x) {
+    const int i = idx % W2, j = idx / W2;
+    sQ[i + j * C::LDG] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+  }
+  for (int it = 0; it < max_inner; ++it) {
+    int any = 0;
+    for (int rho = 0; rho < W2 - 1; ++rho) {
+      int act = 0;
+      if (tid < w) {
+        int i, j;
+        tourney_pair(W2, rho, tid, i, j);
+        double c, s;
+        double2 e;
+        act = jacobi_rotation(sG[i + i * C::LDG].x, sG[j + j * C::LDG].x, sG[i + j * C::LDG], tol,
+                              c, s, e);
+        rs.i[tid] = i;
+        rs.j[tid] = j;
+        rs.act[tid] = act;
+        rs.c[tid] = c;
+        rs.s[tid] = s;
+        rs.e[tid] = e;
+      }
+      any |= __syncthreads_or(act);
+      // columns i, j of G and Q: [x_i, x_j] <- [x_i, x_j] J
+      for (int idx = tid; idx < 2 * W2 * w; idx += blockDim.x) {
+        const int which = idx / (W2 * w), rem = idx % (W2 * w);
+        const int p = rem / W2, k = rem % W2;
+        if (!rs.act[p]) continue;
+        double2* base = which ? sQ : sG;
+        const int i = rs.i[p], j = rs.j[p];
+        const double c = rs.c[p], s = rs.s[p];
+        const double2 ec = cconj(rs.e[p]);
+        const double2 gi = base[k + i * C::LDG], gj = base[k + j * C::LDG];
+        base[k + i * C::LDG] = csub(cscale(gi, c), cmul(cscale(ec, s), gj));
+        base[k + j * C::LDG] = cadd(cscale(gi, s), cmul(cscale(ec, c), gj));
+      }
+      __syncthreads();
+      // rows i, j of G: J^H applied from the left
+      for (int idx = tid; idx < W2 * w; idx += blockDim.x) {
+        const int p = idx / W2, k = idx % W2;
+        if (!rs.act[p]) continue;
+        const int i = rs.i[p], j = rs.j[p];
+        const double c = rs.c[p], s = rs.s[p];
+        const double2 e = rs.e[p];
+        const double2 gi = sG[i + k * C::LDG], gj = sG[j + k * C::LDG];
+        sG[i + k * C::LDG] = csub(cscale(gi, c), cmul(cscale(e, s), gj));
+        sG[j + k * C::LDG] = cadd(cscale(gi, s), cmul(cscale(e, c), gj));
+      }
+      __syncthreads();
+    }
+    if (!any) break;
+  }
+}
+
+// One block-pair visit. Returns true if the fresh panel Gram was not yet
+// orthogonal (a rotation was applied). If `resident`, the whole panel already
+// sits in sP (r <= RC) and is neither loaded nor stored here.
+template <int W2>
+BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, int max_inner,
+                        bool resident, double2* sG, double2* sQ, double2* sP, RotShared& rs) {
+  using C = JacCfg<W2>;
+  const int tid = threadIdx.x;
+  double acc[C::GT][4];
+#pragma unroll
+  for (int u = 0; u < C::GT; ++u)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
+  for (int row0 = 0; row0 < r; row0 += C::RC) {
+    if (!resident) {
+      __syncthreads();
+      jac_load_chunk<W2>(sP, X, r, c, row0, I, J);
+      __syncthreads();
+    }
+    jac_gram_chunk<W2>(acc, sP, min(C::RC, r - row0));
+  }
+  {
+    const int lane = tid & 31, warp = tid >> 5;
+    const int tile0 = warp * C::GT, ti = tile0 / C::NT, tj0 = tile0 % C::NT;
+#pragma unroll
+    for (int u = 0; u < C::GT; ++u)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = ti * 8 + (lane >> 2), j = (tj0 + u) * 8 + (lane & 3) * 2 + h;
+        sG[i + j * C::LDG] = make_double2(acc[u][h], acc[u][2 + h]);
+      }
+  }
+  __syncthreads();
+  int dirty = 0;
+  for (int idx = tid; idx < W2 * W2; idx += blockDim.x) {
+    const int i = idx % W2, j = idx / W2;
+    if (i > j) {
+      sG[i + j * C::LDG] = cconj(sG[j + i * C::LDG]);
+    } else if (i < j) {
+      const double a = sG[i + i * C::LDG].x, b = sG[j + j * C::LDG].x;
+      const double2 g = sG[i + j * C::LDG];
+      if (hypot(g.x, g.y) > tol * sqrt(a * b)) dirty = 1;
+    }
+  }
+  dirty = __syncthreads_or(dirty);
+  for (int i = tid; i < W2; i += blockDim.x) sG[i + i * C::LDG].y = 0.0;
+  __syncthreads();
+  if (!dirty) return false;
+  jac_inner<W2>(sG, sQ, rs, tol, max_inner);
+  for (int row0 = 0; row0 < r; row0 += C::RC) {
+    if (!resident) {
+      if (C::RC < r) {  // multi-chunk panel: reload (single chunk is still staged)
+        __syncthreads();
+        jac_load_chunk<W2>(sP, X, r, c, row0, I, J);
+      }
+      __syncthreads();
+    }
+    jac_apply_chunk<W2>(sP, sQ);
+    if (!resident) jac_store_chunk<W2>(sP, X, r, c, row0, I, J);
+  }
+  __syncthreads();
+  return true;
+}
+
+template <int W2>
+__global__ void __launch_bounds__(256) jacobi_kernel(JacArgs args) {
+  using C = JacCfg<W2>;
+  extern __shared__ __align__(16) double2 jsm[];
+  double2* sG = jsm;
+  double2* sQ = sG + W2 * C::LDG;
+  double2* sP = sQ + W2 * C::LDG;
+  __shared__ RotShared rs;
+  const int item = blockIdx.y;
+  ItemMeta* m = args.meta + item;
+  if (m->conv) return;
+  const int r = m->r, c = m->c;
+  double2* X = args.X + (size_t)item * args.mat_stride;
+  constexpr int w = W2 / 2;
+  int nb = (c + w - 1) / w;
+  nb += nb & 1;
+  const double tol = args.tol_factor * sqrt((double)r) * kEps;
+  if (nb == 2) {
+    // single panel: the whole matrix is one visit, iterated to convergence
+    if (blockIdx.x != 0) return;
+    const bool resident = r <= C::RC;
+    if (resident) {
+      jac_load_chunk<W2>(sP, X, r, c, 0, 0, 1);
+      __syncthreads();
+    }
+    int sweep = 0;
+    bool clean = false;
+    for (; sweep < args.max_sweeps; ++sweep) {
+      if (!jac_visit<W2>(X, r, c, 0, 1, tol, 64, resident, sG, sQ, sP, rs)) {
+        clean = true;
+        break;
+      }
+    }
+    if (resident) jac_store_chunk<W2>(sP, X, r, c, 0, 0, 1);
+    if (threadIdx.x == 0) {
+      m->sweeps = sweep;
+      m->conv = 1;
+      if (!clean) m->status = BMPS_S_SVD_FAILED;
+    }
+    return;
+  }
+  if (args.persistent) {
+    if (blockIdx.x != 0) return;
+    int sweep = 0;
+    bool clean = false;
+    for (; sweep < args.max_sweeps; ++sweep) {
+      bool any = false;
+      for (int rho = 0; rho < nb - 1; ++rho)
+        for (int v = 0; v < nb / 2; ++v) {
+          int I, J;
+          tourney_pair(nb, rho, v, I, J);
+          any |= jac_visit<W2>(X, r, c, I, J, tol, args.max_inner, false, sG, sQ, sP, rs);
+        }
+      if (!any) {
+        clean = true;
+        break;
+      }
+    }
+    if (threadIdx.x == 0) {
+      m->sweeps = sweep;
+      m->conv = 1;
+      if (!clean) m->status = BMPS_S_SVD_FAILED;
+    }
+    return;
+  }
+  const int v = blockIdx.x, rho = args.round;
+  if (v >= nb / 2 || rho >= nb - 1) return;
+  int I, J;
+  tourney_pair(nb, rho, v, I, J);
+  if (jac_visit<W2>(X, r, c, I, J, tol, args.max_inner, false, sG, sQ, sP, rs) &&
+      threadIdx.x == 0)
+    atomicOr(&m->flag, 1);
+}
+
+// End of a round-mode sweep: converge clean items, count the rest.
+__global__ void sweep_end_kernel(ItemMeta* meta, int nitems, int max_sweeps, int* unconverged) {
+  const int item = blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= nitems) return;
+  ItemMeta* m = meta + item;
+  if (m->conv) return;
+  if (!m->flag) {
+    m->conv = 1;
+    return;
+  }
+  m->flag = 0;
+  m->sweeps += 1;
+  if (m->sweeps >= max_sweeps) {
+    m->conv = 1;
+    m->status = BMPS_S_SVD_FAILED;
+    return;
+  }
+  atomicAdd(unconverged, 1);
+}
+
+// ---------------------------------------------------------------------------
+// K4a finalize: sigma_j = ||x_j||, sort descending, keep count (mps.py:43-49),
+// discarded weight (mps.py:121-122), renormalised lambda (mps.py:123-127), new
+// bond dim, and the side of the split read straight from X (U or V^H rows).
+// ---------------------------------------------------------------------------
+constexpr int kMaxCols = 2048;
+
+__global__ void __launch_bounds__(512) finalize_kernel(StateView sv, const int* items,
+                                                       ItemMeta* meta, const double2* X,
+                                                       size_t mat_stride, double* sig_ws,
+                                                       int* perm_ws, int sig_stride,
+                                                       double cutoff, int max_bond, int relative,
+                                                       bmps_update_record* log,
+                                                       const int* log_index) {
+  __shared__ double ssig[kMaxCols];
+  __shared__ int sidx[kMaxCols];
+  __shared__ int s_keep;
+  __shared__ double s_norm;
+  const int item = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  ItemMeta* m = meta + item;
+  const int r = m->r, c = m->c, orient = m->orient, dl = m->dl, dr = m->dr;
+  const int s = items[2 * item], q = items[2 * item + 1];
+  const double2* x = X + (size_t)item * mat_stride;
+  int P2 = 1;
+  while (P2 < c) P2 <<= 1;
+  for (int j = warp; j < P2; j += 16) {
+    double acc = 0.0;
+    if (j < c)
+      for (int i = lane; i < r; i += 32) acc += cabs2(x[(size_t)i + (size_t)j * r]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      ssig[j] = j < c ? sqrt(acc) : -1.0;
+      sidx[j] = j;
+    }
+  }
+  __syncthreads();
+  // bitonic sort: descending sigma, ties by ascending column index
+  for (int k = 2; k <= P2; k <<= 1) {
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      for (int t = tid; t < P2; t += blockDim.x) {
+        const int u = t ^ jj;
+        if (u > t) {
+          const double st = ssig[t], su = ssig[u];
+          const int it = sidx[t], iu = sidx[u];
+          const bool u_first = su > st || (su == st && iu < it);
+          const bool t_first = st > su || (st == su && it < iu);
+          const bool swap = ((t & k) == 0) ? u_first : t_first;
+          if (swap) {
+            ssig[t] = su;
+            ssig[u] = st;
+            sidx[t] = iu;
+            sidx[u] = it;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    int keep;
+    if (cutoff > 0.0) {
+      const double thr = cutoff * (relative ? ssig[0] : 1.0);
+      keep = 0;
+      for (int k = 0; k < c; ++k) keep += ssig[k] >= thr ? 1 : 0;
+    } else {
+      keep = c;
+    }
+    keep = max(keep, 1);
+    if (max_bond > 0) keep = min(keep, max_bond);
+    int status = m->status;
+    if (keep > sv.cap) {
+      keep = sv.cap;
+      if (!status) status = BMPS_S_CAPACITY;
+    }
+    double err = 0.0, nrm2 = 0.0;
+    for (int k = keep; k < c; ++k) err += ssig[k] * ssig[k];
+    for (int k = 0; k < keep; ++k) nrm2 += ssig[k] * ssig[k];
+    const double nrm = sqrt(nrm2);
+    if (nrm == 0.0 && !status) status = BMPS_S_ALL_TRUNCATED;
+    m->keep = keep;
+    m->err = err;
+    m->norm = nrm;
+    m->status = status;
+    s_keep = status ? 0 : keep;
+    s_norm = nrm;
+    if (!status) sv.dimv(s)[q + 1] = keep;
+    bmps_update_record rec;
+    rec.err = err;
+    rec.dl = dl;
+    rec.dm = m->dm;
+    rec.dr = dr;
+    rec.keep = keep;
+    rec.status = status;
+    rec.site = q;
+    log[log_index[item]] = rec;
+  }
+  __syncthreads();
+  const int keep = s_keep;
+  if (keep == 0) return;  // failure: leave the state untouched (host raises)
+  const double nrm = s_norm;
+  double* sig_out = sig_ws + (size_t)item * sig_stride;
+  int* perm_out = perm_ws + (size_t)item * sig_stride;
+  double* lam_new = sv.bond(s, q + 1);
+  for (int k = tid; k < keep; k += blockDim.x) {
+    sig_out[k] = ssig[k];
+    perm_out[k] = sidx[k];
+    lam_new[k] = ssig[k] / nrm;
+  }
+  const int cap = sv.cap;
+  if (orient == 0) {
+    // Gamma_q[l,a,k] = pinv(lam_l[l]) * x[2l+a, perm k] / sigma_k   (mps.py:131,133)
+    double2* gq = sv.site(s, q);
+    const double* ll = sv.bond(s, q);
+    const int rows = 2 * dl;
+    for (int idx = tid; idx < rows * keep; idx += blockDim.x) {
+      const int k = idx % keep, i = idx / keep;
+      const double sk = ssig[k];
+      const double f = sk > 0.0 ? pinv(ll[i >> 1]) / sk : 0.0;
+      gq[(size_t)i * cap + k] = cscale(x[(size_t)i + (size_t)sidx[k] * r], f);
+    }
+  } else {
+    // Gamma_{q+1}[k,b,r] = conj(x[b*dr+r, perm k]) / sigma_k * pinv(lam_r[r])  (mps.py:132,134)
+    double2* gb = sv.site(s, q + 1);
+    const double* lr = sv.bond(s, q + 2);
+    const int cols = 2 * dr;
+    for (int idx = tid; idx < keep * cols; idx += blockDim.x) {
+      const int jcol = idx % cols, k = idx / cols;
+      const int b = jcol / dr, rr = jcol % dr;
+      const double sk = ssig[k];
+      const double f = sk > 0.0 ? pinv(lr[rr]) / sk : 0.0;
+      gb[(size_t)(2 * k + b) * cap + rr] = cscale(cconj(x[(size_t)jcol + (size_t)sidx[k] * r]), f);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4b split GEMM: the other singular vectors W = M0^H Y Sigma^-1 with
+// Y = X[:, perm] / sigma (i.e. W[:,k] = M0^H X[:,perm k] / sigma_k^2), written
+// into Gamma_{q+1} (orient 0, as V^H rows) or Gamma_q (orient 1, as U columns)
+// with the pseudo-inverse bond scaling of mps.py:129-134.
+// ---------------------------------------------------------------------------
+struct SplitOp {
+  static constexpr bool kAKMajor = true;
+  static constexpr bool kBKMajor = true;
+  StateView sv;
+  const int* items;
+  const ItemMeta* meta;
+  const double2* M0;
+  const double2* X;
+  size_t mat_stride;
+  const double* sig_ws;
+  const int* perm_ws;
+  int sig_stride;
+  // per-CTA
+  const double2* m0;
+  const double2* x;
+  const double* sig;
+  const int* perm;
+  double2* dst;
+  const double* lb;
+  int r, orient, dl, dr, cap;
+  BMPS_DEV bool begin(int item, int& M, int& N, int& K) {
+    const ItemMeta* m = meta + item;
+    if (m->status || m->keep <= 0) return false;
+    const int s = items[2 * item], q = items[2 * item + 1];
+    r = m->r;
+    orient = m->orient;
+    dl = m->dl;
+    dr = m->dr;
+    cap = sv.cap;
+    m0 = M0 + (size_t)item * mat_stride;
+    x = X + (size_t)item * mat_stride;
+    sig = sig_ws + (size_t)item * sig_stride;
+    perm = perm_ws + (size_t)item * sig_stride;
+    if (orient == 0) {
+      dst = sv.site(s, q + 1);
+      lb = sv.bond(s, q + 2);
+    } else {
+      dst = sv.site(s, q);
+      lb = sv.bond(s, q);
+    }
+    M = m->c;
+    N = m->keep;
+    K = r;
+    return true;
+  }
+  BMPS_DEV double2 a(int i, int k) const { return cconj(m0[(size_t)k + (size_t)i * r]); }
+  BMPS_DEV double2 b(int k, int j) const { return x[(size_t)k + (size_t)perm[j] * r]; }
+  BMPS_DEV void store(int i, int j, double2 v) const {
+    const double sj = sig[j];
+    const double f = sj > 0.0 ? 1.0 / (sj * sj) : 0.0;
+    if (orient == 0) {
+      const int b = i / dr, rr = i % dr;
+      dst[(size_t)(2 * j + b) * cap + rr] = cscale(cconj(v), f * pinv(lb[rr]));
+    } else {
+      dst[(size_t)i * cap + j] = cscale(v, f * pinv(lb[i >> 1]));
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Stats replayed in program order per state (mps.py:82-84, 122):
+// trunc_error_sq, total entries, peak entries, max_bond_seen, first failure.
+// ---------------------------------------------------------------------------
+__global__ void stats_replay_kernel(const bmps_update_record* log, const int* ranges, int nranges,
+                                    double* trunc_err, long long* entries, long long* peak,
+                                    int* max_bond_seen, int* status, int* status_bond) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nranges) return;
+  const int s = ranges[3 * g], first = ranges[3 * g + 1], count = ranges[3 * g + 2];
+  double te = trunc_err[s];
+  long long ent = entries[s], pk = peak[s];
+  int mb = max_bond_seen[s], st = status[s], sb = status_bond[s];
+  for (int it = first; it < first + count; ++it) {
+    const bmps_update_record m = log[it];
+    if (st) break;  // the reference raises at the first failure
+    if (m.status == BMPS_S_SVD_FAILED) {
+      st = m.status;
+      sb = m.site;
+      break;
+    }
+    te += m.err;  // added before the all-truncated check, as mps.py:122-126
+    if (m.status) {
+      st = m.status;
+      sb = m.site;
+      break;
+    }
+    const long long dl = m.dl, dm = m.dm, dr = m.dr, k = m.keep;
+    ent += 2 * dl * k + 2 * k * dr - 2 * dl * dm - 2 * dm * dr;
+    pk = ent > pk ? ent : pk;
+    mb = m.keep > mb ? m.keep : mb;
+  }
+  trunc_err[s] = te;
+  entries[s] = ent;
+  peak[s] = pk;
+  max_bond_seen[s] = mb;
+  status[s] = st;
+  status_bond[s] = sb;
+}
+
+}  // namespace bmps

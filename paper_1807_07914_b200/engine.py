@@ -1,0 +1,521 @@
+"""Device-resident MPS state batches and the layered program executor.
+
+``MpsBatch`` owns S independent n-qubit Vidal-form states in HBM (torch
+tensors used only as device buffers) and drives ``libbmps.so`` through its C
+ABI. Programs are lowered exactly like the reference's per-gate loop
+(``R:src/mpsqvm/backends.py:47-60``, SWAP routing ``R:src/mpsqvm/mps.py:138-157``)
+and then scheduled ASAP into layers of site-disjoint operations: in Vidal form
+a two-site update on (q, q+1) reads bonds q-1..q+1 and writes Gamma_q,
+Gamma_{q+1}, lambda_q only, so ops sharing no site commute bit-exactly and one
+layer (over all S states) is one batched launch sequence. Bookkeeping
+(``trunc_error_sq``, ``peak_entries``, ``max_bond_seen``; ``mps.py:82-84``) is
+replayed on the device in program order, so it matches the sequential
+reference regardless of the schedule.
+
+Host code never reads device state while a program runs: bond dimensions stay
+on the device, and the host only keeps an upper-bound model
+(``dim_ub[s, b] <= min(2 dim_ub[s, b-1], 2 dim_ub[s, b+1], max_bond)``) to size
+grids and grow the capacity.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from .gates import SWAP_MATRIX, check_unitary, gate_matrix
+from .hamiltonian import encode_pauli
+from .policy import TruncationPolicy
+
+MAX_CAP = 1024
+_RECORD = _native.RECORD_BYTES
+_ZERO2 = np.zeros((2, 2), dtype=np.complex128)
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1807_07914_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+    _native.load()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.type != "cuda":
+        raise RuntimeError(f"device {dev} is not a CUDA device; there is no CPU fallback")
+    return dev
+
+
+# ---------------------------------------------------------------------------
+# lowering and scheduling
+# ---------------------------------------------------------------------------
+
+_SWAP = np.ascontiguousarray(SWAP_MATRIX)
+
+
+def lower_program(program, n: int, validate_matrices: bool = True):
+    """Flatten a program into (arity, site, matrix) ops in reference order.
+
+    Non-adjacent two-qubit gates expand into the reference's SWAP chain
+    (``mps.py:148-157``); MEASURE is skipped (``backends.py:53-54``). Returns
+    arity (int8), site (int32) and a list of matrices.
+    """
+    arity: list[int] = []
+    site: list[int] = []
+    mats: list[np.ndarray] = []
+    for op in program:
+        kind = getattr(op, "kind", None)
+        if kind is not None and kind.value == "MEASURE":
+            continue
+        qs = op.qubits
+        for q in qs:
+            if not 0 <= q < n:
+                raise ValueError(f"site {q} out of range for {n} qubits")
+        m = gate_matrix(op)
+        if validate_matrices and kind is None:
+            check_unitary(m)
+        if len(qs) == 1:
+            arity.append(1)
+            site.append(qs[0])
+            mats.append(m)
+            continue
+        q1, q2 = qs
+        if q1 == q2:
+            raise ValueError("two-qubit gate needs two distinct sites")
+        lo, hi = (q1, q2) if q1 < q2 else (q2, q1)
+        for k in range(hi - 1, lo, -1):
+            arity.append(2); site.append(k); mats.append(_SWAP)
+        arity.append(2); site.append(lo); mats.append(m if q1 < q2 else _SWAP @ m @ _SWAP)
+        for k in range(lo + 1, hi):
+            arity.append(2); site.append(k); mats.append(_SWAP)
+    return np.asarray(arity, dtype=np.int8), np.asarray(site, dtype=np.int32), mats
+
+
+def asap_layers(arity: np.ndarray, site: np.ndarray, n: int) -> np.ndarray:
+    """Earliest layer of each op such that ops sharing a site keep program order."""
+    last = np.zeros(n + 1, dtype=np.int64)
+    layer = np.empty(len(arity), dtype=np.int64)
+    for i in range(len(arity)):
+        q = int(site[i])
+        if arity[i] == 1:
+            L = last[q] + 1
+            last[q] = L
+        else:
+            L = max(last[q], last[q + 1]) + 1
+            last[q] = L
+            last[q + 1] = L
+        layer[i] = L - 1
+    return layer
+
+
+@dataclass
+class Plan:
+    """A batch of lowered programs scheduled into layers (host arrays)."""
+
+    n_layers: int
+    # per layer offsets into the concatenated arrays
+    off1: np.ndarray
+    off2: np.ndarray
+    items1: np.ndarray      # int32 [K1, 2]
+    gates1: np.ndarray      # complex128 [K1, 2, 2]
+    items2: np.ndarray      # int32 [K2, 2]
+    gates2: np.ndarray      # complex128 [K2, 4, 4]
+    logidx2: np.ndarray     # int32 [K2]
+    ranges: np.ndarray      # int32 [R, 3] (state, first record, count), program order
+    n_records: int
+
+
+def compile_batch(programs, n: int, states=None) -> Plan:
+    """Lower and layer ``programs[i]`` for state ``states[i]`` (default i)."""
+    states = list(range(len(programs))) if states is None else list(states)
+    all_layer, all_state, all_ar, all_site, all_mat, all_rec = [], [], [], [], [], []
+    ranges = []
+    rec_base = 0
+    for s, prog in zip(states, programs):
+        ar, st, mats = lower_program(prog, n)
+        lay = asap_layers(ar, st, n)
+        two = ar == 2
+        rec = np.full(len(ar), -1, dtype=np.int64)
+        n2 = int(two.sum())
+        rec[two] = rec_base + np.arange(n2)
+        if n2:
+            ranges.append((s, rec_base, n2))
+        rec_base += n2
+        all_layer.append(lay)
+        all_state.append(np.full(len(ar), s, dtype=np.int32))
+        all_ar.append(ar)
+        all_site.append(st)
+        all_mat.extend(mats)
+        all_rec.append(rec)
+    if not all_layer:
+        return Plan(0, np.zeros(1, np.int64), np.zeros(1, np.int64), np.zeros((0, 2), np.int32),
+                    np.zeros((0, 2, 2), complex), np.zeros((0, 2), np.int32),
+                    np.zeros((0, 4, 4), complex), np.zeros(0, np.int32),
+                    np.zeros((0, 3), np.int32), 0)
+    layer = np.concatenate(all_layer)
+    state = np.concatenate(all_state)
+    ar = np.concatenate(all_ar)
+    site = np.concatenate(all_site)
+    rec = np.concatenate(all_rec)
+    n_layers = int(layer.max()) + 1 if len(layer) else 0
+    # stable order: layer, then original (state-major, program) order
+    order = np.argsort(layer, kind="stable")
+    one = order[ar[order] == 1]
+    two = order[ar[order] == 2]
+    items1 = np.stack([state[one], site[one]], axis=1).astype(np.int32) if len(one) else np.zeros((0, 2), np.int32)
+    items2 = np.stack([state[two], site[two]], axis=1).astype(np.int32) if len(two) else np.zeros((0, 2), np.int32)
+    gates1 = np.array([all_mat[i] for i in one], dtype=np.complex128).reshape(-1, 2, 2)
+    gates2 = np.array([all_mat[i] for i in two], dtype=np.complex128).reshape(-1, 4, 4)
+    off1 = np.searchsorted(layer[one], np.arange(n_layers + 1)) if len(one) else np.zeros(n_layers + 1, np.int64)
+    off2 = np.searchsorted(layer[two], np.arange(n_layers + 1)) if len(two) else np.zeros(n_layers + 1, np.int64)
+    return Plan(n_layers, off1, off2, items1, gates1, items2, gates2, rec[two].astype(np.int32),
+                np.asarray(ranges, dtype=np.int32).reshape(-1, 3), rec_base)
+
+
+# ---------------------------------------------------------------------------
+# device state batch
+# ---------------------------------------------------------------------------
+
+
+class MpsBatch:
+    """S independent n-qubit MPS states resident in HBM, initially |0...0>."""
+
+    def __init__(self, num_states: int, n: int, policy: TruncationPolicy | None = None,
+                 device=None, cap: int | None = None, max_items_per_launch: int = 4096):
+        if n < 1:
+            raise ValueError("need at least one qubit")
+        if num_states < 1:
+            raise ValueError("need at least one state")
+        self.device = require_cuda(device)
+        self.lib = _native.load()
+        self.S = int(num_states)
+        self.n = int(n)
+        self.policy = policy or TruncationPolicy()
+        self.max_items = int(max_items_per_launch)
+        self.cap = 1
+        self._alloc(int(cap) if cap else 1)
+        self.dim_ub = np.ones((self.S, self.n + 1), dtype=np.int64)
+        self._ws = None
+        self._ws_bytes = 0
+        self.reset()
+
+    # -- buffers ---------------------------------------------------------------
+    def _alloc(self, cap: int) -> None:
+        S, n, dev = self.S, self.n, self.device
+        self.cap = cap
+        self.gamma = torch.zeros((S, n, cap, 2, cap), dtype=torch.complex128, device=dev)
+        self.lam = torch.zeros((S, n + 1, cap), dtype=torch.float64, device=dev)
+        self.dims = torch.ones((S, n + 1), dtype=torch.int32, device=dev)
+        if not hasattr(self, "trunc_err"):
+            self.trunc_err = torch.zeros(S, dtype=torch.float64, device=dev)
+            self.entries = torch.zeros(S, dtype=torch.int64, device=dev)
+            self.peak = torch.zeros(S, dtype=torch.int64, device=dev)
+            self.mbs = torch.zeros(S, dtype=torch.int32, device=dev)
+            self.status = torch.zeros(S, dtype=torch.int32, device=dev)
+            self.status_bond = torch.zeros(S, dtype=torch.int32, device=dev)
+
+    def reset(self) -> None:
+        """Re-initialise every state to |0...0> (``mps.py:55-66``)."""
+        self.gamma.zero_()
+        self.lam.zero_()
+        self.dim_ub[:] = 1
+        rc = self.lib.bmps_init_product(
+            _ptr(self.gamma), _ptr(self.lam), _ptr(self.dims), _ptr(self.trunc_err),
+            _ptr(self.entries), _ptr(self.peak), _ptr(self.mbs), _ptr(self.status),
+            _ptr(self.status_bond), self.S, self.n, self.cap, _stream())
+        _native.check(rc, "bmps_init_product")
+
+    def _cap_limit(self) -> int:
+        full = 1 << min(self.n // 2, 30)
+        mb = self.policy.max_bond
+        return min(full, mb) if mb is not None else full
+
+    def ensure_capacity(self, needed: int) -> None:
+        """Grow the bond capacity (power of two) to hold ``needed``; copies state."""
+        if needed <= self.cap:
+            return
+        if needed > MAX_CAP:
+            raise ValueError(
+                f"bond dimension {needed} exceeds the device capacity limit {MAX_CAP}; "
+                "set TruncationPolicy.max_bond")
+        new = 1
+        while new < needed:
+            new <<= 1
+        new = min(new, max(MAX_CAP, needed))
+        old_g, old_l, old_d, oc = self.gamma, self.lam, self.dims, self.cap
+        self._alloc(new)
+        self.gamma[:, :, :oc, :, :oc] = old_g
+        self.lam[:, :, :oc] = old_l
+        self.dims.copy_(old_d)
+
+    def _workspace(self, nitems: int) -> tuple[int, int]:
+        need = int(self.lib.bmps_apply_2q_workspace_bytes(self.cap, nitems))
+        if self._ws is None or self._ws_bytes < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            self._ws_bytes = need
+        return self._ws.data_ptr(), self._ws_bytes
+
+    # -- execution ---------------------------------------------------------------
+    def run(self, programs, states=None, mode: int = 0) -> "MpsBatch":
+        """Apply ``programs[i]`` to state ``states[i]`` (default: i)."""
+        plan = compile_batch(programs, self.n, states)
+        self.execute(plan, mode=mode)
+        return self
+
+    def execute(self, plan: Plan, mode: int = 0) -> None:
+        if plan.n_layers == 0:
+            return
+        dev = self.device
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        it1 = pin(plan.items1).to(dev, non_blocking=True)
+        g1 = pin(plan.gates1.view(np.float64)).to(dev, non_blocking=True)
+        it2 = pin(plan.items2).to(dev, non_blocking=True)
+        g2 = pin(plan.gates2.view(np.float64)).to(dev, non_blocking=True)
+        li2 = pin(plan.logidx2).to(dev, non_blocking=True)
+        rng = pin(plan.ranges).to(dev, non_blocking=True)
+        log = torch.empty(max(plan.n_records, 1) * _RECORD, dtype=torch.uint8, device=dev)
+        pol = self.policy.as_c()
+        lim = self._cap_limit()
+        stream = _stream()
+        for L in range(plan.n_layers):
+            a, b = int(plan.off1[L]), int(plan.off1[L + 1])
+            if b > a:
+                rc = self.lib.bmps_apply_1q(
+                    _ptr(self.gamma), _ptr(self.dims), self.S, self.n, self.cap,
+                    it1.data_ptr() + 8 * a, g1.data_ptr() + 64 * a, b - a, stream)
+                _native.check(rc, "bmps_apply_1q")
+            a, b = int(plan.off2[L]), int(plan.off2[L + 1])
+            if b <= a:
+                continue
+            its = plan.items2[a:b]
+            s_idx, q = its[:, 0], its[:, 1]
+            ub = self.dim_ub
+            bound = int(max(ub[s_idx, q].max(), ub[s_idx, q + 2].max()))
+            new = np.minimum(np.minimum(2 * ub[s_idx, q], 2 * ub[s_idx, q + 2]), lim)
+            self.ensure_capacity(int(max(bound, new.max())))
+            for c0 in range(a, b, self.max_items):
+                c1 = min(b, c0 + self.max_items)
+                ws, wsb = self._workspace(c1 - c0)
+                rc = self.lib.bmps_apply_2q(
+                    _ptr(self.gamma), _ptr(self.lam), _ptr(self.dims), self.S, self.n, self.cap,
+                    it2.data_ptr() + 8 * c0, g2.data_ptr() + 256 * c0, c1 - c0, pol,
+                    log.data_ptr(), li2.data_ptr() + 4 * c0, ws, wsb, min(bound, self.cap), mode, stream)
+                _native.check(rc, "bmps_apply_2q")
+            ub[s_idx, q + 1] = new
+        rc = self.lib.bmps_stats_replay(
+            log.data_ptr(), rng.data_ptr(), len(plan.ranges), _ptr(self.trunc_err), _ptr(self.entries),
+            _ptr(self.peak), _ptr(self.mbs), _ptr(self.status), _ptr(self.status_bond), stream)
+        _native.check(rc, "bmps_stats_replay")
+        self._keep_alive = (it1, g1, it2, g2, li2, rng, log)
+
+    # -- status and host views ---------------------------------------------------
+    def check_status(self) -> None:
+        """Raise the reference's RuntimeError for the first failed state (syncs)."""
+        st = self.status.cpu().numpy()
+        bad = np.nonzero(st)[0]
+        if len(bad) == 0:
+            return
+        s = int(bad[0])
+        code = int(st[s])
+        q = int(self.status_bond[s].item())
+        if code == _native.BMPS_S_SVD_FAILED:
+            raise RuntimeError(f"SVD failed on bond {q}")
+        if code == _native.BMPS_S_ALL_TRUNCATED:
+            raise RuntimeError(f"all singular values truncated on bond {q}")
+        raise RuntimeError(f"state {s}: {self.lib.bmps_status_string(code).decode()} (bond {q})")
+
+    def host_dims(self) -> np.ndarray:
+        return self.dims.cpu().numpy()
+
+    def site_tensors(self, s: int = 0) -> list[np.ndarray]:
+        d = self.host_dims()[s]
+        g = self.gamma[s].cpu().numpy()
+        return [np.ascontiguousarray(g[k, : d[k], :, : d[k + 1]]) for k in range(self.n)]
+
+    def bond_vectors(self, s: int = 0) -> list[np.ndarray]:
+        d = self.host_dims()[s]
+        lam = self.lam[s].cpu().numpy()
+        return [lam[b, : d[b]].copy() for b in range(1, self.n)]
+
+    def load_state(self, s: int, site_tensors, bond_vectors) -> None:
+        """Overwrite state ``s`` with host Gamma/lambda (Vidal form, reference layout)."""
+        dims = [1] + [len(v) for v in bond_vectors] + [1]
+        self.ensure_capacity(max(dims))
+        cap = self.cap
+        g = np.zeros((self.n, cap, 2, cap), dtype=np.complex128)
+        lam = np.zeros((self.n + 1, cap))
+        for k, t in enumerate(site_tensors):
+            t = np.asarray(t, dtype=np.complex128)
+            assert t.shape == (dims[k], 2, dims[k + 1]), (k, t.shape, dims)
+            g[k, : dims[k], :, : dims[k + 1]] = t
+        lam[0, 0] = 1.0
+        lam[self.n, 0] = 1.0
+        for b, v in enumerate(bond_vectors, start=1):
+            lam[b, : len(v)] = v
+        self.gamma[s].copy_(torch.from_numpy(g))
+        self.lam[s].copy_(torch.from_numpy(lam))
+        self.dims[s].copy_(torch.tensor(dims, dtype=torch.int32))
+        self.dim_ub[s] = dims
+        ent = sum(dims[k] * 2 * dims[k + 1] for k in range(self.n))
+        self.entries[s] = ent
+        self.peak[s] = ent
+        self.mbs[s] = max(dims)
+
+    # -- queries -------------------------------------------------------------------
+    def amplitudes(self, state_idx, bitstrings) -> np.ndarray:
+        """<bits|psi_s> for each (s, bits) (``mps.py:172-179``)."""
+        n = self.n
+        bits = np.empty((len(bitstrings), n), dtype=np.uint8)
+        for i, b in enumerate(bitstrings):
+            if len(b) != n or any(c not in "01" for c in b):
+                raise ValueError(f"need a bitstring of length {n}, got {b!r}")
+            bits[i] = np.frombuffer(b.encode(), dtype=np.uint8) - ord("0")
+        self.check_status()
+        sidx = torch.as_tensor(np.asarray(state_idx, dtype=np.int32)).to(self.device)
+        dbits = torch.from_numpy(bits).to(self.device)
+        out = torch.empty(len(bitstrings), dtype=torch.complex128, device=self.device)
+        rc = self.lib.bmps_amplitudes(_ptr(self.gamma), _ptr(self.lam), _ptr(self.dims), self.S, n,
+                                      self.cap, sidx.data_ptr(), dbits.data_ptr(), len(bitstrings),
+                                      out.data_ptr(), _stream())
+        _native.check(rc, "bmps_amplitudes")
+        return out.cpu().numpy()
+
+    def _transfer(self, sidx: torch.Tensor, site: torch.Tensor, codes: torch.Tensor, direction: int,
+                  env_in: torch.Tensor, in_stride: int, env_out: torch.Tensor, out_stride: int,
+                  count: int) -> None:
+        scratch = self._scratch(count)
+        rc = self.lib.bmps_env_transfer(
+            _ptr(self.gamma), _ptr(self.lam), _ptr(self.dims), self.S, self.n, self.cap,
+            sidx.data_ptr(), site.data_ptr(), codes.data_ptr(), direction, env_in.data_ptr(), in_stride,
+            env_out.data_ptr(), out_stride, scratch.data_ptr(), count, _stream())
+        _native.check(rc, "bmps_env_transfer")
+
+    def _scratch(self, count: int) -> torch.Tensor:
+        need = 2 * count * 2 * self.cap * self.cap
+        buf = getattr(self, "_scr", None)
+        if buf is None or buf.numel() < need:
+            buf = torch.empty(need, dtype=torch.complex128, device=self.device)
+            self._scr = buf
+        return buf
+
+    def _env_chunk(self) -> int:
+        # bound transfer scratch to ~2 GiB
+        return max(1, min(4096, (2 << 30) // (64 * self.cap * self.cap)))
+
+    def _identity_env(self, count: int) -> torch.Tensor:
+        e = torch.zeros((count, self.cap, self.cap), dtype=torch.complex128, device=self.device)
+        e[:, 0, 0] = 1.0
+        return e
+
+    def environments(self, states: np.ndarray, direction: int) -> torch.Tensor:
+        """All identity environments L_k (direction 0) or R_k (1), k = 0..n."""
+        ns, n, cap = len(states), self.n, self.cap
+        env = torch.zeros((ns, n + 1, cap, cap), dtype=torch.complex128, device=self.device)
+        sidx = torch.as_tensor(np.asarray(states, dtype=np.int32)).to(self.device)
+        codes = torch.zeros(ns, dtype=torch.uint8, device=self.device)
+        stride = (n + 1) * cap * cap
+        if direction == 0:
+            env[:, 0, 0, 0] = 1.0
+            steps = range(n)
+        else:
+            env[:, n, 0, 0] = 1.0
+            steps = range(n - 1, -1, -1)
+        for k in steps:
+            site = torch.full((ns,), k, dtype=torch.int32, device=self.device)
+            src, dst = (k, k + 1) if direction == 0 else (k + 1, k)
+            for c0 in range(0, ns, self._env_chunk()):
+                c1 = min(ns, c0 + self._env_chunk())
+                self._transfer(sidx[c0:c1], site[c0:c1], codes[c0:c1], direction,
+                               env[c0:, src], stride, env[c0:, dst], stride, c1 - c0)
+        return env
+
+    def expectations(self, state_idx, paulis, use_env: bool | None = None) -> np.ndarray:
+        """<psi_s|P|psi_s> for each (s, P), real part; RuntimeError on |Im| > 1e-10.
+
+        Reassociates the reference's left-to-right sweep (``mps.py:196-204``):
+        each string is swept from its first to its last non-identity site,
+        starting from the cached identity environment L_lo and closed with R_{hi+1}.
+        """
+        n = self.n
+        state_idx = np.asarray(state_idx, dtype=np.int32)
+        codes = np.zeros((len(paulis), n), dtype=np.uint8)
+        for i, p in enumerate(paulis):
+            if len(p) != n:
+                raise ValueError(f"Pauli string length {len(p)} != qubit count {n}")
+            codes[i] = encode_pauli(p)
+        self.check_status()
+        npairs = len(paulis)
+        if npairs == 0:
+            return np.zeros(0)
+        sup = codes != 0
+        lo = np.where(sup.any(1), sup.argmax(1), 0).astype(np.int32)
+        hi = np.where(sup.any(1), n - 1 - sup[:, ::-1].argmax(1), -1).astype(np.int32)
+        uniq, inv = np.unique(state_idx, return_inverse=True)
+        if use_env is None:
+            use_env = npairs > 2 * len(uniq)
+        dev, cap = self.device, self.cap
+        if use_env:
+            Lenv = self.environments(uniq, 0)
+            Renv = self.environments(uniq, 1)
+        else:
+            lo[:] = 0
+            hi[:] = n - 1
+        out = np.empty(npairs, dtype=np.complex128)
+        chunk = self._env_chunk()
+        for c0 in range(0, npairs, chunk):
+            c1 = min(npairs, c0 + chunk)
+            cnt = c1 - c0
+            s_t = torch.as_tensor(state_idx[c0:c1]).to(dev)
+            lo_c, hi_c = lo[c0:c1], hi[c0:c1]
+            if use_env:
+                u = torch.as_tensor(inv[c0:c1]).to(dev)
+                cur = Lenv[u, torch.as_tensor(np.maximum(lo_c, 0)).to(dev)].contiguous()
+                right = Renv[u, torch.as_tensor(np.where(hi_c >= 0, hi_c + 1, lo_c)).to(dev)].contiguous()
+            else:
+                cur = self._identity_env(cnt)
+                right = self._identity_env(cnt)
+            nxt = torch.empty_like(cur)
+            span = np.where(hi_c >= lo_c, hi_c - lo_c + 1, 0)
+            codes_d = torch.from_numpy(codes[c0:c1]).to(dev)
+            for t in range(int(span.max()) if cnt else 0):
+                act = np.nonzero(span > t)[0]
+                if len(act) == 0:
+                    break
+                a_t = torch.as_tensor(act).to(dev)
+                site = torch.as_tensor((lo_c[act] + t).astype(np.int32)).to(dev)
+                cd = codes_d[a_t, site.long()].contiguous()
+                sub_in = cur[a_t].contiguous()
+                sub_out = torch.empty_like(sub_in)
+                self._transfer(s_t[a_t].contiguous(), site, cd, 0, sub_in, cap * cap, sub_out,
+                               cap * cap, len(act))
+                cur[a_t] = sub_out
+            bond = torch.as_tensor(np.where(span > 0, hi_c + 1, lo_c).astype(np.int32)).to(dev)
+            res = torch.empty(cnt, dtype=torch.complex128, device=dev)
+            rc = self.lib.bmps_env_close(_ptr(self.dims), n, cap, s_t.data_ptr(), bond.data_ptr(),
+                                         cur.data_ptr(), cap * cap, right.data_ptr(), cap * cap, cnt,
+                                         res.data_ptr(), _stream())
+            _native.check(rc, "bmps_env_close")
+            out[c0:c1] = res.cpu().numpy()
+            del nxt
+        bad = np.abs(out.imag) > 1e-10
+        if bad.any():
+            raise RuntimeError(f"expectation has imaginary residue {out.imag[bad][0]:.3e}")
+        return out.real.copy()
+
+    # -- stats --------------------------------------------------------------------
+    def stats(self) -> dict:
+        self.check_status()
+        return {
+            "trunc_error_sq": self.trunc_err.cpu().numpy(),
+            "peak_entries": self.peak.cpu().numpy(),
+            "max_bond_seen": self.mbs.cpu().numpy(),
+            "entries": self.entries.cpu().numpy(),
+        }
