@@ -61,6 +61,11 @@ typedef struct bmps_policy {
 int32_t bmps_version(void);
 const char* bmps_status_string(int32_t code);
 
+/* Process-wide tunables of the Jacobi SVD: "tol_factor" (rotate while
+ * |g_ij| > tol_factor * sqrt(rows) * eps * sqrt(g_ii g_jj); default 4),
+ * "max_sweeps" (default 60), "max_inner" (Gram sweeps per block visit, 1). */
+int32_t bmps_set_param(const char* name, double value);
+
 /* MpsState.__init__ (mps.py:55-66): |0...0>, unit boundary bonds, stats reset. */
 int32_t bmps_init_product(double* gamma, double* lam, int32_t* dims, double* trunc_err,
                           int64_t* entries, int64_t* peak, int32_t* max_bond_seen,

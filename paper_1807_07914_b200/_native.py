@@ -34,6 +34,7 @@ _L = ctypes.c_int64
 _SIGNATURES = {
     "bmps_version": ([], _I),
     "bmps_status_string": ([_I], ctypes.c_char_p),
+    "bmps_set_param": ([ctypes.c_char_p, ctypes.c_double], _I),
     "bmps_init_product": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P], _I),
     "bmps_apply_1q": ([_P, _P, _I, _I, _I, _P, _P, _I, _P], _I),
     "bmps_apply_2q_workspace_bytes": ([_I, _I], _SZ),

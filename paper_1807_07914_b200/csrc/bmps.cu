@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <string>
 
 #include "bmps.h"
 #include "bmps_update.cuh"
@@ -17,6 +18,12 @@ using namespace bmps;
 namespace {
 
 constexpr int kNumSMs = 148;
+
+// Tunables (bmps_set_param): Jacobi tolerance factor (tol = f * sqrt(rows) * eps),
+// sweep cap, inner Gram sweeps per block visit.
+double g_tol_factor = 4.0;
+int g_max_sweeps = 60;
+int g_max_inner = 1;
 
 // ---------------------------------------------------------------------------
 // init: product state |0...0> (mps.py:55-66)
@@ -370,6 +377,16 @@ extern "C" {
 
 int32_t bmps_version(void) { return 1; }
 
+int32_t bmps_set_param(const char* name, double value) {
+  if (!name) return BMPS_E_ARG;
+  const std::string k(name);
+  if (k == "tol_factor" && value > 0) g_tol_factor = value;
+  else if (k == "max_sweeps" && value >= 1) g_max_sweeps = (int)value;
+  else if (k == "max_inner" && value >= 1) g_max_inner = (int)value;
+  else return BMPS_E_ARG;
+  return BMPS_OK;
+}
+
 const char* bmps_status_string(int32_t code) {
   switch (code) {
     case BMPS_OK: return "ok";
@@ -426,7 +443,8 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   StateView sv = make_view(gamma, lam, dims, n, cap);
   if (dim_bound <= 0 || dim_bound > cap) dim_bound = cap;
 
-  // K2 theta
+  // K2 theta (meta zeroed first: theta accumulates ||M||_F^2 atomically)
+  cudaMemsetAsync(ws.meta, 0, sizeof(ItemMeta) * (size_t)nitems, st);
   const int tpd = (dim_bound + 31) / 32;
   theta_kernel<<<dim3(tpd * tpd, nitems), 256, kThetaSmem, st>>>(
       sv, items, (const double2*)gates, ws.meta, ws.M0, ws.X, ws.mat_stride, tpd);
@@ -435,15 +453,15 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
 
   // K3 Jacobi SVD
   const int cmax = 2 * dim_bound;
-  const int max_sweeps = 60;
-  const double tol_factor = 4.0;
+  const int max_sweeps = g_max_sweeps;
+  const double tol_factor = g_tol_factor;
   JacArgs ja;
   ja.meta = ws.meta;
   ja.X = ws.X;
   ja.mat_stride = ws.mat_stride;
   ja.round = 0;
   ja.max_sweeps = max_sweeps;
-  ja.max_inner = 1;
+  ja.max_inner = g_max_inner;
   ja.tol_factor = tol_factor;
   const int explicit_mode = mode & 3;
   if (cmax <= 64) {

@@ -63,10 +63,32 @@ BMPS_DEV void tourney_pair(int N, int rho, int p, int& i, int& j) {
 // Complex Jacobi rotation zeroing the (i,j) entry of the 2x2 Hermitian Gram
 // [[a, g], [conj(g), b]]. Column transform [x_i, x_j] <- [x_i, x_j] J with
 // J = [[c, s], [-s*conj(e), c*conj(e)]], e = g/|g| (Rutishauser's tangent).
-BMPS_DEV bool jacobi_rotation(double a, double b, double2 g, double tol, double& c, double& s,
-                              double2& e) {
+// A pair whose smaller squared norm is below kNegligible times the larger one
+// (relative column norm < 1e-125) carries nothing that can reach a float64
+// result; it is never rotated (this also keeps underflowed columns from
+// looking non-orthogonal forever).
+constexpr double kNegligible = 1e-250;
+// Rounding-noise floor of a column relative to ||M||_F. With cutoff 0 the
+// reference keeps numerically-zero singular values (rank-deficient theta);
+// pairs of two such columns carry no information and relative orthogonality
+// between them cannot converge, so they are not rotated, and singular vectors
+// of sigma_k <= kNoiseRel * ||M||_F are written as zero in the split (their
+// lambda entry is kept, so bond dims and spectra still match the reference;
+// the state changes by <= kNoiseRel * ||M||_F).
+constexpr double kNoiseRel = 1e-14;
+
+// noise2 = (kNoiseRel * ||M||_F)^2 for the item.
+BMPS_DEV bool pair_needs_rotation(double a, double b, double2 g, double tol, double noise2) {
+  const double lo = fmin(a, b), hi = fmax(a, b);
+  if (!(hi > noise2)) return false;
+  if (!(lo > kNegligible * hi)) return false;
+  return hypot(g.x, g.y) > tol * sqrt(a) * sqrt(b);
+}
+
+BMPS_DEV bool jacobi_rotation(double a, double b, double2 g, double tol, double noise2, double& c,
+                              double& s, double2& e) {
+  if (!pair_needs_rotation(a, b, g, tol, noise2)) return false;
   const double ag = hypot(g.x, g.y);
-  if (!(ag > tol * sqrt(a * b))) return false;
   const double zeta = (b - a) / (2.0 * ag);
   double t;
   if (fabs(zeta) > 1e150) {
@@ -99,6 +121,8 @@ struct ItemMeta {
   int r, c, orient, dl, dm, dr;   // X rows/cols, orientation, bond dims before update
   int keep, status, sweeps, conv, flag, pad;
   double err, norm;
+  double fro2;   // ||M||_F^2 (accumulated by theta)
+  double pad2;
 };
 
 }  // namespace bmps

@@ -80,13 +80,6 @@ __global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* ite
     m->dl = dl;
     m->dm = dm;
     m->dr = dr;
-    m->keep = 0;
-    m->status = 0;
-    m->sweeps = 0;
-    m->conv = 0;
-    m->flag = 0;
-    m->err = 0.0;
-    m->norm = 0.0;
   }
   const int tm = blockIdx.x / tiles_per_dim, tn = blockIdx.x % tiles_per_dim;
   const int m0 = tm * kTile, n0 = tn * kTile;
@@ -122,6 +115,7 @@ __global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* ite
   __syncthreads();
   double2* m0p = M0 + (size_t)item * mat_stride;
   double2* xp = X + (size_t)item * mat_stride;
+  double fro = 0.0;
   for (int idx = tid; idx < 32 * 32; idx += 256) {
     // orient 0 writes (2l+a) contiguous -> l fastest; orient 1 writes (b*dr+r) -> r fastest
     const int lloc = orient == 0 ? (idx & 31) : (idx >> 5);
@@ -146,7 +140,18 @@ __global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* ite
       }
       m0p[off] = v;
       xp[off] = v;
+      fro += cabs2(v);
     }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
+  __shared__ double sfro[8];
+  if (lane == 0) sfro[warp] = fro;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w8 = 0; w8 < 8; ++w8) t += sfro[w8];
+    atomicAdd(&meta[item].fro2, t);
   }
 }
 
@@ -278,7 +283,8 @@ struct RotShared {
 
 // Cyclic two-sided Jacobi on the W2 x W2 Hermitian Gram, accumulating Q.
 template <int W2>
-BMPS_DEV void jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, int max_inner) {
+BMPS_DEV void jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, double noise2,
+                        int max_inner) {
   using C = JacCfg<W2>;
   constexpr int w = W2 / 2;
   const int tid = threadIdx.x;
@@ -296,7 +302,7 @@ BMPS_DEV void jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, int
         double c, s;
         double2 e;
         act = jacobi_rotation(sG[i + i * C::LDG].x, sG[j + j * C::LDG].x, sG[i + j * C::LDG], tol,
-                              c, s, e);
+                              noise2, c, s, e);
         rs.i[tid] = i;
         rs.j[tid] = j;
         rs.act[tid] = act;
@@ -340,8 +346,9 @@ BMPS_DEV void jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, int
 // orthogonal (a rotation was applied). If `resident`, the whole panel already
 // sits in sP (r <= RC) and is neither loaded nor stored here.
 template <int W2>
-BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, int max_inner,
-                        bool resident, double2* sG, double2* sQ, double2* sP, RotShared& rs) {
+BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, double noise2,
+                        int max_inner, bool resident, double2* sG, double2* sQ, double2* sP,
+                        RotShared& rs) {
   using C = JacCfg<W2>;
   const int tid = threadIdx.x;
   double acc[C::GT][4];
@@ -375,16 +382,16 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, int 
     if (i > j) {
       sG[i + j * C::LDG] = cconj(sG[j + i * C::LDG]);
     } else if (i < j) {
-      const double a = sG[i + i * C::LDG].x, b = sG[j + j * C::LDG].x;
-      const double2 g = sG[i + j * C::LDG];
-      if (hypot(g.x, g.y) > tol * sqrt(a * b)) dirty = 1;
+      if (pair_needs_rotation(sG[i + i * C::LDG].x, sG[j + j * C::LDG].x, sG[i + j * C::LDG], tol,
+                              noise2))
+        dirty = 1;
     }
   }
   dirty = __syncthreads_or(dirty);
   for (int i = tid; i < W2; i += blockDim.x) sG[i + i * C::LDG].y = 0.0;
   __syncthreads();
   if (!dirty) return false;
-  jac_inner<W2>(sG, sQ, rs, tol, max_inner);
+  jac_inner<W2>(sG, sQ, rs, tol, noise2, max_inner);
   for (int row0 = 0; row0 < r; row0 += C::RC) {
     if (!resident) {
       if (C::RC < r) {  // multi-chunk panel: reload (single chunk is still staged)
@@ -417,6 +424,7 @@ __global__ void __launch_bounds__(256) jacobi_kernel(JacArgs args) {
   int nb = (c + w - 1) / w;
   nb += nb & 1;
   const double tol = args.tol_factor * sqrt((double)r) * kEps;
+  const double noise2 = kNoiseRel * kNoiseRel * m->fro2;
   if (nb == 2) {
     // single panel: the whole matrix is one visit, iterated to convergence
     if (blockIdx.x != 0) return;
@@ -428,7 +436,7 @@ __global__ void __launch_bounds__(256) jacobi_kernel(JacArgs args) {
     int sweep = 0;
     bool clean = false;
     for (; sweep < args.max_sweeps; ++sweep) {
-      if (!jac_visit<W2>(X, r, c, 0, 1, tol, 64, resident, sG, sQ, sP, rs)) {
+      if (!jac_visit<W2>(X, r, c, 0, 1, tol, noise2, 64, resident, sG, sQ, sP, rs)) {
         clean = true;
         break;
       }
@@ -451,7 +459,7 @@ __global__ void __launch_bounds__(256) jacobi_kernel(JacArgs args) {
         for (int v = 0; v < nb / 2; ++v) {
           int I, J;
           tourney_pair(nb, rho, v, I, J);
-          any |= jac_visit<W2>(X, r, c, I, J, tol, args.max_inner, false, sG, sQ, sP, rs);
+          any |= jac_visit<W2>(X, r, c, I, J, tol, noise2, args.max_inner, false, sG, sQ, sP, rs);
         }
       if (!any) {
         clean = true;
@@ -469,7 +477,7 @@ __global__ void __launch_bounds__(256) jacobi_kernel(JacArgs args) {
   if (v >= nb / 2 || rho >= nb - 1) return;
   int I, J;
   tourney_pair(nb, rho, v, I, J);
-  if (jac_visit<W2>(X, r, c, I, J, tol, args.max_inner, false, sG, sQ, sP, rs) &&
+  if (jac_visit<W2>(X, r, c, I, J, tol, noise2, args.max_inner, false, sG, sQ, sP, rs) &&
       threadIdx.x == 0)
     atomicOr(&m->flag, 1);
 }
@@ -565,6 +573,7 @@ __global__ void __launch_bounds__(512) finalize_kernel(StateView sv, const int* 
     keep = max(keep, 1);
     if (max_bond > 0) keep = min(keep, max_bond);
     int status = m->status;
+    if (!isfinite(ssig[0])) status = BMPS_S_SVD_FAILED;
     if (keep > sv.cap) {
       keep = sv.cap;
       if (!status) status = BMPS_S_CAPACITY;
@@ -595,6 +604,7 @@ __global__ void __launch_bounds__(512) finalize_kernel(StateView sv, const int* 
   const int keep = s_keep;
   if (keep == 0) return;  // failure: leave the state untouched (host raises)
   const double nrm = s_norm;
+  const double zero_sig = kNoiseRel * sqrt(m->fro2);
   double* sig_out = sig_ws + (size_t)item * sig_stride;
   int* perm_out = perm_ws + (size_t)item * sig_stride;
   double* lam_new = sv.bond(s, q + 1);
@@ -612,7 +622,7 @@ __global__ void __launch_bounds__(512) finalize_kernel(StateView sv, const int* 
     for (int idx = tid; idx < rows * keep; idx += blockDim.x) {
       const int k = idx % keep, i = idx / keep;
       const double sk = ssig[k];
-      const double f = sk > 0.0 ? pinv(ll[i >> 1]) / sk : 0.0;
+      const double f = sk > zero_sig ? pinv(ll[i >> 1]) / sk : 0.0;
       gq[(size_t)i * cap + k] = cscale(x[(size_t)i + (size_t)sidx[k] * r], f);
     }
   } else {
@@ -624,7 +634,7 @@ __global__ void __launch_bounds__(512) finalize_kernel(StateView sv, const int* 
       const int jcol = idx % cols, k = idx / cols;
       const int b = jcol / dr, rr = jcol % dr;
       const double sk = ssig[k];
-      const double f = sk > 0.0 ? pinv(lr[rr]) / sk : 0.0;
+      const double f = sk > zero_sig ? pinv(lr[rr]) / sk : 0.0;
       gb[(size_t)(2 * k + b) * cap + rr] = cscale(cconj(x[(size_t)jcol + (size_t)sidx[k] * r]), f);
     }
   }
@@ -656,9 +666,11 @@ struct SplitOp {
   double2* dst;
   const double* lb;
   int r, orient, dl, dr, cap;
+  double zero_sig;
   BMPS_DEV bool begin(int item, int& M, int& N, int& K) {
     const ItemMeta* m = meta + item;
     if (m->status || m->keep <= 0) return false;
+    zero_sig = kNoiseRel * sqrt(m->fro2);
     const int s = items[2 * item], q = items[2 * item + 1];
     r = m->r;
     orient = m->orient;
@@ -685,7 +697,7 @@ struct SplitOp {
   BMPS_DEV double2 b(int k, int j) const { return x[(size_t)k + (size_t)perm[j] * r]; }
   BMPS_DEV void store(int i, int j, double2 v) const {
     const double sj = sig[j];
-    const double f = sj > 0.0 ? 1.0 / (sj * sj) : 0.0;
+    const double f = sj > zero_sig ? 1.0 / (sj * sj) : 0.0;
     if (orient == 0) {
       const int b = i / dr, rr = i % dr;
       dst[(size_t)(2 * j + b) * cap + rr] = cscale(cconj(v), f * pinv(lb[rr]));

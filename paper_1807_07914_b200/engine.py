@@ -33,6 +33,9 @@ from .policy import TruncationPolicy
 
 MAX_CAP = 1024
 _RECORD = _native.RECORD_BYTES
+RECORD_DTYPE = np.dtype([("err", "<f8"), ("dl", "<i4"), ("dm", "<i4"), ("dr", "<i4"),
+                         ("keep", "<i4"), ("status", "<i4"), ("site", "<i4")])
+assert RECORD_DTYPE.itemsize == _RECORD
 _ZERO2 = np.zeros((2, 2), dtype=np.complex128)
 
 
@@ -205,6 +208,7 @@ class MpsBatch:
         self.dim_ub = np.ones((self.S, self.n + 1), dtype=np.int64)
         self._ws = None
         self._ws_bytes = 0
+        self._logs: list = []
         self.reset()
 
     # -- buffers ---------------------------------------------------------------
@@ -227,6 +231,7 @@ class MpsBatch:
         self.gamma.zero_()
         self.lam.zero_()
         self.dim_ub[:] = 1
+        self._logs = []
         rc = self.lib.bmps_init_product(
             _ptr(self.gamma), _ptr(self.lam), _ptr(self.dims), _ptr(self.trunc_err),
             _ptr(self.entries), _ptr(self.peak), _ptr(self.mbs), _ptr(self.status),
@@ -314,7 +319,25 @@ class MpsBatch:
             log.data_ptr(), rng.data_ptr(), len(plan.ranges), _ptr(self.trunc_err), _ptr(self.entries),
             _ptr(self.peak), _ptr(self.mbs), _ptr(self.status), _ptr(self.status_bond), stream)
         _native.check(rc, "bmps_stats_replay")
-        self._keep_alive = (it1, g1, it2, g2, li2, rng, log)
+        self._keep_alive = (it1, g1, it2, g2, li2, rng)
+        self._logs.append((log, plan.ranges))
+
+    def update_records(self, s: int) -> np.ndarray:
+        """Per-update records of state ``s`` in program order (all executed plans)."""
+        out = []
+        for log, ranges in self._logs:
+            rec = log.cpu().numpy().view(RECORD_DTYPE)
+            for st, first, cnt in ranges:
+                if st == s:
+                    out.append(rec[first:first + cnt])
+        return np.concatenate(out) if out else np.zeros(0, RECORD_DTYPE)
+
+    def bond_truncation(self, s: int = 0) -> np.ndarray:
+        """Discarded weight per bond (reference bond index q = site of the update)."""
+        rec = self.update_records(s)
+        out = np.zeros(max(self.n - 1, 0))
+        np.add.at(out, rec["site"], rec["err"])
+        return out
 
     # -- status and host views ---------------------------------------------------
     def check_status(self) -> None:
