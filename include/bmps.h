@@ -66,6 +66,9 @@ const char* bmps_status_string(int32_t code);
  * "max_sweeps" (default 60), "max_inner" (Gram sweeps per block visit, 1). */
 int32_t bmps_set_param(const char* name, double value);
 
+/* Number of kernels this library has launched so far (process-wide). */
+uint64_t bmps_launch_count(void);
+
 /* MpsState.__init__ (mps.py:55-66): |0...0>, unit boundary bonds, stats reset. */
 int32_t bmps_init_product(double* gamma, double* lam, int32_t* dims, double* trunc_err,
                           int64_t* entries, int64_t* peak, int32_t* max_bond_seen,

@@ -21,6 +21,7 @@ constexpr int kNumSMs = 148;
 
 // Tunables (bmps_set_param): Jacobi tolerance factor (tol = f * sqrt(rows) * eps),
 // sweep cap, inner Gram sweeps per block visit.
+unsigned long long g_launches = 0;  // kernels launched through this library
 double g_tol_factor = 4.0;
 int g_max_sweeps = 60;
 int g_max_inner = 1;
@@ -377,6 +378,8 @@ extern "C" {
 
 int32_t bmps_version(void) { return 1; }
 
+uint64_t bmps_launch_count(void) { return g_launches; }
+
 int32_t bmps_set_param(const char* name, double value) {
   if (!name) return BMPS_E_ARG;
   const std::string k(name);
@@ -409,6 +412,7 @@ int32_t bmps_init_product(double* gamma, double* lam, int32_t* dims, double* tru
   const int total = std::max(S * (n + 1), S);
   init_kernel<<<(total + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
       sv, S, trunc_err, (long long*)entries, (long long*)peak, max_bond_seen, status, status_bond);
+  ++g_launches;
   return launch_status();
 }
 
@@ -420,6 +424,7 @@ int32_t bmps_apply_1q(double* gamma, const int32_t* dims, int32_t S, int32_t n, 
   const int per_item = std::min(std::max((cap * cap + 255) / 256, 1), 64);
   dim3 grid(per_item, nitems);
   apply1q_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(sv, items, (const double2*)gates);
+  ++g_launches;
   return launch_status();
 }
 
@@ -448,6 +453,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   const int tpd = (dim_bound + 31) / 32;
   theta_kernel<<<dim3(tpd * tpd, nitems), 256, kThetaSmem, st>>>(
       sv, items, (const double2*)gates, ws.meta, ws.M0, ws.X, ws.mat_stride, tpd);
+  ++g_launches;
   int32_t rc = launch_status();
   if (rc) return rc;
 
@@ -470,6 +476,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       jacobi_kernel<32><<<dim3(1, nitems), 256, JacCfg<32>::kSmem, st>>>(ja);
     else
       jacobi_kernel<64><<<dim3(1, nitems), 256, JacCfg<64>::kSmem, st>>>(ja);
+    ++g_launches;
     if ((rc = launch_status())) return rc;
   } else {
     const int nbmax = (cmax + 15) / 16 + ((cmax + 15) / 16 & 1);
@@ -478,6 +485,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
     if (persistent) {
       ja.persistent = 1;
       jacobi_kernel<32><<<dim3(1, nitems), 256, JacCfg<32>::kSmem, st>>>(ja);
+      ++g_launches;
       if ((rc = launch_status())) return rc;
     } else {
       ja.persistent = 0;
@@ -488,9 +496,11 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
         for (int rho = 0; rho < nbmax - 1; ++rho) {
           ja.round = rho;
           jacobi_kernel<32><<<dim3(nbmax / 2, nitems), 256, JacCfg<32>::kSmem, st>>>(ja);
+          ++g_launches;
         }
         sweep_end_kernel<<<(nitems + 127) / 128, 128, 0, st>>>(ws.meta, nitems, max_sweeps,
                                                                ws.counter);
+        ++g_launches;
         if ((rc = launch_status())) return rc;
         if (sweep >= 3) {
           cudaMemcpyAsync(h_cnt, ws.counter, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -505,6 +515,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   finalize_kernel<<<nitems, 512, 0, st>>>(sv, items, ws.meta, ws.X, ws.mat_stride, ws.sig,
                                           ws.perm, ws.sig_stride, policy.cutoff, policy.max_bond,
                                           policy.relative, log, log_index);
+  ++g_launches;
   if ((rc = launch_status())) return rc;
   SplitOp sop;
   sop.sv = sv;
@@ -519,6 +530,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   const int kb = policy.max_bond > 0 ? std::min(policy.max_bond, cap) : cap;
   dim3 sgrid((cmax + 63) / 64, (std::min(kb, cmax) + 63) / 64, nitems);
   gemm_kernel<SplitOp><<<sgrid, 256, 0, st>>>(sop);
+  ++g_launches;
   if ((rc = launch_status())) return rc;
   return launch_status();
 }
@@ -532,6 +544,7 @@ int32_t bmps_stats_replay(const bmps_update_record* log, const int32_t* ranges, 
   stats_replay_kernel<<<(nranges + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
       log, ranges, nranges, trunc_err, (long long*)entries, (long long*)peak, max_bond_seen,
       status, status_bond);
+  ++g_launches;
   return launch_status();
 }
 
@@ -541,6 +554,7 @@ int32_t bmps_apply_2q_sweeps(const void* workspace, int32_t nitems, int32_t* swe
   const ItemMeta* meta = (const ItemMeta*)workspace;  // meta sits at offset 0
   item_info_kernel<<<(nitems + 127) / 128, 128, 0, (cudaStream_t)stream>>>(meta, nitems, sweeps,
                                                                            nullptr);
+  ++g_launches;
   return launch_status();
 }
 
@@ -552,6 +566,7 @@ int32_t bmps_amplitudes(const double* gamma, const double* lam, const int32_t* d
   StateView sv = make_view((double*)gamma, (double*)lam, (int32_t*)dims, n, cap);
   amplitude_kernel<<<count, 256, 2 * cap * sizeof(double2), (cudaStream_t)stream>>>(
       sv, state_idx, bits, (double2*)out);
+  ++g_launches;
   return launch_status();
 }
 
@@ -570,6 +585,7 @@ int32_t bmps_env_transfer(const double* gamma, const double* lam, const int32_t*
   double2* f = ot + ot_stride * count;
   const int per_item = std::min(std::max((cap * cap + 255) / 256, 1), 64);
   env_prep_kernel<<<dim3(per_item, count), 256, 0, st>>>(sv, state_idx, site, pauli, ot, ot_stride);
+  ++g_launches;
   int32_t rc = launch_status();
   if (rc) return rc;
   const int t1 = (cap + 63) / 64, t2 = (2 * cap + 63) / 64;
@@ -579,22 +595,26 @@ int32_t bmps_env_transfer(const double* gamma, const double* lam, const int32_t*
     g1.env = (const double2*)env_in; g1.ot = ot; g1.f = f;
     g1.env_stride = (size_t)in_stride; g1.ot_stride = ot_stride;
     gemm_kernel<EnvL1><<<dim3(t1, t2, count), 256, 0, st>>>(g1);
+    ++g_launches;
     if ((rc = launch_status())) return rc;
     EnvL2 g2;
     g2.sv = sv; g2.state_idx = state_idx; g2.site = site;
     g2.f = f; g2.out = (double2*)env_out; g2.ot_stride = ot_stride; g2.env_stride = (size_t)out_stride;
     gemm_kernel<EnvL2><<<dim3(t1, t1, count), 256, 0, st>>>(g2);
+    ++g_launches;
   } else {
     EnvR1 g1;
     g1.sv = sv; g1.state_idx = state_idx; g1.site = site;
     g1.env = (const double2*)env_in; g1.ot = ot; g1.f = f;
     g1.env_stride = (size_t)in_stride; g1.ot_stride = ot_stride;
     gemm_kernel<EnvR1><<<dim3(t2, t1, count), 256, 0, st>>>(g1);
+    ++g_launches;
     if ((rc = launch_status())) return rc;
     EnvR2 g2;
     g2.sv = sv; g2.state_idx = state_idx; g2.site = site;
     g2.f = f; g2.out = (double2*)env_out; g2.ot_stride = ot_stride; g2.env_stride = (size_t)out_stride;
     gemm_kernel<EnvR2><<<dim3(t1, t1, count), 256, 0, st>>>(g2);
+    ++g_launches;
   }
   return launch_status();
 }
@@ -608,6 +628,7 @@ int32_t bmps_env_close(const int32_t* dims, int32_t n, int32_t cap, const int32_
   env_close_kernel<<<count, 256, 0, (cudaStream_t)stream>>>(
       dims, n, cap, state_idx, bond, (const double2*)env_l, (size_t)l_stride,
       (const double2*)env_r, (size_t)r_stride, (double2*)out);
+  ++g_launches;
   return launch_status();
 }
 

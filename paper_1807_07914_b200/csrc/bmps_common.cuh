@@ -77,17 +77,25 @@ constexpr double kNegligible = 1e-250;
 // the state changes by <= kNoiseRel * ||M||_F).
 constexpr double kNoiseRel = 1e-14;
 
-// noise2 = (kNoiseRel * ||M||_F)^2 for the item.
-BMPS_DEV bool pair_needs_rotation(double a, double b, double2 g, double tol, double noise2) {
+// Rotation test for the pair (x_i, x_j) with squared norms a, b and g = x_i^H x_j:
+//   |g| > tol * min(|x_i|, |x_j|) * ||M||_F
+// i.e. relative orthogonality tol for columns near the top of the spectrum and
+// absolute accuracy tol * ||M||_F for small ones (their contribution to any
+// gauge-invariant output is |g| / min(|x_i|, |x_j|)). A purely relative test
+// cannot converge for wide spectra: rounding of the dominant columns keeps
+// re-injecting eps * ||M|| into small columns. fro = ||M||_F; noise2 =
+// (kNoiseRel * fro)^2.
+BMPS_DEV bool pair_needs_rotation(double a, double b, double2 g, double tol, double noise2,
+                                  double fro) {
   const double lo = fmin(a, b), hi = fmax(a, b);
   if (!(hi > noise2)) return false;
   if (!(lo > kNegligible * hi)) return false;
-  return hypot(g.x, g.y) > tol * sqrt(a) * sqrt(b);
+  return hypot(g.x, g.y) > tol * sqrt(lo) * fro;
 }
 
-BMPS_DEV bool jacobi_rotation(double a, double b, double2 g, double tol, double noise2, double& c,
-                              double& s, double2& e) {
-  if (!pair_needs_rotation(a, b, g, tol, noise2)) return false;
+BMPS_DEV bool jacobi_rotation(double a, double b, double2 g, double tol, double noise2, double fro,
+                              double& c, double& s, double2& e) {
+  if (!pair_needs_rotation(a, b, g, tol, noise2, fro)) return false;
   const double ag = hypot(g.x, g.y);
   const double zeta = (b - a) / (2.0 * ag);
   double t;

@@ -284,7 +284,7 @@ struct RotShared {
 // Cyclic two-sided Jacobi on the W2 x W2 Hermitian Gram, accumulating Q.
 template <int W2>
 BMPS_DEV void jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, double noise2,
-                        int max_inner) {
+                        double fro, int max_inner) {
   using C = JacCfg<W2>;
   constexpr int w = W2 / 2;
   const int tid = threadIdx.x;
@@ -302,7 +302,7 @@ BMPS_DEV void jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, dou
         double c, s;
         double2 e;
         act = jacobi_rotation(sG[i + i * C::LDG].x, sG[j + j * C::LDG].x, sG[i + j * C::LDG], tol,
-                              noise2, c, s, e);
+                              noise2, fro, c, s, e);
         rs.i[tid] = i;
         rs.j[tid] = j;
         rs.act[tid] = act;
@@ -347,8 +347,8 @@ BMPS_DEV void jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, dou
 // sits in sP (r <= RC) and is neither loaded nor stored here.
 template <int W2>
 BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, double noise2,
-                        int max_inner, bool resident, double2* sG, double2* sQ, double2* sP,
-                        RotShared& rs) {
+                        double fro, int max_inner, bool resident, double2* sG, double2* sQ,
+                        double2* sP, RotShared& rs) {
   using C = JacCfg<W2>;
   const int tid = threadIdx.x;
   double acc[C::GT][4];
@@ -383,7 +383,7 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
       sG[i + j * C::LDG] = cconj(sG[j + i * C::LDG]);
     } else if (i < j) {
       if (pair_needs_rotation(sG[i + i * C::LDG].x, sG[j + j * C::LDG].x, sG[i + j * C::LDG], tol,
-                              noise2))
+                              noise2, fro))
         dirty = 1;
     }
   }
@@ -391,7 +391,7 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
   for (int i = tid; i < W2; i += blockDim.x) sG[i + i * C::LDG].y = 0.0;
   __syncthreads();
   if (!dirty) return false;
-  jac_inner<W2>(sG, sQ, rs, tol, noise2, max_inner);
+  jac_inner<W2>(sG, sQ, rs, tol, noise2, fro, max_inner);
   for (int row0 = 0; row0 < r; row0 += C::RC) {
     if (!resident) {
       if (C::RC < r) {  // multi-chunk panel: reload (single chunk is still staged)
@@ -425,6 +425,7 @@ __global__ void __launch_bounds__(256) jacobi_kernel(JacArgs args) {
   nb += nb & 1;
   const double tol = args.tol_factor * sqrt((double)r) * kEps;
   const double noise2 = kNoiseRel * kNoiseRel * m->fro2;
+  const double fro = sqrt(m->fro2);
   if (nb == 2) {
     // single panel: the whole matrix is one visit, iterated to convergence
     if (blockIdx.x != 0) return;
@@ -436,7 +437,7 @@ __global__ void __launch_bounds__(256) jacobi_kernel(JacArgs args) {
     int sweep = 0;
     bool clean = false;
     for (; sweep < args.max_sweeps; ++sweep) {
-      if (!jac_visit<W2>(X, r, c, 0, 1, tol, noise2, 64, resident, sG, sQ, sP, rs)) {
+      if (!jac_visit<W2>(X, r, c, 0, 1, tol, noise2, fro, 64, resident, sG, sQ, sP, rs)) {
         clean = true;
         break;
       }
@@ -459,7 +460,7 @@ __global__ void __launch_bounds__(256) jacobi_kernel(JacArgs args) {
         for (int v = 0; v < nb / 2; ++v) {
           int I, J;
           tourney_pair(nb, rho, v, I, J);
-          any |= jac_visit<W2>(X, r, c, I, J, tol, noise2, args.max_inner, false, sG, sQ, sP, rs);
+          any |= jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, args.max_inner, false, sG, sQ, sP, rs);
         }
       if (!any) {
         clean = true;
@@ -477,7 +478,7 @@ __global__ void __launch_bounds__(256) jacobi_kernel(JacArgs args) {
   if (v >= nb / 2 || rho >= nb - 1) return;
   int I, J;
   tourney_pair(nb, rho, v, I, J);
-  if (jac_visit<W2>(X, r, c, I, J, tol, noise2, args.max_inner, false, sG, sQ, sP, rs) &&
+  if (jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, args.max_inner, false, sG, sQ, sP, rs) &&
       threadIdx.x == 0)
     atomicOr(&m->flag, 1);
 }
