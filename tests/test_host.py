@@ -1,0 +1,145 @@
+"""Host-side logic on CPU: IR/gates/policy mirror the reference, lowering and
+layer scheduling, the C ABI library loads and exports every header symbol, and
+the product path refuses to run without a GPU (no CPU fallback)."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_1807_07914_b200 import (
+    GateKind, Instruction, IrError, MatrixGate, SWAP_MATRIX, TruncationPolicy, check_unitary,
+    compile_batch, gate_matrix, num_qubits,
+)
+from paper_1807_07914_b200 import _native
+from paper_1807_07914_b200.engine import asap_layers, lower_program
+from paper_1807_07914_b200.workloads import brick_circuit, config4, haar_unitary, random_program
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def test_gate_conventions_match_oracle():
+    from oracle.mps_oracle import oracle_gate_matrix
+    rng = np.random.default_rng(3)
+    for op in random_program(5, 200, rng):
+        np.testing.assert_array_equal(gate_matrix(op), oracle_gate_matrix(op))
+    cnot = gate_matrix(Instruction(GateKind.CNOT, (0, 1)))
+    assert cnot[3, 2] == 1 and cnot[2, 3] == 1 and cnot[0, 0] == 1
+
+
+def test_check_unitary():
+    check_unitary(SWAP_MATRIX)
+    with pytest.raises(ValueError, match="unitary"):
+        check_unitary(np.diag([1.0, 2.0]))
+    with pytest.raises(ValueError):
+        check_unitary(np.eye(3))
+
+
+def test_ir_validation():
+    with pytest.raises(IrError):
+        Instruction(GateKind.CNOT, (0,))
+    with pytest.raises(IrError):
+        Instruction(GateKind.CNOT, (1, 1))
+    with pytest.raises(IrError):
+        Instruction(GateKind.RX, (0,))
+    with pytest.raises(IrError):
+        MatrixGate(np.eye(2), (0, 1))
+    assert num_qubits([Instruction(GateKind.X, (4,))]) == 5
+
+
+def test_policy_validation_and_keep():
+    with pytest.raises(ValueError):
+        TruncationPolicy(cutoff=-1)
+    with pytest.raises(ValueError):
+        TruncationPolicy(max_bond=0)
+    s = np.array([1.0, 0.5, 0.3, 1e-9])
+    assert TruncationPolicy(1e-4, 2).keep_count(s) == 2
+    assert TruncationPolicy(1e-4).keep_count(s) == 3
+    c = TruncationPolicy(1e-10, 256, False).as_c()
+    assert (c.cutoff, c.max_bond, c.relative) == (1e-10, 256, 0)
+
+
+def test_lowering_routes_like_reference():
+    # CNOT(4, 1): higher index moved down by SWAPs at 3, 2; gate SWAP.G.SWAP at 1; SWAPs back
+    prog = [Instruction(GateKind.CNOT, (4, 1))]
+    ar, site, mats = lower_program(prog, 6)
+    assert ar.tolist() == [2, 2, 2, 2, 2]
+    assert site.tolist() == [3, 2, 1, 2, 3]
+    g = gate_matrix(prog[0])
+    np.testing.assert_array_equal(mats[2], SWAP_MATRIX @ g @ SWAP_MATRIX)
+    with pytest.raises(ValueError):
+        lower_program([Instruction(GateKind.X, (6,))], 6)
+
+
+def test_asap_layers_are_site_disjoint_and_ordered():
+    rng = np.random.default_rng(9)
+    prog = random_program(9, 300, rng)
+    ar, site, _ = lower_program(prog, 9)
+    lay = asap_layers(ar, site, 9)
+    for L in range(lay.max() + 1):
+        used = []
+        for i in np.nonzero(lay == L)[0]:
+            used += [site[i]] if ar[i] == 1 else [site[i], site[i] + 1]
+        assert len(used) == len(set(used))
+    last = {}
+    for i in range(len(ar)):
+        for q in ([site[i]] if ar[i] == 1 else [site[i], site[i] + 1]):
+            assert lay[i] > last.get(q, -1)
+            last[q] = lay[i]
+
+
+def test_compile_batch_records_in_program_order():
+    w = config4(circuits=3)
+    plan = compile_batch(w.programs, w.n)
+    assert plan.n_records == sum(sum(1 for op in p if len(op.qubits) == 2) for p in w.programs)
+    assert plan.ranges.tolist() == [[0, 0, 372], [1, 372, 372], [2, 744, 372]]
+    assert sorted(plan.logidx2.tolist()) == list(range(plan.n_records))
+    # within a state, layer order never reverses program order of records on a site
+    for s in range(3):
+        sel = plan.items2[:, 0] == s
+        assert np.all(np.diff(plan.logidx2[sel][np.argsort(plan.logidx2[sel])]) == 1)
+
+
+def test_workload_generators_deterministic():
+    a = brick_circuit(6, 3, np.random.default_rng(1))
+    b = brick_circuit(6, 3, np.random.default_rng(1))
+    assert [(o.kind, o.qubits, o.params) for o in a] == [(o.kind, o.qubits, o.params) for o in b]
+    u = haar_unitary(np.random.default_rng(2))
+    check_unitary(u)
+
+
+def _header_functions():
+    text = (ROOT / "include" / "bmps.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:int32_t|size_t|uint64_t|const char\*)\s+(bmps_\w+)\(", text, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_1807_07914_b200 import build
+    build.build()
+    lib = _native.load()
+    declared = _header_functions()
+    assert len(declared) >= 10
+    for name in declared:
+        assert hasattr(lib, name), name
+        assert name in _native.EXPORTED, f"{name} missing from the ctypes signature table"
+    assert lib.bmps_version() == 1
+    assert lib.bmps_status_string(1).decode().startswith("SVD failed")
+    assert lib.bmps_apply_2q_workspace_bytes(256, 4) > 4 * 2 * 4 * 256 * 256 * 16
+    assert lib.bmps_set_param(b"nonsense", 1.0) == -1
+
+
+def test_no_cpu_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1807_07914_b200 import MpsState
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        MpsState(3)
+
+
+def test_product_path_never_imports_oracle():
+    pkg = ROOT / "paper_1807_07914_b200"
+    for f in pkg.rglob("*.py"):
+        text = f.read_text()
+        assert "from oracle" not in text and "import oracle" not in text, f
