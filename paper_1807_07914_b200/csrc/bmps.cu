@@ -25,6 +25,7 @@ unsigned long long g_launches = 0;  // kernels launched through this library
 double g_tol_factor = 4.0;
 int g_max_sweeps = 60;
 int g_max_inner = 1;
+int g_qr_min_cols = 65;   // Householder-QR preconditioning for Jacobi matrices with >= this many columns
 
 // ---------------------------------------------------------------------------
 // init: product state |0...0> (mps.py:55-66)
@@ -307,7 +308,10 @@ struct Ws {
   int* counter;
   double2* M0;
   double2* X;
+  double2* Y;
+  double2* aux;
   size_t mat_stride;
+  size_t aux_stride;
   int sig_stride;
 };
 
@@ -329,6 +333,11 @@ size_t ws_layout(int cap, int nitems, char* base, Ws* ws) {
   off = align256(off + sizeof(double2) * mat_stride * nitems);
   const size_t o_x = off;
   off = align256(off + sizeof(double2) * mat_stride * nitems);
+  const size_t o_y = off;
+  off = align256(off + sizeof(double2) * mat_stride * nitems);
+  const size_t aux_stride = 2048 + kQrNb * kQrNb;
+  const size_t o_aux = off;
+  off = align256(off + sizeof(double2) * aux_stride * nitems);
   if (ws && base) {
     ws->meta = (ItemMeta*)(base + o_meta);
     ws->sig = (double*)(base + o_sig);
@@ -336,6 +345,9 @@ size_t ws_layout(int cap, int nitems, char* base, Ws* ws) {
     ws->counter = (int*)(base + o_cnt);
     ws->M0 = (double2*)(base + o_m0);
     ws->X = (double2*)(base + o_x);
+    ws->Y = (double2*)(base + o_y);
+    ws->aux = (double2*)(base + o_aux);
+    ws->aux_stride = aux_stride;
     ws->mat_stride = mat_stride;
     ws->sig_stride = sig_stride;
   }
@@ -346,6 +358,7 @@ bool g_attrs_set = false;
 void set_attrs() {
   if (g_attrs_set) return;
   cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
+  cudaFuncSetAttribute(qr_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQrUpdateSmem);
   cudaFuncSetAttribute(jacobi_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)JacCfg<32>::kSmem);
   cudaFuncSetAttribute(jacobi_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -386,6 +399,7 @@ int32_t bmps_set_param(const char* name, double value) {
   if (k == "tol_factor" && value > 0) g_tol_factor = value;
   else if (k == "max_sweeps" && value >= 1) g_max_sweeps = (int)value;
   else if (k == "max_inner" && value >= 1) g_max_inner = (int)value;
+  else if (k == "qr_min_cols" && value >= 1) g_qr_min_cols = (int)value;
   else return BMPS_E_ARG;
   return BMPS_OK;
 }
@@ -452,18 +466,44 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   cudaMemsetAsync(ws.meta, 0, sizeof(ItemMeta) * (size_t)nitems, st);
   const int tpd = (dim_bound + 31) / 32;
   theta_kernel<<<dim3(tpd * tpd, nitems), 256, kThetaSmem, st>>>(
-      sv, items, (const double2*)gates, ws.meta, ws.M0, ws.X, ws.mat_stride, tpd);
+      sv, items, (const double2*)gates, ws.meta, ws.M0, ws.X, ws.mat_stride, tpd, g_qr_min_cols);
   ++g_launches;
   int32_t rc = launch_status();
   if (rc) return rc;
 
-  // K3 Jacobi SVD
+  // K3a Householder QR preconditioner (items with c >= qr_min_cols)
   const int cmax = 2 * dim_bound;
+  if (cmax >= g_qr_min_cols) {
+    QrArgs qa;
+    qa.meta = ws.meta;
+    qa.X = ws.X;
+    qa.Y = ws.Y;
+    qa.aux = ws.aux;
+    qa.mat_stride = ws.mat_stride;
+    qa.aux_stride = ws.aux_stride;
+    const int npanels = (cmax + kQrNb - 1) / kQrNb;
+    for (int p = 0; p < npanels; ++p) {
+      qa.panel = p;
+      qr_panel_kernel<<<nitems, 512, 0, st>>>(qa);
+      ++g_launches;
+      const int trail = cmax - (p + 1) * kQrNb;
+      if (trail > 0) {
+        qr_update_kernel<<<dim3((trail + kQrChunk - 1) / kQrChunk, nitems), 256, kQrUpdateSmem, st>>>(qa);
+        ++g_launches;
+      }
+    }
+    qr_form_y_kernel<<<dim3(std::min(64, (cmax * cmax + 255) / 256), nitems), 256, 0, st>>>(qa);
+    ++g_launches;
+    if ((rc = launch_status())) return rc;
+  }
+
+  // K3b Jacobi SVD
   const int max_sweeps = g_max_sweeps;
   const double tol_factor = g_tol_factor;
   JacArgs ja;
   ja.meta = ws.meta;
   ja.X = ws.X;
+  ja.Y = ws.Y;
   ja.mat_stride = ws.mat_stride;
   ja.round = 0;
   ja.max_sweeps = max_sweeps;
@@ -512,26 +552,43 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   }
 
   // K4 finalize + split
-  finalize_kernel<<<nitems, 512, 0, st>>>(sv, items, ws.meta, ws.X, ws.mat_stride, ws.sig,
+  finalize_kernel<<<nitems, 512, 0, st>>>(sv, items, ws.meta, ws.X, ws.Y, ws.mat_stride, ws.sig,
                                           ws.perm, ws.sig_stride, policy.cutoff, policy.max_bond,
                                           policy.relative, log, log_index);
   ++g_launches;
   if ((rc = launch_status())) return rc;
-  SplitOp sop;
-  sop.sv = sv;
-  sop.items = items;
-  sop.meta = ws.meta;
-  sop.M0 = ws.M0;
-  sop.X = ws.X;
-  sop.mat_stride = ws.mat_stride;
-  sop.sig_ws = ws.sig;
-  sop.perm_ws = ws.perm;
-  sop.sig_stride = ws.sig_stride;
   const int kb = policy.max_bond > 0 ? std::min(policy.max_bond, cap) : cap;
-  dim3 sgrid((cmax + 63) / 64, (std::min(kb, cmax) + 63) / 64, nitems);
-  gemm_kernel<SplitOp><<<sgrid, 256, 0, st>>>(sop);
-  ++g_launches;
-  if ((rc = launch_status())) return rc;
+  {
+    SplitOp<false> sop;
+    sop.sv = sv;
+    sop.items = items;
+    sop.meta = ws.meta;
+    sop.M0 = ws.M0;
+    sop.X = ws.X;
+    sop.Yq = ws.Y;
+    sop.mat_stride = ws.mat_stride;
+    sop.sig_ws = ws.sig;
+    sop.perm_ws = ws.perm;
+    sop.sig_stride = ws.sig_stride;
+    dim3 sgrid((cmax + 63) / 64, (std::min(kb, cmax) + 63) / 64, nitems);
+    gemm_kernel<SplitOp<false>><<<sgrid, 256, 0, st>>>(sop);
+    ++g_launches;
+    if (cmax >= g_qr_min_cols) {
+      SplitOp<true> pop;
+      pop.sv = sv;
+      pop.items = items;
+      pop.meta = ws.meta;
+      pop.M0 = ws.M0;
+      pop.X = ws.X;
+      pop.Yq = ws.Y;
+      pop.mat_stride = ws.mat_stride;
+      pop.sig_ws = ws.sig;
+      pop.perm_ws = ws.perm;
+      pop.sig_stride = ws.sig_stride;
+      gemm_kernel<SplitOp<true>><<<sgrid, 256, 0, st>>>(pop);
+      ++g_launches;
+    }
+  }
   return launch_status();
 }
 

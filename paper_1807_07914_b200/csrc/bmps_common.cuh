@@ -126,11 +126,14 @@ struct StateView {
 
 // Per-item bookkeeping of one two-site update (lives in the caller's workspace).
 struct ItemMeta {
-  int r, c, orient, dl, dm, dr;   // X rows/cols, orientation, bond dims before update
-  int keep, status, sweeps, conv, flag, pad;
+  int r, c, orient, dl, dm, dr;   // X0 rows/cols, orientation, bond dims before update
+  int keep, status, sweeps, conv, flag;
+  int precond;                    // 1: Jacobi runs on Y = R^H from X0 = QR
+  int jrows;                      // rows of the Jacobi matrix (r, or c if precond)
+  int pad0, pad1, pad2;
   double err, norm;
-  double fro2;   // ||M||_F^2 (accumulated by theta)
-  double pad2;
+  double fro2;                    // ||M||_F^2 (accumulated by theta)
+  double padd;
 };
 
 }  // namespace bmps

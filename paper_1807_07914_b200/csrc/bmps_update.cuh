@@ -2,6 +2,7 @@
 // (K3), truncation + split (K4) and in-order stats (mps.py:94-136, 82-84).
 #pragma once
 #include "bmps_gemm.cuh"
+#include "bmps_qr.cuh"
 
 namespace bmps {
 
@@ -58,7 +59,7 @@ constexpr size_t kThetaSmem = (size_t)kTile * kThetaLdc * sizeof(double2);
 __global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* items,
                                                     const double2* gates, ItemMeta* meta,
                                                     double2* M0, double2* X, size_t mat_stride,
-                                                    int tiles_per_dim) {
+                                                    int tiles_per_dim, int qr_min_cols) {
   __shared__ __align__(16) double2 sA[kKC][kLds];
   __shared__ __align__(16) double2 sB[kKC][kLds];
   __shared__ double2 sG[16];
@@ -80,6 +81,9 @@ __global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* ite
     m->dl = dl;
     m->dm = dm;
     m->dr = dr;
+    const int c = orient == 0 ? 2 * dr : 2 * dl;
+    m->precond = c >= qr_min_cols ? 1 : 0;
+    m->jrows = m->precond ? c : R;
   }
   const int tm = blockIdx.x / tiles_per_dim, tn = blockIdx.x % tiles_per_dim;
   const int m0 = tm * kTile, n0 = tn * kTile;
@@ -183,6 +187,7 @@ struct JacCfg {
 struct JacArgs {
   ItemMeta* meta;
   double2* X;
+  double2* Y;
   size_t mat_stride;
   int round;
   int persistent;
@@ -418,8 +423,8 @@ __global__ void __launch_bounds__(256) jacobi_kernel(JacArgs args) {
   const int item = blockIdx.y;
   ItemMeta* m = args.meta + item;
   if (m->conv) return;
-  const int r = m->r, c = m->c;
-  double2* X = args.X + (size_t)item * args.mat_stride;
+  const int r = m->jrows, c = m->c;
+  double2* X = (m->precond ? args.Y : args.X) + (size_t)item * args.mat_stride;
   constexpr int w = W2 / 2;
   int nb = (c + w - 1) / w;
   nb += nb & 1;
@@ -512,6 +517,7 @@ constexpr int kMaxCols = 2048;
 
 __global__ void __launch_bounds__(512) finalize_kernel(StateView sv, const int* items,
                                                        ItemMeta* meta, const double2* X,
+                                                       const double2* Yq,
                                                        size_t mat_stride, double* sig_ws,
                                                        int* perm_ws, int sig_stride,
                                                        double cutoff, int max_bond, int relative,
@@ -523,9 +529,10 @@ __global__ void __launch_bounds__(512) finalize_kernel(StateView sv, const int* 
   __shared__ double s_norm;
   const int item = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   ItemMeta* m = meta + item;
-  const int r = m->r, c = m->c, orient = m->orient, dl = m->dl, dr = m->dr;
+  const int r = m->jrows, c = m->c, dl = m->dl, dr = m->dr;
+  const int side = m->orient ^ m->precond;   // 0: primary vectors -> Gamma_q, 1: -> Gamma_{q+1}
   const int s = items[2 * item], q = items[2 * item + 1];
-  const double2* x = X + (size_t)item * mat_stride;
+  const double2* x = (m->precond ? Yq : X) + (size_t)item * mat_stride;
   int P2 = 1;
   while (P2 < c) P2 <<= 1;
   for (int j = warp; j < P2; j += 16) {
@@ -615,7 +622,7 @@ __global__ void __launch_bounds__(512) finalize_kernel(StateView sv, const int* 
     lam_new[k] = ssig[k] / nrm;
   }
   const int cap = sv.cap;
-  if (orient == 0) {
+  if (side == 0) {
     // Gamma_q[l,a,k] = pinv(lam_l[l]) * x[2l+a, perm k] / sigma_k   (mps.py:131,133)
     double2* gq = sv.site(s, q);
     const double* ll = sv.bond(s, q);
@@ -647,14 +654,19 @@ __global__ void __launch_bounds__(512) finalize_kernel(StateView sv, const int* 
 // into Gamma_{q+1} (orient 0, as V^H rows) or Gamma_q (orient 1, as U columns)
 // with the pseudo-inverse bond scaling of mps.py:129-134.
 // ---------------------------------------------------------------------------
+// PRE = false: W = X0^H X[:, perm] / sigma^2 (right vectors of X0, c x keep)
+// PRE = true : W = X0 Y[:, perm] / sigma^2   (left vectors of X0, r x keep)
+// side = orient ^ precond: 0 -> W goes to Gamma_{q+1} as V^H rows, 1 -> to Gamma_q.
+template <bool PRE>
 struct SplitOp {
-  static constexpr bool kAKMajor = true;
+  static constexpr bool kAKMajor = !PRE;
   static constexpr bool kBKMajor = true;
   StateView sv;
   const int* items;
   const ItemMeta* meta;
   const double2* M0;
   const double2* X;
+  const double2* Yq;
   size_t mat_stride;
   const double* sig_ws;
   const int* perm_ws;
@@ -666,40 +678,43 @@ struct SplitOp {
   const int* perm;
   double2* dst;
   const double* lb;
-  int r, orient, dl, dr, cap;
+  int r, jr, side, dl, dr, cap;
   double zero_sig;
   BMPS_DEV bool begin(int item, int& M, int& N, int& K) {
     const ItemMeta* m = meta + item;
-    if (m->status || m->keep <= 0) return false;
+    if (m->status || m->keep <= 0 || (m->precond != 0) != PRE) return false;
     zero_sig = kNoiseRel * sqrt(m->fro2);
     const int s = items[2 * item], q = items[2 * item + 1];
     r = m->r;
-    orient = m->orient;
+    jr = m->jrows;
+    side = m->orient ^ m->precond;
     dl = m->dl;
     dr = m->dr;
     cap = sv.cap;
     m0 = M0 + (size_t)item * mat_stride;
-    x = X + (size_t)item * mat_stride;
+    x = (PRE ? Yq : X) + (size_t)item * mat_stride;
     sig = sig_ws + (size_t)item * sig_stride;
     perm = perm_ws + (size_t)item * sig_stride;
-    if (orient == 0) {
+    if (side == 0) {
       dst = sv.site(s, q + 1);
       lb = sv.bond(s, q + 2);
     } else {
       dst = sv.site(s, q);
       lb = sv.bond(s, q);
     }
-    M = m->c;
+    M = PRE ? r : m->c;
     N = m->keep;
-    K = r;
+    K = PRE ? m->c : r;
     return true;
   }
-  BMPS_DEV double2 a(int i, int k) const { return cconj(m0[(size_t)k + (size_t)i * r]); }
-  BMPS_DEV double2 b(int k, int j) const { return x[(size_t)k + (size_t)perm[j] * r]; }
+  BMPS_DEV double2 a(int i, int k) const {
+    return PRE ? m0[(size_t)i + (size_t)k * r] : cconj(m0[(size_t)k + (size_t)i * r]);
+  }
+  BMPS_DEV double2 b(int k, int j) const { return x[(size_t)k + (size_t)perm[j] * jr]; }
   BMPS_DEV void store(int i, int j, double2 v) const {
     const double sj = sig[j];
     const double f = sj > zero_sig ? 1.0 / (sj * sj) : 0.0;
-    if (orient == 0) {
+    if (side == 0) {
       const int b = i / dr, rr = i % dr;
       dst[(size_t)(2 * j + b) * cap + rr] = cscale(cconj(v), f * pinv(lb[rr]));
     } else {
