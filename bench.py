@@ -202,6 +202,7 @@ def main() -> None:
     ap.add_argument("--mode", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-circuit", action="store_true")
+    ap.add_argument("--param", action="append", default=[], help="libbmps tunable name=value")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -220,6 +221,9 @@ def main() -> None:
     from paper_1807_07914_b200 import MpsBatch, TruncationPolicy, compile_batch, _native
 
     lib = _native.load()
+    for kv in args.param:
+        k, v = kv.split("=")
+        assert lib.bmps_set_param(k.encode(), float(v)) == 0, kv
     R = args.replicas
     policy = TruncationPolicy(CUTOFF, CHI)
     batch = MpsBatch(R, N_QUBITS, policy)

@@ -25,7 +25,9 @@ unsigned long long g_launches = 0;  // kernels launched through this library
 double g_tol_factor = 4.0;
 int g_max_sweeps = 60;
 int g_max_inner = 1;
-int g_qr_min_cols = 65;   // Householder-QR preconditioning for Jacobi matrices with >= this many columns
+int g_qr_min_cols = 65;
+int g_jacobi_mode = 2;
+int g_cluster_size = 8;    // block-mode Jacobi: 1 persistent CTA/item, 2 round launches, 3 cluster/item   // Householder-QR preconditioning for Jacobi matrices with >= this many columns
 
 // ---------------------------------------------------------------------------
 // init: product state |0...0> (mps.py:55-66)
@@ -400,6 +402,8 @@ int32_t bmps_set_param(const char* name, double value) {
   else if (k == "max_sweeps" && value >= 1) g_max_sweeps = (int)value;
   else if (k == "max_inner" && value >= 1) g_max_inner = (int)value;
   else if (k == "qr_min_cols" && value >= 1) g_qr_min_cols = (int)value;
+  else if (k == "jacobi_mode" && value >= 1 && value <= 3) g_jacobi_mode = (int)value;
+  else if (k == "cluster_size" && value >= 1 && value <= 16) g_cluster_size = (int)value;
   else return BMPS_E_ARG;
   return BMPS_OK;
 }
@@ -509,7 +513,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   ja.max_sweeps = max_sweeps;
   ja.max_inner = g_max_inner;
   ja.tol_factor = tol_factor;
-  const int explicit_mode = mode & 3;
+  const int explicit_mode = mode & 3;  // 0 = library default (g_jacobi_mode)
   if (cmax <= 64) {
     ja.persistent = 1;
     if (cmax <= 32)
@@ -520,12 +524,35 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
     if ((rc = launch_status())) return rc;
   } else {
     const int nbmax = (cmax + 15) / 16 + ((cmax + 15) / 16 & 1);
-    const bool persistent =
-        explicit_mode == 1 || (explicit_mode == 0 && (long)nitems * 2 >= 2L * kNumSMs * 2);
-    if (persistent) {
+    const int cl_mode = explicit_mode == 0 ? g_jacobi_mode : explicit_mode;
+    if (cl_mode == 1) {
       ja.persistent = 1;
       jacobi_kernel<32><<<dim3(1, nitems), 256, JacCfg<32>::kSmem, st>>>(ja);
       ++g_launches;
+      if ((rc = launch_status())) return rc;
+    } else if (cl_mode == 3) {
+      ja.persistent = 2;
+      const int csize = std::min(g_cluster_size, nbmax / 2);
+      if (csize > 8)
+        cudaFuncSetAttribute(jacobi_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(csize, nitems, 1);
+      cfg.blockDim = dim3(256, 1, 1);
+      cfg.dynamicSmemBytes = JacCfg<32>::kSmem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = csize;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaError_t e = cudaLaunchKernelEx(&cfg, jacobi_kernel<32>, ja);
+      ++g_launches;
+      if (e != cudaSuccess) {
+        fprintf(stderr, "libbmps: cluster launch failed: %s\n", cudaGetErrorString(e));
+        return BMPS_E_LAUNCH;
+      }
       if ((rc = launch_status())) return rc;
     } else {
       ja.persistent = 0;

@@ -1,0 +1,459 @@
+// K3 block one-sided (Hestenes) Jacobi SVD, Gram-based, on FP64 tensor cores.
+//
+// X (r x c, column-major, r >= c) is orthogonalised in place by unitary column
+// rotations, X <- X V. Columns are grouped in blocks of w = W2/2. A visit of
+// the block pair (I, J):
+//   1. Gram  G = P^H P of the panel P = [X_I X_J] (r x W2) on DMMA, the panel
+//      streamed through shared memory in 64-row chunks with cp.async double
+//      buffering (chunk k+1 lands while chunk k feeds the tensor cores);
+//   2. one cyclic Jacobi sweep on G in shared memory, accumulating Q: the full
+//      round robin over all W2 columns on the first tournament round of an
+//      outer sweep, the w cross rounds (i in I, j in J) otherwise. Each round
+//      updates G <- J^H G J as independent 2x2 blocks (one thread per block)
+//      and Q <- Q J, two barriers per round;
+//   3. P <- P Q on DMMA, streamed the same way, only if a rotation happened.
+// Block pairs follow a round-robin tournament over the nb column blocks; an
+// item has converged when a whole outer sweep performed no rotation. The
+// rotation test (pair_needs_rotation) is relative for dominant columns and
+// absolute (tol * ||M||_F) for small ones.
+// V is not accumulated: the split recovers the other singular vectors from the
+// preserved X0 by a GEMM (SplitOp).
+#pragma once
+#include <cooperative_groups.h>
+
+#include "bmps_common.cuh"
+
+namespace bmps {
+
+template <int W2>
+struct JacCfg {
+  static constexpr int RC = 64;                 // rows per staged chunk
+  static constexpr int RCP = RC + 4;            // padded chunk column (bank spread)
+  static constexpr int LDG = W2 + 4;            // padded Gram / Q column
+  static constexpr int NBUF = (W2 == 32) ? 2 : 1;
+  static constexpr int NT = W2 / 8;             // 8x8 tiles per Gram dimension
+  static constexpr int GT = NT * NT / 8;        // Gram tiles per warp
+  static constexpr int AT = (RC / 8) * NT / 8;  // apply tiles per warp
+  static constexpr int RPW = AT / NT;           // apply tile rows per warp
+  static constexpr int BUF = RCP * W2;          // one staging buffer (complex elements)
+  static constexpr size_t kSmem = (size_t)(2 * W2 * LDG + NBUF * BUF) * sizeof(double2);
+};
+
+struct JacArgs {
+  ItemMeta* meta;
+  double2* X;
+  double2* Y;
+  size_t mat_stride;
+  int round;
+  int persistent;
+  int max_sweeps;
+  int max_inner;
+  double tol_factor;
+};
+
+struct RotShared {
+  double c[32], s[32];
+  double2 e[32];
+  int i[32], j[32];
+};
+
+BMPS_DEV void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(valid ? 16 : 0));
+}
+BMPS_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+BMPS_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int W2>
+BMPS_DEV int panel_col(int p, int I, int J) {
+  constexpr int w = W2 / 2;
+  return p < w ? I * w + p : J * w + (p - w);
+}
+
+// Asynchronous (cp.async, zero-filled) load of rows [row0, row0+RC) of the panel.
+template <int W2>
+BMPS_DEV void jac_issue_chunk(double2* buf, const double2* X, int r, int c, int row0, int I, int J) {
+  using C = JacCfg<W2>;
+  for (int idx = threadIdx.x; idx < C::RC * W2; idx += blockDim.x) {
+    const int m = idx % C::RC, p = idx / C::RC;
+    const int row = row0 + m, col = panel_col<W2>(p, I, J);
+    const bool ok = row < r && col < c;
+    cp_async16(buf + m + p * C::RCP, ok ? X + (size_t)row + (size_t)col * r : X, ok);
+  }
+  cp_async_commit();
+}
+
+template <int W2>
+BMPS_DEV void jac_store_chunk(const double2* buf, double2* X, int r, int c, int row0, int I, int J) {
+  using C = JacCfg<W2>;
+  for (int idx = threadIdx.x; idx < C::RC * W2; idx += blockDim.x) {
+    const int m = idx % C::RC, p = idx / C::RC;
+    const int row = row0 + m, col = panel_col<W2>(p, I, J);
+    if (row < r && col < c) X[(size_t)row + (size_t)col * r] = buf[m + p * C::RCP];
+  }
+}
+
+// G += P^H P over one staged chunk (rows beyond nrows are zero-filled).
+template <int W2>
+BMPS_DEV void jac_gram_chunk(double (&acc)[JacCfg<W2>::GT][4], const double2* sP, int nrows) {
+  using C = JacCfg<W2>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tile0 = warp * C::GT, ti = tile0 / C::NT, tj0 = tile0 % C::NT;
+  const int kr = lane & 3, rc = lane >> 2;
+  const int nk4 = (nrows + 3) >> 2;
+  for (int k4 = 0; k4 < nk4; ++k4) {
+    const int k = k4 * 4 + kr;
+    const double2 a = cconj(sP[k + (ti * 8 + rc) * C::RCP]);
+#pragma unroll
+    for (int u = 0; u < C::GT; ++u) {
+      const double2 b = sP[k + ((tj0 + u) * 8 + rc) * C::RCP];
+      zmma(acc[u], a, b);
+    }
+  }
+}
+
+// acc = P_chunk (RC x W2) * Q (W2 x W2).
+template <int W2>
+BMPS_DEV void jac_apply_mma(double (&acc)[JacCfg<W2>::AT][4], const double2* sP, const double2* sQ) {
+  using C = JacCfg<W2>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int kr = lane & 3, rc = lane >> 2;
+  const int mi0 = warp * C::RPW;
+#pragma unroll
+  for (int u = 0; u < C::AT; ++u)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
+#pragma unroll 2
+  for (int k4 = 0; k4 < W2 / 4; ++k4) {
+    const int k = k4 * 4 + kr;
+    double2 b[C::NT];
+#pragma unroll
+    for (int nj = 0; nj < C::NT; ++nj) b[nj] = sQ[k + (nj * 8 + rc) * C::LDG];
+#pragma unroll
+    for (int rr = 0; rr < C::RPW; ++rr) {
+      const double2 a = sP[(mi0 + rr) * 8 + rc + k * C::RCP];
+#pragma unroll
+      for (int nj = 0; nj < C::NT; ++nj) zmma(acc[rr * C::NT + nj], a, b[nj]);
+    }
+  }
+}
+
+template <int W2>
+BMPS_DEV void jac_apply_writeback(const double (&acc)[JacCfg<W2>::AT][4], double2* sP) {
+  using C = JacCfg<W2>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int kr = lane & 3, rc = lane >> 2;
+  const int mi0 = warp * C::RPW;
+#pragma unroll
+  for (int rr = 0; rr < C::RPW; ++rr)
+#pragma unroll
+    for (int nj = 0; nj < C::NT; ++nj)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = (mi0 + rr) * 8 + rc, nn = nj * 8 + kr * 2 + h;
+        sP[m + nn * C::RCP] = make_double2(acc[rr * C::NT + nj][h], acc[rr * C::NT + nj][2 + h]);
+      }
+}
+
+// Pairing of inner round rho: full round robin over W2 columns, or cross
+// pairs (p, w + (p + rho) mod w) between the two blocks of the panel.
+template <int W2>
+BMPS_DEV void inner_pair(bool full, int rho, int p, int& i, int& j) {
+  constexpr int w = W2 / 2;
+  if (full) {
+    tourney_pair(W2, rho, p, i, j);
+  } else {
+    i = p;
+    j = w + (p + rho) % w;
+  }
+}
+
+// One (or more) cyclic Jacobi sweeps on the W2 x W2 Gram, accumulating Q.
+// Returns the number of rotations of the first sweep (block-uniform).
+template <int W2>
+BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, double noise2,
+                       double fro, bool full, int max_inner) {
+  using C = JacCfg<W2>;
+  constexpr int w = W2 / 2;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < W2 * W2; idx += blockDim.x) {
+    const int i = idx % W2, j = idx / W2;
+    sQ[i + j * C::LDG] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+  }
+  int first = 0;
+  const int rounds = full ? W2 - 1 : w;
+  for (int it = 0; it < max_inner; ++it) {
+    int any = 0;
+    for (int rho = 0; rho < rounds; ++rho) {
+      int act = 0;
+      if (tid < w) {
+        int i, j;
+        inner_pair<W2>(full, rho, tid, i, j);
+        double c = 1.0, s = 0.0;
+        double2 e = make_double2(1.0, 0.0);
+        act = jacobi_rotation(sG[i + i * C::LDG].x, sG[j + j * C::LDG].x, sG[i + j * C::LDG], tol,
+                              noise2, fro, c, s, e);
+        if (!act) {
+          c = 1.0;
+          s = 0.0;
+          e = make_double2(1.0, 0.0);
+        }
+        rs.i[tid] = i;
+        rs.j[tid] = j;
+        rs.c[tid] = c;
+        rs.s[tid] = s;
+        rs.e[tid] = e;
+      }
+      const int nact = __syncthreads_count(act);
+      any += nact;
+      if (nact == 0) continue;
+      // G <- J^H G J as w x w independent 2x2 blocks; Q <- Q J
+      for (int idx = tid; idx < w * w; idx += blockDim.x) {
+        const int p = idx % w, q = idx / w;
+        const int ip = rs.i[p], jp = rs.j[p], iq = rs.i[q], jq = rs.j[q];
+        const double cp = rs.c[p], sp = rs.s[p], cq = rs.c[q], sq = rs.s[q];
+        const double2 ep = rs.e[p], eq = cconj(rs.e[q]);
+        const double2 g00 = sG[ip + iq * C::LDG], g01 = sG[ip + jq * C::LDG];
+        const double2 g10 = sG[jp + iq * C::LDG], g11 = sG[jp + jq * C::LDG];
+        // right: [x_iq, x_jq] <- [x_iq, x_jq] [[cq, sq], [-sq e*, cq e*]]
+        const double2 sqe = cscale(eq, sq), cqe = cscale(eq, cq);
+        const double2 r00 = csub(cscale(g00, cq), cmul(sqe, g01));
+        const double2 r01 = cadd(cscale(g00, sq), cmul(cqe, g01));
+        const double2 r10 = csub(cscale(g10, cq), cmul(sqe, g11));
+        const double2 r11 = cadd(cscale(g10, sq), cmul(cqe, g11));
+        // left: rows ip, jp by J_p^H = [[cp, -sp e], [sp, cp e]]
+        const double2 spe = cscale(ep, sp), cpe = cscale(ep, cp);
+        sG[ip + iq * C::LDG] = csub(cscale(r00, cp), cmul(spe, r10));
+        sG[ip + jq * C::LDG] = csub(cscale(r01, cp), cmul(spe, r11));
+        sG[jp + iq * C::LDG] = cadd(cscale(r00, sp), cmul(cpe, r10));
+        sG[jp + jq * C::LDG] = cadd(cscale(r01, sp), cmul(cpe, r11));
+      }
+      for (int idx = tid; idx < W2 * w; idx += blockDim.x) {
+        const int k = idx % W2, q = idx / W2;
+        const int iq = rs.i[q], jq = rs.j[q];
+        const double cq = rs.c[q], sq = rs.s[q];
+        const double2 eq = cconj(rs.e[q]);
+        const double2 qi = sQ[k + iq * C::LDG], qj = sQ[k + jq * C::LDG];
+        sQ[k + iq * C::LDG] = csub(cscale(qi, cq), cmul(cscale(eq, sq), qj));
+        sQ[k + jq * C::LDG] = cadd(cscale(qi, sq), cmul(cscale(eq, cq), qj));
+      }
+      __syncthreads();
+    }
+    if (it == 0) first = any;
+    if (!any) break;
+  }
+  return first;
+}
+
+// One block-pair visit; returns true if any rotation was applied. If
+// `resident`, the whole panel (r <= RC) already sits in buffer 0 and is
+// neither loaded nor stored here.
+template <int W2>
+BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, double noise2,
+                        double fro, bool full, int max_inner, bool resident, double2* sG,
+                        double2* sQ, double2* sP, RotShared& rs) {
+  using C = JacCfg<W2>;
+  const int tid = threadIdx.x;
+  const int nch = (r + C::RC - 1) / C::RC;
+  double gacc[C::GT][4];
+#pragma unroll
+  for (int u = 0; u < C::GT; ++u)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) gacc[u][q] = 0.0;
+  if (resident) {
+    jac_gram_chunk<W2>(gacc, sP, r);
+  } else {
+    __syncthreads();
+    jac_issue_chunk<W2>(sP, X, r, c, 0, I, J);
+    for (int k = 0; k < nch; ++k) {
+      double2* cur = sP + (k % C::NBUF) * C::BUF;
+      if (C::NBUF == 2 && k + 1 < nch) {
+        jac_issue_chunk<W2>(sP + ((k + 1) % 2) * C::BUF, X, r, c, (k + 1) * C::RC, I, J);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      jac_gram_chunk<W2>(gacc, cur, min(C::RC, r - k * C::RC));
+      __syncthreads();
+      if (C::NBUF == 1 && k + 1 < nch) jac_issue_chunk<W2>(sP, X, r, c, (k + 1) * C::RC, I, J);
+    }
+  }
+  {
+    const int lane = tid & 31, warp = tid >> 5;
+    const int tile0 = warp * C::GT, ti = tile0 / C::NT, tj0 = tile0 % C::NT;
+#pragma unroll
+    for (int u = 0; u < C::GT; ++u)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = ti * 8 + (lane >> 2), j = (tj0 + u) * 8 + (lane & 3) * 2 + h;
+        sG[i + j * C::LDG] = make_double2(gacc[u][h], gacc[u][2 + h]);
+      }
+  }
+  __syncthreads();
+  const int nrot = jac_inner<W2>(sG, sQ, rs, tol, noise2, fro, full, max_inner);
+  if (nrot == 0) return false;
+  double aacc[C::AT][4];
+  if (resident) {
+    jac_apply_mma<W2>(aacc, sP, sQ);
+    __syncthreads();
+    jac_apply_writeback<W2>(aacc, sP);
+    __syncthreads();
+    return true;
+  }
+  // re-stream the panel: load chunk k+1 while chunk k is multiplied and stored
+  const bool staged = nch == 1;  // single chunk still in buffer 0 from the Gram pass
+  if (!staged) jac_issue_chunk<W2>(sP, X, r, c, 0, I, J);
+  for (int k = 0; k < nch; ++k) {
+    double2* cur = sP + (k % C::NBUF) * C::BUF;
+    if (!staged) {
+      if (C::NBUF == 2 && k + 1 < nch) {
+        jac_issue_chunk<W2>(sP + ((k + 1) % 2) * C::BUF, X, r, c, (k + 1) * C::RC, I, J);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+    }
+    __syncthreads();
+    jac_apply_mma<W2>(aacc, cur, sQ);
+    __syncthreads();
+    jac_apply_writeback<W2>(aacc, cur);
+    __syncthreads();
+    jac_store_chunk<W2>(cur, X, r, c, k * C::RC, I, J);
+    __syncthreads();
+    if (C::NBUF == 1 && !staged && k + 1 < nch) jac_issue_chunk<W2>(sP, X, r, c, (k + 1) * C::RC, I, J);
+  }
+  return true;
+}
+
+template <int W2>
+BMPS_DEV void jac_load_resident(double2* sP, const double2* X, int r, int c) {
+  jac_issue_chunk<W2>(sP, X, r, c, 0, 0, 1);
+  cp_async_wait<0>();
+  __syncthreads();
+}
+
+template <int W2>
+__global__ void __launch_bounds__(256, 2) jacobi_kernel(JacArgs args) {
+  using C = JacCfg<W2>;
+  extern __shared__ __align__(16) double2 jsm[];
+  double2* sG = jsm;
+  double2* sQ = sG + W2 * C::LDG;
+  double2* sP = sQ + W2 * C::LDG;
+  __shared__ RotShared rs;
+  const int item = blockIdx.y;
+  ItemMeta* m = args.meta + item;
+  if (m->conv) return;
+  const int r = m->jrows, c = m->c;
+  double2* X = (m->precond ? args.Y : args.X) + (size_t)item * args.mat_stride;
+  constexpr int w = W2 / 2;
+  int nb = (c + w - 1) / w;
+  nb += nb & 1;
+  const double tol = args.tol_factor * sqrt((double)r) * kEps;
+  const double noise2 = kNoiseRel * kNoiseRel * m->fro2;
+  const double fro = sqrt(m->fro2);
+  if (nb == 2) {
+    // single panel: the whole matrix is one visit, iterated to convergence
+    if (blockIdx.x != 0) return;
+    const bool resident = r <= C::RC;
+    if (resident) jac_load_resident<W2>(sP, X, r, c);
+    int sweep = 0;
+    bool clean = false;
+    for (; sweep < args.max_sweeps; ++sweep) {
+      if (!jac_visit<W2>(X, r, c, 0, 1, tol, noise2, fro, true, 64, resident, sG, sQ, sP, rs)) {
+        clean = true;
+        break;
+      }
+    }
+    if (resident) {
+      __syncthreads();
+      jac_store_chunk<W2>(sP, X, r, c, 0, 0, 1);
+    }
+    if (threadIdx.x == 0) {
+      m->sweeps = sweep;
+      m->conv = 1;
+      if (!clean) m->status = BMPS_S_SVD_FAILED;
+    }
+    return;
+  }
+  if (args.persistent == 2) {
+    // one thread-block cluster per item; rounds separated by cluster barriers,
+    // the sweep's dirty flag OR-reduced in rank 0's shared memory (DSMEM)
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ int sflag[2];
+    const int rank = (int)cl.block_rank(), P = (int)cl.num_blocks();
+    if (threadIdx.x < 2) sflag[threadIdx.x] = 0;
+    cl.sync();
+    int* flag0 = cl.map_shared_rank(sflag, 0);
+    int sweep = 0;
+    bool clean = false;
+    for (; sweep < args.max_sweeps; ++sweep) {
+      bool any = false;
+      for (int rho = 0; rho < nb - 1; ++rho) {
+        for (int v = rank; v < nb / 2; v += P) {
+          int I, J;
+          tourney_pair(nb, rho, v, I, J);
+          any |= jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, rho == 0, args.max_inner, false, sG,
+                               sQ, sP, rs);
+        }
+        __threadfence();
+        cl.sync();
+      }
+      if (any && threadIdx.x == 0) atomicOr(flag0 + (sweep & 1), 1);
+      cl.sync();
+      const int dirty = *((volatile int*)(flag0 + (sweep & 1)));
+      if (rank == 0 && threadIdx.x == 0) sflag[(sweep + 1) & 1] = 0;
+      if (!dirty) {
+        clean = true;
+        break;
+      }
+    }
+    if (rank == 0 && threadIdx.x == 0) {
+      m->sweeps = sweep;
+      m->conv = 1;
+      if (!clean) m->status = BMPS_S_SVD_FAILED;
+    }
+    cl.sync();
+    return;
+  }
+  if (args.persistent) {
+    if (blockIdx.x != 0) return;
+    int sweep = 0;
+    bool clean = false;
+    for (; sweep < args.max_sweeps; ++sweep) {
+      bool any = false;
+      for (int rho = 0; rho < nb - 1; ++rho)
+        for (int v = 0; v < nb / 2; ++v) {
+          int I, J;
+          tourney_pair(nb, rho, v, I, J);
+          any |= jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, rho == 0, args.max_inner, false, sG,
+                               sQ, sP, rs);
+        }
+      if (!any) {
+        clean = true;
+        break;
+      }
+    }
+    if (threadIdx.x == 0) {
+      m->sweeps = sweep;
+      m->conv = 1;
+      if (!clean) m->status = BMPS_S_SVD_FAILED;
+    }
+    return;
+  }
+  const int v = blockIdx.x, rho = args.round;
+  if (v >= nb / 2 || rho >= nb - 1) return;
+  int I, J;
+  tourney_pair(nb, rho, v, I, J);
+  if (jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, rho == 0, args.max_inner, false, sG, sQ, sP,
+                    rs) &&
+      threadIdx.x == 0)
+    atomicOr(&m->flag, 1);
+}
+
+}  // namespace bmps

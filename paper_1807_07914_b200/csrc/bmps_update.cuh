@@ -1,6 +1,8 @@
 // Two-site update kernels: theta contraction (K2), block one-sided Jacobi SVD
 // (K3), truncation + split (K4) and in-order stats (mps.py:94-136, 82-84).
 #pragma once
+#include <cooperative_groups.h>
+
 #include "bmps_gemm.cuh"
 #include "bmps_qr.cuh"
 
@@ -159,334 +161,11 @@ __global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* ite
   }
 }
 
-// ---------------------------------------------------------------------------
-// K3 block one-sided (Hestenes) Jacobi SVD, Gram-based, on DMMA.
-//
-// X (r x c, column-major, r >= c) is orthogonalised in place by unitary column
-// rotations: X <- X V. Columns are grouped into blocks of w = W2/2; a visit of
-// block pair (I, J) forms the W2 x W2 Gram of the panel [X_I X_J] on FP64
-// tensor cores, runs cyclic two-sided Jacobi sweeps on the Gram in shared
-// memory (accumulating Q), and applies X_panel <- X_panel Q on tensor cores.
-// Block pairs follow a round-robin tournament; an item converges when a full
-// sweep finds every fresh panel Gram off-diagonal below tol*sqrt(G_ii G_jj).
-// V is not accumulated: the split recovers the other singular vectors from the
-// preserved M0 by a GEMM (V = M0^H U Sigma^-1, see split_kernel).
-// ---------------------------------------------------------------------------
-template <int W2>
-struct JacCfg {
-  static constexpr int RC = (W2 == 32) ? 128 : 64;
-  static constexpr int RCP = RC + 4;
-  static constexpr int LDG = W2 + 4;
-  static constexpr int NT = W2 / 8;
-  static constexpr int GT = NT * NT / 8;
-  static constexpr int AT = (RC / 8) * NT / 8;
-  static constexpr int RPW = AT / NT;
-  static constexpr size_t kSmem = (size_t)(2 * W2 * LDG + RCP * W2) * sizeof(double2);
-};
+}  // namespace bmps
 
-struct JacArgs {
-  ItemMeta* meta;
-  double2* X;
-  double2* Y;
-  size_t mat_stride;
-  int round;
-  int persistent;
-  int max_sweeps;
-  int max_inner;
-  double tol_factor;
-};
+#include "bmps_jacobi.cuh"
 
-template <int W2>
-BMPS_DEV int panel_col(int p, int I, int J) {
-  constexpr int w = W2 / 2;
-  return p < w ? I * w + p : J * w + (p - w);
-}
-
-template <int W2>
-BMPS_DEV void jac_load_chunk(double2* sP, const double2* X, int r, int c, int row0, int I, int J) {
-  using C = JacCfg<W2>;
-  for (int idx = threadIdx.x; idx < C::RC * W2; idx += blockDim.x) {
-    const int m = idx % C::RC, p = idx / C::RC;
-    const int row = row0 + m, col = panel_col<W2>(p, I, J);
-    sP[m + p * C::RCP] =
-        (row < r && col < c) ? X[(size_t)row + (size_t)col * r] : make_double2(0.0, 0.0);
-  }
-}
-
-template <int W2>
-BMPS_DEV void jac_store_chunk(const double2* sP, double2* X, int r, int c, int row0, int I, int J) {
-  using C = JacCfg<W2>;
-  for (int idx = threadIdx.x; idx < C::RC * W2; idx += blockDim.x) {
-    const int m = idx % C::RC, p = idx / C::RC;
-    const int row = row0 + m, col = panel_col<W2>(p, I, J);
-    if (row < r && col < c) X[(size_t)row + (size_t)col * r] = sP[m + p * C::RCP];
-  }
-}
-
-// Accumulate G += P^H P over one staged chunk (rows < nrows are meaningful).
-template <int W2>
-BMPS_DEV void jac_gram_chunk(double (&acc)[JacCfg<W2>::GT][4], const double2* sP, int nrows) {
-  using C = JacCfg<W2>;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tile0 = warp * C::GT, ti = tile0 / C::NT, tj0 = tile0 % C::NT;
-  const int kr = lane & 3, rc = lane >> 2;
-  const int nk4 = (nrows + 3) >> 2;
-  for (int k4 = 0; k4 < nk4; ++k4) {
-    const int k = k4 * 4 + kr;
-    const double2 a = cconj(sP[k + (ti * 8 + rc) * C::RCP]);
-#pragma unroll
-    for (int u = 0; u < C::GT; ++u) {
-      const double2 b = sP[k + ((tj0 + u) * 8 + rc) * C::RCP];
-      zmma(acc[u], a, b);
-    }
-  }
-}
-
-// Out(chunk) = P_chunk (RC x W2) * Q (W2 x W2), written back into sP.
-template <int W2>
-BMPS_DEV void jac_apply_chunk(double2* sP, const double2* sQ) {
-  using C = JacCfg<W2>;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int kr = lane & 3, rc = lane >> 2;
-  const int mi0 = warp * C::RPW;
-  double acc[C::AT][4];
-#pragma unroll
-  for (int u = 0; u < C::AT; ++u)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
-#pragma unroll 2
-  for (int k4 = 0; k4 < W2 / 4; ++k4) {
-    const int k = k4 * 4 + kr;
-    double2 b[C::NT];
-#pragma unroll
-    for (int nj = 0; nj < C::NT; ++nj) b[nj] = sQ[k + (nj * 8 + rc) * C::LDG];
-#pragma unroll
-    for (int rr = 0; rr < C::RPW; ++rr) {
-      const double2 a = sP[(mi0 + rr) * 8 + rc + k * C::RCP];
-#pragma unroll
-      for (int nj = 0; nj < C::NT; ++nj) zmma(acc[rr * C::NT + nj], a, b[nj]);
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int rr = 0; rr < C::RPW; ++rr)
-#pragma unroll
-    for (int nj = 0; nj < C::NT; ++nj)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int m = (mi0 + rr) * 8 + rc, nn = nj * 8 + kr * 2 + h;
-        sP[m + nn * C::RCP] = make_double2(acc[rr * C::NT + nj][h], acc[rr * C::NT + nj][2 + h]);
-      }
-  __syncthreads();
-}
-
-struct RotShared {
-  double c[32], s[32];
-  double2 e[32];
-  int i[32], j[32], act[32];
-};
-
-// Cyclic two-sided Jacobi on the W2 x W2 Hermitian Gram, accumulating Q.
-template <int W2>
-BMPS_DEV void jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, double noise2,
-                        double fro, int max_inner) {
-  using C = JacCfg<W2>;
-  constexpr int w = W2 / 2;
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < W2 * W2; idx += blockDim.x) {
-    const int i = idx % W2, j = idx / W2;
-    sQ[i + j * C::LDG] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-  }
-  for (int it = 0; it < max_inner; ++it) {
-    int any = 0;
-    for (int rho = 0; rho < W2 - 1; ++rho) {
-      int act = 0;
-      if (tid < w) {
-        int i, j;
-        tourney_pair(W2, rho, tid, i, j);
-        double c, s;
-        double2 e;
-        act = jacobi_rotation(sG[i + i * C::LDG].x, sG[j + j * C::LDG].x, sG[i + j * C::LDG], tol,
-                              noise2, fro, c, s, e);
-        rs.i[tid] = i;
-        rs.j[tid] = j;
-        rs.act[tid] = act;
-        rs.c[tid] = c;
-        rs.s[tid] = s;
-        rs.e[tid] = e;
-      }
-      any |= __syncthreads_or(act);
-      // columns i, j of G and Q: [x_i, x_j] <- [x_i, x_j] J
-      for (int idx = tid; idx < 2 * W2 * w; idx += blockDim.x) {
-        const int which = idx / (W2 * w), rem = idx % (W2 * w);
-        const int p = rem / W2, k = rem % W2;
-        if (!rs.act[p]) continue;
-        double2* base = which ? sQ : sG;
-        const int i = rs.i[p], j = rs.j[p];
-        const double c = rs.c[p], s = rs.s[p];
-        const double2 ec = cconj(rs.e[p]);
-        const double2 gi = base[k + i * C::LDG], gj = base[k + j * C::LDG];
-        base[k + i * C::LDG] = csub(cscale(gi, c), cmul(cscale(ec, s), gj));
-        base[k + j * C::LDG] = cadd(cscale(gi, s), cmul(cscale(ec, c), gj));
-      }
-      __syncthreads();
-      // rows i, j of G: J^H applied from the left
-      for (int idx = tid; idx < W2 * w; idx += blockDim.x) {
-        const int p = idx / W2, k = idx % W2;
-        if (!rs.act[p]) continue;
-        const int i = rs.i[p], j = rs.j[p];
-        const double c = rs.c[p], s = rs.s[p];
-        const double2 e = rs.e[p];
-        const double2 gi = sG[i + k * C::LDG], gj = sG[j + k * C::LDG];
-        sG[i + k * C::LDG] = csub(cscale(gi, c), cmul(cscale(e, s), gj));
-        sG[j + k * C::LDG] = cadd(cscale(gi, s), cmul(cscale(e, c), gj));
-      }
-      __syncthreads();
-    }
-    if (!any) break;
-  }
-}
-
-// One block-pair visit. Returns true if the fresh panel Gram was not yet
-// orthogonal (a rotation was applied). If `resident`, the whole panel already
-// sits in sP (r <= RC) and is neither loaded nor stored here.
-template <int W2>
-BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, double noise2,
-                        double fro, int max_inner, bool resident, double2* sG, double2* sQ,
-                        double2* sP, RotShared& rs) {
-  using C = JacCfg<W2>;
-  const int tid = threadIdx.x;
-  double acc[C::GT][4];
-#pragma unroll
-  for (int u = 0; u < C::GT; ++u)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
-  for (int row0 = 0; row0 < r; row0 += C::RC) {
-    if (!resident) {
-      __syncthreads();
-      jac_load_chunk<W2>(sP, X, r, c, row0, I, J);
-      __syncthreads();
-    }
-    jac_gram_chunk<W2>(acc, sP, min(C::RC, r - row0));
-  }
-  {
-    const int lane = tid & 31, warp = tid >> 5;
-    const int tile0 = warp * C::GT, ti = tile0 / C::NT, tj0 = tile0 % C::NT;
-#pragma unroll
-    for (int u = 0; u < C::GT; ++u)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int i = ti * 8 + (lane >> 2), j = (tj0 + u) * 8 + (lane & 3) * 2 + h;
-        sG[i + j * C::LDG] = make_double2(acc[u][h], acc[u][2 + h]);
-      }
-  }
-  __syncthreads();
-  int dirty = 0;
-  for (int idx = tid; idx < W2 * W2; idx += blockDim.x) {
-    const int i = idx % W2, j = idx / W2;
-    if (i > j) {
-      sG[i + j * C::LDG] = cconj(sG[j + i * C::LDG]);
-    } else if (i < j) {
-      if (pair_needs_rotation(sG[i + i * C::LDG].x, sG[j + j * C::LDG].x, sG[i + j * C::LDG], tol,
-                              noise2, fro))
-        dirty = 1;
-    }
-  }
-  dirty = __syncthreads_or(dirty);
-  for (int i = tid; i < W2; i += blockDim.x) sG[i + i * C::LDG].y = 0.0;
-  __syncthreads();
-  if (!dirty) return false;
-  jac_inner<W2>(sG, sQ, rs, tol, noise2, fro, max_inner);
-  for (int row0 = 0; row0 < r; row0 += C::RC) {
-    if (!resident) {
-      if (C::RC < r) {  // multi-chunk panel: reload (single chunk is still staged)
-        __syncthreads();
-        jac_load_chunk<W2>(sP, X, r, c, row0, I, J);
-      }
-      __syncthreads();
-    }
-    jac_apply_chunk<W2>(sP, sQ);
-    if (!resident) jac_store_chunk<W2>(sP, X, r, c, row0, I, J);
-  }
-  __syncthreads();
-  return true;
-}
-
-template <int W2>
-__global__ void __launch_bounds__(256) jacobi_kernel(JacArgs args) {
-  using C = JacCfg<W2>;
-  extern __shared__ __align__(16) double2 jsm[];
-  double2* sG = jsm;
-  double2* sQ = sG + W2 * C::LDG;
-  double2* sP = sQ + W2 * C::LDG;
-  __shared__ RotShared rs;
-  const int item = blockIdx.y;
-  ItemMeta* m = args.meta + item;
-  if (m->conv) return;
-  const int r = m->jrows, c = m->c;
-  double2* X = (m->precond ? args.Y : args.X) + (size_t)item * args.mat_stride;
-  constexpr int w = W2 / 2;
-  int nb = (c + w - 1) / w;
-  nb += nb & 1;
-  const double tol = args.tol_factor * sqrt((double)r) * kEps;
-  const double noise2 = kNoiseRel * kNoiseRel * m->fro2;
-  const double fro = sqrt(m->fro2);
-  if (nb == 2) {
-    // single panel: the whole matrix is one visit, iterated to convergence
-    if (blockIdx.x != 0) return;
-    const bool resident = r <= C::RC;
-    if (resident) {
-      jac_load_chunk<W2>(sP, X, r, c, 0, 0, 1);
-      __syncthreads();
-    }
-    int sweep = 0;
-    bool clean = false;
-    for (; sweep < args.max_sweeps; ++sweep) {
-      if (!jac_visit<W2>(X, r, c, 0, 1, tol, noise2, fro, 64, resident, sG, sQ, sP, rs)) {
-        clean = true;
-        break;
-      }
-    }
-    if (resident) jac_store_chunk<W2>(sP, X, r, c, 0, 0, 1);
-    if (threadIdx.x == 0) {
-      m->sweeps = sweep;
-      m->conv = 1;
-      if (!clean) m->status = BMPS_S_SVD_FAILED;
-    }
-    return;
-  }
-  if (args.persistent) {
-    if (blockIdx.x != 0) return;
-    int sweep = 0;
-    bool clean = false;
-    for (; sweep < args.max_sweeps; ++sweep) {
-      bool any = false;
-      for (int rho = 0; rho < nb - 1; ++rho)
-        for (int v = 0; v < nb / 2; ++v) {
-          int I, J;
-          tourney_pair(nb, rho, v, I, J);
-          any |= jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, args.max_inner, false, sG, sQ, sP, rs);
-        }
-      if (!any) {
-        clean = true;
-        break;
-      }
-    }
-    if (threadIdx.x == 0) {
-      m->sweeps = sweep;
-      m->conv = 1;
-      if (!clean) m->status = BMPS_S_SVD_FAILED;
-    }
-    return;
-  }
-  const int v = blockIdx.x, rho = args.round;
-  if (v >= nb / 2 || rho >= nb - 1) return;
-  int I, J;
-  tourney_pair(nb, rho, v, I, J);
-  if (jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, args.max_inner, false, sG, sQ, sP, rs) &&
-      threadIdx.x == 0)
-    atomicOr(&m->flag, 1);
-}
+namespace bmps {
 
 // End of a round-mode sweep: converge clean items, count the rest.
 __global__ void sweep_end_kernel(ItemMeta* meta, int nitems, int max_sweeps, int* unconverged) {
