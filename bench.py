@@ -262,6 +262,7 @@ def main() -> None:
     launches = int(lib.bmps_launch_count() - l0)
     ms = e0.elapsed_time(e1)
     batch.check_status()
+    sw = batch.last_sweeps(int(upd[total_steps - 1]))
     n_upd = sum(upd[args.warmup:])
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -323,6 +324,8 @@ def main() -> None:
                     "d2h_bytes_per_step": int(d2h),
                     "path": "MpsBatch.execute(compile_batch(host programs)) + D2H of all bond vectors"},
             "gpu_launches": launches,
+            "jacobi_sweeps_last_step": {"mean": float(sw.mean()), "max": int(sw.max()),
+                                        "p50": float(np.median(sw))},
             "clocks": clk.summary(),
         }
         if not args.no_circuit and world == 1:

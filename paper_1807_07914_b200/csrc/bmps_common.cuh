@@ -95,9 +95,14 @@ BMPS_DEV bool pair_needs_rotation(double a, double b, double2 g, double tol, dou
 
 BMPS_DEV bool jacobi_rotation(double a, double b, double2 g, double tol, double noise2, double fro,
                               double& c, double& s, double2& e) {
-  if (!pair_needs_rotation(a, b, g, tol, noise2, fro)) return false;
-  const double ag = hypot(g.x, g.y);
-  const double zeta = (b - a) / (2.0 * ag);
+  const double lo = fmin(a, b), hi = fmax(a, b);
+  if (!(hi > noise2) || !(lo > kNegligible * hi)) return false;
+  const double g2 = cabs2(g);
+  const double thr = tol * fro;
+  if (!(g2 > thr * thr * lo)) return false;            // |g| > tol * sqrt(lo) * fro
+  // short dependent chain: one rsqrt, one sqrt, one reciprocal, one rsqrt
+  const double rg = rsqrt(g2);                         // 1 / |g|
+  const double zeta = 0.5 * (b - a) * rg;
   double t;
   if (fabs(zeta) > 1e150) {
     t = 0.5 / zeta;
@@ -105,9 +110,9 @@ BMPS_DEV bool jacobi_rotation(double a, double b, double2 g, double tol, double 
     t = 1.0 / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
     if (zeta < 0) t = -t;
   }
-  c = 1.0 / sqrt(fma(t, t, 1.0));
+  c = rsqrt(fma(t, t, 1.0));
   s = c * t;
-  e = make_double2(g.x / ag, g.y / ag);
+  e = make_double2(g.x * rg, g.y * rg);
   return true;
 }
 

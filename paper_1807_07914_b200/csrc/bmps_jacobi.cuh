@@ -54,7 +54,7 @@ struct JacArgs {
 struct RotShared {
   double c[32], s[32];
   double2 e[32];
-  int i[32], j[32];
+  int i[32], j[32], act[32];
 };
 
 BMPS_DEV void cp_async16(void* smem, const void* gmem, bool valid) {
@@ -204,6 +204,7 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
         }
         rs.i[tid] = i;
         rs.j[tid] = j;
+        rs.act[tid] = act;
         rs.c[tid] = c;
         rs.s[tid] = s;
         rs.e[tid] = e;
@@ -214,6 +215,7 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
       // G <- J^H G J as w x w independent 2x2 blocks; Q <- Q J
       for (int idx = tid; idx < w * w; idx += blockDim.x) {
         const int p = idx % w, q = idx / w;
+        if (!(rs.act[p] | rs.act[q])) continue;  // identity on both sides
         const int ip = rs.i[p], jp = rs.j[p], iq = rs.i[q], jq = rs.j[q];
         const double cp = rs.c[p], sp = rs.s[p], cq = rs.c[q], sq = rs.s[q];
         const double2 ep = rs.e[p], eq = cconj(rs.e[q]);
@@ -234,6 +236,7 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
       }
       for (int idx = tid; idx < W2 * w; idx += blockDim.x) {
         const int k = idx % W2, q = idx / W2;
+        if (!rs.act[q]) continue;
         const int iq = rs.i[q], jq = rs.j[q];
         const double cq = rs.c[q], sq = rs.s[q];
         const double2 eq = cconj(rs.e[q]);

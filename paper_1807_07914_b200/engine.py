@@ -322,6 +322,16 @@ class MpsBatch:
         self._keep_alive = (it1, g1, it2, g2, li2, rng)
         self._logs.append((log, plan.ranges))
 
+    def last_sweeps(self, count: int | None = None) -> np.ndarray:
+        """Jacobi sweeps of the items of the most recent bmps_apply_2q launch."""
+        if self._ws is None:
+            return np.zeros(0, np.int32)
+        n = count if count is not None else self.max_items
+        out = torch.zeros(n, dtype=torch.int32, device=self.device)
+        rc = self.lib.bmps_apply_2q_sweeps(self._ws.data_ptr(), n, out.data_ptr(), _stream())
+        _native.check(rc, "bmps_apply_2q_sweeps")
+        return out.cpu().numpy()
+
     def update_records(self, s: int) -> np.ndarray:
         """Per-update records of state ``s`` in program order (all executed plans)."""
         out = []
