@@ -32,7 +32,10 @@ struct JacCfg {
   static constexpr int LDG = W2 + 4;            // padded Gram / Q column
   static constexpr int NBUF = (W2 == 32) ? 2 : 1;
   static constexpr int NT = W2 / 8;             // 8x8 tiles per Gram dimension
-  static constexpr int GT = NT * NT / 8;        // Gram tiles per warp
+  static constexpr int UT = NT * (NT + 1) / 2;  // upper-triangle Gram tiles
+  static constexpr int GT = UT / 8;             // whole upper tiles per warp
+  static constexpr int GREM = UT - 8 * GT;      // leftover tiles, split over k
+  static constexpr int GSPLIT = GREM ? 8 / GREM : 1;  // warps sharing one leftover tile
   static constexpr int AT = (RC / 8) * NT / 8;  // apply tiles per warp
   static constexpr int RPW = AT / NT;           // apply tile rows per warp
   static constexpr int BUF = RCP * W2;          // one staging buffer (complex elements)
@@ -97,21 +100,80 @@ BMPS_DEV void jac_store_chunk(const double2* buf, double2* X, int r, int c, int 
   }
 }
 
-// G += P^H P over one staged chunk (rows beyond nrows are zero-filled).
+// Upper-triangle Gram tile t -> (ti, tj), ti <= tj.
+template <int NT>
+BMPS_DEV void upper_tile(int t, int& ti, int& tj) {
+  ti = 0;
+  while (t >= NT - ti) {
+    t -= NT - ti;
+    ++ti;
+  }
+  tj = ti + t;
+}
+
+// G += P^H P over one staged chunk (rows beyond nrows are zero-filled), upper
+// triangle only: each warp owns GT whole tiles plus a 1/GSPLIT k-slice of one
+// leftover tile (slot GT of acc), so the 8 warps carry equal DMMA work.
 template <int W2>
-BMPS_DEV void jac_gram_chunk(double (&acc)[JacCfg<W2>::GT][4], const double2* sP, int nrows) {
+BMPS_DEV void jac_gram_chunk(double (&acc)[JacCfg<W2>::GT + 1][4], const double2* sP, int nrows) {
   using C = JacCfg<W2>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tile0 = warp * C::GT, ti = tile0 / C::NT, tj0 = tile0 % C::NT;
   const int kr = lane & 3, rc = lane >> 2;
   const int nk4 = (nrows + 3) >> 2;
-  for (int k4 = 0; k4 < nk4; ++k4) {
-    const int k = k4 * 4 + kr;
-    const double2 a = cconj(sP[k + (ti * 8 + rc) * C::RCP]);
 #pragma unroll
-    for (int u = 0; u < C::GT; ++u) {
-      const double2 b = sP[k + ((tj0 + u) * 8 + rc) * C::RCP];
-      zmma(acc[u], a, b);
+  for (int u = 0; u < C::GT; ++u) {
+    int ti, tj;
+    upper_tile<C::NT>(warp * C::GT + u, ti, tj);
+    for (int k4 = 0; k4 < nk4; ++k4) {
+      const int k = k4 * 4 + kr;
+      zmma(acc[u], cconj(sP[k + (ti * 8 + rc) * C::RCP]), sP[k + (tj * 8 + rc) * C::RCP]);
+    }
+  }
+  if (C::GREM) {
+    int ti, tj;
+    upper_tile<C::NT>(8 * C::GT + warp / C::GSPLIT, ti, tj);
+    const int part = warp % C::GSPLIT;
+    const int k0 = part * nk4 / C::GSPLIT, k1 = (part + 1) * nk4 / C::GSPLIT;
+    for (int k4 = k0; k4 < k1; ++k4) {
+      const int k = k4 * 4 + kr;
+      zmma(acc[C::GT], cconj(sP[k + (ti * 8 + rc) * C::RCP]), sP[k + (tj * 8 + rc) * C::RCP]);
+    }
+  }
+}
+
+// Scatter the Gram accumulators into sG (both triangles); scratch holds the
+// k-split partials of the leftover tiles (8 warps x 64 complex).
+template <int W2>
+BMPS_DEV void jac_gram_store(const double (&acc)[JacCfg<W2>::GT + 1][4], double2* sG, double2* scratch) {
+  using C = JacCfg<W2>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rr = lane >> 2, cc = (lane & 3) * 2;
+#pragma unroll
+  for (int u = 0; u < C::GT; ++u) {
+    int ti, tj;
+    upper_tile<C::NT>(warp * C::GT + u, ti, tj);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = ti * 8 + rr, j = tj * 8 + cc + h;
+      const double2 v = make_double2(acc[u][h], acc[u][2 + h]);
+      sG[i + j * C::LDG] = v;
+      if (ti != tj) sG[j + i * C::LDG] = cconj(v);
+    }
+  }
+  if (C::GREM) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      scratch[warp * 64 + rr * 8 + cc + h] = make_double2(acc[C::GT][h], acc[C::GT][2 + h]);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < C::GREM * 64; idx += blockDim.x) {
+      const int t = idx / 64, e = idx % 64;
+      double2 v = make_double2(0.0, 0.0);
+      for (int p = 0; p < C::GSPLIT; ++p) v = cadd(v, scratch[(t * C::GSPLIT + p) * 64 + e]);
+      int ti, tj;
+      upper_tile<C::NT>(8 * C::GT + t, ti, tj);
+      const int i = ti * 8 + e / 8, j = tj * 8 + e % 8;
+      sG[i + j * C::LDG] = v;
+      if (ti != tj) sG[j + i * C::LDG] = cconj(v);
     }
   }
 }
@@ -262,9 +324,9 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
   using C = JacCfg<W2>;
   const int tid = threadIdx.x;
   const int nch = (r + C::RC - 1) / C::RC;
-  double gacc[C::GT][4];
+  double gacc[C::GT + 1][4];
 #pragma unroll
-  for (int u = 0; u < C::GT; ++u)
+  for (int u = 0; u < C::GT + 1; ++u)
 #pragma unroll
     for (int q = 0; q < 4; ++q) gacc[u][q] = 0.0;
   if (resident) {
@@ -286,17 +348,7 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
       if (C::NBUF == 1 && k + 1 < nch) jac_issue_chunk<W2>(sP, X, r, c, (k + 1) * C::RC, I, J);
     }
   }
-  {
-    const int lane = tid & 31, warp = tid >> 5;
-    const int tile0 = warp * C::GT, ti = tile0 / C::NT, tj0 = tile0 % C::NT;
-#pragma unroll
-    for (int u = 0; u < C::GT; ++u)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int i = ti * 8 + (lane >> 2), j = (tj0 + u) * 8 + (lane & 3) * 2 + h;
-        sG[i + j * C::LDG] = make_double2(gacc[u][h], gacc[u][2 + h]);
-      }
-  }
+  jac_gram_store<W2>(gacc, sG, sQ);
   __syncthreads();
   const int nrot = jac_inner<W2>(sG, sQ, rs, tol, noise2, fro, full, max_inner);
   if (nrot == 0) return false;
