@@ -303,6 +303,10 @@ def main() -> None:
     if rank == 0:
         f_upd = nominal_update_flops(CHI, CHI, CHI, CHI)
         achieved = f_upd * value / world / 1e12   # per GPU
+        prof = {}
+        tp = ROOT / "profiles" / "r01_traffic.json"
+        if tp.exists():
+            prof = json.loads(tp.read_text())
         line = {
             "metric": "MPS 2-qubit gate updates/sec at chi=256 (contract+SVD)",
             "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
@@ -315,7 +319,11 @@ def main() -> None:
                        "l2": "inputs larger than L2 (states + workspace > 126 MB), no flush",
                        "parallelism": f"dp{world} (independent replicas)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                         "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                         "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+                         "traffic": prof.get("dram_bytes_per_update"),
+                         "traffic_unit": "DRAM bytes per chi=256 update (ncu capture, profiles/r01_traffic.json)",
+                         "executed_fp64_tflops": (prof["fp64_tensor_flops_per_update"] * value / world / 1e12
+                                                  if prof else None),
                          "basis": "nominal SURVEY §8(d) flops per chi=256 update "
                                   f"({f_upd:.4g}) x updates / device step time; peak = measured "
                                   "FP64 cuBLAS ZGEMM (MEASURED_PEAKS.json has no FP64 entry)",

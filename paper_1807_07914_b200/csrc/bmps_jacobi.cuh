@@ -350,8 +350,14 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
   }
   jac_gram_store<W2>(gacc, sG, sQ);
   __syncthreads();
+  const bool staged = nch == 1;  // single chunk still in buffer 0 from the Gram pass
+  // prefetch the first apply chunk so its load overlaps the inner sweep
+  if (!resident && !staged) jac_issue_chunk<W2>(sP, X, r, c, 0, I, J);
   const int nrot = jac_inner<W2>(sG, sQ, rs, tol, noise2, fro, full, max_inner);
-  if (nrot == 0) return false;
+  if (nrot == 0) {
+    if (!resident && !staged) cp_async_wait<0>();
+    return false;
+  }
   double aacc[C::AT][4];
   if (resident) {
     jac_apply_mma<W2>(aacc, sP, sQ);
@@ -361,8 +367,6 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
     return true;
   }
   // re-stream the panel: load chunk k+1 while chunk k is multiplied and stored
-  const bool staged = nch == 1;  // single chunk still in buffer 0 from the Gram pass
-  if (!staged) jac_issue_chunk<W2>(sP, X, r, c, 0, I, J);
   for (int k = 0; k < nch; ++k) {
     double2* cur = sP + (k % C::NBUF) * C::BUF;
     if (!staged) {
