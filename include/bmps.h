@@ -126,6 +126,13 @@ int32_t bmps_amplitudes(const double* gamma, const double* lam, const int32_t* d
                         int32_t n, int32_t cap, const int32_t* state_idx, const uint8_t* bits,
                         int32_t count, double* out, void* stream);
 
+/* MpsState.sample / conditional_prob_zero (mps.py:206-237) for a batch of
+ * shots: uniforms is float64 [shots][n] (the reference's rng.random() draws,
+ * one per qubit per shot in qubit order), bits out uint8 [shots][n]. */
+int32_t bmps_sample(const double* gamma, const double* lam, const int32_t* dims, int32_t S,
+                    int32_t n, int32_t cap, const int32_t* state_idx, const double* uniforms,
+                    int32_t shots, uint8_t* bits, void* stream);
+
 /* One environment transfer step for a batch of (state, site, pauli) items,
  * the building block of MpsState.expectation_pauli / norm_sq
  * (mps.py:181-204): direction 0 (left, E_{k+1} from E_k, mps.py:200) or

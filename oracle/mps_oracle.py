@@ -253,6 +253,31 @@ class OracleMps:
         return out
 
 
+def oracle_sample(o: "OracleMps", shots: int, rng: np.random.Generator) -> dict[str, int]:
+    """Sequential conditional sampling, mps.py:206-237 (one rng.random() per qubit per shot)."""
+    counts: dict[str, int] = {}
+    mats = [o.site_matrix(k) for k in range(o.n)]
+    for _ in range(shots):
+        vec = np.ones(1, dtype=complex)
+        key = []
+        for k in range(o.n):
+            w0 = vec @ mats[k][:, 0, :]
+            w1 = vec @ mats[k][:, 1, :]
+            p0 = float(np.vdot(w0, w0).real)
+            p1 = float(np.vdot(w1, w1).real)
+            tot = p0 + p1
+            pz = p0 / tot if tot > 0 else 0.5
+            if rng.random() < pz:
+                key.append("0")
+                vec = w0
+            else:
+                key.append("1")
+                vec = w1
+        s = "".join(key)
+        counts[s] = counts.get(s, 0) + 1
+    return counts
+
+
 def oracle_run(program, n: int, cutoff: float = 1e-4, max_bond: int | None = None,
                relative: bool = True, verbatim: bool = False) -> OracleMps:
     return OracleMps(n, cutoff, max_bond, relative, verbatim).run(program)

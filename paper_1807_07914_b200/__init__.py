@@ -7,7 +7,7 @@ runs in ``libbmps.so`` (hand-written sm_100a CUDA behind the C ABI in
 ``include/bmps.h``); there is no CPU fallback.
 """
 
-from .backends import BACKENDS, mps_run, run_program, simulate_batch
+from .backends import BACKENDS, RunRecord, execute, measured_qubits, mps_run, run_program, simulate_batch
 from .engine import MpsBatch, compile_batch
 from .gates import SWAP_MATRIX, check_unitary, gate_matrix
 from .hamiltonian import PauliHamiltonian, pauli_matrix
@@ -16,7 +16,7 @@ from .mps import MpsState
 from .policy import TruncationPolicy
 
 __all__ = [
-    "BACKENDS", "GateKind", "Instruction", "IrError", "MatrixGate", "MpsBatch", "MpsState",
+    "BACKENDS", "RunRecord", "execute", "measured_qubits", "GateKind", "Instruction", "IrError", "MatrixGate", "MpsBatch", "MpsState",
     "PauliHamiltonian", "SWAP_MATRIX", "TruncationPolicy", "check_unitary", "compile_batch",
     "gate_matrix", "mps_run", "num_qubits", "pauli_matrix", "run_program", "simulate_batch",
 ]

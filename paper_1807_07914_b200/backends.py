@@ -10,6 +10,11 @@ the natural shard).
 
 from __future__ import annotations
 
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
 from .engine import MpsBatch, compile_batch
 from .ir import num_qubits
 from .mps import MpsState
@@ -43,3 +48,47 @@ def simulate_batch(programs, n: int, policy: TruncationPolicy | None = None, *, 
     batch = MpsBatch(len(programs), n, policy, device=device)
     batch.execute(compile_batch(programs, n), mode=mode)
     return batch
+
+
+@dataclass
+class RunRecord:
+    """Results of one program execution (``backends.py:25-44``)."""
+
+    counts: dict[str, int] = field(default_factory=dict)
+    max_bond_seen: int | None = None
+    memory_estimate_bytes: int = 0
+    trunc_error_sq: float = 0.0
+    wall_time: float = 0.0
+
+    def to_json_dict(self, include_wall_time: bool = True) -> dict:
+        out = {"counts": self.counts, "max_bond_seen": self.max_bond_seen,
+               "memory_estimate_bytes": self.memory_estimate_bytes,
+               "trunc_error_sq": self.trunc_error_sq}
+        if include_wall_time:
+            out["wall_time"] = self.wall_time
+        return out
+
+
+def measured_qubits(program) -> list[int]:
+    """Qubits of the MEASURE instructions, in program order (``backends.py:82-84``)."""
+    return [i.qubits[0] for i in program
+            if getattr(i, "kind", None) is not None and i.kind.value == "MEASURE"]
+
+
+def execute(program, n: int | None = None, backend: str = "mps",
+            policy: TruncationPolicy | None = None, shots: int = 1024,
+            seed: int | None = None, *, device=None) -> RunRecord:
+    """Run, sample the measured qubits on the GPU, collect stats (``backends.py:87-113``)."""
+    start = time.perf_counter()
+    state = run_program(program, n, backend, policy, device=device)
+    record = RunRecord(max_bond_seen=state.max_bond_seen,
+                       memory_estimate_bytes=state.memory_estimate_bytes(),
+                       trunc_error_sq=state.trunc_error_sq)
+    targets = measured_qubits(program)
+    if targets and shots > 0:
+        full = state.sample(shots, np.random.default_rng(seed))
+        for bits, count in sorted(full.items()):
+            key = "".join(bits[q] for q in targets)
+            record.counts[key] = record.counts.get(key, 0) + count
+    record.wall_time = time.perf_counter() - start
+    return record

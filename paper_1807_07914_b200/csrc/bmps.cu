@@ -111,6 +111,68 @@ __global__ void __launch_bounds__(256) amplitude_kernel(StateView sv, const int*
 }
 
 // ---------------------------------------------------------------------------
+// Sequential conditional sampling (mps.py:206-237): per shot, left to right,
+// w_b = vec @ T_k[:, b, :], p0 = |w0|^2 / (|w0|^2 + |w1|^2) (0.5 if both
+// vanish), bit 0 iff u < p0 with the host's pre-drawn uniform u (one per qubit
+// per shot, in qubit order), vec <- w_bit (unnormalised, like the reference).
+// One CTA per shot.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) sample_kernel(StateView sv, const int* state_idx,
+                                                     const double* uniforms, unsigned char* bits) {
+  extern __shared__ __align__(16) double2 sbuf[];  // cur[cap], w0[cap], w1[cap]
+  __shared__ double red[2][8];
+  const int shot = blockIdx.x, s = state_idx[shot], n = sv.n, cap = sv.cap;
+  const int* d = sv.dimv(s);
+  double2* cur = sbuf;
+  double2* w0 = sbuf + cap;
+  double2* w1 = sbuf + 2 * cap;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) cur[0] = make_double2(1.0, 0.0);
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    const int dl = d[k], dr = d[k + 1];
+    const double2* t = sv.site(s, k);
+    const double* lam = sv.bond(s, k + 1);
+    double p0 = 0.0, p1 = 0.0;
+    for (int r = tid; r < dr; r += blockDim.x) {
+      double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+      for (int l = 0; l < dl; ++l) {
+        a0 = cfma(cur[l], t[(size_t)(2 * l) * cap + r], a0);
+        a1 = cfma(cur[l], t[(size_t)(2 * l + 1) * cap + r], a1);
+      }
+      a0 = cscale(a0, lam[r]);
+      a1 = cscale(a1, lam[r]);
+      w0[r] = a0;
+      w1[r] = a1;
+      p0 += cabs2(a0);
+      p1 += cabs2(a1);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      p0 += __shfl_xor_sync(0xffffffffu, p0, o);
+      p1 += __shfl_xor_sync(0xffffffffu, p1, o);
+    }
+    if (lane == 0) {
+      red[0][warp] = p0;
+      red[1][warp] = p1;
+    }
+    __syncthreads();
+    double t0 = 0.0, t1 = 0.0;
+    for (int i = 0; i < 8; ++i) {
+      t0 += red[0][i];
+      t1 += red[1][i];
+    }
+    const double total = t0 + t1;
+    const double pz = total > 0.0 ? t0 / total : 0.5;
+    const int bit = uniforms[(size_t)shot * n + k] < pz ? 0 : 1;
+    if (tid == 0) bits[(size_t)shot * n + k] = (unsigned char)bit;
+    const double2* src = bit ? w1 : w0;
+    for (int r = tid; r < dr; r += blockDim.x) cur[r] = src[r];
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K5: environment transfers (mps.py:196-204 reassociated into two GEMMs).
 //   prep : OT[b,s,q] = sum_t O[s,t] Gamma[b,t,q] lam[q]   (Pauli O)
 //   left : F = E_k @ OT (dl x 2dr);   E_{k+1} = T^H F  (T as (2dl x dr))
@@ -650,6 +712,20 @@ int32_t bmps_amplitudes(const double* gamma, const double* lam, const int32_t* d
   StateView sv = make_view((double*)gamma, (double*)lam, (int32_t*)dims, n, cap);
   amplitude_kernel<<<count, 256, 2 * cap * sizeof(double2), (cudaStream_t)stream>>>(
       sv, state_idx, bits, (double2*)out);
+  ++g_launches;
+  return launch_status();
+}
+
+int32_t bmps_sample(const double* gamma, const double* lam, const int32_t* dims, int32_t S,
+                    int32_t n, int32_t cap, const int32_t* state_idx, const double* uniforms,
+                    int32_t shots, uint8_t* bits, void* stream) {
+  if (shots == 0) return BMPS_OK;
+  if (shots < 0 || S < 1 || n < 1 || cap < 1) return BMPS_E_ARG;
+  StateView sv = make_view((double*)gamma, (double*)lam, (int32_t*)dims, n, cap);
+  const size_t smem = 3 * (size_t)cap * sizeof(double2);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  sample_kernel<<<shots, 256, smem, (cudaStream_t)stream>>>(sv, state_idx, uniforms, bits);
   ++g_launches;
   return launch_status();
 }

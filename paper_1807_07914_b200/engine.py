@@ -421,6 +421,31 @@ class MpsBatch:
         _native.check(rc, "bmps_amplitudes")
         return out.cpu().numpy()
 
+    def sample_bits(self, s: int, uniforms: np.ndarray) -> np.ndarray:
+        """Sampled bitstrings (uint8 [shots, n]) of state ``s`` for pre-drawn uniforms."""
+        self.check_status()
+        shots = uniforms.shape[0]
+        u = torch.from_numpy(np.ascontiguousarray(uniforms, dtype=np.float64)).to(self.device)
+        sidx = torch.full((shots,), s, dtype=torch.int32, device=self.device)
+        bits = torch.empty((shots, self.n), dtype=torch.uint8, device=self.device)
+        rc = self.lib.bmps_sample(_ptr(self.gamma), _ptr(self.lam), _ptr(self.dims), self.S, self.n,
+                                  self.cap, sidx.data_ptr(), u.data_ptr(), shots, bits.data_ptr(),
+                                  _stream())
+        _native.check(rc, "bmps_sample")
+        return bits.cpu().numpy()
+
+    def sample(self, s: int, shots: int, rng: np.random.Generator) -> dict[str, int]:
+        """Counts of full-register bitstrings (``mps.py:216-237``, same uniform stream)."""
+        if shots < 1:
+            raise ValueError("shots must be >= 1")
+        uniforms = rng.random((shots, self.n))   # one draw per qubit per shot, qubit order
+        bits = self.sample_bits(s, uniforms)
+        counts: dict[str, int] = {}
+        for row in bits:
+            key = row.tobytes().translate(bytes.maketrans(b"\x00\x01", b"01")).decode()
+            counts[key] = counts.get(key, 0) + 1
+        return counts
+
     def _transfer(self, sidx: torch.Tensor, site: torch.Tensor, codes: torch.Tensor, direction: int,
                   env_in: torch.Tensor, in_stride: int, env_out: torch.Tensor, out_stride: int,
                   count: int) -> None:

@@ -142,6 +142,9 @@ class MpsState:
         return self._batch.expectations(np.zeros(len(paulis), np.int32), list(paulis))
 
     def sample(self, shots: int, rng: np.random.Generator) -> dict[str, int]:
-        if shots < 1:
-            raise ValueError("shots must be >= 1")
-        raise NotImplementedError("GPU sampling (SURVEY §8(f) rank 1) is not implemented yet")
+        """Full-register bitstrings by sequential conditional sampling (mps.py:216-237).
+
+        One uniform variate is consumed per qubit per shot, in qubit order, so a
+        seeded generator reproduces the reference's counts.
+        """
+        return self._batch.sample(0, shots, rng)

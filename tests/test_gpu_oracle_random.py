@@ -1,0 +1,113 @@
+"""Fresh seeded inputs (not in the fixtures) vs the CPU oracle, across bond-size
+regimes: single-panel Jacobi (<= 64 columns), block Jacobi + QR preconditioning
+(> 64 columns), orientation M / M^H, cutoff / cap / absolute modes, routing."""
+
+import numpy as np
+import pytest
+
+from conftest import assert_scaled_close
+
+pytestmark = pytest.mark.gpu
+
+from oracle.mps_oracle import OracleMps, oracle_gate_matrix, oracle_run
+from paper_1807_07914_b200 import MatrixGate, MpsBatch, TruncationPolicy, mps_run
+from paper_1807_07914_b200.workloads import brick_circuit, haar_unitary, random_bitstrings, random_program
+
+RTOL = 1e-10
+
+
+def _compare(prog, n, cutoff, chi, relative=True, nbits=32, seed=0):
+    st = mps_run(prog, n, TruncationPolicy(cutoff, chi, relative))
+    ref = oracle_run(prog, n, cutoff, chi, relative)
+    assert [len(v) for v in st.bond_vectors] == ref.dims()
+    bits = random_bitstrings(n, nbits, np.random.default_rng(seed))
+    assert_scaled_close(st.amplitudes(bits), [ref.amplitude(b) for b in bits], RTOL, "amplitudes")
+    paulis = ["I" * q + "Z" + "I" * (n - q - 1) for q in range(n)]
+    paulis += ["".join("IXYZ"[int(c)] for c in np.random.default_rng(seed + 1).integers(0, 4, n)) for _ in range(4)]
+    assert_scaled_close(st.expectations_pauli(paulis), ref.expectations_env(paulis), RTOL, "expectations")
+    for x, y in zip(st.bond_vectors, ref.lams):
+        assert_scaled_close(x, y, RTOL, "lambda")
+    assert abs(st.trunc_error_sq - ref.trunc_error_sq) <= 1e-10 * max(1.0, ref.trunc_error_sq)
+    assert st.max_bond_seen == ref.max_bond_seen and st.peak_entries == ref.peak_entries
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_random_programs_with_routing(seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(5, 11))
+    _compare(random_program(n, 80, rng), n, [0.0, 1e-3, 1e-8][seed - 1], [None, 6, 16][seed - 1], seed=seed)
+
+
+def test_absolute_cutoff_mode():
+    rng = np.random.default_rng(11)
+    _compare(random_program(8, 60, rng), 8, 1e-3, None, relative=False)
+
+
+@pytest.mark.parametrize("n,depth,chi", [(14, 12, 64), (14, 14, 128)])
+def test_block_jacobi_regime(n, depth, chi):
+    # chi 64/128 at the centre -> 128/256-column Jacobi with QR preconditioning
+    prog = brick_circuit(n, depth, np.random.default_rng(n + depth))
+    _compare(prog, n, 1e-12, chi, seed=depth)
+
+
+def test_haar_two_qubit_gates_and_orientation():
+    rng = np.random.default_rng(5)
+    n = 12
+    prog = []
+    for d in range(10):
+        for a in range(d % 2, n - 1, 2):
+            prog.append(MatrixGate(haar_unitary(rng), (a, a + 1)))
+    _compare(prog, n, 1e-12, 48, seed=3)
+
+
+def test_batched_states_independent():
+    rng = np.random.default_rng(21)
+    n = 10
+    progs = [brick_circuit(n, 8, rng) for _ in range(5)]
+    b = MpsBatch(5, n, TruncationPolicy(1e-8, 16))
+    b.run(progs)
+    paulis = ["Z" + "I" * (n - 2) + "Z", "X" * n]
+    for s, p in enumerate(progs):
+        ref = oracle_run(p, n, 1e-8, 16)
+        vals = b.expectations(np.full(2, s, np.int32), paulis)
+        assert_scaled_close(vals, [ref.expectation(x) for x in paulis], RTOL)
+        np.testing.assert_array_equal(b.host_dims()[s, 1:n], ref.dims())
+
+
+def test_load_state_and_single_update_against_oracle():
+    """Per-gate drop-in call on an arbitrary (non-canonical) loaded state."""
+    rng = np.random.default_rng(8)
+    n = 6
+    ref = oracle_run(brick_circuit(n, 6, rng), n, 0.0, None)
+    st = mps_run([], n, TruncationPolicy(1e-6))
+    st._batch.load_state(0, ref.gammas, ref.lams)
+    g = haar_unitary(rng)
+    st.apply_two_qubit_adjacent(g, 2)
+    o = OracleMps(n, 1e-6, None)
+    o.gammas = [x.copy() for x in ref.gammas]
+    o.lams = [x.copy() for x in ref.lams]
+    o.apply_2q(g, 2)
+    bits = random_bitstrings(n, 20, rng)
+    assert_scaled_close(st.amplitudes(bits), [o.amplitude(b) for b in bits], RTOL)
+    assert [len(v) for v in st.bond_vectors] == o.dims()
+
+
+def test_distributed_energies_nccl_world1():
+    import os
+    import torch.distributed as dist
+    from paper_1807_07914_b200 import workloads as W
+    from paper_1807_07914_b200.distributed import vqe_energies
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        w = W.config2(batch=4)
+        pol = TruncationPolicy(w.cutoff, w.max_bond)
+        e1 = vqe_energies(w.programs, w.n, w.paulis, w.coeffs, pol, mode="by_vector")
+        e2 = vqe_energies(w.programs, w.n, w.paulis, w.coeffs, pol, mode="by_term")
+    finally:
+        dist.destroy_process_group()
+    from conftest import load_golden
+    g, _ = load_golden("cfg2")
+    assert_scaled_close(e1, g["energies"][:4], RTOL)
+    assert_scaled_close(e2, g["energies"][:4], RTOL)

@@ -143,3 +143,28 @@ def test_product_path_never_imports_oracle():
     for f in pkg.rglob("*.py"):
         text = f.read_text()
         assert "from oracle" not in text and "import oracle" not in text, f
+
+
+def test_reference_instruction_objects_are_accepted():
+    """Duck typing: programs built with the reference's own mpsqvm.ir lower identically."""
+    import sys
+    ref_src = "/root/reference/pkg/src"
+    if not Path(ref_src).exists():
+        pytest.skip("reference not mounted (GPU box)")
+    sys.path.insert(0, ref_src)
+    sys.dont_write_bytecode = True
+    try:
+        import mpsqvm
+        rng = np.random.default_rng(4)
+        ours = random_program(6, 50, rng)
+        theirs = [mpsqvm.Instruction(mpsqvm.GateKind(o.kind.value), o.qubits, o.params) for o in ours]
+        a1, s1, m1 = lower_program(ours, 6)
+        a2, s2, m2 = lower_program(theirs, 6)
+        assert a1.tolist() == a2.tolist() and s1.tolist() == s2.tolist()
+        for x, y in zip(m1, m2):
+            np.testing.assert_array_equal(x, y)
+        from mpsqvm.gates import gate_matrix as ref_gate_matrix
+        for o in theirs:
+            np.testing.assert_array_equal(gate_matrix(o), ref_gate_matrix(o))
+    finally:
+        sys.path.remove(ref_src)
