@@ -27,7 +27,7 @@ namespace bmps {
 
 template <int W2>
 struct JacCfg {
-  static constexpr int RC = 64;                 // rows per staged chunk
+  static constexpr int RC = (W2 == 32) ? 32 : 64;  // rows per staged chunk
   static constexpr int RCP = RC + 4;            // padded chunk column (bank spread)
   static constexpr int LDG = W2 + 4;            // padded Gram / Q column
   static constexpr int NBUF = (W2 == 32) ? 2 : 1;
@@ -37,7 +37,6 @@ struct JacCfg {
   static constexpr int GREM = UT - 8 * GT;      // leftover tiles, split over k
   static constexpr int GSPLIT = GREM ? 8 / GREM : 1;  // warps sharing one leftover tile
   static constexpr int AT = (RC / 8) * NT / 8;  // apply tiles per warp
-  static constexpr int RPW = AT / NT;           // apply tile rows per warp
   static constexpr int BUF = RCP * W2;          // one staging buffer (complex elements)
   static constexpr size_t kSmem = (size_t)(2 * W2 * LDG + NBUF * BUF) * sizeof(double2);
 };
@@ -178,13 +177,13 @@ BMPS_DEV void jac_gram_store(const double (&acc)[JacCfg<W2>::GT + 1][4], double2
   }
 }
 
-// acc = P_chunk (RC x W2) * Q (W2 x W2).
+// acc = P_chunk (RC x W2) * Q (W2 x W2). Warp w owns output tiles
+// t = w*AT .. w*AT+AT-1 in row-major (tile row mi = t / NT, tile col nj = t % NT).
 template <int W2>
 BMPS_DEV void jac_apply_mma(double (&acc)[JacCfg<W2>::AT][4], const double2* sP, const double2* sQ) {
   using C = JacCfg<W2>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int kr = lane & 3, rc = lane >> 2;
-  const int mi0 = warp * C::RPW;
 #pragma unroll
   for (int u = 0; u < C::AT; ++u)
 #pragma unroll
@@ -192,14 +191,12 @@ BMPS_DEV void jac_apply_mma(double (&acc)[JacCfg<W2>::AT][4], const double2* sP,
 #pragma unroll 2
   for (int k4 = 0; k4 < W2 / 4; ++k4) {
     const int k = k4 * 4 + kr;
-    double2 b[C::NT];
 #pragma unroll
-    for (int nj = 0; nj < C::NT; ++nj) b[nj] = sQ[k + (nj * 8 + rc) * C::LDG];
-#pragma unroll
-    for (int rr = 0; rr < C::RPW; ++rr) {
-      const double2 a = sP[(mi0 + rr) * 8 + rc + k * C::RCP];
-#pragma unroll
-      for (int nj = 0; nj < C::NT; ++nj) zmma(acc[rr * C::NT + nj], a, b[nj]);
+    for (int u = 0; u < C::AT; ++u) {
+      const int t = warp * C::AT + u, mi = t / C::NT, nj = t % C::NT;
+      const double2 a = sP[mi * 8 + rc + k * C::RCP];
+      const double2 b = sQ[k + (nj * 8 + rc) * C::LDG];
+      zmma(acc[u], a, b);
     }
   }
 }
@@ -209,16 +206,14 @@ BMPS_DEV void jac_apply_writeback(const double (&acc)[JacCfg<W2>::AT][4], double
   using C = JacCfg<W2>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int kr = lane & 3, rc = lane >> 2;
-  const int mi0 = warp * C::RPW;
 #pragma unroll
-  for (int rr = 0; rr < C::RPW; ++rr)
+  for (int u = 0; u < C::AT; ++u)
 #pragma unroll
-    for (int nj = 0; nj < C::NT; ++nj)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int m = (mi0 + rr) * 8 + rc, nn = nj * 8 + kr * 2 + h;
-        sP[m + nn * C::RCP] = make_double2(acc[rr * C::NT + nj][h], acc[rr * C::NT + nj][2 + h]);
-      }
+    for (int h = 0; h < 2; ++h) {
+      const int t = warp * C::AT + u, mi = t / C::NT, nj = t % C::NT;
+      const int m = mi * 8 + rc, nn = nj * 8 + kr * 2 + h;
+      sP[m + nn * C::RCP] = make_double2(acc[u][h], acc[u][2 + h]);
+    }
 }
 
 // Pairing of inner round rho: full round robin over W2 columns, or cross
@@ -397,7 +392,7 @@ BMPS_DEV void jac_load_resident(double2* sP, const double2* X, int r, int c) {
 }
 
 template <int W2>
-__global__ void __launch_bounds__(256, 2) jacobi_kernel(JacArgs args) {
+__global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_kernel(JacArgs args) {
   using C = JacCfg<W2>;
   extern __shared__ __align__(16) double2 jsm[];
   double2* sG = jsm;
