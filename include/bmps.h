@@ -96,10 +96,12 @@ size_t bmps_apply_2q_workspace_bytes(int32_t cap, int32_t nitems);
  * written to log[log_index[i]]; bookkeeping is applied by bmps_stats_replay in
  * program order. dim_bound (<= cap, 0 = cap) is an upper bound on the left /
  * right bond dims of every item, used only to size grids. mode (block
- * Jacobi for > 64 columns): 0 library default (3), 1 persistent (one CTA per
+ * Jacobi for > 64 columns): 0 library default (4), 1 persistent (one CTA per
  * item), 2 round-parallel (one launch per Jacobi round; polls convergence with
  * one stream sync per sweep), 3 one thread-block cluster per item (rounds
- * separated by cluster barriers, no host sync). */
+ * separated by cluster barriers, no host sync), 4 dynamic: one persistent
+ * wave of CTAs claims block-pair visits from any item whose round is open
+ * (no host sync, stragglers overlap other items). */
 int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int32_t n,
                       int32_t cap, const int32_t* items, const double* gates, int32_t nitems,
                       bmps_policy policy, bmps_update_record* log, const int32_t* log_index,

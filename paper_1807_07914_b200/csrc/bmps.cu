@@ -26,7 +26,7 @@ double g_tol_factor = 4.0;
 int g_max_sweeps = 60;
 int g_max_inner = 1;
 int g_qr_min_cols = 65;
-int g_jacobi_mode = 2;
+int g_jacobi_mode = 4;
 int g_cluster_size = 8;    // block-mode Jacobi: 1 persistent CTA/item, 2 round launches, 3 cluster/item   // Householder-QR preconditioning for Jacobi matrices with >= this many columns
 
 // ---------------------------------------------------------------------------
@@ -357,6 +357,10 @@ __global__ void __launch_bounds__(256) env_close_kernel(const int* dims, int n, 
   if (threadIdx.x == 0) out[it] = red[0];
 }
 
+__global__ void init_active_kernel(int* active, int nitems) {
+  if (threadIdx.x == 0) *active = nitems;
+}
+
 __global__ void item_info_kernel(const ItemMeta* meta, int nitems, int* sweeps, int* keep) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nitems) return;
@@ -374,6 +378,7 @@ struct Ws {
   double2* X;
   double2* Y;
   double2* aux;
+  JacSched* sched;
   size_t mat_stride;
   size_t aux_stride;
   int sig_stride;
@@ -402,6 +407,8 @@ size_t ws_layout(int cap, int nitems, char* base, Ws* ws) {
   const size_t aux_stride = 2048 + kQrNb * kQrNb;
   const size_t o_aux = off;
   off = align256(off + sizeof(double2) * aux_stride * nitems);
+  const size_t o_sched = off;
+  off = align256(off + sizeof(JacSched) * (size_t)nitems);
   if (ws && base) {
     ws->meta = (ItemMeta*)(base + o_meta);
     ws->sig = (double*)(base + o_sig);
@@ -411,6 +418,7 @@ size_t ws_layout(int cap, int nitems, char* base, Ws* ws) {
     ws->X = (double2*)(base + o_x);
     ws->Y = (double2*)(base + o_y);
     ws->aux = (double2*)(base + o_aux);
+    ws->sched = (JacSched*)(base + o_sched);
     ws->aux_stride = aux_stride;
     ws->mat_stride = mat_stride;
     ws->sig_stride = sig_stride;
@@ -427,6 +435,8 @@ void set_attrs() {
                        (int)JacCfg<32>::kSmem);
   cudaFuncSetAttribute(jacobi_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)JacCfg<64>::kSmem);
+  cudaFuncSetAttribute(jacobi_dynamic_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)JacCfg<32>::kSmem);
   g_attrs_set = true;
 }
 
@@ -464,7 +474,7 @@ int32_t bmps_set_param(const char* name, double value) {
   else if (k == "max_sweeps" && value >= 1) g_max_sweeps = (int)value;
   else if (k == "max_inner" && value >= 1) g_max_inner = (int)value;
   else if (k == "qr_min_cols" && value >= 1) g_qr_min_cols = (int)value;
-  else if (k == "jacobi_mode" && value >= 1 && value <= 3) g_jacobi_mode = (int)value;
+  else if (k == "jacobi_mode" && value >= 1 && value <= 4) g_jacobi_mode = (int)value;
   else if (k == "cluster_size" && value >= 1 && value <= 16) g_cluster_size = (int)value;
   else return BMPS_E_ARG;
   return BMPS_OK;
@@ -575,7 +585,10 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   ja.max_sweeps = max_sweeps;
   ja.max_inner = g_max_inner;
   ja.tol_factor = tol_factor;
-  const int explicit_mode = mode & 3;  // 0 = library default (g_jacobi_mode)
+  ja.sched = ws.sched;
+  ja.active = ws.counter;
+  ja.nitems = nitems;
+  const int explicit_mode = mode & 7;  // 0 = library default (g_jacobi_mode)
   if (cmax <= 64) {
     ja.persistent = 1;
     if (cmax <= 32)
@@ -587,7 +600,25 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   } else {
     const int nbmax = (cmax + 15) / 16 + ((cmax + 15) / 16 & 1);
     const int cl_mode = explicit_mode == 0 ? g_jacobi_mode : explicit_mode;
-    if (cl_mode == 1) {
+    if (cl_mode == 4) {
+      cudaMemsetAsync(ws.sched, 0, sizeof(JacSched) * (size_t)nitems, st);
+      init_active_kernel<<<1, 32, 0, st>>>(ws.counter, nitems);
+      ++g_launches;
+      static int n_slots = 0;
+      if (!n_slots) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_dynamic_kernel<32>, 256,
+                                                      JacCfg<32>::kSmem);
+        int dev = 0, sms = kNumSMs;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        n_slots = std::max(1, per_sm) * sms;
+      }
+      const int grid = std::min(n_slots, nitems * (nbmax / 2));
+      jacobi_dynamic_kernel<32><<<grid, 256, JacCfg<32>::kSmem, st>>>(ja);
+      ++g_launches;
+      if ((rc = launch_status())) return rc;
+    } else if (cl_mode == 1) {
       ja.persistent = 1;
       jacobi_kernel<32><<<dim3(1, nitems), 256, JacCfg<32>::kSmem, st>>>(ja);
       ++g_launches;

@@ -41,6 +41,14 @@ struct JacCfg {
   static constexpr size_t kSmem = (size_t)(2 * W2 * LDG + NBUF * BUF) * sizeof(double2);
 };
 
+// Per-item scheduling word of the dynamic (persistent, work-claiming) mode.
+struct JacSched {
+  unsigned long long ticket;  // (round << 32) | next visit index to claim
+  int done;                   // visits of the current round completed
+  int dirty;                  // any rotation in the current sweep
+  int pad[4];
+};
+
 struct JacArgs {
   ItemMeta* meta;
   double2* X;
@@ -51,6 +59,9 @@ struct JacArgs {
   int max_sweeps;
   int max_inner;
   double tol_factor;
+  JacSched* sched;   // dynamic mode
+  int* active;       // dynamic mode: items not yet converged
+  int nitems;
 };
 
 struct RotShared {
@@ -508,6 +519,140 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_kernel(JacArgs
                     rs) &&
       threadIdx.x == 0)
     atomicOr(&m->flag, 1);
+}
+
+// Dynamic mode: a persistent grid (one wave of resident CTAs) claims block-pair
+// visits from any item whose current tournament round still has unclaimed
+// visits. The CTA finishing the last visit of a round opens the next round (and
+// at the end of a sweep converges the item or clears its dirty flag). CTAs
+// never wait on each other -- when nothing is claimable they back off and
+// re-probe -- so there is no deadlock, no host polling and no per-round
+// launch, and stragglers' rounds overlap other items' work.
+template <int W2>
+__global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_dynamic_kernel(JacArgs args) {
+  using C = JacCfg<W2>;
+  extern __shared__ __align__(16) double2 jsm[];
+  double2* sG = jsm;
+  double2* sQ = sG + W2 * C::LDG;
+  double2* sP = sQ + W2 * C::LDG;
+  __shared__ RotShared rs;
+  __shared__ int s_item, s_v;
+  __shared__ unsigned s_round;
+  constexpr int w = W2 / 2;
+  const int nitems = args.nitems;
+  int cursor = blockIdx.x % nitems;
+  volatile int* active = args.active;
+  while (*active > 0) {
+    if (threadIdx.x == 0) {
+      s_item = -1;
+      for (int probe = 0; probe < nitems; ++probe) {
+        const int i = (cursor + probe) % nitems;
+        JacSched* sc = args.sched + i;
+        if (args.meta[i].conv) continue;
+        const int c = args.meta[i].c;
+        int nb = (c + w - 1) / w;
+        nb += nb & 1;
+        const unsigned nbv = (unsigned)(nb / 2);
+        const unsigned long long peek = *((volatile unsigned long long*)&sc->ticket);
+        if ((unsigned)(peek & 0xffffffffull) >= nbv) continue;
+        const unsigned long long old = atomicAdd(&sc->ticket, 1ull);
+        const unsigned v = (unsigned)(old & 0xffffffffull);
+        if (v >= nbv) continue;
+        s_item = i;
+        s_v = (int)v;
+        s_round = (unsigned)(old >> 32);
+        cursor = i;
+        break;
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    const int i = s_item;
+    if (i < 0) {
+      if (threadIdx.x == 0) __nanosleep(2000);
+      __syncthreads();
+      cursor = (cursor + 1) % nitems;
+      continue;
+    }
+    const int v = s_v;
+    const unsigned rnd = s_round;
+    ItemMeta* m = args.meta + i;
+    const int r = m->jrows, c = m->c;
+    double2* X = (m->precond ? args.Y : args.X) + (size_t)i * args.mat_stride;
+    int nb = (c + w - 1) / w;
+    nb += nb & 1;
+    const double tol = args.tol_factor * sqrt((double)r) * kEps;
+    const double noise2 = kNoiseRel * kNoiseRel * m->fro2;
+    const double fro = sqrt(m->fro2);
+    JacSched* sc = args.sched + i;
+    if (nb == 2) {
+      // single panel: the one claimer iterates the whole item to convergence
+      const bool resident = r <= C::RC;
+      if (resident) jac_load_resident<W2>(sP, X, r, c);
+      int sweep = 0;
+      bool clean = false;
+      for (; sweep < args.max_sweeps; ++sweep) {
+        if (!jac_visit<W2>(X, r, c, 0, 1, tol, noise2, fro, true, 64, resident, sG, sQ, sP, rs)) {
+          clean = true;
+          break;
+        }
+      }
+      if (resident) {
+        __syncthreads();
+        jac_store_chunk<W2>(sP, X, r, c, 0, 0, 1);
+      }
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        m->sweeps = sweep;
+        if (!clean) m->status = BMPS_S_SVD_FAILED;
+        __threadfence();
+        m->conv = 1;
+        atomicSub(args.active, 1);
+      }
+      __syncthreads();
+      continue;
+    }
+    const int rounds = nb - 1;
+    const int sweep = (int)(rnd / (unsigned)rounds), rho = (int)(rnd % (unsigned)rounds);
+    int I, J;
+    tourney_pair(nb, rho, v, I, J);
+    const bool dirty = jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, rho == 0, args.max_inner,
+                                     false, sG, sQ, sP, rs);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (dirty) atomicOr(&sc->dirty, 1);
+      __threadfence();
+      const int d = atomicAdd(&sc->done, 1);
+      if (d == nb / 2 - 1) {
+        // last visit of the round: open the next round (or finish the item)
+        sc->done = 0;
+        bool finished = false;
+        if (rho == rounds - 1) {
+          const int dsw = atomicAdd(&sc->dirty, 0);
+          if (!dsw) {
+            m->sweeps = sweep;
+            finished = true;
+          } else if (sweep + 1 >= args.max_sweeps) {
+            m->sweeps = sweep + 1;
+            m->status = BMPS_S_SVD_FAILED;
+            finished = true;
+          } else {
+            sc->dirty = 0;
+          }
+        }
+        __threadfence();
+        if (finished) {
+          m->conv = 1;
+          atomicSub(args.active, 1);
+        } else {
+          atomicExch(&sc->ticket, (unsigned long long)(rnd + 1) << 32);
+        }
+      }
+    }
+    __syncthreads();
+  }
 }
 
 }  // namespace bmps
