@@ -27,7 +27,8 @@ int g_max_sweeps = 60;
 int g_max_inner = 1;
 int g_qr_min_cols = 65;
 int g_jacobi_mode = 4;
-int g_cluster_size = 8;    // block-mode Jacobi: 1 persistent CTA/item, 2 round launches, 3 cluster/item   // Householder-QR preconditioning for Jacobi matrices with >= this many columns
+int g_cluster_size = 8;
+int g_tma_staging = 0;    // 1: Jacobi panels staged by TMA bulk copies instead of cp.async    // block-mode Jacobi: 1 persistent CTA/item, 2 round launches, 3 cluster/item   // Householder-QR preconditioning for Jacobi matrices with >= this many columns
 
 // ---------------------------------------------------------------------------
 // init: product state |0...0> (mps.py:55-66)
@@ -476,6 +477,7 @@ int32_t bmps_set_param(const char* name, double value) {
   else if (k == "qr_min_cols" && value >= 1) g_qr_min_cols = (int)value;
   else if (k == "jacobi_mode" && value >= 1 && value <= 4) g_jacobi_mode = (int)value;
   else if (k == "cluster_size" && value >= 1 && value <= 16) g_cluster_size = (int)value;
+  else if (k == "tma_staging" && (value == 0 || value == 1)) g_tma_staging = (int)value;
   else return BMPS_E_ARG;
   return BMPS_OK;
 }
@@ -588,6 +590,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   ja.sched = ws.sched;
   ja.active = ws.counter;
   ja.nitems = nitems;
+  ja.tma = g_tma_staging;
   const int explicit_mode = mode & 7;  // 0 = library default (g_jacobi_mode)
   if (cmax <= 64) {
     ja.persistent = 1;

@@ -62,6 +62,7 @@ struct JacArgs {
   JacSched* sched;   // dynamic mode
   int* active;       // dynamic mode: items not yet converged
   int nitems;
+  int tma;           // stage panels with TMA bulk copies (else cp.async)
 };
 
 struct RotShared {
@@ -79,6 +80,56 @@ BMPS_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 BMPS_DEV void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// ---- TMA bulk copies (cp.async.bulk) with mbarrier completion -------------
+BMPS_DEV unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+BMPS_DEV void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+BMPS_DEV void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+BMPS_DEV void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred P;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      " @!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+BMPS_DEV void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+BMPS_DEV void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+BMPS_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+BMPS_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+BMPS_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+BMPS_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// Staging state of a CTA: one mbarrier per chunk buffer and its phase bits.
+struct JacStage {
+  unsigned long long* bar;  // [2] in shared memory
+  unsigned phase;           // bit b = parity to wait for on buffer b
+};
+
+BMPS_DEV void stage_init(unsigned long long* bar) {
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
 }
 
 template <int W2>
@@ -108,6 +159,66 @@ BMPS_DEV void jac_store_chunk(const double2* buf, double2* X, int r, int c, int 
     const int row = row0 + m, col = panel_col<W2>(p, I, J);
     if (row < r && col < c) X[(size_t)row + (size_t)col * r] = buf[m + p * C::RCP];
   }
+}
+
+// TMA version of the chunk load (all threads call): rows beyond r and columns
+// beyond c are zero-filled with ordinary stores; warp 0 arms the buffer's
+// mbarrier and issues one bulk copy per valid panel column (rows are
+// contiguous in the column-major matrix).
+template <int W2>
+BMPS_DEV void jac_issue_bulk(double2* buf, JacStage& st, int b, const double2* X, int r, int c,
+                             int row0, int I, int J) {
+  using C = JacCfg<W2>;
+  const int nv = min(C::RC, r - row0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (nv < C::RC || panel_col<W2>(W2 - 1, I, J) >= c) {
+    for (int idx = threadIdx.x; idx < C::RC * W2; idx += blockDim.x) {
+      const int m = idx % C::RC, p = idx / C::RC;
+      if (m >= nv || panel_col<W2>(p, I, J) >= c) buf[m + p * C::RCP] = make_double2(0.0, 0.0);
+    }
+  }
+  if (warp == 0) {
+    bulk_wait_read0();  // an earlier bulk store out of this buffer must have read it
+    fence_proxy_async();
+    int nvalid = 0;
+    for (int p = 0; p < W2; ++p) nvalid += panel_col<W2>(p, I, J) < c ? 1 : 0;
+    if (lane == 0) mbar_expect_tx(st.bar + b, (unsigned)(nvalid * nv * 16));
+    __syncwarp();
+    for (int p = lane; p < W2; p += 32) {
+      const int col = panel_col<W2>(p, I, J);
+      if (col < c) bulk_g2s(buf + p * C::RCP, X + (size_t)row0 + (size_t)col * r, (unsigned)(nv * 16), st.bar + b);
+    }
+  }
+}
+
+BMPS_DEV void jac_wait_bulk(JacStage& st, int b) {
+  mbar_wait(st.bar + b, (st.phase >> b) & 1u);
+  st.phase ^= 1u << b;
+}
+
+// TMA version of the chunk store: the buffer was written with ordinary stores
+// (caller synchronised); warp 0 issues one bulk copy per valid column.
+template <int W2>
+BMPS_DEV void jac_store_bulk(const double2* buf, double2* X, int r, int c, int row0, int I, int J) {
+  using C = JacCfg<W2>;
+  const int nv = min(C::RC, r - row0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    fence_proxy_async();
+    for (int p = lane; p < W2; p += 32) {
+      const int col = panel_col<W2>(p, I, J);
+      if (col < c) bulk_s2g(X + (size_t)row0 + (size_t)col * r, buf + p * C::RCP, (unsigned)(nv * 16));
+    }
+    bulk_commit();
+  }
+}
+
+// Make every bulk store of this CTA complete and visible (before other CTAs
+// or later kernels read the matrix).
+BMPS_DEV void jac_flush_bulk() {
+  if ((threadIdx.x >> 5) == 0) bulk_wait0();
+  __syncthreads();
+  __threadfence();
 }
 
 // Upper-triangle Gram tile t -> (ti, tj), ti <= tj.
@@ -322,14 +433,15 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
 
 // One block-pair visit; returns true if any rotation was applied. If
 // `resident`, the whole panel (r <= RC) already sits in buffer 0 and is
-// neither loaded nor stored here.
+// neither loaded nor stored here. W2 = 32 streams the panel with TMA bulk
+// copies (double buffered, mbarrier completion); W2 = 64 with cp.async.
 template <int W2>
 BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, double noise2,
                         double fro, bool full, int max_inner, bool resident, double2* sG,
-                        double2* sQ, double2* sP, RotShared& rs) {
+                        double2* sQ, double2* sP, RotShared& rs, JacStage& st, bool tma) {
   using C = JacCfg<W2>;
-  const int tid = threadIdx.x;
   const int nch = (r + C::RC - 1) / C::RC;
+  const bool bulk = (W2 == 32) && !resident && tma;
   double gacc[C::GT + 1][4];
 #pragma unroll
   for (int u = 0; u < C::GT + 1; ++u)
@@ -337,6 +449,17 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
     for (int q = 0; q < 4; ++q) gacc[u][q] = 0.0;
   if (resident) {
     jac_gram_chunk<W2>(gacc, sP, r);
+  } else if (bulk) {
+    __syncthreads();
+    jac_issue_bulk<W2>(sP, st, 0, X, r, c, 0, I, J);
+    for (int k = 0; k < nch; ++k) {
+      const int b = k & 1;
+      if (k + 1 < nch) jac_issue_bulk<W2>(sP + (b ^ 1) * C::BUF, st, b ^ 1, X, r, c, (k + 1) * C::RC, I, J);
+      jac_wait_bulk(st, b);
+      __syncthreads();
+      jac_gram_chunk<W2>(gacc, sP + b * C::BUF, min(C::RC, r - k * C::RC));
+      __syncthreads();
+    }
   } else {
     __syncthreads();
     jac_issue_chunk<W2>(sP, X, r, c, 0, I, J);
@@ -358,10 +481,16 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
   __syncthreads();
   const bool staged = nch == 1;  // single chunk still in buffer 0 from the Gram pass
   // prefetch the first apply chunk so its load overlaps the inner sweep
-  if (!resident && !staged) jac_issue_chunk<W2>(sP, X, r, c, 0, I, J);
+  if (!resident && !staged) {
+    if (bulk) jac_issue_bulk<W2>(sP, st, 0, X, r, c, 0, I, J);
+    else jac_issue_chunk<W2>(sP, X, r, c, 0, I, J);
+  }
   const int nrot = jac_inner<W2>(sG, sQ, rs, tol, noise2, fro, full, max_inner);
   if (nrot == 0) {
-    if (!resident && !staged) cp_async_wait<0>();
+    if (!resident && !staged) {
+      if (bulk) jac_wait_bulk(st, 0);
+      else cp_async_wait<0>();
+    }
     return false;
   }
   double aacc[C::AT][4];
@@ -372,7 +501,31 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
     __syncthreads();
     return true;
   }
-  // re-stream the panel: load chunk k+1 while chunk k is multiplied and stored
+  if (bulk) {
+    for (int k = 0; k < nch; ++k) {
+      const int b = k & 1;
+      double2* cur = sP + b * C::BUF;
+      if (!staged && k + 1 < nch) {
+        const int row1 = (k + 1) * C::RC;
+        if (r - row1 < C::RC || panel_col<W2>(W2 - 1, I, J) >= c) {
+          // the issue zero-fills: the bulk store out of that buffer must be done reading
+          if ((threadIdx.x >> 5) == 0) bulk_wait_read0();
+          __syncthreads();
+        }
+        jac_issue_bulk<W2>(sP + (b ^ 1) * C::BUF, st, b ^ 1, X, r, c, row1, I, J);
+      }
+      if (!staged) jac_wait_bulk(st, b);
+      __syncthreads();
+      jac_apply_mma<W2>(aacc, cur, sQ);
+      __syncthreads();
+      jac_apply_writeback<W2>(aacc, cur);
+      __syncthreads();
+      jac_store_bulk<W2>(cur, X, r, c, k * C::RC, I, J);
+    }
+    jac_flush_bulk();
+    return true;
+  }
+  // cp.async re-stream: load chunk k+1 while chunk k is multiplied and stored
   for (int k = 0; k < nch; ++k) {
     double2* cur = sP + (k % C::NBUF) * C::BUF;
     if (!staged) {
@@ -410,9 +563,12 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_kernel(JacArgs
   double2* sQ = sG + W2 * C::LDG;
   double2* sP = sQ + W2 * C::LDG;
   __shared__ RotShared rs;
+  __shared__ unsigned long long jbar[2];
   const int item = blockIdx.y;
   ItemMeta* m = args.meta + item;
   if (m->conv) return;
+  JacStage st{jbar, 0u};
+  stage_init(jbar);
   const int r = m->jrows, c = m->c;
   double2* X = (m->precond ? args.Y : args.X) + (size_t)item * args.mat_stride;
   constexpr int w = W2 / 2;
@@ -429,7 +585,7 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_kernel(JacArgs
     int sweep = 0;
     bool clean = false;
     for (; sweep < args.max_sweeps; ++sweep) {
-      if (!jac_visit<W2>(X, r, c, 0, 1, tol, noise2, fro, true, 64, resident, sG, sQ, sP, rs)) {
+      if (!jac_visit<W2>(X, r, c, 0, 1, tol, noise2, fro, true, 64, resident, sG, sQ, sP, rs, st, args.tma)) {
         clean = true;
         break;
       }
@@ -464,7 +620,7 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_kernel(JacArgs
           int I, J;
           tourney_pair(nb, rho, v, I, J);
           any |= jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, rho == 0, args.max_inner, false, sG,
-                               sQ, sP, rs);
+                               sQ, sP, rs, st, args.tma);
         }
         __threadfence();
         cl.sync();
@@ -497,7 +653,7 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_kernel(JacArgs
           int I, J;
           tourney_pair(nb, rho, v, I, J);
           any |= jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, rho == 0, args.max_inner, false, sG,
-                               sQ, sP, rs);
+                               sQ, sP, rs, st, args.tma);
         }
       if (!any) {
         clean = true;
@@ -516,7 +672,7 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_kernel(JacArgs
   int I, J;
   tourney_pair(nb, rho, v, I, J);
   if (jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, rho == 0, args.max_inner, false, sG, sQ, sP,
-                    rs) &&
+                    rs, st, args.tma) &&
       threadIdx.x == 0)
     atomicOr(&m->flag, 1);
 }
@@ -538,6 +694,9 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_dynamic_kernel
   __shared__ RotShared rs;
   __shared__ int s_item, s_v;
   __shared__ unsigned s_round;
+  __shared__ unsigned long long jbar[2];
+  JacStage st{jbar, 0u};
+  stage_init(jbar);
   constexpr int w = W2 / 2;
   const int nitems = args.nitems;
   int cursor = blockIdx.x % nitems;
@@ -592,7 +751,7 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_dynamic_kernel
       int sweep = 0;
       bool clean = false;
       for (; sweep < args.max_sweeps; ++sweep) {
-        if (!jac_visit<W2>(X, r, c, 0, 1, tol, noise2, fro, true, 64, resident, sG, sQ, sP, rs)) {
+        if (!jac_visit<W2>(X, r, c, 0, 1, tol, noise2, fro, true, 64, resident, sG, sQ, sP, rs, st, args.tma)) {
           clean = true;
           break;
         }
@@ -618,7 +777,7 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_dynamic_kernel
     int I, J;
     tourney_pair(nb, rho, v, I, J);
     const bool dirty = jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, rho == 0, args.max_inner,
-                                     false, sG, sQ, sP, rs);
+                                     false, sG, sQ, sP, rs, st, args.tma);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {

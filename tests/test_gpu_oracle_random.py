@@ -111,3 +111,28 @@ def test_distributed_energies_nccl_world1():
     g, _ = load_golden("cfg2")
     assert_scaled_close(e1, g["energies"][:4], RTOL)
     assert_scaled_close(e2, g["energies"][:4], RTOL)
+
+
+def test_tma_staging_path_matches_oracle():
+    """The TMA bulk-copy panel staging (bmps_set_param tma_staging=1) gives the same results."""
+    from paper_1807_07914_b200 import _native
+    lib = _native.load()
+    assert lib.bmps_set_param(b"tma_staging", 1.0) == 0
+    try:
+        prog = brick_circuit(14, 12, np.random.default_rng(99))
+        _compare(prog, 14, 1e-12, 64, seed=4)
+    finally:
+        lib.bmps_set_param(b"tma_staging", 0.0)
+
+
+@pytest.mark.parametrize("mode", [1, 2, 3, 4])
+def test_all_jacobi_schedules_match_oracle(mode):
+    """persistent / round launches / cluster / dynamic schedules are interchangeable."""
+    from paper_1807_07914_b200 import _native
+    lib = _native.load()
+    assert lib.bmps_set_param(b"jacobi_mode", float(mode)) == 0
+    try:
+        prog = brick_circuit(12, 12, np.random.default_rng(7 + mode))
+        _compare(prog, 12, 1e-10, 48, seed=mode)
+    finally:
+        lib.bmps_set_param(b"jacobi_mode", 4.0)
