@@ -192,7 +192,8 @@ class MpsBatch:
     """S independent n-qubit MPS states resident in HBM, initially |0...0>."""
 
     def __init__(self, num_states: int, n: int, policy: TruncationPolicy | None = None,
-                 device=None, cap: int | None = None, max_items_per_launch: int = 4096):
+                 device=None, cap: int | None = None, max_items_per_launch: int = 4096,
+                 workspace_budget: int = 24 << 30):
         if n < 1:
             raise ValueError("need at least one qubit")
         if num_states < 1:
@@ -203,6 +204,7 @@ class MpsBatch:
         self.n = int(n)
         self.policy = policy or TruncationPolicy()
         self.max_items = int(max_items_per_launch)
+        self.workspace_budget = int(workspace_budget)
         self.cap = 1
         self._alloc(int(cap) if cap else 1)
         self.dim_ub = np.ones((self.S, self.n + 1), dtype=np.int64)
@@ -306,8 +308,10 @@ class MpsBatch:
             bound = int(max(ub[s_idx, q].max(), ub[s_idx, q + 2].max()))
             new = np.minimum(np.minimum(2 * ub[s_idx, q], 2 * ub[s_idx, q + 2]), lim)
             self.ensure_capacity(int(max(bound, new.max())))
-            for c0 in range(a, b, self.max_items):
-                c1 = min(b, c0 + self.max_items)
+            per_item = int(self.lib.bmps_apply_2q_workspace_bytes(self.cap, 1))
+            chunk = max(1, min(self.max_items, self.workspace_budget // max(per_item, 1)))
+            for c0 in range(a, b, chunk):
+                c1 = min(b, c0 + chunk)
                 ws, wsb = self._workspace(c1 - c0)
                 rc = self.lib.bmps_apply_2q(
                     _ptr(self.gamma), _ptr(self.lam), _ptr(self.dims), self.S, self.n, self.cap,
