@@ -139,14 +139,27 @@ BMPS_DEV int panel_col(int p, int I, int J) {
 }
 
 // Asynchronous (cp.async, zero-filled) load of rows [row0, row0+RC) of the panel.
+// With RC = W2 = 32 and 256 threads each thread owns row `lane` of panel columns
+// warp, warp+8, warp+16, warp+24 (a warp moves one 512-byte column segment).
 template <int W2>
 BMPS_DEV void jac_issue_chunk(double2* buf, const double2* X, int r, int c, int row0, int I, int J) {
   using C = JacCfg<W2>;
-  for (int idx = threadIdx.x; idx < C::RC * W2; idx += blockDim.x) {
-    const int m = idx % C::RC, p = idx / C::RC;
-    const int row = row0 + m, col = panel_col<W2>(p, I, J);
-    const bool ok = row < r && col < c;
-    cp_async16(buf + m + p * C::RCP, ok ? X + (size_t)row + (size_t)col * r : X, ok);
+  if (C::RC == 32 && W2 == 32) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int row = row0 + lane;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int p = warp + 8 * u, col = panel_col<W2>(p, I, J);
+      const bool ok = row < r && col < c;
+      cp_async16(buf + lane + p * C::RCP, ok ? X + (size_t)row + (size_t)col * r : X, ok);
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < C::RC * W2; idx += blockDim.x) {
+      const int m = idx % C::RC, p = idx / C::RC;
+      const int row = row0 + m, col = panel_col<W2>(p, I, J);
+      const bool ok = row < r && col < c;
+      cp_async16(buf + m + p * C::RCP, ok ? X + (size_t)row + (size_t)col * r : X, ok);
+    }
   }
   cp_async_commit();
 }
@@ -154,10 +167,22 @@ BMPS_DEV void jac_issue_chunk(double2* buf, const double2* X, int r, int c, int 
 template <int W2>
 BMPS_DEV void jac_store_chunk(const double2* buf, double2* X, int r, int c, int row0, int I, int J) {
   using C = JacCfg<W2>;
-  for (int idx = threadIdx.x; idx < C::RC * W2; idx += blockDim.x) {
-    const int m = idx % C::RC, p = idx / C::RC;
-    const int row = row0 + m, col = panel_col<W2>(p, I, J);
-    if (row < r && col < c) X[(size_t)row + (size_t)col * r] = buf[m + p * C::RCP];
+  if (C::RC == 32 && W2 == 32) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int row = row0 + lane;
+    if (row < r) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int p = warp + 8 * u, col = panel_col<W2>(p, I, J);
+        if (col < c) X[(size_t)row + (size_t)col * r] = buf[lane + p * C::RCP];
+      }
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < C::RC * W2; idx += blockDim.x) {
+      const int m = idx % C::RC, p = idx / C::RC;
+      const int row = row0 + m, col = panel_col<W2>(p, I, J);
+      if (row < r && col < c) X[(size_t)row + (size_t)col * r] = buf[m + p * C::RCP];
+    }
   }
 }
 
