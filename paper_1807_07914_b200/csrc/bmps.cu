@@ -28,7 +28,8 @@ int g_max_inner = 1;
 int g_qr_min_cols = 65;
 int g_jacobi_mode = 4;
 int g_cluster_size = 8;
-int g_tma_staging = 0;    // 1: Jacobi panels staged by TMA bulk copies instead of cp.async    // block-mode Jacobi: 1 persistent CTA/item, 2 round launches, 3 cluster/item   // Householder-QR preconditioning for Jacobi matrices with >= this many columns
+int g_tma_staging = 0;
+int g_gram_cache = 1;     // cross visits reuse rotated intra-block Grams    // 1: Jacobi panels staged by TMA bulk copies instead of cp.async    // block-mode Jacobi: 1 persistent CTA/item, 2 round launches, 3 cluster/item   // Householder-QR preconditioning for Jacobi matrices with >= this many columns
 
 // ---------------------------------------------------------------------------
 // init: product state |0...0> (mps.py:55-66)
@@ -380,6 +381,8 @@ struct Ws {
   double2* Y;
   double2* aux;
   JacSched* sched;
+  double2* gcache;
+  size_t gcache_stride;
   size_t mat_stride;
   size_t aux_stride;
   int sig_stride;
@@ -410,6 +413,9 @@ size_t ws_layout(int cap, int nitems, char* base, Ws* ws) {
   off = align256(off + sizeof(double2) * aux_stride * nitems);
   const size_t o_sched = off;
   off = align256(off + sizeof(JacSched) * (size_t)nitems);
+  const size_t gcache_stride = (size_t)((2 * cap + 15) / 16 + 1) * 256;
+  const size_t o_gc = off;
+  off = align256(off + sizeof(double2) * gcache_stride * nitems);
   if (ws && base) {
     ws->meta = (ItemMeta*)(base + o_meta);
     ws->sig = (double*)(base + o_sig);
@@ -420,6 +426,8 @@ size_t ws_layout(int cap, int nitems, char* base, Ws* ws) {
     ws->Y = (double2*)(base + o_y);
     ws->aux = (double2*)(base + o_aux);
     ws->sched = (JacSched*)(base + o_sched);
+    ws->gcache = (double2*)(base + o_gc);
+    ws->gcache_stride = gcache_stride;
     ws->aux_stride = aux_stride;
     ws->mat_stride = mat_stride;
     ws->sig_stride = sig_stride;
@@ -478,6 +486,7 @@ int32_t bmps_set_param(const char* name, double value) {
   else if (k == "jacobi_mode" && value >= 1 && value <= 4) g_jacobi_mode = (int)value;
   else if (k == "cluster_size" && value >= 1 && value <= 16) g_cluster_size = (int)value;
   else if (k == "tma_staging" && (value == 0 || value == 1)) g_tma_staging = (int)value;
+  else if (k == "gram_cache" && (value == 0 || value == 1)) g_gram_cache = (int)value;
   else return BMPS_E_ARG;
   return BMPS_OK;
 }
@@ -591,6 +600,8 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   ja.active = ws.counter;
   ja.nitems = nitems;
   ja.tma = g_tma_staging;
+  ja.gcache = g_gram_cache ? ws.gcache : nullptr;
+  ja.gcache_stride = ws.gcache_stride;
   const int explicit_mode = mode & 7;  // 0 = library default (g_jacobi_mode)
   if (cmax <= 64) {
     ja.persistent = 1;

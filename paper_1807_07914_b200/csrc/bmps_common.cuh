@@ -93,6 +93,14 @@ BMPS_DEV bool pair_needs_rotation(double a, double b, double2 g, double tol, dou
   return hypot(g.x, g.y) > tol * sqrt(lo) * fro;
 }
 
+// Same test as jacobi_rotation's early exits (no rotation math).
+BMPS_DEV bool jacobi_needs(double a, double b, double2 g, double tol, double noise2, double fro) {
+  const double lo = fmin(a, b), hi = fmax(a, b);
+  if (!(hi > noise2) || !(lo > kNegligible * hi)) return false;
+  const double thr = tol * fro;
+  return cabs2(g) > thr * thr * lo;
+}
+
 BMPS_DEV bool jacobi_rotation(double a, double b, double2 g, double tol, double noise2, double fro,
                               double& c, double& s, double2& e) {
   const double lo = fmin(a, b), hi = fmax(a, b);

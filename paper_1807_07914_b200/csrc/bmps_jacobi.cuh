@@ -63,6 +63,8 @@ struct JacArgs {
   int* active;       // dynamic mode: items not yet converged
   int nitems;
   int tma;           // stage panels with TMA bulk copies (else cp.async)
+  double2* gcache;   // per item: rotated 16x16 intra-block Grams (nullptr: off)
+  size_t gcache_stride;
 };
 
 struct RotShared {
@@ -324,6 +326,61 @@ BMPS_DEV void jac_gram_store(const double (&acc)[JacCfg<W2>::GT + 1][4], double2
   }
 }
 
+// Cross-block Gram only (G_IJ, 16x16 = 2x2 tiles of 8x8; W2 = 32): warp w
+// accumulates tile w/2 over half of the chunk's k range (acc[0]).
+template <int W2>
+BMPS_DEV void jac_gram_chunk_cross(double (&acc)[JacCfg<W2>::GT + 1][4], const double2* sP,
+                                   int nrows) {
+  using C = JacCfg<W2>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int kr = lane & 3, rc = lane >> 2;
+  const int nk4 = (nrows + 3) >> 2;
+  const int t = warp >> 1, part = warp & 1;
+  const int ti = t >> 1, tj = 2 + (t & 1);
+  const int k0 = part * nk4 / 2, k1 = (part + 1) * nk4 / 2;
+  for (int k4 = k0; k4 < k1; ++k4) {
+    const int k = k4 * 4 + kr;
+    zmma(acc[0], cconj(sP[k + (ti * 8 + rc) * C::RCP]), sP[k + (tj * 8 + rc) * C::RCP]);
+  }
+}
+
+// sG <- [[cache_I, G_IJ], [G_IJ^H, cache_J]] (scratch: 8 warps x 64 partials).
+template <int W2>
+BMPS_DEV void jac_gram_store_cross(const double (&acc)[JacCfg<W2>::GT + 1][4], double2* sG,
+                                   double2* scratch, const double2* cI, const double2* cJ) {
+  using C = JacCfg<W2>;
+  constexpr int w = W2 / 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rr = lane >> 2, cc = (lane & 3) * 2;
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    scratch[warp * 64 + rr * 8 + cc + h] = make_double2(acc[0][h], acc[0][2 + h]);
+  for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
+    const int i = idx % w, j = idx / w;
+    sG[i + j * C::LDG] = cI[i + j * w];
+    sG[(w + i) + (w + j) * C::LDG] = cJ[i + j * w];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < 4 * 64; idx += blockDim.x) {
+    const int t = idx / 64, e = idx % 64;
+    const double2 v = cadd(scratch[(2 * t) * 64 + e], scratch[(2 * t + 1) * 64 + e]);
+    const int i = (t >> 1) * 8 + e / 8, j = w + (t & 1) * 8 + e % 8;
+    sG[i + j * C::LDG] = v;
+    sG[j + i * C::LDG] = cconj(v);
+  }
+}
+
+template <int W2>
+BMPS_DEV void jac_cache_store(const double2* sG, double2* cI, double2* cJ) {
+  using C = JacCfg<W2>;
+  constexpr int w = W2 / 2;
+  for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
+    const int i = idx % w, j = idx / w;
+    cI[i + j * w] = sG[i + j * C::LDG];
+    cJ[i + j * w] = sG[(w + i) + (w + j) * C::LDG];
+  }
+}
+
 // acc = P_chunk (RC x W2) * Q (W2 x W2). Warp w owns output tiles
 // t = w*AT .. w*AT+AT-1 in row-major (tile row mi = t / NT, tile col nj = t % NT).
 template <int W2>
@@ -463,10 +520,15 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
 template <int W2>
 BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, double noise2,
                         double fro, bool full, int max_inner, bool resident, double2* sG,
-                        double2* sQ, double2* sP, RotShared& rs, JacStage& st, bool tma) {
+                        double2* sQ, double2* sP, RotShared& rs, JacStage& st, bool tma,
+                        double2* gcache = nullptr) {
   using C = JacCfg<W2>;
   const int nch = (r + C::RC - 1) / C::RC;
   const bool bulk = (W2 == 32) && !resident && tma;
+  // cross visits reuse the rotated intra-block Grams cached by earlier visits
+  const bool cross_gram = (W2 == 32) && gcache != nullptr && !full && !resident;
+  double2* cI = gcache ? gcache + (size_t)I * (W2 / 2) * (W2 / 2) : nullptr;
+  double2* cJ = gcache ? gcache + (size_t)J * (W2 / 2) * (W2 / 2) : nullptr;
   double gacc[C::GT + 1][4];
 #pragma unroll
   for (int u = 0; u < C::GT + 1; ++u)
@@ -482,7 +544,8 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
       if (k + 1 < nch) jac_issue_bulk<W2>(sP + (b ^ 1) * C::BUF, st, b ^ 1, X, r, c, (k + 1) * C::RC, I, J);
       jac_wait_bulk(st, b);
       __syncthreads();
-      jac_gram_chunk<W2>(gacc, sP + b * C::BUF, min(C::RC, r - k * C::RC));
+      if (cross_gram) jac_gram_chunk_cross<W2>(gacc, sP + b * C::BUF, min(C::RC, r - k * C::RC));
+      else jac_gram_chunk<W2>(gacc, sP + b * C::BUF, min(C::RC, r - k * C::RC));
       __syncthreads();
     }
   } else {
@@ -497,12 +560,14 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
         cp_async_wait<0>();
       }
       __syncthreads();
-      jac_gram_chunk<W2>(gacc, cur, min(C::RC, r - k * C::RC));
+      if (cross_gram) jac_gram_chunk_cross<W2>(gacc, cur, min(C::RC, r - k * C::RC));
+      else jac_gram_chunk<W2>(gacc, cur, min(C::RC, r - k * C::RC));
       __syncthreads();
       if (C::NBUF == 1 && k + 1 < nch) jac_issue_chunk<W2>(sP, X, r, c, (k + 1) * C::RC, I, J);
     }
   }
-  jac_gram_store<W2>(gacc, sG, sQ);
+  if (cross_gram) jac_gram_store_cross<W2>(gacc, sG, sQ, cI, cJ);
+  else jac_gram_store<W2>(gacc, sG, sQ);
   __syncthreads();
   const bool staged = nch == 1;  // single chunk still in buffer 0 from the Gram pass
   // prefetch the first apply chunk so its load overlaps the inner sweep
@@ -510,7 +575,28 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
     if (bulk) jac_issue_bulk<W2>(sP, st, 0, X, r, c, 0, I, J);
     else jac_issue_chunk<W2>(sP, X, r, c, 0, I, J);
   }
-  const int nrot = jac_inner<W2>(sG, sQ, rs, tol, noise2, fro, full, max_inner);
+  // fast path: one parallel test of every pair the inner sweep would visit
+  int need = 0;
+  {
+    constexpr int w = W2 / 2;
+    const int npairs = full ? W2 * W2 : w * w;
+    for (int idx = threadIdx.x; idx < npairs && !need; idx += blockDim.x) {
+      int i, j;
+      if (full) {
+        i = idx % W2;
+        j = idx / W2;
+        if (i >= j) continue;
+      } else {
+        i = idx % w;
+        j = w + idx / w;
+      }
+      need = jacobi_needs(sG[i + i * C::LDG].x, sG[j + j * C::LDG].x, sG[i + j * C::LDG], tol,
+                          noise2, fro);
+    }
+  }
+  const int nrot = __syncthreads_or(need) ? jac_inner<W2>(sG, sQ, rs, tol, noise2, fro, full, max_inner)
+                                          : 0;
+  if (gcache != nullptr && !resident && (full || nrot > 0)) jac_cache_store<W2>(sG, cI, cJ);
   if (nrot == 0) {
     if (!resident && !staged) {
       if (bulk) jac_wait_bulk(st, 0);
@@ -596,6 +682,7 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_kernel(JacArgs
   stage_init(jbar);
   const int r = m->jrows, c = m->c;
   double2* X = (m->precond ? args.Y : args.X) + (size_t)item * args.mat_stride;
+  double2* gc = args.gcache ? args.gcache + (size_t)item * args.gcache_stride : nullptr;
   constexpr int w = W2 / 2;
   int nb = (c + w - 1) / w;
   nb += nb & 1;
@@ -645,7 +732,7 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_kernel(JacArgs
           int I, J;
           tourney_pair(nb, rho, v, I, J);
           any |= jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, rho == 0, args.max_inner, false, sG,
-                               sQ, sP, rs, st, args.tma);
+                               sQ, sP, rs, st, args.tma, gc);
         }
         __threadfence();
         cl.sync();
@@ -678,7 +765,7 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_kernel(JacArgs
           int I, J;
           tourney_pair(nb, rho, v, I, J);
           any |= jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, rho == 0, args.max_inner, false, sG,
-                               sQ, sP, rs, st, args.tma);
+                               sQ, sP, rs, st, args.tma, gc);
         }
       if (!any) {
         clean = true;
@@ -697,7 +784,7 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_kernel(JacArgs
   int I, J;
   tourney_pair(nb, rho, v, I, J);
   if (jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, rho == 0, args.max_inner, false, sG, sQ, sP,
-                    rs, st, args.tma) &&
+                    rs, st, args.tma, gc) &&
       threadIdx.x == 0)
     atomicOr(&m->flag, 1);
 }
@@ -801,8 +888,9 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_dynamic_kernel
     const int sweep = (int)(rnd / (unsigned)rounds), rho = (int)(rnd % (unsigned)rounds);
     int I, J;
     tourney_pair(nb, rho, v, I, J);
+    double2* gc = args.gcache ? args.gcache + (size_t)i * args.gcache_stride : nullptr;
     const bool dirty = jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, rho == 0, args.max_inner,
-                                     false, sG, sQ, sP, rs, st, args.tma);
+                                     false, sG, sQ, sP, rs, st, args.tma, gc);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
