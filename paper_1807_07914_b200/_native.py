@@ -69,6 +69,11 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
+    # optional tunables, e.g. BMPS_PARAMS="block_w2=64,tol_factor=4"
+    for kv in filter(None, os.environ.get("BMPS_PARAMS", "").split(",")):
+        k, v = kv.split("=")
+        if lib.bmps_set_param(k.strip().encode(), float(v)) != 0:
+            raise ValueError(f"bad BMPS_PARAMS entry {kv!r}")
     if path is None:
         _lib = lib
     return lib

@@ -29,7 +29,8 @@ int g_qr_min_cols = 65;
 int g_jacobi_mode = 4;
 int g_cluster_size = 8;
 int g_tma_staging = 0;
-int g_gram_cache = 1;     // cross visits reuse rotated intra-block Grams    // 1: Jacobi panels staged by TMA bulk copies instead of cp.async    // block-mode Jacobi: 1 persistent CTA/item, 2 round launches, 3 cluster/item   // Householder-QR preconditioning for Jacobi matrices with >= this many columns
+int g_gram_cache = 1;     // cross visits reuse rotated intra-block Grams
+int g_block_w2 = 32;      // block-mode panel width (32 or 64 columns)    // 1: Jacobi panels staged by TMA bulk copies instead of cp.async    // block-mode Jacobi: 1 persistent CTA/item, 2 round launches, 3 cluster/item   // Householder-QR preconditioning for Jacobi matrices with >= this many columns
 
 // ---------------------------------------------------------------------------
 // init: product state |0...0> (mps.py:55-66)
@@ -413,7 +414,8 @@ size_t ws_layout(int cap, int nitems, char* base, Ws* ws) {
   off = align256(off + sizeof(double2) * aux_stride * nitems);
   const size_t o_sched = off;
   off = align256(off + sizeof(JacSched) * (size_t)nitems);
-  const size_t gcache_stride = (size_t)((2 * cap + 15) / 16 + 1) * 256;
+  const size_t gcache_stride = std::max((size_t)((2 * cap + 15) / 16 + 1) * 256,
+                                        (size_t)((2 * cap + 31) / 32 + 1) * 1024);
   const size_t o_gc = off;
   off = align256(off + sizeof(double2) * gcache_stride * nitems);
   if (ws && base) {
@@ -446,6 +448,8 @@ void set_attrs() {
                        (int)JacCfg<64>::kSmem);
   cudaFuncSetAttribute(jacobi_dynamic_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)JacCfg<32>::kSmem);
+  cudaFuncSetAttribute(jacobi_dynamic_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)JacCfg<64>::kSmem);
   g_attrs_set = true;
 }
 
@@ -487,6 +491,7 @@ int32_t bmps_set_param(const char* name, double value) {
   else if (k == "cluster_size" && value >= 1 && value <= 16) g_cluster_size = (int)value;
   else if (k == "tma_staging" && (value == 0 || value == 1)) g_tma_staging = (int)value;
   else if (k == "gram_cache" && (value == 0 || value == 1)) g_gram_cache = (int)value;
+  else if (k == "block_w2" && (value == 32 || value == 64)) g_block_w2 = (int)value;
   else return BMPS_E_ARG;
   return BMPS_OK;
 }
@@ -618,18 +623,27 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       cudaMemsetAsync(ws.sched, 0, sizeof(JacSched) * (size_t)nitems, st);
       init_active_kernel<<<1, 32, 0, st>>>(ws.counter, nitems);
       ++g_launches;
-      static int n_slots = 0;
-      if (!n_slots) {
+      static int n_slots[2] = {0, 0};
+      const int wi = g_block_w2 == 64 ? 1 : 0;
+      if (!n_slots[wi]) {
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_dynamic_kernel<32>, 256,
-                                                      JacCfg<32>::kSmem);
+        if (wi)
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_dynamic_kernel<64>, 256,
+                                                        JacCfg<64>::kSmem);
+        else
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_dynamic_kernel<32>, 256,
+                                                        JacCfg<32>::kSmem);
         int dev = 0, sms = kNumSMs;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        n_slots = std::max(1, per_sm) * sms;
+        n_slots[wi] = std::max(1, per_sm) * sms;
       }
-      const int grid = std::min(n_slots, nitems * (nbmax / 2));
-      jacobi_dynamic_kernel<32><<<grid, 256, JacCfg<32>::kSmem, st>>>(ja);
+      const int vis = wi ? std::max(1, (cmax + 63) / 64) : nbmax / 2;
+      const int grid = std::min(n_slots[wi], nitems * vis);
+      if (wi)
+        jacobi_dynamic_kernel<64><<<grid, 256, JacCfg<64>::kSmem, st>>>(ja);
+      else
+        jacobi_dynamic_kernel<32><<<grid, 256, JacCfg<32>::kSmem, st>>>(ja);
       ++g_launches;
       if ((rc = launch_status())) return rc;
     } else if (cl_mode == 1) {

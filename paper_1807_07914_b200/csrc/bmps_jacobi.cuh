@@ -27,10 +27,10 @@ namespace bmps {
 
 template <int W2>
 struct JacCfg {
-  static constexpr int RC = (W2 == 32) ? 32 : 64;  // rows per staged chunk
+  static constexpr int RC = 32;                 // rows per staged chunk
   static constexpr int RCP = RC + 4;            // padded chunk column (bank spread)
   static constexpr int LDG = W2 + 4;            // padded Gram / Q column
-  static constexpr int NBUF = (W2 == 32) ? 2 : 1;
+  static constexpr int NBUF = 2;                // double-buffered chunks
   static constexpr int NT = W2 / 8;             // 8x8 tiles per Gram dimension
   static constexpr int UT = NT * (NT + 1) / 2;  // upper-triangle Gram tiles
   static constexpr int GT = UT / 8;             // whole upper tiles per warp
@@ -146,11 +146,11 @@ BMPS_DEV int panel_col(int p, int I, int J) {
 template <int W2>
 BMPS_DEV void jac_issue_chunk(double2* buf, const double2* X, int r, int c, int row0, int I, int J) {
   using C = JacCfg<W2>;
-  if (C::RC == 32 && W2 == 32) {
+  if (C::RC == 32) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int row = row0 + lane;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < W2 / 8; ++u) {
       const int p = warp + 8 * u, col = panel_col<W2>(p, I, J);
       const bool ok = row < r && col < c;
       cp_async16(buf + lane + p * C::RCP, ok ? X + (size_t)row + (size_t)col * r : X, ok);
@@ -169,12 +169,12 @@ BMPS_DEV void jac_issue_chunk(double2* buf, const double2* X, int r, int c, int 
 template <int W2>
 BMPS_DEV void jac_store_chunk(const double2* buf, double2* X, int r, int c, int row0, int I, int J) {
   using C = JacCfg<W2>;
-  if (C::RC == 32 && W2 == 32) {
+  if (C::RC == 32) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int row = row0 + lane;
     if (row < r) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < W2 / 8; ++u) {
         const int p = warp + 8 * u, col = panel_col<W2>(p, I, J);
         if (col < c) X[(size_t)row + (size_t)col * r] = buf[lane + p * C::RCP];
       }
@@ -326,21 +326,35 @@ BMPS_DEV void jac_gram_store(const double (&acc)[JacCfg<W2>::GT + 1][4], double2
   }
 }
 
-// Cross-block Gram only (G_IJ, 16x16 = 2x2 tiles of 8x8; W2 = 32): warp w
-// accumulates tile w/2 over half of the chunk's k range (acc[0]).
+// Cross-block Gram only (G_IJ, w x w with w = W2/2). W2 = 32: 4 tiles, warp w
+// accumulates tile w/2 over half of the chunk's k range (acc[0]); W2 = 64: 16
+// tiles, two whole tiles per warp (acc[0], acc[1]).
 template <int W2>
 BMPS_DEV void jac_gram_chunk_cross(double (&acc)[JacCfg<W2>::GT + 1][4], const double2* sP,
                                    int nrows) {
   using C = JacCfg<W2>;
+  constexpr int NTc = W2 / 16, CT = NTc * NTc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int kr = lane & 3, rc = lane >> 2;
   const int nk4 = (nrows + 3) >> 2;
-  const int t = warp >> 1, part = warp & 1;
-  const int ti = t >> 1, tj = 2 + (t & 1);
-  const int k0 = part * nk4 / 2, k1 = (part + 1) * nk4 / 2;
-  for (int k4 = k0; k4 < k1; ++k4) {
-    const int k = k4 * 4 + kr;
-    zmma(acc[0], cconj(sP[k + (ti * 8 + rc) * C::RCP]), sP[k + (tj * 8 + rc) * C::RCP]);
+  if (CT >= 8) {
+    constexpr int TPW = CT >= 8 ? CT / 8 : 1;
+    for (int k4 = 0; k4 < nk4; ++k4) {
+      const int k = k4 * 4 + kr;
+#pragma unroll
+      for (int u = 0; u < TPW; ++u) {
+        const int t = warp * TPW + u, ti = t / NTc, tj = NTc + t % NTc;
+        zmma(acc[u], cconj(sP[k + (ti * 8 + rc) * C::RCP]), sP[k + (tj * 8 + rc) * C::RCP]);
+      }
+    }
+  } else {
+    const int t = warp >> 1, part = warp & 1;
+    const int ti = t / NTc, tj = NTc + t % NTc;
+    const int k0 = part * nk4 / 2, k1 = (part + 1) * nk4 / 2;
+    for (int k4 = k0; k4 < k1; ++k4) {
+      const int k = k4 * 4 + kr;
+      zmma(acc[0], cconj(sP[k + (ti * 8 + rc) * C::RCP]), sP[k + (tj * 8 + rc) * C::RCP]);
+    }
   }
 }
 
@@ -349,22 +363,37 @@ template <int W2>
 BMPS_DEV void jac_gram_store_cross(const double (&acc)[JacCfg<W2>::GT + 1][4], double2* sG,
                                    double2* scratch, const double2* cI, const double2* cJ) {
   using C = JacCfg<W2>;
-  constexpr int w = W2 / 2;
+  constexpr int w = W2 / 2, NTc = W2 / 16, CT = NTc * NTc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rr = lane >> 2, cc = (lane & 3) * 2;
-#pragma unroll
-  for (int h = 0; h < 2; ++h)
-    scratch[warp * 64 + rr * 8 + cc + h] = make_double2(acc[0][h], acc[0][2 + h]);
   for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
     const int i = idx % w, j = idx / w;
     sG[i + j * C::LDG] = cI[i + j * w];
     sG[(w + i) + (w + j) * C::LDG] = cJ[i + j * w];
   }
+  if (CT >= 8) {
+    constexpr int TPW = CT >= 8 ? CT / 8 : 1;
+#pragma unroll
+    for (int u = 0; u < TPW; ++u) {
+      const int t = warp * TPW + u, ti = t / NTc, tj = NTc + t % NTc;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = ti * 8 + rr, j = tj * 8 + cc + h;
+        const double2 v = make_double2(acc[u][h], acc[u][2 + h]);
+        sG[i + j * C::LDG] = v;
+        sG[j + i * C::LDG] = cconj(v);
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    scratch[warp * 64 + rr * 8 + cc + h] = make_double2(acc[0][h], acc[0][2 + h]);
   __syncthreads();
-  for (int idx = threadIdx.x; idx < 4 * 64; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < CT * 64; idx += blockDim.x) {
     const int t = idx / 64, e = idx % 64;
     const double2 v = cadd(scratch[(2 * t) * 64 + e], scratch[(2 * t + 1) * 64 + e]);
-    const int i = (t >> 1) * 8 + e / 8, j = w + (t & 1) * 8 + e % 8;
+    const int i = (t / NTc) * 8 + e / 8, j = w + (t % NTc) * 8 + e % 8;
     sG[i + j * C::LDG] = v;
     sG[j + i * C::LDG] = cconj(v);
   }
@@ -524,9 +553,9 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
                         double2* gcache = nullptr) {
   using C = JacCfg<W2>;
   const int nch = (r + C::RC - 1) / C::RC;
-  const bool bulk = (W2 == 32) && !resident && tma;
+  const bool bulk = !resident && tma;
   // cross visits reuse the rotated intra-block Grams cached by earlier visits
-  const bool cross_gram = (W2 == 32) && gcache != nullptr && !full && !resident;
+  const bool cross_gram = gcache != nullptr && !full && !resident;
   double2* cI = gcache ? gcache + (size_t)I * (W2 / 2) * (W2 / 2) : nullptr;
   double2* cJ = gcache ? gcache + (size_t)J * (W2 / 2) * (W2 / 2) : nullptr;
   double gacc[C::GT + 1][4];
