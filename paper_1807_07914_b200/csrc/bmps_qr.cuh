@@ -137,14 +137,19 @@ __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
   }
 }
 
-// A[:, chunk] <- A - V T^H (V^H A[:, chunk]) for the 64 trailing columns of this CTA.
-constexpr size_t kQrUpdateSmem = (size_t)kQrChunk * (kQrChunk + 1) * sizeof(double2);
+// A[:, chunk] <- A - V T^H (V^H A[:, chunk]) for the 64 trailing columns of this CTA,
+// both products on FP64 tensor cores (DMMA), rows streamed in blocks of 32.
+constexpr int kQrRB = 32;
+constexpr int kQrLdA = kQrChunk + 1;
+constexpr size_t kQrUpdateSmem =
+    (size_t)(kQrRB * (kQrNb + 1) + kQrRB * kQrLdA + kQrNb * kQrLdA + kQrNb * kQrNb) * sizeof(double2);
 
 __global__ void __launch_bounds__(256) qr_update_kernel(QrArgs a) {
-  __shared__ double2 sV[kQrChunk][kQrNb + 1];   // row block of V
-  __shared__ double2 sW[kQrNb][kQrChunk + 1];   // W = V^H A_chunk, then T^H W
-  __shared__ double2 sT[kQrNb][kQrNb];
-  extern __shared__ __align__(16) double2 sAq[]; // [kQrChunk cols][kQrChunk + 1 rows]
+  extern __shared__ __align__(16) double2 qsm[];
+  double2* sV = qsm;                                 // [kQrRB][kQrNb + 1]
+  double2* sA = sV + kQrRB * (kQrNb + 1);            // [kQrRB][kQrLdA]
+  double2* sW = sA + kQrRB * kQrLdA;                 // [kQrNb][kQrLdA]
+  double2* sT = sW + kQrNb * kQrLdA;                 // [kQrNb][kQrNb]
   const int item = blockIdx.y;
   const ItemMeta* m = a.meta + item;
   if (!m->precond) return;
@@ -157,79 +162,96 @@ __global__ void __launch_bounds__(256) qr_update_kernel(QrArgs a) {
   const int nc = min(kQrChunk, c - c0);
   double2* A = a.X + (size_t)item * a.mat_stride;
   const double2* T = a.aux + (size_t)item * a.aux_stride + 2048;
-  const int tid = threadIdx.x;
-  constexpr int LA = kQrChunk + 1;
-  for (int i = tid; i < kQrNb * kQrNb; i += blockDim.x) sT[i / kQrNb][i % kQrNb] = T[i];
-  double2 acc[4];
-  for (int u = 0; u < 4; ++u) acc[u] = make_double2(0.0, 0.0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kr = lane & 3, rc = lane >> 2;
+  for (int i = tid; i < kQrNb * kQrNb; i += blockDim.x) sT[i] = T[i];
   auto stage = [&](int rb) {
-    for (int i = tid; i < kQrChunk * kQrNb; i += blockDim.x) {
-      const int row = i % kQrChunk, p = i / kQrChunk;
+    for (int i = tid; i < kQrRB * kQrNb; i += blockDim.x) {
+      const int row = i % kQrRB, p = i / kQrRB;
       const int gr = rb + row, k = j0 + p;
       double2 v = make_double2(0.0, 0.0);
       if (p < nbp && gr < r) {
         if (gr == k) v = make_double2(1.0, 0.0);
         else if (gr > k) v = A[(size_t)k * r + gr];
       }
-      sV[row][p] = v;
+      sV[row * (kQrNb + 1) + p] = v;
     }
-    for (int i = tid; i < kQrChunk * kQrChunk; i += blockDim.x) {
-      const int row = i % kQrChunk, q = i / kQrChunk;
+    for (int i = tid; i < kQrRB * kQrChunk; i += blockDim.x) {
+      const int row = i % kQrRB, q = i / kQrRB;
       const int gr = rb + row;
-      sAq[q * LA + row] = (gr < r && q < nc) ? A[(size_t)(c0 + q) * r + gr] : make_double2(0.0, 0.0);
+      sA[row * kQrLdA + q] =
+          (gr < r && q < nc) ? A[(size_t)(c0 + q) * r + gr] : make_double2(0.0, 0.0);
     }
   };
-  // W = V^H A_chunk; thread owns (p, q) = (idx / 64, idx % 64), idx = tid + 256 u
-  for (int rb = j0; rb < r; rb += kQrChunk) {
+  // W = V^H A_chunk (16 x 64): warp -> tile row w/4, tile cols 2*(w%4) + {0,1}
+  double acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
+  const int tr = warp >> 2, tc0 = (warp & 3) * 2;
+  for (int rb = j0; rb < r; rb += kQrRB) {
     __syncthreads();
     stage(rb);
     __syncthreads();
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int idx = tid + u * 256;
-      const int p = idx / kQrChunk, q = idx % kQrChunk;
-      double2 sacc = acc[u];
-      const double2* aq = sAq + q * LA;
-      for (int row = 0; row < kQrChunk; ++row) sacc = cfma(cconj(sV[row][p]), aq[row], sacc);
-      acc[u] = sacc;
+    for (int k4 = 0; k4 < kQrRB / 4; ++k4) {
+      const int k = k4 * 4 + kr;
+      const double2 av = cconj(sV[k * (kQrNb + 1) + tr * 8 + rc]);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) zmma(acc[u], av, sA[k * kQrLdA + (tc0 + u) * 8 + rc]);
     }
   }
   __syncthreads();
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int idx = tid + u * 256;
-    sW[idx / kQrChunk][idx % kQrChunk] = acc[u];
-  }
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      sW[(tr * 8 + rc) * kQrLdA + (tc0 + u) * 8 + kr * 2 + h] = make_double2(acc[u][h], acc[u][2 + h]);
   __syncthreads();
-  // W <- T^H W
+  // W <- T^H W (small, scalar)
+  double2 wt[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int idx = tid + u * 256;
     const int p = idx / kQrChunk, q = idx % kQrChunk;
     double2 sacc = make_double2(0.0, 0.0);
-    for (int z = 0; z <= p; ++z) sacc = cfma(cconj(sT[z][p]), sW[z][q], sacc);
-    acc[u] = sacc;
+    for (int z = 0; z <= p; ++z) sacc = cfma(cconj(sT[z * kQrNb + p]), sW[z * kQrLdA + q], sacc);
+    wt[u] = sacc;
   }
   __syncthreads();
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int idx = tid + u * 256;
-    sW[idx / kQrChunk][idx % kQrChunk] = acc[u];
+    sW[(idx / kQrChunk) * kQrLdA + idx % kQrChunk] = wt[u];
   }
-  // A_chunk -= V W
-  for (int rb = j0; rb < r; rb += kQrChunk) {
+  // A_chunk -= V W: per 32-row block, 4 x 8 output tiles, 4 per warp (row tile w/2, cols 4*(w%2)+u)
+  const int orow = warp >> 1, oc0 = (warp & 1) * 4;
+  for (int rb = j0; rb < r; rb += kQrRB) {
     __syncthreads();
     stage(rb);
     __syncthreads();
-    for (int i = tid; i < kQrChunk * nc; i += blockDim.x) {
-      const int row = i % kQrChunk, q = i / kQrChunk;
-      const int gr = rb + row;
-      if (gr >= r) continue;
-      double2 sacc = sAq[q * LA + row];
 #pragma unroll
-      for (int p = 0; p < kQrNb; ++p) sacc = csub(sacc, cmul(sV[row][p], sW[p][q]));
-      A[(size_t)(c0 + q) * r + gr] = sacc;
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
+#pragma unroll
+    for (int k4 = 0; k4 < kQrNb / 4; ++k4) {
+      const int k = k4 * 4 + kr;
+      const double2 av = sV[(orow * 8 + rc) * (kQrNb + 1) + k];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) zmma(acc[u], av, sW[k * kQrLdA + (oc0 + u) * 8 + rc]);
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = orow * 8 + rc, q = (oc0 + u) * 8 + kr * 2 + h;
+        const int gr = rb + row;
+        if (gr < r && q < nc)
+          A[(size_t)(c0 + q) * r + gr] =
+              csub(sA[row * kQrLdA + q], make_double2(acc[u][h], acc[u][2 + h]));
+      }
   }
 }
 
