@@ -108,18 +108,21 @@ BMPS_DEV bool jacobi_rotation(double a, double b, double2 g, double tol, double 
   const double g2 = cabs2(g);
   const double thr = tol * fro;
   if (!(g2 > thr * thr * lo)) return false;            // |g| > tol * sqrt(lo) * fro
-  // short dependent chain: one rsqrt, one sqrt, one reciprocal, one rsqrt
+  // division-free chain: rsqrt, sqrt, rsqrt. With tau = |zeta|, h = sqrt(1 + tau^2),
+  // t = 1/(tau + h) gives s = 1/sqrt(2h(tau + h)), c = (tau + h) s (same rotation
+  // as Rutishauser's tangent formula).
   const double rg = rsqrt(g2);                         // 1 / |g|
   const double zeta = 0.5 * (b - a) * rg;
-  double t;
-  if (fabs(zeta) > 1e150) {
-    t = 0.5 / zeta;
+  const double tau = fabs(zeta);
+  if (tau > 1e150) {
+    s = 0.5 / zeta;
+    c = 1.0;
   } else {
-    t = 1.0 / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-    if (zeta < 0) t = -t;
+    const double h = sqrt(fma(tau, tau, 1.0));
+    const double d = rsqrt(2.0 * h * (tau + h));
+    c = (tau + h) * d;
+    s = zeta < 0 ? -d : d;
   }
-  c = rsqrt(fma(t, t, 1.0));
-  s = c * t;
   e = make_double2(g.x * rg, g.y * rg);
   return true;
 }
