@@ -69,6 +69,11 @@ int32_t bmps_set_param(const char* name, double value);
 /* Number of kernels this library has launched so far (process-wide). */
 uint64_t bmps_launch_count(void);
 
+/* Development aid: cumulative cycles of the Jacobi phases (Gram pass, inner
+ * sweep, apply pass, visit count) in a -DBMPS_PHASE_TIMERS build; returns
+ * BMPS_E_ARG in normal builds. out4 is a host array of 4 uint64. */
+int32_t bmps_phase_cycles(uint64_t* out4);
+
 /* MpsState.__init__ (mps.py:55-66): |0...0>, unit boundary bonds, stats reset. */
 int32_t bmps_init_product(double* gamma, double* lam, int32_t* dims, double* trunc_err,
                           int64_t* entries, int64_t* peak, int32_t* max_bond_seen,

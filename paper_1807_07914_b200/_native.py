@@ -36,6 +36,7 @@ _SIGNATURES = {
     "bmps_status_string": ([_I], ctypes.c_char_p),
     "bmps_set_param": ([ctypes.c_char_p, ctypes.c_double], _I),
     "bmps_launch_count": ([], ctypes.c_uint64),
+    "bmps_phase_cycles": ([_P], _I),
     "bmps_init_product": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P], _I),
     "bmps_apply_1q": ([_P, _P, _I, _I, _I, _P, _P, _I, _P], _I),
     "bmps_apply_2q_workspace_bytes": ([_I, _I], _SZ),

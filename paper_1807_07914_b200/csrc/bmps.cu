@@ -480,6 +480,17 @@ int32_t bmps_version(void) { return 1; }
 
 uint64_t bmps_launch_count(void) { return g_launches; }
 
+// Development aid: cumulative Jacobi phase cycles (builds with -DBMPS_PHASE_TIMERS only).
+int32_t bmps_phase_cycles(uint64_t* out4) {
+#ifdef BMPS_PHASE_TIMERS
+  cudaMemcpyFromSymbol(out4, g_phase_cycles, 8 * sizeof(unsigned long long));
+  return BMPS_OK;
+#else
+  (void)out4;
+  return BMPS_E_ARG;
+#endif
+}
+
 int32_t bmps_set_param(const char* name, double value) {
   if (!name) return BMPS_E_ARG;
   const std::string k(name);

@@ -93,6 +93,17 @@ BMPS_DEV bool pair_needs_rotation(double a, double b, double2 g, double tol, dou
   return hypot(g.x, g.y) > tol * sqrt(lo) * fro;
 }
 
+// 1/sqrt(x) for normal positive x: hardware approximation (MUFU, ~2^-23) plus two
+// Newton steps -> full float64 accuracy without the library's special-case paths.
+BMPS_DEV double fast_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+
 // Same test as jacobi_rotation's early exits (no rotation math).
 BMPS_DEV bool jacobi_needs(double a, double b, double2 g, double tol, double noise2, double fro) {
   const double lo = fmin(a, b), hi = fmax(a, b);
@@ -111,15 +122,16 @@ BMPS_DEV bool jacobi_rotation(double a, double b, double2 g, double tol, double 
   // division-free chain: rsqrt, sqrt, rsqrt. With tau = |zeta|, h = sqrt(1 + tau^2),
   // t = 1/(tau + h) gives s = 1/sqrt(2h(tau + h)), c = (tau + h) s (same rotation
   // as Rutishauser's tangent formula).
-  const double rg = rsqrt(g2);                         // 1 / |g|
+  const double rg = g2 > 1e-290 ? fast_rsqrt(g2) : rsqrt(g2);   // 1 / |g|
   const double zeta = 0.5 * (b - a) * rg;
   const double tau = fabs(zeta);
   if (tau > 1e150) {
     s = 0.5 / zeta;
     c = 1.0;
   } else {
-    const double h = sqrt(fma(tau, tau, 1.0));
-    const double d = rsqrt(2.0 * h * (tau + h));
+    const double h2 = fma(tau, tau, 1.0);
+    const double h = h2 * fast_rsqrt(h2);             // sqrt(1 + tau^2)
+    const double d = fast_rsqrt(2.0 * h * (tau + h));
     c = (tau + h) * d;
     s = zeta < 0 ? -d : d;
   }

@@ -25,6 +25,17 @@
 
 namespace bmps {
 
+#ifdef BMPS_PHASE_TIMERS
+// cycles spent in [0] Gram pass, [1] inner sweep (incl. check), [2] apply pass, [3] visits
+__device__ unsigned long long g_phase_cycles[8];
+#define BMPS_TICK(var) const long long var = clock64()
+#define BMPS_ACC(slot, t0, t1) \
+  if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[slot], (unsigned long long)((t1) - (t0)))
+#else
+#define BMPS_TICK(var)
+#define BMPS_ACC(slot, t0, t1)
+#endif
+
 template <int W2>
 struct JacCfg {
   static constexpr int RC = 32;                 // rows per staged chunk
@@ -479,6 +490,7 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
   for (int it = 0; it < max_inner; ++it) {
     int any = 0;
     for (int rho = 0; rho < rounds; ++rho) {
+      BMPS_TICK(tr0);
       int act = 0;
       if (tid < w) {
         int i, j;
@@ -500,6 +512,9 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
         rs.e[tid] = e;
       }
       const int nact = __syncthreads_count(act);
+      BMPS_TICK(tr1);
+      BMPS_ACC(4, tr0, tr1);
+      BMPS_ACC(6, 0, 1);
       any += nact;
       if (nact == 0) continue;
       // G <- J^H G J as w x w independent 2x2 blocks; Q <- Q J
@@ -535,6 +550,8 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
         sQ[k + jq * C::LDG] = cadd(cscale(qi, sq), cmul(cscale(eq, cq), qj));
       }
       __syncthreads();
+      BMPS_TICK(tr2);
+      BMPS_ACC(5, tr1, tr2);
     }
     if (it == 0) first = any;
     if (!any) break;
@@ -552,6 +569,7 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
                         double2* sQ, double2* sP, RotShared& rs, JacStage& st, bool tma,
                         double2* gcache = nullptr) {
   using C = JacCfg<W2>;
+  BMPS_TICK(tv0);
   const int nch = (r + C::RC - 1) / C::RC;
   const bool bulk = !resident && tma;
   // cross visits reuse the rotated intra-block Grams cached by earlier visits
@@ -595,6 +613,8 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
       if (C::NBUF == 1 && k + 1 < nch) jac_issue_chunk<W2>(sP, X, r, c, (k + 1) * C::RC, I, J);
     }
   }
+  BMPS_TICK(tv1);
+  BMPS_ACC(0, tv0, tv1);
   if (cross_gram) jac_gram_store_cross<W2>(gacc, sG, sQ, cI, cJ);
   else jac_gram_store<W2>(gacc, sG, sQ);
   __syncthreads();
@@ -625,6 +645,9 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
   }
   const int nrot = __syncthreads_or(need) ? jac_inner<W2>(sG, sQ, rs, tol, noise2, fro, full, max_inner)
                                           : 0;
+  BMPS_TICK(tv2);
+  BMPS_ACC(1, tv1, tv2);
+  BMPS_ACC(3, 0, 1);
   if (gcache != nullptr && !resident && (full || nrot > 0)) jac_cache_store<W2>(sG, cI, cJ);
   if (nrot == 0) {
     if (!resident && !staged) {
@@ -665,6 +688,7 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
     jac_flush_bulk();
     return true;
   }
+
   // cp.async re-stream: load chunk k+1 while chunk k is multiplied and stored
   for (int k = 0; k < nch; ++k) {
     double2* cur = sP + (k % C::NBUF) * C::BUF;
@@ -685,6 +709,8 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
     __syncthreads();
     if (C::NBUF == 1 && !staged && k + 1 < nch) jac_issue_chunk<W2>(sP, X, r, c, (k + 1) * C::RC, I, J);
   }
+  BMPS_TICK(tv3);
+  BMPS_ACC(2, tv2, tv3);
   return true;
 }
 
