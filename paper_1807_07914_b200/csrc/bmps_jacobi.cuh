@@ -517,9 +517,11 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
       BMPS_ACC(6, 0, 1);
       any += nact;
       if (nact == 0) continue;
-      // G <- J^H G J as w x w independent 2x2 blocks; Q <- Q J
-      for (int idx = tid; idx < w * w; idx += blockDim.x) {
-        const int p = idx % w, q = idx / w;
+      // G <- J^H G J as independent 2x2 blocks (p <= q computed, (q, p) mirrored);
+      // Q <- Q J
+      for (int idx = tid; idx < w * (w + 1) / 2; idx += blockDim.x) {
+        const int q = (int)((sqrtf(8.0f * (float)idx + 1.0f) - 1.0f) * 0.5f);
+        const int p = idx - q * (q + 1) / 2;
         if (!(rs.act[p] | rs.act[q])) continue;  // identity on both sides
         const int ip = rs.i[p], jp = rs.j[p], iq = rs.i[q], jq = rs.j[q];
         const double cp = rs.c[p], sp = rs.s[p], cq = rs.c[q], sq = rs.s[q];
@@ -534,10 +536,20 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
         const double2 r11 = cadd(cscale(g10, sq), cmul(cqe, g11));
         // left: rows ip, jp by J_p^H = [[cp, -sp e], [sp, cp e]]
         const double2 spe = cscale(ep, sp), cpe = cscale(ep, cp);
-        sG[ip + iq * C::LDG] = csub(cscale(r00, cp), cmul(spe, r10));
-        sG[ip + jq * C::LDG] = csub(cscale(r01, cp), cmul(spe, r11));
-        sG[jp + iq * C::LDG] = cadd(cscale(r00, sp), cmul(cpe, r10));
-        sG[jp + jq * C::LDG] = cadd(cscale(r01, sp), cmul(cpe, r11));
+        const double2 n00 = csub(cscale(r00, cp), cmul(spe, r10));
+        const double2 n01 = csub(cscale(r01, cp), cmul(spe, r11));
+        const double2 n10 = cadd(cscale(r00, sp), cmul(cpe, r10));
+        const double2 n11 = cadd(cscale(r01, sp), cmul(cpe, r11));
+        sG[ip + iq * C::LDG] = n00;
+        sG[ip + jq * C::LDG] = n01;
+        sG[jp + iq * C::LDG] = n10;
+        sG[jp + jq * C::LDG] = n11;
+        if (p != q) {
+          sG[iq + ip * C::LDG] = cconj(n00);
+          sG[jq + ip * C::LDG] = cconj(n01);
+          sG[iq + jp * C::LDG] = cconj(n10);
+          sG[jq + jp * C::LDG] = cconj(n11);
+        }
       }
       for (int idx = tid; idx < W2 * w; idx += blockDim.x) {
         const int k = idx % W2, q = idx / W2;
