@@ -460,6 +460,25 @@ BMPS_DEV void jac_apply_writeback(const double (&acc)[JacCfg<W2>::AT][4], double
     }
 }
 
+// Write the apply accumulators straight to the matrix in global memory (each
+// store instruction covers 8 rows x 8 columns of a DMMA tile).
+template <int W2>
+BMPS_DEV void jac_apply_store_global(const double (&acc)[JacCfg<W2>::AT][4], double2* X, int r,
+                                     int c, int row0, int I, int J) {
+  using C = JacCfg<W2>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int kr = lane & 3, rc = lane >> 2;
+#pragma unroll
+  for (int u = 0; u < C::AT; ++u)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = warp * C::AT + u, mi = t / C::NT, nj = t % C::NT;
+      const int row = row0 + mi * 8 + rc, col = panel_col<W2>(nj * 8 + kr * 2 + h, I, J);
+      if (row < r && col < c)
+        X[(size_t)row + (size_t)col * r] = make_double2(acc[u][h], acc[u][2 + h]);
+    }
+}
+
 // Pairing of inner round rho: full round robin over W2 columns, or cross
 // pairs (p, w + (p + rho) mod w) between the two blocks of the panel.
 template <int W2>
@@ -714,11 +733,8 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
     }
     __syncthreads();
     jac_apply_mma<W2>(aacc, cur, sQ);
-    __syncthreads();
-    jac_apply_writeback<W2>(aacc, cur);
-    __syncthreads();
-    jac_store_chunk<W2>(cur, X, r, c, k * C::RC, I, J);
-    __syncthreads();
+    jac_apply_store_global<W2>(aacc, X, r, c, k * C::RC, I, J);
+    __syncthreads();  // every warp is done reading `cur` before it is refilled
     if (C::NBUF == 1 && !staged && k + 1 < nch) jac_issue_chunk<W2>(sP, X, r, c, (k + 1) * C::RC, I, J);
   }
   BMPS_TICK(tv3);
