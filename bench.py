@@ -336,6 +336,25 @@ def main() -> None:
                                         "p50": float(np.median(sw))},
             "clocks": clk.summary(),
         }
+        if world == 1:
+            # SURVEY §8(d)(i) second batch size: one brick layer of ONE circuit (B ~ 24-33)
+            k0 = total_steps
+            single = [[bulk_layer(k0 + k, 0, full[0])] + [[] for _ in range(R - 1)] for k in range(4)]
+            sp = [compile_batch(s, N_QUBITS) for s in single]
+            batch.execute(sp[0], mode=args.mode)
+            torch.cuda.synchronize()
+            h0 = torch.cuda.Event(enable_timing=True)
+            h1 = torch.cuda.Event(enable_timing=True)
+            h0.record(stream)
+            for p in sp[1:]:
+                batch.execute(p, mode=args.mode)
+            h1.record(stream)
+            torch.cuda.synchronize()
+            batch.check_status()
+            nb = sum(n_updates(s[0]) for s in single[1:])
+            line["single_circuit_layer"] = {
+                "updates_per_layer": nb / 3, "updates_per_s": nb / (h0.elapsed_time(h1) / 1e3),
+                "ms_per_layer": h0.elapsed_time(h1) / 3}
         if not args.no_circuit and world == 1:
             from paper_1807_07914_b200 import workloads as W
             w3 = W.config3()

@@ -25,12 +25,14 @@ unsigned long long g_launches = 0;  // kernels launched through this library
 double g_tol_factor = 4.0;
 int g_max_sweeps = 60;
 int g_max_inner = 1;
-int g_qr_min_cols = 65;
-int g_jacobi_mode = 4;
+int g_qr_min_cols = 65;    // Householder-QR preconditioning for Jacobi matrices with >= this many columns
+int g_jacobi_mode = 4;     // block-mode Jacobi: 1 persistent CTA/item, 2 round launches,
+                           // 3 cluster/item, 4 dynamic persistent scheduler
 int g_cluster_size = 8;
-int g_tma_staging = 0;
-int g_gram_cache = 1;     // cross visits reuse rotated intra-block Grams
-int g_block_w2 = 32;      // block-mode panel width (32 or 64 columns)    // 1: Jacobi panels staged by TMA bulk copies instead of cp.async    // block-mode Jacobi: 1 persistent CTA/item, 2 round launches, 3 cluster/item   // Householder-QR preconditioning for Jacobi matrices with >= this many columns
+int g_tma_staging = 0;     // 1: Jacobi panels staged by TMA bulk copies instead of cp.async
+int g_gram_cache = 1;      // cross visits reuse rotated intra-block Grams
+int g_block_w2 = 32;       // block-mode panel width (32 or 64 columns)
+int g_double_qr = 1;       // second QR of R^H before the Jacobi (preconditioned items)
 
 // ---------------------------------------------------------------------------
 // init: product state |0...0> (mps.py:55-66)
@@ -380,6 +382,7 @@ struct Ws {
   double2* M0;
   double2* X;
   double2* Y;
+  double2* Z;
   double2* aux;
   JacSched* sched;
   double2* gcache;
@@ -409,7 +412,9 @@ size_t ws_layout(int cap, int nitems, char* base, Ws* ws) {
   off = align256(off + sizeof(double2) * mat_stride * nitems);
   const size_t o_y = off;
   off = align256(off + sizeof(double2) * mat_stride * nitems);
-  const size_t aux_stride = 2048 + kQrNb * kQrNb;
+  const size_t o_z = off;
+  off = align256(off + sizeof(double2) * (size_t)(2 * cap) * (2 * cap) * nitems);
+  const size_t aux_stride = 2 * kQrAuxHalf;
   const size_t o_aux = off;
   off = align256(off + sizeof(double2) * aux_stride * nitems);
   const size_t o_sched = off;
@@ -426,6 +431,7 @@ size_t ws_layout(int cap, int nitems, char* base, Ws* ws) {
     ws->M0 = (double2*)(base + o_m0);
     ws->X = (double2*)(base + o_x);
     ws->Y = (double2*)(base + o_y);
+    ws->Z = (double2*)(base + o_z);
     ws->aux = (double2*)(base + o_aux);
     ws->sched = (JacSched*)(base + o_sched);
     ws->gcache = (double2*)(base + o_gc);
@@ -442,6 +448,7 @@ void set_attrs() {
   if (g_attrs_set) return;
   cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
   cudaFuncSetAttribute(qr_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQrUpdateSmem);
+  cudaFuncSetAttribute(dq_apply_q1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQ1Smem);
   cudaFuncSetAttribute(jacobi_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)JacCfg<32>::kSmem);
   cudaFuncSetAttribute(jacobi_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -503,6 +510,7 @@ int32_t bmps_set_param(const char* name, double value) {
   else if (k == "tma_staging" && (value == 0 || value == 1)) g_tma_staging = (int)value;
   else if (k == "gram_cache" && (value == 0 || value == 1)) g_gram_cache = (int)value;
   else if (k == "block_w2" && (value == 32 || value == 64)) g_block_w2 = (int)value;
+  else if (k == "double_qr" && (value == 0 || value == 1)) g_double_qr = (int)value;
   else return BMPS_E_ARG;
   return BMPS_OK;
 }
@@ -569,7 +577,8 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   cudaMemsetAsync(ws.meta, 0, sizeof(ItemMeta) * (size_t)nitems, st);
   const int tpd = (dim_bound + 31) / 32;
   theta_kernel<<<dim3(tpd * tpd, nitems), 256, kThetaSmem, st>>>(
-      sv, items, (const double2*)gates, ws.meta, ws.M0, ws.X, ws.mat_stride, tpd, g_qr_min_cols);
+      sv, items, (const double2*)gates, ws.meta, ws.M0, ws.X, ws.mat_stride, tpd, g_qr_min_cols,
+      g_double_qr);
   ++g_launches;
   int32_t rc = launch_status();
   if (rc) return rc;
@@ -581,22 +590,27 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
     qa.meta = ws.meta;
     qa.X = ws.X;
     qa.Y = ws.Y;
+    qa.Z = ws.Z;
     qa.aux = ws.aux;
     qa.mat_stride = ws.mat_stride;
     qa.aux_stride = ws.aux_stride;
     const int npanels = (cmax + kQrNb - 1) / kQrNb;
-    for (int p = 0; p < npanels; ++p) {
-      qa.panel = p;
-      qr_panel_kernel<<<nitems, 512, 0, st>>>(qa);
-      ++g_launches;
-      const int trail = cmax - (p + 1) * kQrNb;
-      if (trail > 0) {
-        qr_update_kernel<<<dim3((trail + kQrChunk - 1) / kQrChunk, nitems), 256, kQrUpdateSmem, st>>>(qa);
+    for (int second = 0; second <= (g_double_qr ? 1 : 0); ++second) {
+      qa.second = second;
+      for (int p = 0; p < npanels; ++p) {
+        qa.panel = p;
+        qr_panel_kernel<<<nitems, 512, 0, st>>>(qa);
         ++g_launches;
+        const int trail = cmax - (p + 1) * kQrNb;
+        if (trail > 0) {
+          qr_update_kernel<<<dim3((trail + kQrChunk - 1) / kQrChunk, nitems), 256, kQrUpdateSmem,
+                             st>>>(qa);
+          ++g_launches;
+        }
       }
+      qr_form_y_kernel<<<dim3(std::min(64, (cmax * cmax + 255) / 256), nitems), 256, 0, st>>>(qa);
+      ++g_launches;
     }
-    qr_form_y_kernel<<<dim3(std::min(64, (cmax * cmax + 255) / 256), nitems), 256, 0, st>>>(qa);
-    ++g_launches;
     if ((rc = launch_status())) return rc;
   }
 
@@ -607,6 +621,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   ja.meta = ws.meta;
   ja.X = ws.X;
   ja.Y = ws.Y;
+  ja.Z = ws.Z;
   ja.mat_stride = ws.mat_stride;
   ja.round = 0;
   ja.max_sweeps = max_sweeps;
@@ -708,6 +723,30 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
         }
       }
     }
+  }
+
+  // K3c double-QR epilogue: L = Q1 [Z sorted; 0] for the kept columns
+  if (g_double_qr && cmax >= g_qr_min_cols) {
+    dq_sort_kernel<<<nitems, 512, 0, st>>>(ws.meta, ws.Z, ws.Y, ws.mat_stride, ws.sig,
+                                           ws.sig_stride, policy.cutoff, policy.max_bond,
+                                           policy.relative);
+    ++g_launches;
+    QrArgs qa;
+    qa.meta = ws.meta;
+    qa.X = ws.X;
+    qa.Y = ws.Y;
+    qa.Z = ws.Z;
+    qa.aux = ws.aux;
+    qa.mat_stride = ws.mat_stride;
+    qa.aux_stride = ws.aux_stride;
+    qa.second = 0;
+    const int kq = policy.max_bond > 0 ? std::min(policy.max_bond, cmax) : cmax;
+    for (int p = (cmax + kQrNb - 1) / kQrNb - 1; p >= 0; --p) {
+      qa.panel = p;
+      dq_apply_q1_kernel<<<dim3((kq + kQrChunk - 1) / kQrChunk, nitems), 256, kQ1Smem, st>>>(qa);
+      ++g_launches;
+    }
+    if ((rc = launch_status())) return rc;
   }
 
   // K4 finalize + split

@@ -158,7 +158,9 @@ struct ItemMeta {
   int keep, status, sweeps, conv, flag;
   int precond;                    // 1: Jacobi runs on Y = R^H from X0 = QR
   int jrows;                      // rows of the Jacobi matrix (r, or c if precond)
-  int pad0, pad1, pad2;
+  int dq;                         // 1: second QR (R1^H = Q2 R2), Jacobi on Z = R2^H
+  int msel;                       // finalize/split read the result matrix from Y (not X)
+  int keep_pre;                   // keep count known before finalize (double-QR path)
   double err, norm;
   double fro2;                    // ||M||_F^2 (accumulated by theta)
   double padd;

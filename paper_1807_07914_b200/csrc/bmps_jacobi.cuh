@@ -64,6 +64,7 @@ struct JacArgs {
   ItemMeta* meta;
   double2* X;
   double2* Y;
+  double2* Z;        // double-QR items: Jacobi on Z = R2^H
   size_t mat_stride;
   int round;
   int persistent;
@@ -764,7 +765,7 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_kernel(JacArgs
   JacStage st{jbar, 0u};
   stage_init(jbar);
   const int r = m->jrows, c = m->c;
-  double2* X = (m->precond ? args.Y : args.X) + (size_t)item * args.mat_stride;
+  double2* X = (m->dq ? args.Z : m->precond ? args.Y : args.X) + (size_t)item * args.mat_stride;
   double2* gc = args.gcache ? args.gcache + (size_t)item * args.gcache_stride : nullptr;
   constexpr int w = W2 / 2;
   int nb = (c + w - 1) / w;
@@ -932,7 +933,7 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_dynamic_kernel
     const unsigned rnd = s_round;
     ItemMeta* m = args.meta + i;
     const int r = m->jrows, c = m->c;
-    double2* X = (m->precond ? args.Y : args.X) + (size_t)i * args.mat_stride;
+    double2* X = (m->dq ? args.Z : m->precond ? args.Y : args.X) + (size_t)i * args.mat_stride;
     int nb = (c + w - 1) / w;
     nb += nb & 1;
     const double tol = args.tol_factor * sqrt((double)r) * kEps;

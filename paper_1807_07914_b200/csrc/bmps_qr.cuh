@@ -27,11 +27,25 @@ struct QrArgs {
   ItemMeta* meta;
   double2* X;        // working copy of X0 (r x c, ld r): overwritten by V (below diag) and R
   double2* Y;        // Jacobi input Y = R^H (c x c, ld c)
-  double2* aux;      // per item: tau[kMaxQrCols] followed by T[kQrNb * kQrNb]
+  double2* Z;        // double-QR Jacobi input Z = R2^H (c x c, ld c)
+  double2* aux;      // per item: [tau1 2048][T 256][tau2 2048][T 256]
   size_t mat_stride;
   size_t aux_stride;
   int panel;
+  int second;        // 0: QR of X (r x c); 1: QR of Y = R1^H (c x c), double-QR items only
 };
+
+constexpr int kQrAuxHalf = 2048 + kQrNb * kQrNb;
+
+// matrix, rows and tau/T base of the pass
+BMPS_DEV bool qr_pass(const QrArgs& a, int item, double2*& A, int& rows, double2*& tau) {
+  const ItemMeta* m = a.meta + item;
+  if (!m->precond || (a.second && !m->dq)) return false;
+  A = (a.second ? a.Y : a.X) + (size_t)item * a.mat_stride;
+  rows = a.second ? m->c : m->r;
+  tau = a.aux + (size_t)item * a.aux_stride + (a.second ? kQrAuxHalf : 0);
+  return true;
+}
 
 BMPS_DEV double block_sum(double v, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -51,13 +65,14 @@ __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
   __shared__ double2 s_S[kQrNb][kQrNb];
   const int item = blockIdx.x;
   const ItemMeta* m = a.meta + item;
-  if (!m->precond) return;
-  const int r = m->r, c = m->c;
+  double2* A;
+  double2* tau;
+  int r;
+  if (!qr_pass(a, item, A, r, tau)) return;
+  const int c = m->c;
   const int j0 = a.panel * kQrNb;
   if (j0 >= c) return;
   const int j1 = min(j0 + kQrNb, c);
-  double2* A = a.X + (size_t)item * a.mat_stride;
-  double2* tau = a.aux + (size_t)item * a.aux_stride;
   double2* T = tau + 2048;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int k = j0; k < j1; ++k) {
@@ -152,16 +167,18 @@ __global__ void __launch_bounds__(256) qr_update_kernel(QrArgs a) {
   double2* sT = sW + kQrNb * kQrLdA;                 // [kQrNb][kQrNb]
   const int item = blockIdx.y;
   const ItemMeta* m = a.meta + item;
-  if (!m->precond) return;
-  const int r = m->r, c = m->c;
+  double2* A;
+  double2* tauw;
+  int r;
+  if (!qr_pass(a, item, A, r, tauw)) return;
+  const int c = m->c;
   const int j0 = a.panel * kQrNb;
   const int j1 = min(j0 + kQrNb, c);
   const int nbp = j1 - j0;
   const int c0 = j1 + blockIdx.x * kQrChunk;
   if (c0 >= c || nbp <= 0) return;
   const int nc = min(kQrChunk, c - c0);
-  double2* A = a.X + (size_t)item * a.mat_stride;
-  const double2* T = a.aux + (size_t)item * a.aux_stride + 2048;
+  const double2* T = tauw + 2048;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kr = lane & 3, rc = lane >> 2;
   for (int i = tid; i < kQrNb * kQrNb; i += blockDim.x) sT[i] = T[i];
@@ -259,13 +276,246 @@ __global__ void __launch_bounds__(256) qr_update_kernel(QrArgs a) {
 __global__ void __launch_bounds__(256) qr_form_y_kernel(QrArgs a) {
   const int item = blockIdx.y;
   const ItemMeta* m = a.meta + item;
-  if (!m->precond) return;
-  const int r = m->r, c = m->c;
-  const double2* A = a.X + (size_t)item * a.mat_stride;
-  double2* Y = a.Y + (size_t)item * a.mat_stride;
+  double2* Aw;
+  double2* tau;
+  int r;
+  if (!qr_pass(a, item, Aw, r, tau)) return;
+  const int c = m->c;
+  const double2* A = Aw;
+  double2* Y = (a.second ? a.Z : a.Y) + (size_t)item * a.mat_stride;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < c * c; idx += gridDim.x * blockDim.x) {
     const int i = idx % c, j = idx / c;   // Y row i, col j
     Y[(size_t)i + (size_t)j * c] = j <= i ? cconj(A[(size_t)j + (size_t)i * r]) : make_double2(0.0, 0.0);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Double-QR path: after the Jacobi on Z = R2^H, L = Q1 [Z sorted; 0] are the
+// left singular vectors of X0 scaled by sigma (exactly what Jacobi on X0 would
+// produce), so finalize/split run their ordinary (non-preconditioned) path on L.
+// ---------------------------------------------------------------------------
+
+// sigma_j = ||z_j||, sort descending, keep (policy), L[:, k] = [Z[:, perm k]; 0]
+// into the Y buffer (r x c, ld r). Marks the item as "result in Y, rows r".
+__global__ void __launch_bounds__(512) dq_sort_kernel(ItemMeta* meta, const double2* Zb,
+                                                      double2* Yb, size_t mat_stride,
+                                                      double* sig_ws, int sig_stride,
+                                                      double cutoff, int max_bond, int relative) {
+  __shared__ double ssig[2048];
+  __shared__ int sidx[2048];
+  const int item = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  ItemMeta* m = meta + item;
+  if (!m->dq || m->status) return;
+  const int r = m->r, c = m->c;
+  const double2* z = Zb + (size_t)item * mat_stride;
+  double2* L = Yb + (size_t)item * mat_stride;
+  int P2 = 1;
+  while (P2 < c) P2 <<= 1;
+  for (int j = warp; j < P2; j += 16) {
+    double acc = 0.0;
+    if (j < c)
+      for (int i = lane; i < c; i += 32) acc += cabs2(z[(size_t)i + (size_t)j * c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      ssig[j] = j < c ? sqrt(acc) : -1.0;
+      sidx[j] = j;
+    }
+  }
+  __syncthreads();
+  for (int k = 2; k <= P2; k <<= 1) {
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      for (int t = tid; t < P2; t += blockDim.x) {
+        const int u = t ^ jj;
+        if (u > t) {
+          const double st = ssig[t], su = ssig[u];
+          const int it = sidx[t], iu = sidx[u];
+          const bool u_first = su > st || (su == st && iu < it);
+          const bool t_first = st > su || (st == su && it < iu);
+          if (((t & k) == 0) ? u_first : t_first) {
+            ssig[t] = su;
+            ssig[u] = st;
+            sidx[t] = iu;
+            sidx[u] = it;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    int keep;
+    if (cutoff > 0.0) {
+      const double thr = cutoff * (relative ? ssig[0] : 1.0);
+      keep = 0;
+      for (int k = 0; k < c; ++k) keep += ssig[k] >= thr ? 1 : 0;
+    } else {
+      keep = c;
+    }
+    keep = max(keep, 1);
+    if (max_bond > 0) keep = min(keep, max_bond);
+    m->keep_pre = keep;
+    m->precond = 0;
+    m->msel = 1;
+    m->jrows = r;
+  }
+  double* sg = sig_ws + (size_t)item * sig_stride;
+  for (int k = tid; k < c; k += blockDim.x) sg[k] = ssig[k];
+  for (int idx = tid; idx < r * c; idx += blockDim.x) {
+    const int i = idx % r, k = idx / r;
+    L[(size_t)i + (size_t)k * r] =
+        i < c ? z[(size_t)i + (size_t)sidx[k] * c] : make_double2(0.0, 0.0);
+  }
+}
+
+// L[:, 0:keep] <- (I - V T V^H) L for the panel's Householder block (V from the
+// first QR, stored below the diagonal of X; T rebuilt from tau1). Called for the
+// panels in reverse order so that L <- H_1 ... H_c L = Q1 L.
+constexpr size_t kQ1Smem =
+    (size_t)(kQrRB * (kQrNb + 1) + kQrRB * kQrLdA + kQrNb * kQrLdA + 2 * kQrNb * kQrNb) *
+    sizeof(double2);
+
+__global__ void __launch_bounds__(256) dq_apply_q1_kernel(QrArgs a) {
+  extern __shared__ __align__(16) double2 qsm[];
+  double2* sV = qsm;                                 // [kQrRB][kQrNb + 1]
+  double2* sA = sV + kQrRB * (kQrNb + 1);            // [kQrRB][kQrLdA]
+  double2* sW = sA + kQrRB * kQrLdA;                 // [kQrNb][kQrLdA]
+  double2* sT = sW + kQrNb * kQrLdA;                 // [kQrNb][kQrNb]
+  double2* sS = sT + kQrNb * kQrNb;                  // [kQrNb][kQrNb]
+  const int item = blockIdx.y;
+  const ItemMeta* m = a.meta + item;
+  if (!m->dq || !m->msel || m->status) return;
+  const int r = m->r, c = m->c, keep = m->keep_pre;
+  const int j0 = a.panel * kQrNb;
+  if (j0 >= c) return;
+  const int j1 = min(j0 + kQrNb, c);
+  const int nbp = j1 - j0;
+  const int c0 = blockIdx.x * kQrChunk;
+  if (c0 >= keep) return;
+  const int nc = min(kQrChunk, keep - c0);
+  const double2* V = a.X + (size_t)item * a.mat_stride;      // Householder vectors of QR 1
+  const double2* tau = a.aux + (size_t)item * a.aux_stride;  // tau1
+  double2* Lm = a.Y + (size_t)item * a.mat_stride;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kr = lane & 3, rc = lane >> 2;
+  // S = V^H V (strict upper part), then T by the forward recurrence
+  for (int p = warp; p < nbp * nbp; p += 8) {
+    const int x = p / nbp, y = p % nbp;
+    if (x >= y) continue;
+    const int kx = j0 + x, ky = j0 + y;
+    double2 acc = lane == 0 ? cconj(V[(size_t)kx * r + ky]) : make_double2(0.0, 0.0);
+    for (int i = ky + 1 + lane; i < r; i += 32)
+      acc = cfma(cconj(V[(size_t)kx * r + i]), V[(size_t)ky * r + i], acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if (lane == 0) sS[x * kQrNb + y] = acc;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double2 wv[kQrNb];
+    for (int y = 0; y < nbp; ++y) {
+      const double2 ty = tau[j0 + y];
+      for (int x = 0; x < y; ++x) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (int zz = x; zz < y; ++zz) acc = cfma(sT[x * kQrNb + zz], sS[zz * kQrNb + y], acc);
+        wv[x] = acc;
+      }
+      for (int x = 0; x < y; ++x) sT[x * kQrNb + y] = cmul(make_double2(-ty.x, -ty.y), wv[x]);
+      sT[y * kQrNb + y] = ty;
+      for (int x = y + 1; x < kQrNb; ++x) sT[x * kQrNb + y] = make_double2(0.0, 0.0);
+    }
+    for (int y = nbp; y < kQrNb; ++y)
+      for (int x = 0; x < kQrNb; ++x) sT[x * kQrNb + y] = make_double2(0.0, 0.0);
+  }
+  auto stage = [&](int rb) {
+    for (int i = tid; i < kQrRB * kQrNb; i += blockDim.x) {
+      const int row = i % kQrRB, p = i / kQrRB;
+      const int gr = rb + row, k = j0 + p;
+      double2 v = make_double2(0.0, 0.0);
+      if (p < nbp && gr < r) {
+        if (gr == k) v = make_double2(1.0, 0.0);
+        else if (gr > k) v = V[(size_t)k * r + gr];
+      }
+      sV[row * (kQrNb + 1) + p] = v;
+    }
+    for (int i = tid; i < kQrRB * kQrChunk; i += blockDim.x) {
+      const int row = i % kQrRB, q = i / kQrRB;
+      const int gr = rb + row;
+      sA[row * kQrLdA + q] =
+          (gr < r && q < nc) ? Lm[(size_t)(c0 + q) * r + gr] : make_double2(0.0, 0.0);
+    }
+  };
+  double acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
+  const int tr = warp >> 2, tc0 = (warp & 3) * 2;
+  for (int rb = j0; rb < r; rb += kQrRB) {
+    __syncthreads();
+    stage(rb);
+    __syncthreads();
+#pragma unroll
+    for (int k4 = 0; k4 < kQrRB / 4; ++k4) {
+      const int k = k4 * 4 + kr;
+      const double2 av = cconj(sV[k * (kQrNb + 1) + tr * 8 + rc]);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) zmma(acc[u], av, sA[k * kQrLdA + (tc0 + u) * 8 + rc]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      sW[(tr * 8 + rc) * kQrLdA + (tc0 + u) * 8 + kr * 2 + h] = make_double2(acc[u][h], acc[u][2 + h]);
+  __syncthreads();
+  // W <- T W (T upper triangular)
+  double2 wt[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int idx = tid + u * 256;
+    const int p = idx / kQrChunk, q = idx % kQrChunk;
+    double2 sacc = make_double2(0.0, 0.0);
+    for (int zz = p; zz < kQrNb; ++zz) sacc = cfma(sT[p * kQrNb + zz], sW[zz * kQrLdA + q], sacc);
+    wt[u] = sacc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int idx = tid + u * 256;
+    sW[(idx / kQrChunk) * kQrLdA + idx % kQrChunk] = wt[u];
+  }
+  // L -= V W
+  const int orow = warp >> 1, oc0 = (warp & 1) * 4;
+  for (int rb = j0; rb < r; rb += kQrRB) {
+    __syncthreads();
+    stage(rb);
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
+#pragma unroll
+    for (int k4 = 0; k4 < kQrNb / 4; ++k4) {
+      const int k = k4 * 4 + kr;
+      const double2 av = sV[(orow * 8 + rc) * (kQrNb + 1) + k];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) zmma(acc[u], av, sW[k * kQrLdA + (oc0 + u) * 8 + rc]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = orow * 8 + rc, q = (oc0 + u) * 8 + kr * 2 + h;
+        const int gr = rb + row;
+        if (gr < r && q < nc)
+          Lm[(size_t)(c0 + q) * r + gr] =
+              csub(sA[row * kQrLdA + q], make_double2(acc[u][h], acc[u][2 + h]));
+      }
   }
 }
 

@@ -61,7 +61,8 @@ constexpr size_t kThetaSmem = (size_t)kTile * kThetaLdc * sizeof(double2);
 __global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* items,
                                                     const double2* gates, ItemMeta* meta,
                                                     double2* M0, double2* X, size_t mat_stride,
-                                                    int tiles_per_dim, int qr_min_cols) {
+                                                    int tiles_per_dim, int qr_min_cols,
+                                                    int double_qr) {
   __shared__ __align__(16) double2 sA[kKC][kLds];
   __shared__ __align__(16) double2 sB[kKC][kLds];
   __shared__ double2 sG[16];
@@ -85,6 +86,7 @@ __global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* ite
     m->dr = dr;
     const int c = orient == 0 ? 2 * dr : 2 * dl;
     m->precond = c >= qr_min_cols ? 1 : 0;
+    m->dq = m->precond && double_qr ? 1 : 0;
     m->jrows = m->precond ? c : R;
   }
   const int tm = blockIdx.x / tiles_per_dim, tn = blockIdx.x % tiles_per_dim;
@@ -211,10 +213,18 @@ __global__ void __launch_bounds__(512) finalize_kernel(StateView sv, const int* 
   const int r = m->jrows, c = m->c, dl = m->dl, dr = m->dr;
   const int side = m->orient ^ m->precond;   // 0: primary vectors -> Gamma_q, 1: -> Gamma_{q+1}
   const int s = items[2 * item], q = items[2 * item + 1];
-  const double2* x = (m->precond ? Yq : X) + (size_t)item * mat_stride;
+  const double2* x = (m->precond || m->msel ? Yq : X) + (size_t)item * mat_stride;
+  const bool presorted = m->msel != 0;  // double-QR: sigma already sorted by dq_sort_kernel
   int P2 = 1;
   while (P2 < c) P2 <<= 1;
-  for (int j = warp; j < P2; j += 16) {
+  if (presorted) {
+    const double* sg = sig_ws + (size_t)item * sig_stride;
+    for (int j = tid; j < P2; j += blockDim.x) {
+      ssig[j] = j < c ? sg[j] : -1.0;
+      sidx[j] = j;
+    }
+  }
+  for (int j = presorted ? P2 : warp; j < P2; j += 16) {
     double acc = 0.0;
     if (j < c)
       for (int i = lane; i < r; i += 32) acc += cabs2(x[(size_t)i + (size_t)j * r]);
@@ -227,7 +237,7 @@ __global__ void __launch_bounds__(512) finalize_kernel(StateView sv, const int* 
   }
   __syncthreads();
   // bitonic sort: descending sigma, ties by ascending column index
-  for (int k = 2; k <= P2; k <<= 1) {
+  for (int k = 2; k <= (presorted ? 1 : P2); k <<= 1) {
     for (int jj = k >> 1; jj > 0; jj >>= 1) {
       for (int t = tid; t < P2; t += blockDim.x) {
         const int u = t ^ jj;
@@ -371,7 +381,7 @@ struct SplitOp {
     dr = m->dr;
     cap = sv.cap;
     m0 = M0 + (size_t)item * mat_stride;
-    x = (PRE ? Yq : X) + (size_t)item * mat_stride;
+    x = (PRE || m->msel ? Yq : X) + (size_t)item * mat_stride;
     sig = sig_ws + (size_t)item * sig_stride;
     perm = perm_ws + (size_t)item * sig_stride;
     if (side == 0) {

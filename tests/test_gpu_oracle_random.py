@@ -136,3 +136,17 @@ def test_all_jacobi_schedules_match_oracle(mode):
         _compare(prog, 12, 1e-10, 48, seed=mode)
     finally:
         lib.bmps_set_param(b"jacobi_mode", 4.0)
+
+
+@pytest.mark.parametrize("dq", [0, 1])
+@pytest.mark.parametrize("chi,cutoff", [(64, 1e-12), (128, 1e-10), (128, 0.0)])
+def test_double_qr_preconditioning_matches_oracle(dq, chi, cutoff):
+    """Single vs double Householder-QR preconditioning (bmps_set_param double_qr)."""
+    from paper_1807_07914_b200 import _native
+    lib = _native.load()
+    assert lib.bmps_set_param(b"double_qr", float(dq)) == 0
+    try:
+        prog = brick_circuit(14, 14, np.random.default_rng(chi + dq))
+        _compare(prog, 14, cutoff, chi, seed=chi)
+    finally:
+        lib.bmps_set_param(b"double_qr", float(_native.DEFAULT_PARAMS["double_qr"]))
