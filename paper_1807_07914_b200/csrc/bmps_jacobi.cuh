@@ -39,8 +39,12 @@ __device__ unsigned long long g_phase_cycles[8];
 template <int W2>
 struct JacCfg {
   static constexpr int RC = 32;                 // rows per staged chunk
-  static constexpr int RCP = RC + 4;            // padded chunk column (bank spread)
-  static constexpr int LDG = W2 + 4;            // padded Gram / Q column
+  // W2 = 32: the Gram lives in staging buffer 1 during the inner sweep (it is dead
+  // before the apply streams into that buffer), so a CTA needs 53 KB and 4 fit per SM.
+  static constexpr bool G_IN_BUF = W2 == 32;
+  static constexpr int RCP = G_IN_BUF ? RC + 2 : RC + 4;  // padded chunk column (bank spread)
+  static constexpr int LDG = W2 + 4;            // padded Q column
+  static constexpr int LDGG = G_IN_BUF ? RCP : W2 + 4;  // Gram column (fits a buffer)
   static constexpr int NBUF = 2;                // double-buffered chunks
   static constexpr int NT = W2 / 8;             // 8x8 tiles per Gram dimension
   static constexpr int UT = NT * (NT + 1) / 2;  // upper-triangle Gram tiles
@@ -49,7 +53,9 @@ struct JacCfg {
   static constexpr int GSPLIT = GREM ? 8 / GREM : 1;  // warps sharing one leftover tile
   static constexpr int AT = (RC / 8) * NT / 8;  // apply tiles per warp
   static constexpr int BUF = RCP * W2;          // one staging buffer (complex elements)
-  static constexpr size_t kSmem = (size_t)(2 * W2 * LDG + NBUF * BUF) * sizeof(double2);
+  static constexpr size_t kSmem =
+      (size_t)(W2 * LDG + (G_IN_BUF ? 0 : W2 * LDGG) + NBUF * BUF) * sizeof(double2);
+  static_assert(!G_IN_BUF || (W2 * LDGG <= BUF && NBUF == 2), "Gram must fit staging buffer 1");
 };
 
 // Per-item scheduling word of the dynamic (persistent, work-claiming) mode.
@@ -82,6 +88,7 @@ struct JacArgs {
 struct RotShared {
   double c[32], s[32];
   double2 e[32];
+  double2 se[32], ce[32];   // s e, c e
   int i[32], j[32], act[32];
 };
 
@@ -316,8 +323,8 @@ BMPS_DEV void jac_gram_store(const double (&acc)[JacCfg<W2>::GT + 1][4], double2
     for (int h = 0; h < 2; ++h) {
       const int i = ti * 8 + rr, j = tj * 8 + cc + h;
       const double2 v = make_double2(acc[u][h], acc[u][2 + h]);
-      sG[i + j * C::LDG] = v;
-      if (ti != tj) sG[j + i * C::LDG] = cconj(v);
+      sG[i + j * C::LDGG] = v;
+      if (ti != tj) sG[j + i * C::LDGG] = cconj(v);
     }
   }
   if (C::GREM) {
@@ -332,8 +339,8 @@ BMPS_DEV void jac_gram_store(const double (&acc)[JacCfg<W2>::GT + 1][4], double2
       int ti, tj;
       upper_tile<C::NT>(8 * C::GT + t, ti, tj);
       const int i = ti * 8 + e / 8, j = tj * 8 + e % 8;
-      sG[i + j * C::LDG] = v;
-      if (ti != tj) sG[j + i * C::LDG] = cconj(v);
+      sG[i + j * C::LDGG] = v;
+      if (ti != tj) sG[j + i * C::LDGG] = cconj(v);
     }
   }
 }
@@ -380,8 +387,8 @@ BMPS_DEV void jac_gram_store_cross(const double (&acc)[JacCfg<W2>::GT + 1][4], d
   const int rr = lane >> 2, cc = (lane & 3) * 2;
   for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
     const int i = idx % w, j = idx / w;
-    sG[i + j * C::LDG] = cI[i + j * w];
-    sG[(w + i) + (w + j) * C::LDG] = cJ[i + j * w];
+    sG[i + j * C::LDGG] = cI[i + j * w];
+    sG[(w + i) + (w + j) * C::LDGG] = cJ[i + j * w];
   }
   if (CT >= 8) {
     constexpr int TPW = CT >= 8 ? CT / 8 : 1;
@@ -392,8 +399,8 @@ BMPS_DEV void jac_gram_store_cross(const double (&acc)[JacCfg<W2>::GT + 1][4], d
       for (int h = 0; h < 2; ++h) {
         const int i = ti * 8 + rr, j = tj * 8 + cc + h;
         const double2 v = make_double2(acc[u][h], acc[u][2 + h]);
-        sG[i + j * C::LDG] = v;
-        sG[j + i * C::LDG] = cconj(v);
+        sG[i + j * C::LDGG] = v;
+        sG[j + i * C::LDGG] = cconj(v);
       }
     }
     return;
@@ -406,8 +413,8 @@ BMPS_DEV void jac_gram_store_cross(const double (&acc)[JacCfg<W2>::GT + 1][4], d
     const int t = idx / 64, e = idx % 64;
     const double2 v = cadd(scratch[(2 * t) * 64 + e], scratch[(2 * t + 1) * 64 + e]);
     const int i = (t / NTc) * 8 + e / 8, j = w + (t % NTc) * 8 + e % 8;
-    sG[i + j * C::LDG] = v;
-    sG[j + i * C::LDG] = cconj(v);
+    sG[i + j * C::LDGG] = v;
+    sG[j + i * C::LDGG] = cconj(v);
   }
 }
 
@@ -417,8 +424,8 @@ BMPS_DEV void jac_cache_store(const double2* sG, double2* cI, double2* cJ) {
   constexpr int w = W2 / 2;
   for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
     const int i = idx % w, j = idx / w;
-    cI[i + j * w] = sG[i + j * C::LDG];
-    cJ[i + j * w] = sG[(w + i) + (w + j) * C::LDG];
+    cI[i + j * w] = sG[i + j * C::LDGG];
+    cJ[i + j * w] = sG[(w + i) + (w + j) * C::LDGG];
   }
 }
 
@@ -517,7 +524,7 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
         inner_pair<W2>(full, rho, tid, i, j);
         double c = 1.0, s = 0.0;
         double2 e = make_double2(1.0, 0.0);
-        act = jacobi_rotation(sG[i + i * C::LDG].x, sG[j + j * C::LDG].x, sG[i + j * C::LDG], tol,
+        act = jacobi_rotation(sG[i + i * C::LDGG].x, sG[j + j * C::LDGG].x, sG[i + j * C::LDGG], tol,
                               noise2, fro, c, s, e);
         if (!act) {
           c = 1.0;
@@ -530,6 +537,8 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
         rs.c[tid] = c;
         rs.s[tid] = s;
         rs.e[tid] = e;
+        rs.se[tid] = cscale(e, s);
+        rs.ce[tid] = cscale(e, c);
       }
       const int nact = __syncthreads_count(act);
       BMPS_TICK(tr1);
@@ -545,30 +554,28 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
         if (!(rs.act[p] | rs.act[q])) continue;  // identity on both sides
         const int ip = rs.i[p], jp = rs.j[p], iq = rs.i[q], jq = rs.j[q];
         const double cp = rs.c[p], sp = rs.s[p], cq = rs.c[q], sq = rs.s[q];
-        const double2 ep = rs.e[p], eq = cconj(rs.e[q]);
-        const double2 g00 = sG[ip + iq * C::LDG], g01 = sG[ip + jq * C::LDG];
-        const double2 g10 = sG[jp + iq * C::LDG], g11 = sG[jp + jq * C::LDG];
-        // right: [x_iq, x_jq] <- [x_iq, x_jq] [[cq, sq], [-sq e*, cq e*]]
-        const double2 sqe = cscale(eq, sq), cqe = cscale(eq, cq);
-        const double2 r00 = csub(cscale(g00, cq), cmul(sqe, g01));
-        const double2 r01 = cadd(cscale(g00, sq), cmul(cqe, g01));
-        const double2 r10 = csub(cscale(g10, cq), cmul(sqe, g11));
-        const double2 r11 = cadd(cscale(g10, sq), cmul(cqe, g11));
-        // left: rows ip, jp by J_p^H = [[cp, -sp e], [sp, cp e]]
-        const double2 spe = cscale(ep, sp), cpe = cscale(ep, cp);
-        const double2 n00 = csub(cscale(r00, cp), cmul(spe, r10));
-        const double2 n01 = csub(cscale(r01, cp), cmul(spe, r11));
-        const double2 n10 = cadd(cscale(r00, sp), cmul(cpe, r10));
-        const double2 n11 = cadd(cscale(r01, sp), cmul(cpe, r11));
-        sG[ip + iq * C::LDG] = n00;
-        sG[ip + jq * C::LDG] = n01;
-        sG[jp + iq * C::LDG] = n10;
-        sG[jp + jq * C::LDG] = n11;
+        const double2 sep = rs.se[p], cep = rs.ce[p], seq = rs.se[q], ceq = rs.ce[q];
+        const double2 g00 = sG[ip + iq * C::LDGG], g01 = sG[ip + jq * C::LDGG];
+        const double2 g10 = sG[jp + iq * C::LDGG], g11 = sG[jp + jq * C::LDGG];
+        // right: [x_iq, x_jq] <- [x_iq, x_jq] [[cq, sq], [-sq e_q*, cq e_q*]]
+        const double2 r00 = cmsc(g00, cq, seq, g01);
+        const double2 r01 = cmac(g00, sq, ceq, g01);
+        const double2 r10 = cmsc(g10, cq, seq, g11);
+        const double2 r11 = cmac(g10, sq, ceq, g11);
+        // left: rows ip, jp by J_p^H = [[cp, -sp e_p], [sp, cp e_p]]
+        const double2 n00 = cms(r00, cp, sep, r10);
+        const double2 n01 = cms(r01, cp, sep, r11);
+        const double2 n10 = cma(r00, sp, cep, r10);
+        const double2 n11 = cma(r01, sp, cep, r11);
+        sG[ip + iq * C::LDGG] = n00;
+        sG[ip + jq * C::LDGG] = n01;
+        sG[jp + iq * C::LDGG] = n10;
+        sG[jp + jq * C::LDGG] = n11;
         if (p != q) {
-          sG[iq + ip * C::LDG] = cconj(n00);
-          sG[jq + ip * C::LDG] = cconj(n01);
-          sG[iq + jp * C::LDG] = cconj(n10);
-          sG[jq + jp * C::LDG] = cconj(n11);
+          sG[iq + ip * C::LDGG] = cconj(n00);
+          sG[jq + ip * C::LDGG] = cconj(n01);
+          sG[iq + jp * C::LDGG] = cconj(n10);
+          sG[jq + jp * C::LDGG] = cconj(n11);
         }
       }
       for (int idx = tid; idx < W2 * w; idx += blockDim.x) {
@@ -576,10 +583,9 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
         if (!rs.act[q]) continue;
         const int iq = rs.i[q], jq = rs.j[q];
         const double cq = rs.c[q], sq = rs.s[q];
-        const double2 eq = cconj(rs.e[q]);
         const double2 qi = sQ[k + iq * C::LDG], qj = sQ[k + jq * C::LDG];
-        sQ[k + iq * C::LDG] = csub(cscale(qi, cq), cmul(cscale(eq, sq), qj));
-        sQ[k + jq * C::LDG] = cadd(cscale(qi, sq), cmul(cscale(eq, cq), qj));
+        sQ[k + iq * C::LDG] = cmsc(qi, cq, rs.se[q], qj);
+        sQ[k + jq * C::LDG] = cmac(qi, sq, rs.ce[q], qj);
       }
       __syncthreads();
       BMPS_TICK(tr2);
@@ -671,7 +677,7 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
         i = idx % w;
         j = w + idx / w;
       }
-      need = jacobi_needs(sG[i + i * C::LDG].x, sG[j + j * C::LDG].x, sG[i + j * C::LDG], tol,
+      need = jacobi_needs(sG[i + i * C::LDGG].x, sG[j + j * C::LDGG].x, sG[i + j * C::LDGG], tol,
                           noise2, fro);
     }
   }
@@ -681,6 +687,7 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
   BMPS_ACC(1, tv1, tv2);
   BMPS_ACC(3, 0, 1);
   if (gcache != nullptr && !resident && (full || nrot > 0)) jac_cache_store<W2>(sG, cI, cJ);
+  if (C::G_IN_BUF) __syncthreads();  // sG (buffer 1) is read before the apply refills it
   if (nrot == 0) {
     if (!resident && !staged) {
       if (bulk) jac_wait_bulk(st, 0);
@@ -751,12 +758,12 @@ BMPS_DEV void jac_load_resident(double2* sP, const double2* X, int r, int c) {
 }
 
 template <int W2>
-__global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_kernel(JacArgs args) {
+__global__ void __launch_bounds__(256, (W2 == 32) ? 4 : 1) jacobi_kernel(JacArgs args) {
   using C = JacCfg<W2>;
   extern __shared__ __align__(16) double2 jsm[];
-  double2* sG = jsm;
-  double2* sQ = sG + W2 * C::LDG;
+  double2* sQ = jsm;
   double2* sP = sQ + W2 * C::LDG;
+  double2* sG = C::G_IN_BUF ? sP + C::BUF : sP + C::NBUF * C::BUF;
   __shared__ RotShared rs;
   __shared__ unsigned long long jbar[2];
   const int item = blockIdx.y;
@@ -881,12 +888,12 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_kernel(JacArgs
 // re-probe -- so there is no deadlock, no host polling and no per-round
 // launch, and stragglers' rounds overlap other items' work.
 template <int W2>
-__global__ void __launch_bounds__(256, (W2 == 32) ? 3 : 1) jacobi_dynamic_kernel(JacArgs args) {
+__global__ void __launch_bounds__(256, (W2 == 32) ? 4 : 1) jacobi_dynamic_kernel(JacArgs args) {
   using C = JacCfg<W2>;
   extern __shared__ __align__(16) double2 jsm[];
-  double2* sG = jsm;
-  double2* sQ = sG + W2 * C::LDG;
+  double2* sQ = jsm;
   double2* sP = sQ + W2 * C::LDG;
+  double2* sG = C::G_IN_BUF ? sP + C::BUF : sP + C::NBUF * C::BUF;
   __shared__ RotShared rs;
   __shared__ int s_item, s_v;
   __shared__ unsigned s_round;
