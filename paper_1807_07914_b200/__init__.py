@@ -11,12 +11,13 @@ from .backends import BACKENDS, RunRecord, execute, measured_qubits, mps_run, ru
 from .engine import MpsBatch, compile_batch
 from .gates import SWAP_MATRIX, check_unitary, gate_matrix
 from .hamiltonian import PauliHamiltonian, pauli_matrix
-from .ir import GateKind, Instruction, IrError, MatrixGate, num_qubits
+from .ir import (CompositeInstruction, GateKind, Instruction, IrError, MatrixGate, bind_parameters,
+                 flatten, num_qubits)
 from .mps import MpsState
 from .policy import TruncationPolicy
 
 __all__ = [
-    "BACKENDS", "RunRecord", "execute", "measured_qubits", "GateKind", "Instruction", "IrError", "MatrixGate", "MpsBatch", "MpsState",
+    "BACKENDS", "CompositeInstruction", "bind_parameters", "flatten", "RunRecord", "execute", "measured_qubits", "GateKind", "Instruction", "IrError", "MatrixGate", "MpsBatch", "MpsState",
     "PauliHamiltonian", "SWAP_MATRIX", "TruncationPolicy", "check_unitary", "compile_batch",
     "gate_matrix", "mps_run", "num_qubits", "pauli_matrix", "run_program", "simulate_batch",
 ]
