@@ -20,8 +20,38 @@
 
 namespace bmps {
 
-constexpr int kQrNb = 16;
+#ifndef BMPS_QR_NB
+#define BMPS_QR_NB 32
+#endif
+constexpr int kQrNb = BMPS_QR_NB;   // panel width (16 or 32)
 constexpr int kQrChunk = 64;
+static_assert(kQrNb == 16 || kQrNb == 32, "panel width");
+constexpr int kWT = kQrNb / 8;      // 8x8 row tiles of W = V^H A
+constexpr int kWPR = 8 / kWT;       // warps per W row tile
+constexpr int kNU = 8 / kWPR;       // W column tiles per warp
+constexpr int kWU = kQrNb * kQrChunk / 256;  // W entries per thread
+
+// T (upper triangular, row-major T[x * kQrNb + y]) of the compact WY form from tau
+// and the strict upper part of S = V^H V (S[z * lds + y]): T_yy = tau_y,
+// T[0:y, y] = -tau_y T[0:y, 0:y] S[0:y, y]. Run by one warp, lane = row x: a lane
+// only reads back entries of its own row, so the y recurrence needs no barrier.
+BMPS_DEV void build_t(double2* T, const double2* S, int lds, const double2* tau, int nbp) {
+  const int lane = threadIdx.x & 31;
+  for (int y = 0; y < kQrNb; ++y) {
+    double2 v = make_double2(0.0, 0.0);
+    if (y < nbp) {
+      const double2 ty = tau[y];
+      if (lane < y) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (int z = lane; z < y; ++z) acc = cfma(T[lane * kQrNb + z], S[z * lds + y], acc);
+        v = cmul(make_double2(-ty.x, -ty.y), acc);
+      } else if (lane == y) {
+        v = ty;
+      }
+    }
+    if (lane < kQrNb) T[lane * kQrNb + y] = v;
+  }
+}
 
 struct QrArgs {
   ItemMeta* meta;
@@ -61,7 +91,6 @@ BMPS_DEV double block_sum(double v, double* red) {
 
 __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
   __shared__ double red[16];
-  __shared__ double2 s_w[kQrNb];
   __shared__ double2 s_S[kQrNb][kQrNb];
   const int item = blockIdx.x;
   const ItemMeta* m = a.meta + item;
@@ -100,8 +129,7 @@ __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
     }
     __syncthreads();
     // apply P_k = I - conj(tau) v v^H to panel columns k+1 .. j1-1 (one warp per column)
-    const int jj = k + 1 + warp;
-    if (jj < j1 && (t.x != 0.0 || t.y != 0.0)) {
+    for (int jj = k + 1 + warp; jj < j1 && (t.x != 0.0 || t.y != 0.0); jj += blockDim.x >> 5) {
       double2* cj = A + (size_t)jj * r;
       double2 w = lane == 0 ? cj[k] : make_double2(0.0, 0.0);
       for (int i = k + 1 + lane; i < r; i += 32) w = cfma(cconj(col[i]), cj[i], w);
@@ -136,20 +164,7 @@ __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
     if (lane == 0) s_S[x][y] = acc;
   }
   __syncthreads();
-  // T (upper triangular): T_jj = tau_j; T[0:j, j] = -tau_j T[0:j, 0:j] S[0:j, j]
-  if (tid == 0) {
-    for (int y = 0; y < nbp; ++y) {
-      const double2 ty = tau[j0 + y];
-      for (int x = 0; x < y; ++x) {
-        double2 acc = make_double2(0.0, 0.0);
-        for (int z = x; z < y; ++z) acc = cfma(T[x * kQrNb + z], s_S[z][y], acc);
-        s_w[x] = acc;
-      }
-      for (int x = 0; x < y; ++x) T[x * kQrNb + y] = cmul(make_double2(-ty.x, -ty.y), s_w[x]);
-      T[y * kQrNb + y] = ty;
-      for (int x = y + 1; x < kQrNb; ++x) T[x * kQrNb + y] = make_double2(0.0, 0.0);
-    }
-  }
+  if (warp == 0) build_t(T, &s_S[0][0], kQrNb, tau + j0, nbp);
 }
 
 // A[:, chunk] <- A - V T^H (V^H A[:, chunk]) for the 64 trailing columns of this CTA,
@@ -200,13 +215,13 @@ __global__ void __launch_bounds__(256) qr_update_kernel(QrArgs a) {
           (gr < r && q < nc) ? A[(size_t)(c0 + q) * r + gr] : make_double2(0.0, 0.0);
     }
   };
-  // W = V^H A_chunk (16 x 64): warp -> tile row w/4, tile cols 2*(w%4) + {0,1}
+  // W = V^H A_chunk (kQrNb x 64): warp -> W row tile warp / kWPR, kNU column tiles
   double acc[4][4];
 #pragma unroll
   for (int u = 0; u < 4; ++u)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
-  const int tr = warp >> 2, tc0 = (warp & 3) * 2;
+  const int tr = warp / kWPR, tc0 = (warp % kWPR) * kNU;
   for (int rb = j0; rb < r; rb += kQrRB) {
     __syncthreads();
     stage(rb);
@@ -216,20 +231,20 @@ __global__ void __launch_bounds__(256) qr_update_kernel(QrArgs a) {
       const int k = k4 * 4 + kr;
       const double2 av = cconj(sV[k * (kQrNb + 1) + tr * 8 + rc]);
 #pragma unroll
-      for (int u = 0; u < 2; ++u) zmma(acc[u], av, sA[k * kQrLdA + (tc0 + u) * 8 + rc]);
+      for (int u = 0; u < kNU; ++u) zmma(acc[u], av, sA[k * kQrLdA + (tc0 + u) * 8 + rc]);
     }
   }
   __syncthreads();
 #pragma unroll
-  for (int u = 0; u < 2; ++u)
+  for (int u = 0; u < kNU; ++u)
 #pragma unroll
     for (int h = 0; h < 2; ++h)
       sW[(tr * 8 + rc) * kQrLdA + (tc0 + u) * 8 + kr * 2 + h] = make_double2(acc[u][h], acc[u][2 + h]);
   __syncthreads();
   // W <- T^H W (small, scalar)
-  double2 wt[4];
+  double2 wt[kWU];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < kWU; ++u) {
     const int idx = tid + u * 256;
     const int p = idx / kQrChunk, q = idx % kQrChunk;
     double2 sacc = make_double2(0.0, 0.0);
@@ -238,7 +253,7 @@ __global__ void __launch_bounds__(256) qr_update_kernel(QrArgs a) {
   }
   __syncthreads();
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < kWU; ++u) {
     const int idx = tid + u * 256;
     sW[(idx / kQrChunk) * kQrLdA + idx % kQrChunk] = wt[u];
   }
@@ -372,8 +387,9 @@ __global__ void __launch_bounds__(512) dq_sort_kernel(ItemMeta* meta, const doub
 // first QR, stored below the diagonal of X; T rebuilt from tau1). Called for the
 // panels in reverse order so that L <- H_1 ... H_c L = Q1 L.
 constexpr size_t kQ1Smem =
-    (size_t)(kQrRB * (kQrNb + 1) + kQrRB * kQrLdA + kQrNb * kQrLdA + 2 * kQrNb * kQrNb) *
+    (size_t)(kQrRB * (kQrNb + 1) + kQrRB * kQrLdA + kQrNb * kQrLdA + kQrNb * kQrNb) *
     sizeof(double2);
+static_assert(kQrNb * kQrNb <= kQrRB * kQrLdA, "S aliases the A staging block");
 
 __global__ void __launch_bounds__(256) dq_apply_q1_kernel(QrArgs a) {
   extern __shared__ __align__(16) double2 qsm[];
@@ -381,7 +397,7 @@ __global__ void __launch_bounds__(256) dq_apply_q1_kernel(QrArgs a) {
   double2* sA = sV + kQrRB * (kQrNb + 1);            // [kQrRB][kQrLdA]
   double2* sW = sA + kQrRB * kQrLdA;                 // [kQrNb][kQrLdA]
   double2* sT = sW + kQrNb * kQrLdA;                 // [kQrNb][kQrNb]
-  double2* sS = sT + kQrNb * kQrNb;                  // [kQrNb][kQrNb]
+  double2* sS = sA;                                  // [kQrNb][kQrNb], dead before staging
   const int item = blockIdx.y;
   const ItemMeta* m = a.meta + item;
   if (!m->dq || !m->msel || m->status) return;
@@ -414,22 +430,8 @@ __global__ void __launch_bounds__(256) dq_apply_q1_kernel(QrArgs a) {
     if (lane == 0) sS[x * kQrNb + y] = acc;
   }
   __syncthreads();
-  if (tid == 0) {
-    double2 wv[kQrNb];
-    for (int y = 0; y < nbp; ++y) {
-      const double2 ty = tau[j0 + y];
-      for (int x = 0; x < y; ++x) {
-        double2 acc = make_double2(0.0, 0.0);
-        for (int zz = x; zz < y; ++zz) acc = cfma(sT[x * kQrNb + zz], sS[zz * kQrNb + y], acc);
-        wv[x] = acc;
-      }
-      for (int x = 0; x < y; ++x) sT[x * kQrNb + y] = cmul(make_double2(-ty.x, -ty.y), wv[x]);
-      sT[y * kQrNb + y] = ty;
-      for (int x = y + 1; x < kQrNb; ++x) sT[x * kQrNb + y] = make_double2(0.0, 0.0);
-    }
-    for (int y = nbp; y < kQrNb; ++y)
-      for (int x = 0; x < kQrNb; ++x) sT[x * kQrNb + y] = make_double2(0.0, 0.0);
-  }
+  if (warp == 0) build_t(sT, sS, kQrNb, tau + j0, nbp);
+  __syncthreads();
   auto stage = [&](int rb) {
     for (int i = tid; i < kQrRB * kQrNb; i += blockDim.x) {
       const int row = i % kQrRB, p = i / kQrRB;
@@ -453,7 +455,7 @@ __global__ void __launch_bounds__(256) dq_apply_q1_kernel(QrArgs a) {
   for (int u = 0; u < 4; ++u)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
-  const int tr = warp >> 2, tc0 = (warp & 3) * 2;
+  const int tr = warp / kWPR, tc0 = (warp % kWPR) * kNU;
   for (int rb = j0; rb < r; rb += kQrRB) {
     __syncthreads();
     stage(rb);
@@ -463,20 +465,20 @@ __global__ void __launch_bounds__(256) dq_apply_q1_kernel(QrArgs a) {
       const int k = k4 * 4 + kr;
       const double2 av = cconj(sV[k * (kQrNb + 1) + tr * 8 + rc]);
 #pragma unroll
-      for (int u = 0; u < 2; ++u) zmma(acc[u], av, sA[k * kQrLdA + (tc0 + u) * 8 + rc]);
+      for (int u = 0; u < kNU; ++u) zmma(acc[u], av, sA[k * kQrLdA + (tc0 + u) * 8 + rc]);
     }
   }
   __syncthreads();
 #pragma unroll
-  for (int u = 0; u < 2; ++u)
+  for (int u = 0; u < kNU; ++u)
 #pragma unroll
     for (int h = 0; h < 2; ++h)
       sW[(tr * 8 + rc) * kQrLdA + (tc0 + u) * 8 + kr * 2 + h] = make_double2(acc[u][h], acc[u][2 + h]);
   __syncthreads();
   // W <- T W (T upper triangular)
-  double2 wt[4];
+  double2 wt[kWU];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < kWU; ++u) {
     const int idx = tid + u * 256;
     const int p = idx / kQrChunk, q = idx % kQrChunk;
     double2 sacc = make_double2(0.0, 0.0);
@@ -485,7 +487,7 @@ __global__ void __launch_bounds__(256) dq_apply_q1_kernel(QrArgs a) {
   }
   __syncthreads();
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < kWU; ++u) {
     const int idx = tid + u * 256;
     sW[(idx / kQrChunk) * kQrLdA + idx % kQrChunk] = wt[u];
   }
