@@ -152,6 +152,18 @@ BMPS_DEV bool jacobi_rotation(double a, double b, double2 g, double tol, double 
   return true;
 }
 
+// cp.async 16-byte global -> shared copy, zero-filled when !valid.
+BMPS_DEV void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(valid ? 16 : 0));
+}
+BMPS_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+BMPS_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
 struct StateView {
   double2* gamma;
   double* lam;

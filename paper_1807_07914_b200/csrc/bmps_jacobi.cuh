@@ -92,17 +92,6 @@ struct RotShared {
   int i[32], j[32], act[32];
 };
 
-BMPS_DEV void cp_async16(void* smem, const void* gmem, bool valid) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
-               "r"(valid ? 16 : 0));
-}
-BMPS_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-BMPS_DEV void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
 // ---- TMA bulk copies (cp.async.bulk) with mbarrier completion -------------
 BMPS_DEV unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 BMPS_DEV void mbar_init(unsigned long long* bar, int count) {

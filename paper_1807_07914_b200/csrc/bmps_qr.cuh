@@ -23,12 +23,17 @@ namespace bmps {
 #ifndef BMPS_QR_NB
 #define BMPS_QR_NB 32
 #endif
+#ifndef BMPS_QR_CHUNK
+#define BMPS_QR_CHUNK 64
+#endif
 constexpr int kQrNb = BMPS_QR_NB;   // panel width (16 or 32)
-constexpr int kQrChunk = 64;
+constexpr int kQrChunk = BMPS_QR_CHUNK;  // trailing columns per CTA (32 or 64)
 static_assert(kQrNb == 16 || kQrNb == 32, "panel width");
+static_assert(kQrChunk == 32 || kQrChunk == 64, "chunk width");
 constexpr int kWT = kQrNb / 8;      // 8x8 row tiles of W = V^H A
-constexpr int kWPR = 8 / kWT;       // warps per W row tile
-constexpr int kNU = 8 / kWPR;       // W column tiles per warp
+constexpr int kCT = kQrChunk / 8;   // 8x8 column tiles of the chunk
+constexpr int kNU = kWT * kCT / 8;  // W column tiles per warp (one row tile)
+constexpr int kWPR = kCT / kNU;     // warps per W row tile
 constexpr int kWU = kQrNb * kQrChunk / 256;  // W entries per thread
 
 // T (upper triangular, row-major T[x * kQrNb + y]) of the compact WY form from tau
@@ -167,19 +172,145 @@ __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
   if (warp == 0) build_t(T, &s_S[0][0], kQrNb, tau + j0, nbp);
 }
 
-// A[:, chunk] <- A - V T^H (V^H A[:, chunk]) for the 64 trailing columns of this CTA,
-// both products on FP64 tensor cores (DMMA), rows streamed in blocks of 32.
-constexpr int kQrRB = 32;
+// Compact-WY application to one 64-column chunk of A (rows [j0, r), ld r):
+//   W = V^H A (kQrNb x 64) -> W <- T^H W (TH) or T W -> A <- A - V W,
+// V = the panel's Householder vectors (columns j0.., unit diagonal implied, zero
+// above) stored below the diagonal of Vm (ld r). Both products on DMMA; row blocks
+// of kQrRB stream through two cp.async stages (zero-filled beyond r / the chunk),
+// and the first block of the second pass is in flight during the T product.
+constexpr int kQrRB = 16;
 constexpr int kQrLdA = kQrChunk + 1;
-constexpr size_t kQrUpdateSmem =
-    (size_t)(kQrRB * (kQrNb + 1) + kQrRB * kQrLdA + kQrNb * kQrLdA + kQrNb * kQrNb) * sizeof(double2);
+constexpr int kQrLdV = kQrNb + 1;
+constexpr int kQrStage = kQrRB * (kQrLdV + kQrLdA);
+constexpr size_t kWyApplySmem =
+    (size_t)(2 * kQrStage + kQrNb * kQrLdA + kQrNb * kQrNb) * sizeof(double2);
+constexpr size_t kQrUpdateSmem = kWyApplySmem;
 
+BMPS_DEV void wy_issue(double2* smem, int b, const double2* Vm, const double2* A, int r, int j0,
+                       int nbp, int c0, int nc) {
+  double2* sV = smem + (b & 1) * kQrStage;
+  double2* sA = sV + kQrRB * kQrLdV;
+  const int rb = j0 + b * kQrRB;
+  for (int i = threadIdx.x; i < kQrRB * kQrNb; i += blockDim.x) {
+    const int row = i % kQrRB, p = i / kQrRB;
+    const int gr = rb + row, k = j0 + p;
+    double2* dst = sV + row * kQrLdV + p;
+    if (p < nbp && gr > k && gr < r) cp_async16(dst, Vm + (size_t)k * r + gr, true);
+    else *dst = make_double2(p < nbp && gr == k ? 1.0 : 0.0, 0.0);
+  }
+  for (int i = threadIdx.x; i < kQrRB * kQrChunk; i += blockDim.x) {
+    const int row = i % kQrRB, q = i / kQrRB;
+    const int gr = rb + row;
+    const bool ok = gr < r && q < nc;
+    cp_async16(sA + row * kQrLdA + q, ok ? A + (size_t)(c0 + q) * r + gr : A, ok);
+  }
+  cp_async_commit();
+}
+
+template <bool TH>
+BMPS_DEV void wy_apply(double2* smem, const double2* Vm, double2* A, int r, int j0, int nbp,
+                       int c0, int nc) {
+  double2* sW = smem + 2 * kQrStage;  // [kQrNb][kQrLdA]
+  const double2* sT = sW + kQrNb * kQrLdA;  // [kQrNb][kQrNb], filled by the caller
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kr = lane & 3, rc = lane >> 2;
+  const int nblk = (r - j0 + kQrRB - 1) / kQrRB;
+  // pass 1: W = V^H A; warp -> W row tile warp / kWPR, kNU column tiles
+  double acc[kNU][4];
+#pragma unroll
+  for (int u = 0; u < kNU; ++u)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
+  const int tr = warp / kWPR, tc0 = (warp % kWPR) * kNU;
+  wy_issue(smem, 0, Vm, A, r, j0, nbp, c0, nc);
+  for (int b = 0; b < nblk; ++b) {
+    if (b + 1 < nblk) {
+      wy_issue(smem, b + 1, Vm, A, r, j0, nbp, c0, nc);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double2* sV = smem + (b & 1) * kQrStage;
+    const double2* sA = sV + kQrRB * kQrLdV;
+#pragma unroll
+    for (int k4 = 0; k4 < kQrRB / 4; ++k4) {
+      const int k = k4 * 4 + kr;
+      const double2 av = cconj(sV[k * kQrLdV + tr * 8 + rc]);
+#pragma unroll
+      for (int u = 0; u < kNU; ++u) zmma(acc[u], av, sA[k * kQrLdA + (tc0 + u) * 8 + rc]);
+    }
+    __syncthreads();
+  }
+  wy_issue(smem, 0, Vm, A, r, j0, nbp, c0, nc);  // pass 2's first block, in flight below
+#pragma unroll
+  for (int u = 0; u < kNU; ++u)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      sW[(tr * 8 + rc) * kQrLdA + (tc0 + u) * 8 + kr * 2 + h] = make_double2(acc[u][h], acc[u][2 + h]);
+  __syncthreads();
+  double2 wt[kWU];
+#pragma unroll
+  for (int u = 0; u < kWU; ++u) {
+    const int idx = tid + u * 256;
+    const int p = idx / kQrChunk, q = idx % kQrChunk;
+    double2 sacc = make_double2(0.0, 0.0);
+    if (TH) {
+      for (int z = 0; z <= p; ++z) sacc = cfma(cconj(sT[z * kQrNb + p]), sW[z * kQrLdA + q], sacc);
+    } else {
+      for (int z = p; z < kQrNb; ++z) sacc = cfma(sT[p * kQrNb + z], sW[z * kQrLdA + q], sacc);
+    }
+    wt[u] = sacc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kWU; ++u) {
+    const int idx = tid + u * 256;
+    sW[(idx / kQrChunk) * kQrLdA + idx % kQrChunk] = wt[u];
+  }
+  // pass 2: A -= V W; a kQrRB x kQrChunk block = (kQrRB / 8) x kCT tiles, kOU per warp
+  constexpr int kOU = (kQrRB / 8) * kCT / 8;   // output column tiles per warp
+  const int orow = warp / (kCT / kOU), oc0 = (warp % (kCT / kOU)) * kOU;
+  for (int b = 0; b < nblk; ++b) {
+    if (b + 1 < nblk) {
+      wy_issue(smem, b + 1, Vm, A, r, j0, nbp, c0, nc);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double2* sV = smem + (b & 1) * kQrStage;
+    const double2* sA = sV + kQrRB * kQrLdV;
+    double oacc[kOU][4];
+#pragma unroll
+    for (int u = 0; u < kOU; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) oacc[u][q] = 0.0;
+#pragma unroll
+    for (int k4 = 0; k4 < kQrNb / 4; ++k4) {
+      const int k = k4 * 4 + kr;
+      const double2 av = sV[(orow * 8 + rc) * kQrLdV + k];
+#pragma unroll
+      for (int u = 0; u < kOU; ++u) zmma(oacc[u], av, sW[k * kQrLdA + (oc0 + u) * 8 + rc]);
+    }
+    const int rb = j0 + b * kQrRB;
+#pragma unroll
+    for (int u = 0; u < kOU; ++u)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = orow * 8 + rc, q = (oc0 + u) * 8 + kr * 2 + h;
+        const int gr = rb + row;
+        if (gr < r && q < nc)
+          A[(size_t)(c0 + q) * r + gr] =
+              csub(sA[row * kQrLdA + q], make_double2(oacc[u][h], oacc[u][2 + h]));
+      }
+    __syncthreads();
+  }
+}
+
+// A[:, chunk] <- A - V T^H (V^H A[:, chunk]) for the 64 trailing columns of this CTA.
 __global__ void __launch_bounds__(256) qr_update_kernel(QrArgs a) {
   extern __shared__ __align__(16) double2 qsm[];
-  double2* sV = qsm;                                 // [kQrRB][kQrNb + 1]
-  double2* sA = sV + kQrRB * (kQrNb + 1);            // [kQrRB][kQrLdA]
-  double2* sW = sA + kQrRB * kQrLdA;                 // [kQrNb][kQrLdA]
-  double2* sT = sW + kQrNb * kQrLdA;                 // [kQrNb][kQrNb]
   const int item = blockIdx.y;
   const ItemMeta* m = a.meta + item;
   double2* A;
@@ -192,99 +323,10 @@ __global__ void __launch_bounds__(256) qr_update_kernel(QrArgs a) {
   const int nbp = j1 - j0;
   const int c0 = j1 + blockIdx.x * kQrChunk;
   if (c0 >= c || nbp <= 0) return;
-  const int nc = min(kQrChunk, c - c0);
+  double2* sT = qsm + 2 * kQrStage + kQrNb * kQrLdA;
   const double2* T = tauw + 2048;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int kr = lane & 3, rc = lane >> 2;
-  for (int i = tid; i < kQrNb * kQrNb; i += blockDim.x) sT[i] = T[i];
-  auto stage = [&](int rb) {
-    for (int i = tid; i < kQrRB * kQrNb; i += blockDim.x) {
-      const int row = i % kQrRB, p = i / kQrRB;
-      const int gr = rb + row, k = j0 + p;
-      double2 v = make_double2(0.0, 0.0);
-      if (p < nbp && gr < r) {
-        if (gr == k) v = make_double2(1.0, 0.0);
-        else if (gr > k) v = A[(size_t)k * r + gr];
-      }
-      sV[row * (kQrNb + 1) + p] = v;
-    }
-    for (int i = tid; i < kQrRB * kQrChunk; i += blockDim.x) {
-      const int row = i % kQrRB, q = i / kQrRB;
-      const int gr = rb + row;
-      sA[row * kQrLdA + q] =
-          (gr < r && q < nc) ? A[(size_t)(c0 + q) * r + gr] : make_double2(0.0, 0.0);
-    }
-  };
-  // W = V^H A_chunk (kQrNb x 64): warp -> W row tile warp / kWPR, kNU column tiles
-  double acc[4][4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
-  const int tr = warp / kWPR, tc0 = (warp % kWPR) * kNU;
-  for (int rb = j0; rb < r; rb += kQrRB) {
-    __syncthreads();
-    stage(rb);
-    __syncthreads();
-#pragma unroll
-    for (int k4 = 0; k4 < kQrRB / 4; ++k4) {
-      const int k = k4 * 4 + kr;
-      const double2 av = cconj(sV[k * (kQrNb + 1) + tr * 8 + rc]);
-#pragma unroll
-      for (int u = 0; u < kNU; ++u) zmma(acc[u], av, sA[k * kQrLdA + (tc0 + u) * 8 + rc]);
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < kNU; ++u)
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-      sW[(tr * 8 + rc) * kQrLdA + (tc0 + u) * 8 + kr * 2 + h] = make_double2(acc[u][h], acc[u][2 + h]);
-  __syncthreads();
-  // W <- T^H W (small, scalar)
-  double2 wt[kWU];
-#pragma unroll
-  for (int u = 0; u < kWU; ++u) {
-    const int idx = tid + u * 256;
-    const int p = idx / kQrChunk, q = idx % kQrChunk;
-    double2 sacc = make_double2(0.0, 0.0);
-    for (int z = 0; z <= p; ++z) sacc = cfma(cconj(sT[z * kQrNb + p]), sW[z * kQrLdA + q], sacc);
-    wt[u] = sacc;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < kWU; ++u) {
-    const int idx = tid + u * 256;
-    sW[(idx / kQrChunk) * kQrLdA + idx % kQrChunk] = wt[u];
-  }
-  // A_chunk -= V W: per 32-row block, 4 x 8 output tiles, 4 per warp (row tile w/2, cols 4*(w%2)+u)
-  const int orow = warp >> 1, oc0 = (warp & 1) * 4;
-  for (int rb = j0; rb < r; rb += kQrRB) {
-    __syncthreads();
-    stage(rb);
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
-#pragma unroll
-    for (int k4 = 0; k4 < kQrNb / 4; ++k4) {
-      const int k = k4 * 4 + kr;
-      const double2 av = sV[(orow * 8 + rc) * (kQrNb + 1) + k];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) zmma(acc[u], av, sW[k * kQrLdA + (oc0 + u) * 8 + rc]);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int row = orow * 8 + rc, q = (oc0 + u) * 8 + kr * 2 + h;
-        const int gr = rb + row;
-        if (gr < r && q < nc)
-          A[(size_t)(c0 + q) * r + gr] =
-              csub(sA[row * kQrLdA + q], make_double2(acc[u][h], acc[u][2 + h]));
-      }
-  }
+  for (int i = threadIdx.x; i < kQrNb * kQrNb; i += blockDim.x) sT[i] = T[i];
+  wy_apply<true>(qsm, A, A, r, j0, nbp, c0, min(kQrChunk, c - c0));
 }
 
 // Y = R^H (c x c, ld c): Y[i][j] = conj(R[j][i]) for j <= i, else 0.
@@ -386,18 +428,13 @@ __global__ void __launch_bounds__(512) dq_sort_kernel(ItemMeta* meta, const doub
 // L[:, 0:keep] <- (I - V T V^H) L for the panel's Householder block (V from the
 // first QR, stored below the diagonal of X; T rebuilt from tau1). Called for the
 // panels in reverse order so that L <- H_1 ... H_c L = Q1 L.
-constexpr size_t kQ1Smem =
-    (size_t)(kQrRB * (kQrNb + 1) + kQrRB * kQrLdA + kQrNb * kQrLdA + kQrNb * kQrNb) *
-    sizeof(double2);
-static_assert(kQrNb * kQrNb <= kQrRB * kQrLdA, "S aliases the A staging block");
+constexpr size_t kQ1Smem = kWyApplySmem;
+static_assert(kQrNb * kQrNb <= 2 * kQrStage, "S aliases the staging buffers");
 
 __global__ void __launch_bounds__(256) dq_apply_q1_kernel(QrArgs a) {
   extern __shared__ __align__(16) double2 qsm[];
-  double2* sV = qsm;                                 // [kQrRB][kQrNb + 1]
-  double2* sA = sV + kQrRB * (kQrNb + 1);            // [kQrRB][kQrLdA]
-  double2* sW = sA + kQrRB * kQrLdA;                 // [kQrNb][kQrLdA]
-  double2* sT = sW + kQrNb * kQrLdA;                 // [kQrNb][kQrNb]
-  double2* sS = sA;                                  // [kQrNb][kQrNb], dead before staging
+  double2* sT = qsm + 2 * kQrStage + kQrNb * kQrLdA;  // [kQrNb][kQrNb]
+  double2* sS = qsm;                                  // [kQrNb][kQrNb], dead before staging
   const int item = blockIdx.y;
   const ItemMeta* m = a.meta + item;
   if (!m->dq || !m->msel || m->status) return;
@@ -408,12 +445,10 @@ __global__ void __launch_bounds__(256) dq_apply_q1_kernel(QrArgs a) {
   const int nbp = j1 - j0;
   const int c0 = blockIdx.x * kQrChunk;
   if (c0 >= keep) return;
-  const int nc = min(kQrChunk, keep - c0);
   const double2* V = a.X + (size_t)item * a.mat_stride;      // Householder vectors of QR 1
   const double2* tau = a.aux + (size_t)item * a.aux_stride;  // tau1
   double2* Lm = a.Y + (size_t)item * a.mat_stride;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int kr = lane & 3, rc = lane >> 2;
   // S = V^H V (strict upper part), then T by the forward recurrence
   for (int p = warp; p < nbp * nbp; p += 8) {
     const int x = p / nbp, y = p % nbp;
@@ -432,93 +467,7 @@ __global__ void __launch_bounds__(256) dq_apply_q1_kernel(QrArgs a) {
   __syncthreads();
   if (warp == 0) build_t(sT, sS, kQrNb, tau + j0, nbp);
   __syncthreads();
-  auto stage = [&](int rb) {
-    for (int i = tid; i < kQrRB * kQrNb; i += blockDim.x) {
-      const int row = i % kQrRB, p = i / kQrRB;
-      const int gr = rb + row, k = j0 + p;
-      double2 v = make_double2(0.0, 0.0);
-      if (p < nbp && gr < r) {
-        if (gr == k) v = make_double2(1.0, 0.0);
-        else if (gr > k) v = V[(size_t)k * r + gr];
-      }
-      sV[row * (kQrNb + 1) + p] = v;
-    }
-    for (int i = tid; i < kQrRB * kQrChunk; i += blockDim.x) {
-      const int row = i % kQrRB, q = i / kQrRB;
-      const int gr = rb + row;
-      sA[row * kQrLdA + q] =
-          (gr < r && q < nc) ? Lm[(size_t)(c0 + q) * r + gr] : make_double2(0.0, 0.0);
-    }
-  };
-  double acc[4][4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
-  const int tr = warp / kWPR, tc0 = (warp % kWPR) * kNU;
-  for (int rb = j0; rb < r; rb += kQrRB) {
-    __syncthreads();
-    stage(rb);
-    __syncthreads();
-#pragma unroll
-    for (int k4 = 0; k4 < kQrRB / 4; ++k4) {
-      const int k = k4 * 4 + kr;
-      const double2 av = cconj(sV[k * (kQrNb + 1) + tr * 8 + rc]);
-#pragma unroll
-      for (int u = 0; u < kNU; ++u) zmma(acc[u], av, sA[k * kQrLdA + (tc0 + u) * 8 + rc]);
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < kNU; ++u)
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-      sW[(tr * 8 + rc) * kQrLdA + (tc0 + u) * 8 + kr * 2 + h] = make_double2(acc[u][h], acc[u][2 + h]);
-  __syncthreads();
-  // W <- T W (T upper triangular)
-  double2 wt[kWU];
-#pragma unroll
-  for (int u = 0; u < kWU; ++u) {
-    const int idx = tid + u * 256;
-    const int p = idx / kQrChunk, q = idx % kQrChunk;
-    double2 sacc = make_double2(0.0, 0.0);
-    for (int zz = p; zz < kQrNb; ++zz) sacc = cfma(sT[p * kQrNb + zz], sW[zz * kQrLdA + q], sacc);
-    wt[u] = sacc;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < kWU; ++u) {
-    const int idx = tid + u * 256;
-    sW[(idx / kQrChunk) * kQrLdA + idx % kQrChunk] = wt[u];
-  }
-  // L -= V W
-  const int orow = warp >> 1, oc0 = (warp & 1) * 4;
-  for (int rb = j0; rb < r; rb += kQrRB) {
-    __syncthreads();
-    stage(rb);
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
-#pragma unroll
-    for (int k4 = 0; k4 < kQrNb / 4; ++k4) {
-      const int k = k4 * 4 + kr;
-      const double2 av = sV[(orow * 8 + rc) * (kQrNb + 1) + k];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) zmma(acc[u], av, sW[k * kQrLdA + (oc0 + u) * 8 + rc]);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int row = orow * 8 + rc, q = (oc0 + u) * 8 + kr * 2 + h;
-        const int gr = rb + row;
-        if (gr < r && q < nc)
-          Lm[(size_t)(c0 + q) * r + gr] =
-              csub(sA[row * kQrLdA + q], make_double2(acc[u][h], acc[u][2 + h]));
-      }
-  }
+  wy_apply<false>(qsm, V, Lm, r, j0, nbp, c0, min(kQrChunk, keep - c0));
 }
 
 }  // namespace bmps
