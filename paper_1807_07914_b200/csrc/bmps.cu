@@ -389,6 +389,7 @@ struct Ws {
   size_t gcache_stride;
   size_t mat_stride;
   size_t aux_stride;
+  int maxp;
   int sig_stride;
 };
 
@@ -414,7 +415,8 @@ size_t ws_layout(int cap, int nitems, char* base, Ws* ws) {
   off = align256(off + sizeof(double2) * mat_stride * nitems);
   const size_t o_z = off;
   off = align256(off + sizeof(double2) * (size_t)(2 * cap) * (2 * cap) * nitems);
-  const size_t aux_stride = 2 * kQrAuxHalf;
+  const int maxp = (2 * cap + kQrNb - 1) / kQrNb;
+  const size_t aux_stride = qr_aux_stride(maxp);
   const size_t o_aux = off;
   off = align256(off + sizeof(double2) * aux_stride * nitems);
   const size_t o_sched = off;
@@ -437,6 +439,7 @@ size_t ws_layout(int cap, int nitems, char* base, Ws* ws) {
     ws->gcache = (double2*)(base + o_gc);
     ws->gcache_stride = gcache_stride;
     ws->aux_stride = aux_stride;
+    ws->maxp = maxp;
     ws->mat_stride = mat_stride;
     ws->sig_stride = sig_stride;
   }
@@ -594,6 +597,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
     qa.aux = ws.aux;
     qa.mat_stride = ws.mat_stride;
     qa.aux_stride = ws.aux_stride;
+    qa.maxp = ws.maxp;
     const int npanels = (cmax + kQrNb - 1) / kQrNb;
     for (int second = 0; second <= (g_double_qr ? 1 : 0); ++second) {
       qa.second = second;
@@ -739,6 +743,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
     qa.aux = ws.aux;
     qa.mat_stride = ws.mat_stride;
     qa.aux_stride = ws.aux_stride;
+    qa.maxp = ws.maxp;
     qa.second = 0;
     const int kq = policy.max_bond > 0 ? std::min(policy.max_bond, cmax) : cmax;
     for (int p = (cmax + kQrNb - 1) / kQrNb - 1; p >= 0; --p) {

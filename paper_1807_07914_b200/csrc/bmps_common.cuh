@@ -7,6 +7,7 @@
 #include "bmps.h"
 
 #define BMPS_DEV __device__ __forceinline__
+#define BMPS_HOSTDEV __host__ __device__
 
 namespace bmps {
 

@@ -68,9 +68,16 @@ struct QrArgs {
   size_t aux_stride;
   int panel;
   int second;        // 0: QR of X (r x c); 1: QR of Y = R1^H (c x c), double-QR items only
+  int maxp;          // panel capacity: the first QR keeps the T of every panel (reused by Q1)
 };
 
-constexpr int kQrAuxHalf = 2048 + kQrNb * kQrNb;
+// aux per item: [tau1: 2048][T1: maxp x kQrNb^2][tau2: 2048][T2: kQrNb^2]
+BMPS_HOSTDEV inline size_t qr_aux_stride(int maxp) {
+  return (size_t)2 * 2048 + (size_t)(maxp + 1) * kQrNb * kQrNb;
+}
+BMPS_DEV double2* qr_tslot(const QrArgs& a, double2* tau) {
+  return tau + 2048 + (a.second ? 0 : (size_t)a.panel * kQrNb * kQrNb);
+}
 
 // matrix, rows and tau/T base of the pass
 BMPS_DEV bool qr_pass(const QrArgs& a, int item, double2*& A, int& rows, double2*& tau) {
@@ -78,7 +85,8 @@ BMPS_DEV bool qr_pass(const QrArgs& a, int item, double2*& A, int& rows, double2
   if (!m->precond || (a.second && !m->dq)) return false;
   A = (a.second ? a.Y : a.X) + (size_t)item * a.mat_stride;
   rows = a.second ? m->c : m->r;
-  tau = a.aux + (size_t)item * a.aux_stride + (a.second ? kQrAuxHalf : 0);
+  tau = a.aux + (size_t)item * a.aux_stride +
+        (a.second ? 2048 + (size_t)a.maxp * kQrNb * kQrNb : 0);
   return true;
 }
 
@@ -107,7 +115,7 @@ __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
   const int j0 = a.panel * kQrNb;
   if (j0 >= c) return;
   const int j1 = min(j0 + kQrNb, c);
-  double2* T = tau + 2048;
+  double2* T = qr_tslot(a, tau);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int k = j0; k < j1; ++k) {
     double2* col = A + (size_t)k * r;
@@ -149,26 +157,43 @@ __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
     }
     __syncthreads();
   }
-  // S = V^H V for the panel (v_k[k] = 1, zero above k)
+  // S = V^H V for the panel on DMMA (v_k[k] = 1, zero above k): 32-row chunks of V
+  // staged in shared memory, warp w accumulates 8x8 tile (w / 4, w % 4)
   const int nbp = j1 - j0;
-  for (int p = warp; p < nbp * nbp; p += blockDim.x >> 5) {
-    const int x = p / nbp, y = p % nbp;
-    if (x >= y) continue;  // only the strict upper part is used
-    const int kx = j0 + x, ky = j0 + y;
-    const double2* vx = A + (size_t)kx * r;
-    const double2* vy = A + (size_t)ky * r;
-    double2 acc = make_double2(0.0, 0.0);
-    // rows >= ky: v_x[ky] is a stored entry, v_y[ky] = 1
-    if (lane == 0) acc = cconj(vx[ky]);
-    for (int i = ky + 1 + lane; i < r; i += 32) acc = cfma(cconj(vx[i]), vy[i], acc);
+  {
+    __shared__ double2 sVc[32][kQrNb + 1];
+    double sacc[4] = {0.0, 0.0, 0.0, 0.0};
+    const int kr = lane & 3, rc = lane >> 2;
+    const int ti = warp >> 2, tj = warp & 3;   // 512 threads: 16 warps cover 4 x 4 tiles
+    const bool own = ti < kQrNb / 8 && tj < kQrNb / 8;
+    for (int rb = j0; rb < r; rb += 32) {
+      for (int i = tid; i < 32 * kQrNb; i += blockDim.x) {
+        const int row = i % 32, p = i / 32;
+        const int gr = rb + row, k = j0 + p;
+        double2 v = make_double2(0.0, 0.0);
+        if (p < nbp && gr < r) {
+          if (gr == k) v = make_double2(1.0, 0.0);
+          else if (gr > k) v = A[(size_t)k * r + gr];
+        }
+        sVc[row][p] = v;
+      }
+      __syncthreads();
+      if (own) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        for (int k4 = 0; k4 < 8; ++k4) {
+          const int k = k4 * 4 + kr;
+          zmma(sacc, cconj(sVc[k][ti * 8 + rc]), sVc[k][tj * 8 + rc]);
+        }
+      }
+      __syncthreads();
     }
-    if (lane == 0) s_S[x][y] = acc;
+    if (own) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        s_S[ti * 8 + rc][tj * 8 + kr * 2 + h] = make_double2(sacc[h], sacc[2 + h]);
+    }
+    __syncthreads();
   }
-  __syncthreads();
   if (warp == 0) build_t(T, &s_S[0][0], kQrNb, tau + j0, nbp);
 }
 
@@ -324,7 +349,7 @@ __global__ void __launch_bounds__(256) qr_update_kernel(QrArgs a) {
   const int c0 = j1 + blockIdx.x * kQrChunk;
   if (c0 >= c || nbp <= 0) return;
   double2* sT = qsm + 2 * kQrStage + kQrNb * kQrLdA;
-  const double2* T = tauw + 2048;
+  const double2* T = qr_tslot(a, tauw);
   for (int i = threadIdx.x; i < kQrNb * kQrNb; i += blockDim.x) sT[i] = T[i];
   wy_apply<true>(qsm, A, A, r, j0, nbp, c0, min(kQrChunk, c - c0));
 }
@@ -429,12 +454,10 @@ __global__ void __launch_bounds__(512) dq_sort_kernel(ItemMeta* meta, const doub
 // first QR, stored below the diagonal of X; T rebuilt from tau1). Called for the
 // panels in reverse order so that L <- H_1 ... H_c L = Q1 L.
 constexpr size_t kQ1Smem = kWyApplySmem;
-static_assert(kQrNb * kQrNb <= 2 * kQrStage, "S aliases the staging buffers");
 
 __global__ void __launch_bounds__(256) dq_apply_q1_kernel(QrArgs a) {
   extern __shared__ __align__(16) double2 qsm[];
   double2* sT = qsm + 2 * kQrStage + kQrNb * kQrLdA;  // [kQrNb][kQrNb]
-  double2* sS = qsm;                                  // [kQrNb][kQrNb], dead before staging
   const int item = blockIdx.y;
   const ItemMeta* m = a.meta + item;
   if (!m->dq || !m->msel || m->status) return;
@@ -446,26 +469,9 @@ __global__ void __launch_bounds__(256) dq_apply_q1_kernel(QrArgs a) {
   const int c0 = blockIdx.x * kQrChunk;
   if (c0 >= keep) return;
   const double2* V = a.X + (size_t)item * a.mat_stride;      // Householder vectors of QR 1
-  const double2* tau = a.aux + (size_t)item * a.aux_stride;  // tau1
+  const double2* T = a.aux + (size_t)item * a.aux_stride + 2048 + (size_t)a.panel * kQrNb * kQrNb;
   double2* Lm = a.Y + (size_t)item * a.mat_stride;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // S = V^H V (strict upper part), then T by the forward recurrence
-  for (int p = warp; p < nbp * nbp; p += 8) {
-    const int x = p / nbp, y = p % nbp;
-    if (x >= y) continue;
-    const int kx = j0 + x, ky = j0 + y;
-    double2 acc = lane == 0 ? cconj(V[(size_t)kx * r + ky]) : make_double2(0.0, 0.0);
-    for (int i = ky + 1 + lane; i < r; i += 32)
-      acc = cfma(cconj(V[(size_t)kx * r + i]), V[(size_t)ky * r + i], acc);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-    }
-    if (lane == 0) sS[x * kQrNb + y] = acc;
-  }
-  __syncthreads();
-  if (warp == 0) build_t(sT, sS, kQrNb, tau + j0, nbp);
+  for (int i = threadIdx.x; i < kQrNb * kQrNb; i += blockDim.x) sT[i] = T[i];  // T1 of this panel
   __syncthreads();
   wy_apply<false>(qsm, V, Lm, r, j0, nbp, c0, min(kQrChunk, keep - c0));
 }
