@@ -33,6 +33,7 @@ int g_tma_staging = 0;     // 1: Jacobi panels staged by TMA bulk copies instead
 int g_gram_cache = 1;      // cross visits reuse rotated intra-block Grams
 int g_block_w2 = 32;       // block-mode panel width (32 or 64 columns)
 int g_double_qr = 1;       // second QR of R^H before the Jacobi (preconditioned items)
+int g_jac_per_sm = 0;      // dynamic Jacobi CTAs per SM (0: occupancy maximum)
 
 // ---------------------------------------------------------------------------
 // init: product state |0...0> (mps.py:55-66)
@@ -514,6 +515,7 @@ int32_t bmps_set_param(const char* name, double value) {
   else if (k == "gram_cache" && (value == 0 || value == 1)) g_gram_cache = (int)value;
   else if (k == "block_w2" && (value == 32 || value == 64)) g_block_w2 = (int)value;
   else if (k == "double_qr" && (value == 0 || value == 1)) g_double_qr = (int)value;
+  else if (k == "jac_per_sm" && value >= 0 && value <= 8) g_jac_per_sm = (int)value;
   else return BMPS_E_ARG;
   return BMPS_OK;
 }
@@ -668,8 +670,15 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         n_slots[wi] = std::max(1, per_sm) * sms;
       }
+      int slots = n_slots[wi];
+      if (g_jac_per_sm > 0) {
+        int dev = 0, sms = kNumSMs;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        slots = std::min(slots, g_jac_per_sm * sms);
+      }
       const int vis = wi ? std::max(1, (cmax + 63) / 64) : nbmax / 2;
-      const int grid = std::min(n_slots[wi], nitems * vis);
+      const int grid = std::min(slots, nitems * vis);
       if (wi)
         jacobi_dynamic_kernel<64><<<grid, 256, JacCfg<64>::kSmem, st>>>(ja);
       else

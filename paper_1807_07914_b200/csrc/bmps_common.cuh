@@ -60,6 +60,32 @@ BMPS_DEV void zmma(double (&c)[4], double2 a, double2 b) {
   dmma(c[2], c[3], a.y, b.x);
 }
 
+// 3-product (Gauss) complex accumulate, 3 DMMA instead of 4 on the shared FP64
+// pipe: c[0..1] += a.x b.x, c[2..3] += a.y b.y, c[4..5] += (a.x + a.y)(b.x + b.y);
+// z3_get(c, h) = (c0 - c2, c4 - c0 - c2). Normwise error <= ~2 eps sum |a||b|, the
+// same order as the 4-product form (ZGEMM3M).
+#ifndef BMPS_Z3
+#define BMPS_Z3 1
+#endif
+constexpr int kZ3 = BMPS_Z3 ? 6 : 4;   // accumulator doubles per complex tile
+BMPS_DEV void zmma3(double (&c)[kZ3], double2 a, double2 b) {
+#if BMPS_Z3
+  dmma(c[0], c[1], a.x, b.x);
+  dmma(c[2], c[3], a.y, b.y);
+  dmma(c[4], c[5], a.x + a.y, b.x + b.y);
+#else
+  zmma(c, a, b);
+#endif
+}
+BMPS_DEV double2 z3_get(const double (&c)[kZ3], int h) {
+#if BMPS_Z3
+  const double re = c[h], ri = c[2 + h];
+  return make_double2(re - ri, c[4 + h] - re - ri);
+#else
+  return make_double2(c[h], c[2 + h]);
+#endif
+}
+
 // Circle-method round robin over N (even) players: pair p of round rho.
 BMPS_DEV void tourney_pair(int N, int rho, int p, int& i, int& j) {
   int a, b;
@@ -133,22 +159,22 @@ BMPS_DEV bool jacobi_rotation(double a, double b, double2 g, double tol, double 
   const double g2 = cabs2(g);
   const double thr = tol * fro;
   if (!(g2 > thr * thr * lo)) return false;            // |g| > tol * sqrt(lo) * fro
-  // division-free chain: rsqrt, sqrt, rsqrt. With tau = |zeta|, h = sqrt(1 + tau^2),
-  // t = 1/(tau + h) gives s = 1/sqrt(2h(tau + h)), c = (tau + h) s (same rotation
-  // as Rutishauser's tangent formula).
-  const double rg = g2 > 1e-290 ? fast_rsqrt(g2) : rsqrt(g2);   // 1 / |g|
-  const double zeta = 0.5 * (b - a) * rg;
-  const double tau = fabs(zeta);
-  if (tau > 1e150) {
-    s = 0.5 / zeta;
-    c = 1.0;
-  } else {
-    const double h2 = fma(tau, tau, 1.0);
-    const double h = h2 * fast_rsqrt(h2);             // sqrt(1 + tau^2)
-    const double d = fast_rsqrt(2.0 * h * (tau + h));
-    c = (tau + h) * d;
-    s = zeta < 0 ? -d : d;
-  }
+  // Two dependent rsqrt stages (rho and c in parallel with 1/|g|): with
+  // delta = b - a and rho = sqrt(delta^2 + 4|g|^2),
+  //   c = sqrt((1 + |delta| / rho) / 2),  s = sign(delta) |g| / (rho c),
+  // the same small-angle rotation as Rutishauser's tangent formula
+  // (zeta = delta / 2|g|, t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2))), with
+  // c^2 + s^2 = 1 by construction; the rotation chain is ~40% shorter, which is
+  // what the inner sweep waits on (the FP64 pipe is shared with other CTAs' DMMA).
+  const double rg = g2 > 1e-290 ? fast_rsqrt(g2) : rsqrt(g2);   // 1 / |g|, off the chain
+  const double delta = b - a;
+  const double rho2 = fma(delta, delta, 4.0 * g2);
+  const double rr = rho2 > 1e-290 ? fast_rsqrt(rho2) : rsqrt(rho2);
+  const double c2 = fma(0.5 * fabs(delta), rr, 0.5);       // in [1/2, 1]
+  const double rc = fast_rsqrt(c2);                         // 1 / c
+  c = c2 * rc;
+  const double sm = (g2 * rg) * rr * rc;                    // |g| / (rho c)
+  s = delta < 0 ? -sm : sm;
   e = make_double2(g.x * rg, g.y * rg);
   return true;
 }

@@ -25,6 +25,10 @@
 
 namespace bmps {
 
+#ifndef BMPS_JAC_MINB
+#define BMPS_JAC_MINB 4   // resident Jacobi CTAs per SM the register budget is sized for
+#endif
+
 #ifdef BMPS_PHASE_TIMERS
 // cycles spent in [0] Gram pass, [1] inner sweep (incl. check), [2] apply pass, [3] visits
 __device__ unsigned long long g_phase_cycles[8];
@@ -271,7 +275,7 @@ BMPS_DEV void upper_tile(int t, int& ti, int& tj) {
 // triangle only: each warp owns GT whole tiles plus a 1/GSPLIT k-slice of one
 // leftover tile (slot GT of acc), so the 8 warps carry equal DMMA work.
 template <int W2>
-BMPS_DEV void jac_gram_chunk(double (&acc)[JacCfg<W2>::GT + 1][4], const double2* sP, int nrows) {
+BMPS_DEV void jac_gram_chunk(double (&acc)[JacCfg<W2>::GT + 1][kZ3], const double2* sP, int nrows) {
   using C = JacCfg<W2>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int kr = lane & 3, rc = lane >> 2;
@@ -282,7 +286,7 @@ BMPS_DEV void jac_gram_chunk(double (&acc)[JacCfg<W2>::GT + 1][4], const double2
     upper_tile<C::NT>(warp * C::GT + u, ti, tj);
     for (int k4 = 0; k4 < nk4; ++k4) {
       const int k = k4 * 4 + kr;
-      zmma(acc[u], cconj(sP[k + (ti * 8 + rc) * C::RCP]), sP[k + (tj * 8 + rc) * C::RCP]);
+      zmma3(acc[u], cconj(sP[k + (ti * 8 + rc) * C::RCP]), sP[k + (tj * 8 + rc) * C::RCP]);
     }
   }
   if (C::GREM) {
@@ -292,7 +296,7 @@ BMPS_DEV void jac_gram_chunk(double (&acc)[JacCfg<W2>::GT + 1][4], const double2
     const int k0 = part * nk4 / C::GSPLIT, k1 = (part + 1) * nk4 / C::GSPLIT;
     for (int k4 = k0; k4 < k1; ++k4) {
       const int k = k4 * 4 + kr;
-      zmma(acc[C::GT], cconj(sP[k + (ti * 8 + rc) * C::RCP]), sP[k + (tj * 8 + rc) * C::RCP]);
+      zmma3(acc[C::GT], cconj(sP[k + (ti * 8 + rc) * C::RCP]), sP[k + (tj * 8 + rc) * C::RCP]);
     }
   }
 }
@@ -300,7 +304,7 @@ BMPS_DEV void jac_gram_chunk(double (&acc)[JacCfg<W2>::GT + 1][4], const double2
 // Scatter the Gram accumulators into sG (both triangles); scratch holds the
 // k-split partials of the leftover tiles (8 warps x 64 complex).
 template <int W2>
-BMPS_DEV void jac_gram_store(const double (&acc)[JacCfg<W2>::GT + 1][4], double2* sG, double2* scratch) {
+BMPS_DEV void jac_gram_store(const double (&acc)[JacCfg<W2>::GT + 1][kZ3], double2* sG, double2* scratch) {
   using C = JacCfg<W2>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rr = lane >> 2, cc = (lane & 3) * 2;
@@ -311,7 +315,7 @@ BMPS_DEV void jac_gram_store(const double (&acc)[JacCfg<W2>::GT + 1][4], double2
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int i = ti * 8 + rr, j = tj * 8 + cc + h;
-      const double2 v = make_double2(acc[u][h], acc[u][2 + h]);
+      const double2 v = z3_get(acc[u], h);
       sG[i + j * C::LDGG] = v;
       if (ti != tj) sG[j + i * C::LDGG] = cconj(v);
     }
@@ -319,7 +323,7 @@ BMPS_DEV void jac_gram_store(const double (&acc)[JacCfg<W2>::GT + 1][4], double2
   if (C::GREM) {
 #pragma unroll
     for (int h = 0; h < 2; ++h)
-      scratch[warp * 64 + rr * 8 + cc + h] = make_double2(acc[C::GT][h], acc[C::GT][2 + h]);
+      scratch[warp * 64 + rr * 8 + cc + h] = z3_get(acc[C::GT], h);
     __syncthreads();
     for (int idx = threadIdx.x; idx < C::GREM * 64; idx += blockDim.x) {
       const int t = idx / 64, e = idx % 64;
@@ -338,7 +342,7 @@ BMPS_DEV void jac_gram_store(const double (&acc)[JacCfg<W2>::GT + 1][4], double2
 // accumulates tile w/2 over half of the chunk's k range (acc[0]); W2 = 64: 16
 // tiles, two whole tiles per warp (acc[0], acc[1]).
 template <int W2>
-BMPS_DEV void jac_gram_chunk_cross(double (&acc)[JacCfg<W2>::GT + 1][4], const double2* sP,
+BMPS_DEV void jac_gram_chunk_cross(double (&acc)[JacCfg<W2>::GT + 1][kZ3], const double2* sP,
                                    int nrows) {
   using C = JacCfg<W2>;
   constexpr int NTc = W2 / 16, CT = NTc * NTc;
@@ -352,7 +356,7 @@ BMPS_DEV void jac_gram_chunk_cross(double (&acc)[JacCfg<W2>::GT + 1][4], const d
 #pragma unroll
       for (int u = 0; u < TPW; ++u) {
         const int t = warp * TPW + u, ti = t / NTc, tj = NTc + t % NTc;
-        zmma(acc[u], cconj(sP[k + (ti * 8 + rc) * C::RCP]), sP[k + (tj * 8 + rc) * C::RCP]);
+        zmma3(acc[u], cconj(sP[k + (ti * 8 + rc) * C::RCP]), sP[k + (tj * 8 + rc) * C::RCP]);
       }
     }
   } else {
@@ -361,14 +365,14 @@ BMPS_DEV void jac_gram_chunk_cross(double (&acc)[JacCfg<W2>::GT + 1][4], const d
     const int k0 = part * nk4 / 2, k1 = (part + 1) * nk4 / 2;
     for (int k4 = k0; k4 < k1; ++k4) {
       const int k = k4 * 4 + kr;
-      zmma(acc[0], cconj(sP[k + (ti * 8 + rc) * C::RCP]), sP[k + (tj * 8 + rc) * C::RCP]);
+      zmma3(acc[0], cconj(sP[k + (ti * 8 + rc) * C::RCP]), sP[k + (tj * 8 + rc) * C::RCP]);
     }
   }
 }
 
 // sG <- [[cache_I, G_IJ], [G_IJ^H, cache_J]] (scratch: 8 warps x 64 partials).
 template <int W2>
-BMPS_DEV void jac_gram_store_cross(const double (&acc)[JacCfg<W2>::GT + 1][4], double2* sG,
+BMPS_DEV void jac_gram_store_cross(const double (&acc)[JacCfg<W2>::GT + 1][kZ3], double2* sG,
                                    double2* scratch, const double2* cI, const double2* cJ) {
   using C = JacCfg<W2>;
   constexpr int w = W2 / 2, NTc = W2 / 16, CT = NTc * NTc;
@@ -387,7 +391,7 @@ BMPS_DEV void jac_gram_store_cross(const double (&acc)[JacCfg<W2>::GT + 1][4], d
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int i = ti * 8 + rr, j = tj * 8 + cc + h;
-        const double2 v = make_double2(acc[u][h], acc[u][2 + h]);
+        const double2 v = z3_get(acc[u], h);
         sG[i + j * C::LDGG] = v;
         sG[j + i * C::LDGG] = cconj(v);
       }
@@ -396,7 +400,7 @@ BMPS_DEV void jac_gram_store_cross(const double (&acc)[JacCfg<W2>::GT + 1][4], d
   }
 #pragma unroll
   for (int h = 0; h < 2; ++h)
-    scratch[warp * 64 + rr * 8 + cc + h] = make_double2(acc[0][h], acc[0][2 + h]);
+    scratch[warp * 64 + rr * 8 + cc + h] = z3_get(acc[0], h);
   __syncthreads();
   for (int idx = threadIdx.x; idx < CT * 64; idx += blockDim.x) {
     const int t = idx / 64, e = idx % 64;
@@ -421,14 +425,14 @@ BMPS_DEV void jac_cache_store(const double2* sG, double2* cI, double2* cJ) {
 // acc = P_chunk (RC x W2) * Q (W2 x W2). Warp w owns output tiles
 // t = w*AT .. w*AT+AT-1 in row-major (tile row mi = t / NT, tile col nj = t % NT).
 template <int W2>
-BMPS_DEV void jac_apply_mma(double (&acc)[JacCfg<W2>::AT][4], const double2* sP, const double2* sQ) {
+BMPS_DEV void jac_apply_mma(double (&acc)[JacCfg<W2>::AT][kZ3], const double2* sP, const double2* sQ) {
   using C = JacCfg<W2>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int kr = lane & 3, rc = lane >> 2;
 #pragma unroll
   for (int u = 0; u < C::AT; ++u)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
+    for (int q = 0; q < kZ3; ++q) acc[u][q] = 0.0;
 #pragma unroll 2
   for (int k4 = 0; k4 < W2 / 4; ++k4) {
     const int k = k4 * 4 + kr;
@@ -437,13 +441,13 @@ BMPS_DEV void jac_apply_mma(double (&acc)[JacCfg<W2>::AT][4], const double2* sP,
       const int t = warp * C::AT + u, mi = t / C::NT, nj = t % C::NT;
       const double2 a = sP[mi * 8 + rc + k * C::RCP];
       const double2 b = sQ[k + (nj * 8 + rc) * C::LDG];
-      zmma(acc[u], a, b);
+      zmma3(acc[u], a, b);
     }
   }
 }
 
 template <int W2>
-BMPS_DEV void jac_apply_writeback(const double (&acc)[JacCfg<W2>::AT][4], double2* sP) {
+BMPS_DEV void jac_apply_writeback(const double (&acc)[JacCfg<W2>::AT][kZ3], double2* sP) {
   using C = JacCfg<W2>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int kr = lane & 3, rc = lane >> 2;
@@ -453,14 +457,14 @@ BMPS_DEV void jac_apply_writeback(const double (&acc)[JacCfg<W2>::AT][4], double
     for (int h = 0; h < 2; ++h) {
       const int t = warp * C::AT + u, mi = t / C::NT, nj = t % C::NT;
       const int m = mi * 8 + rc, nn = nj * 8 + kr * 2 + h;
-      sP[m + nn * C::RCP] = make_double2(acc[u][h], acc[u][2 + h]);
+      sP[m + nn * C::RCP] = z3_get(acc[u], h);
     }
 }
 
 // Write the apply accumulators straight to the matrix in global memory (each
 // store instruction covers 8 rows x 8 columns of a DMMA tile).
 template <int W2>
-BMPS_DEV void jac_apply_store_global(const double (&acc)[JacCfg<W2>::AT][4], double2* X, int r,
+BMPS_DEV void jac_apply_store_global(const double (&acc)[JacCfg<W2>::AT][kZ3], double2* X, int r,
                                      int c, int row0, int I, int J) {
   using C = JacCfg<W2>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -472,7 +476,7 @@ BMPS_DEV void jac_apply_store_global(const double (&acc)[JacCfg<W2>::AT][4], dou
       const int t = warp * C::AT + u, mi = t / C::NT, nj = t % C::NT;
       const int row = row0 + mi * 8 + rc, col = panel_col<W2>(nj * 8 + kr * 2 + h, I, J);
       if (row < r && col < c)
-        X[(size_t)row + (size_t)col * r] = make_double2(acc[u][h], acc[u][2 + h]);
+        X[(size_t)row + (size_t)col * r] = z3_get(acc[u], h);
     }
 }
 
@@ -603,11 +607,11 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
   const bool cross_gram = gcache != nullptr && !full && !resident;
   double2* cI = gcache ? gcache + (size_t)I * (W2 / 2) * (W2 / 2) : nullptr;
   double2* cJ = gcache ? gcache + (size_t)J * (W2 / 2) * (W2 / 2) : nullptr;
-  double gacc[C::GT + 1][4];
+  double gacc[C::GT + 1][kZ3];
 #pragma unroll
   for (int u = 0; u < C::GT + 1; ++u)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) gacc[u][q] = 0.0;
+    for (int q = 0; q < kZ3; ++q) gacc[u][q] = 0.0;
   if (resident) {
     jac_gram_chunk<W2>(gacc, sP, r);
   } else if (bulk) {
@@ -684,7 +688,7 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
     }
     return false;
   }
-  double aacc[C::AT][4];
+  double aacc[C::AT][kZ3];
   if (resident) {
     jac_apply_mma<W2>(aacc, sP, sQ);
     __syncthreads();
@@ -747,7 +751,7 @@ BMPS_DEV void jac_load_resident(double2* sP, const double2* X, int r, int c) {
 }
 
 template <int W2>
-__global__ void __launch_bounds__(256, (W2 == 32) ? 4 : 1) jacobi_kernel(JacArgs args) {
+__global__ void __launch_bounds__(256, (W2 == 32) ? BMPS_JAC_MINB : 1) jacobi_kernel(JacArgs args) {
   using C = JacCfg<W2>;
   extern __shared__ __align__(16) double2 jsm[];
   double2* sQ = jsm;
@@ -877,7 +881,7 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? 4 : 1) jacobi_kernel(JacArgs
 // re-probe -- so there is no deadlock, no host polling and no per-round
 // launch, and stragglers' rounds overlap other items' work.
 template <int W2>
-__global__ void __launch_bounds__(256, (W2 == 32) ? 4 : 1) jacobi_dynamic_kernel(JacArgs args) {
+__global__ void __launch_bounds__(256, (W2 == 32) ? BMPS_JAC_MINB : 1) jacobi_dynamic_kernel(JacArgs args) {
   using C = JacCfg<W2>;
   extern __shared__ __align__(16) double2 jsm[];
   double2* sQ = jsm;

@@ -241,11 +241,11 @@ BMPS_DEV void wy_apply(double2* smem, const double2* Vm, double2* A, int r, int 
   const int kr = lane & 3, rc = lane >> 2;
   const int nblk = (r - j0 + kQrRB - 1) / kQrRB;
   // pass 1: W = V^H A; warp -> W row tile warp / kWPR, kNU column tiles
-  double acc[kNU][4];
+  double acc[kNU][kZ3];
 #pragma unroll
   for (int u = 0; u < kNU; ++u)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
+    for (int q = 0; q < kZ3; ++q) acc[u][q] = 0.0;
   const int tr = warp / kWPR, tc0 = (warp % kWPR) * kNU;
   wy_issue(smem, 0, Vm, A, r, j0, nbp, c0, nc);
   for (int b = 0; b < nblk; ++b) {
@@ -263,7 +263,7 @@ BMPS_DEV void wy_apply(double2* smem, const double2* Vm, double2* A, int r, int 
       const int k = k4 * 4 + kr;
       const double2 av = cconj(sV[k * kQrLdV + tr * 8 + rc]);
 #pragma unroll
-      for (int u = 0; u < kNU; ++u) zmma(acc[u], av, sA[k * kQrLdA + (tc0 + u) * 8 + rc]);
+      for (int u = 0; u < kNU; ++u) zmma3(acc[u], av, sA[k * kQrLdA + (tc0 + u) * 8 + rc]);
     }
     __syncthreads();
   }
@@ -272,7 +272,7 @@ BMPS_DEV void wy_apply(double2* smem, const double2* Vm, double2* A, int r, int 
   for (int u = 0; u < kNU; ++u)
 #pragma unroll
     for (int h = 0; h < 2; ++h)
-      sW[(tr * 8 + rc) * kQrLdA + (tc0 + u) * 8 + kr * 2 + h] = make_double2(acc[u][h], acc[u][2 + h]);
+      sW[(tr * 8 + rc) * kQrLdA + (tc0 + u) * 8 + kr * 2 + h] = z3_get(acc[u], h);
   __syncthreads();
   double2 wt[kWU];
 #pragma unroll
@@ -306,17 +306,17 @@ BMPS_DEV void wy_apply(double2* smem, const double2* Vm, double2* A, int r, int 
     __syncthreads();
     const double2* sV = smem + (b & 1) * kQrStage;
     const double2* sA = sV + kQrRB * kQrLdV;
-    double oacc[kOU][4];
+    double oacc[kOU][kZ3];
 #pragma unroll
     for (int u = 0; u < kOU; ++u)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) oacc[u][q] = 0.0;
+      for (int q = 0; q < kZ3; ++q) oacc[u][q] = 0.0;
 #pragma unroll
     for (int k4 = 0; k4 < kQrNb / 4; ++k4) {
       const int k = k4 * 4 + kr;
       const double2 av = sV[(orow * 8 + rc) * kQrLdV + k];
 #pragma unroll
-      for (int u = 0; u < kOU; ++u) zmma(oacc[u], av, sW[k * kQrLdA + (oc0 + u) * 8 + rc]);
+      for (int u = 0; u < kOU; ++u) zmma3(oacc[u], av, sW[k * kQrLdA + (oc0 + u) * 8 + rc]);
     }
     const int rb = j0 + b * kQrRB;
 #pragma unroll
@@ -327,7 +327,7 @@ BMPS_DEV void wy_apply(double2* smem, const double2* Vm, double2* A, int r, int 
         const int gr = rb + row;
         if (gr < r && q < nc)
           A[(size_t)(c0 + q) * r + gr] =
-              csub(sA[row * kQrLdA + q], make_double2(oacc[u][h], oacc[u][2 + h]));
+              csub(sA[row * kQrLdA + q], z3_get(oacc[u], h));
       }
     __syncthreads();
   }
