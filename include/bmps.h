@@ -161,6 +161,48 @@ int32_t bmps_env_close(const int32_t* dims, int32_t n, int32_t cap, const int32_
                        const double* env_r, int64_t r_stride, int32_t count, double* out,
                        void* stream);
 
+/* ---- dense statevector backend (R:src/mpsqvm/dense.py) --------------------
+ * amps: complex128 [S][2^n], flat index with qubit 0 as the HIGH bit
+ * (dense.py:23); n <= 33. Gates passed by host pointer are read during the
+ * call (kernel parameters); no device allocation. */
+
+/* DenseState.__init__ (dense.py:26-32): |0...0> for each of S states. */
+int32_t bmps_dense_init(double* amps, int32_t S, int32_t n, void* stream);
+
+/* DenseState.apply_one_qubit (dense.py:39-44): gate_host complex128 2x2. */
+int32_t bmps_dense_apply_1q(double* amps, int32_t n, int32_t q, const double* gate_host,
+                            void* stream);
+
+/* DenseState.apply_two_qubit (dense.py:46-54): gate_host complex128 4x4
+ * indexed [2a+b][2s+t], a/s on q1 (the first listed qubit), any q1 != q2. */
+int32_t bmps_dense_apply_2q(double* amps, int32_t n, int32_t q1, int32_t q2,
+                            const double* gate_host, void* stream);
+
+/* dense_run (dense.py:112-123) of S states of n <= 12 qubits in one launch
+ * (state resident in shared memory): ops int32 [S][nops][3] = (arity, q1,
+ * q2), mats complex128 [S][nops][16] (a 2x2 gate in the first 4), device. */
+int32_t bmps_dense_run_smem(double* amps, int32_t S, int32_t n, const int32_t* ops,
+                            const double* mats, int32_t nops, void* stream);
+
+/* DenseState.expectation_pauli / norm_sq (dense.py:61-81) for a batch of
+ * (state, Pauli string): masks uint64 [count][2] = (X|Y bit mask, Z|Y bit
+ * mask), ny int32 [count] = number of Y; out complex128 [count] (the caller
+ * applies the 1e-10 imaginary-residue check). */
+size_t bmps_dense_expect_workspace_bytes(int32_t count);
+int32_t bmps_dense_expect(const double* amps, int32_t S, int32_t n, const int32_t* state_idx,
+                          const uint64_t* masks, const int32_t* ny, int32_t count,
+                          void* workspace, size_t workspace_bytes, double* out, void* stream);
+
+/* Marginal-probability heap for DenseState.conditional_prob_zero / sample
+ * (dense.py:88-110): tree float64 [2^(n+1)], node (level k, prefix v) at
+ * tree[2^k + v], leaves |amp_i|^2 at tree[2^n + i]. */
+int32_t bmps_dense_prob_tree(const double* amps, int32_t n, double* tree, void* stream);
+
+/* DenseState.sample: uniforms float64 [shots][n] (rng.random() draws, one per
+ * qubit per shot in qubit order), out uint64 [shots] basis indices. */
+int32_t bmps_dense_sample(const double* tree, int32_t n, const double* uniforms, int32_t shots,
+                          uint64_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

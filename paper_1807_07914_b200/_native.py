@@ -47,6 +47,14 @@ _SIGNATURES = {
     "bmps_sample": ([_P, _P, _P, _I, _I, _I, _P, _P, _I, _P, _P], _I),
     "bmps_env_transfer": ([_P, _P, _P, _I, _I, _I, _P, _P, _P, _I, _P, _L, _P, _L, _P, _I, _P], _I),
     "bmps_env_close": ([_P, _I, _I, _P, _P, _P, _L, _P, _L, _I, _P, _P], _I),
+    "bmps_dense_init": ([_P, _I, _I, _P], _I),
+    "bmps_dense_apply_1q": ([_P, _I, _I, _P, _P], _I),
+    "bmps_dense_apply_2q": ([_P, _I, _I, _I, _P, _P], _I),
+    "bmps_dense_run_smem": ([_P, _I, _I, _P, _P, _I, _P], _I),
+    "bmps_dense_expect_workspace_bytes": ([_I], _SZ),
+    "bmps_dense_expect": ([_P, _I, _I, _P, _P, _P, _I, _P, _SZ, _P, _P], _I),
+    "bmps_dense_prob_tree": ([_P, _I, _P, _P], _I),
+    "bmps_dense_sample": ([_P, _I, _P, _I, _P, _P], _I),
 }
 
 EXPORTED = tuple(_SIGNATURES)

@@ -1,8 +1,9 @@
 """Execution contract for the MPS backend (``R:src/mpsqvm/backends.py:47-79``).
 
 ``mps_run`` / ``run_program`` keep the reference signatures and semantics
-(MEASURE skipped, register-size check, backend string). Programs run through
-the layered GPU executor instead of a per-gate Python loop.
+(MEASURE skipped, register-size check, backend string; ``backend="dense"`` is
+the GPU statevector of ``dense.py``). Programs run through the layered GPU
+executor instead of a per-gate Python loop.
 ``simulate_batch`` is the batched entry point: many independent programs on
 one device in shared launches (circuits / parameter vectors are
 the natural shard).
@@ -15,12 +16,13 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from .dense import DenseState, dense_run
 from .engine import MpsBatch, compile_batch
 from .ir import num_qubits
 from .mps import MpsState
 from .policy import TruncationPolicy
 
-BACKENDS = ("mps",)
+BACKENDS = ("mps", "dense")
 
 
 def mps_run(program, n: int, policy: TruncationPolicy | None = None, *, device=None) -> MpsState:
@@ -31,15 +33,16 @@ def mps_run(program, n: int, policy: TruncationPolicy | None = None, *, device=N
 
 
 def run_program(program, n: int | None = None, backend: str = "mps",
-                policy: TruncationPolicy | None = None, *, device=None) -> MpsState:
+                policy: TruncationPolicy | None = None, *, device=None) -> MpsState | DenseState:
     if n is None:
         n = num_qubits(program)
     elif n < num_qubits(program):
         raise ValueError(f"program touches qubit {num_qubits(program) - 1}, register has {n}")
     if backend == "mps":
         return mps_run(program, n, policy, device=device)
-    raise ValueError(f"unknown backend {backend!r}; expected one of {BACKENDS} "
-                     "(the dense oracle is out of scope for this framework)")
+    if backend == "dense":
+        return dense_run(program, n, device=device)
+    raise ValueError(f"unknown backend {backend!r}; expected one of {BACKENDS}")
 
 
 def simulate_batch(programs, n: int, policy: TruncationPolicy | None = None, *, device=None,
@@ -81,9 +84,12 @@ def execute(program, n: int | None = None, backend: str = "mps",
     """Run, sample the measured qubits on the GPU, collect stats (``backends.py:87-113``)."""
     start = time.perf_counter()
     state = run_program(program, n, backend, policy, device=device)
-    record = RunRecord(max_bond_seen=state.max_bond_seen,
-                       memory_estimate_bytes=state.memory_estimate_bytes(),
-                       trunc_error_sq=state.trunc_error_sq)
+    if isinstance(state, MpsState):
+        record = RunRecord(max_bond_seen=state.max_bond_seen,
+                           memory_estimate_bytes=state.memory_estimate_bytes(),
+                           trunc_error_sq=state.trunc_error_sq)
+    else:
+        record = RunRecord(memory_estimate_bytes=16 * 2 ** state.n)
     targets = measured_qubits(program)
     if targets and shots > 0:
         full = state.sample(shots, np.random.default_rng(seed))

@@ -11,6 +11,7 @@
 #include <string>
 
 #include "bmps.h"
+#include "bmps_dense.cuh"
 #include "bmps_update.cuh"
 
 using namespace bmps;
@@ -911,6 +912,110 @@ int32_t bmps_env_close(const int32_t* dims, int32_t n, int32_t cap, const int32_
   env_close_kernel<<<count, 256, 0, (cudaStream_t)stream>>>(
       dims, n, cap, state_idx, bond, (const double2*)env_l, (size_t)l_stride,
       (const double2*)env_r, (size_t)r_stride, (double2*)out);
+  ++g_launches;
+  return launch_status();
+}
+
+// ---- dense statevector backend (R:src/mpsqvm/dense.py) ---------------------
+
+namespace {
+int dense_grid(unsigned long long work) {
+  const unsigned long long b = (work + 255) / 256;
+  return (int)std::max(1ull, std::min(b, (unsigned long long)kNumSMs * 8));
+}
+}  // namespace
+
+int32_t bmps_dense_init(double* amps, int32_t S, int32_t n, void* stream) {
+  if (!amps || S < 1 || n < 1 || n > kDenseMaxQubits) return BMPS_E_ARG;
+  const unsigned long long N = 1ull << n;
+  dense_init_kernel<<<dense_grid(N * S), 256, 0, (cudaStream_t)stream>>>((double2*)amps, S, N);
+  ++g_launches;
+  return launch_status();
+}
+
+int32_t bmps_dense_apply_1q(double* amps, int32_t n, int32_t q, const double* gate_host,
+                            void* stream) {
+  if (!amps || !gate_host || n < 1 || n > kDenseMaxQubits || q < 0 || q >= n) return BMPS_E_ARG;
+  DenseGate2 g;
+  for (int k = 0; k < 4; ++k) g.m[k] = make_double2(gate_host[2 * k], gate_host[2 * k + 1]);
+  dense_1q_kernel<<<dense_grid(1ull << (n - 1)), 256, 0, (cudaStream_t)stream>>>(
+      (double2*)amps, n, q, g);
+  ++g_launches;
+  return launch_status();
+}
+
+int32_t bmps_dense_apply_2q(double* amps, int32_t n, int32_t q1, int32_t q2,
+                            const double* gate_host, void* stream) {
+  if (!amps || !gate_host || n < 2 || n > kDenseMaxQubits || q1 < 0 || q1 >= n || q2 < 0 ||
+      q2 >= n || q1 == q2)
+    return BMPS_E_ARG;
+  DenseGate4 g;
+  for (int k = 0; k < 16; ++k) g.m[k] = make_double2(gate_host[2 * k], gate_host[2 * k + 1]);
+  dense_2q_kernel<<<dense_grid(1ull << (n - 2)), 256, 0, (cudaStream_t)stream>>>(
+      (double2*)amps, n, q1, q2, g);
+  ++g_launches;
+  return launch_status();
+}
+
+int32_t bmps_dense_run_smem(double* amps, int32_t S, int32_t n, const int32_t* ops,
+                            const double* mats, int32_t nops, void* stream) {
+  if (nops == 0) return BMPS_OK;
+  if (!amps || !ops || !mats || S < 1 || n < 1 || n > kDenseSmemQubits || nops < 0) return BMPS_E_ARG;
+  const size_t smem = sizeof(double2) << n;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dense_run_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double2) << kDenseSmemQubits));
+    attr = true;
+  }
+  dense_run_smem_kernel<<<S, 512, smem, (cudaStream_t)stream>>>((double2*)amps, n, ops,
+                                                                (const double2*)mats, nops);
+  ++g_launches;
+  return launch_status();
+}
+
+size_t bmps_dense_expect_workspace_bytes(int32_t count) {
+  return sizeof(double2) * (size_t)kDenseExpBlocks * (size_t)std::max(count, 0);
+}
+
+int32_t bmps_dense_expect(const double* amps, int32_t S, int32_t n, const int32_t* state_idx,
+                          const uint64_t* masks, const int32_t* ny, int32_t count,
+                          void* workspace, size_t workspace_bytes, double* out, void* stream) {
+  if (count == 0) return BMPS_OK;
+  if (!amps || !state_idx || !masks || !ny || !out || S < 1 || n < 1 || n > kDenseMaxQubits ||
+      count < 0)
+    return BMPS_E_ARG;
+  if (workspace_bytes < bmps_dense_expect_workspace_bytes(count)) return BMPS_E_WORKSPACE;
+  const unsigned long long N = 1ull << n;
+  const int nblk = (int)std::min<unsigned long long>(kDenseExpBlocks, (N + 255) / 256);
+  cudaStream_t st = (cudaStream_t)stream;
+  dense_expect_partial_kernel<<<dim3(nblk, count), 256, 0, st>>>(
+      (const double2*)amps, n, state_idx, (const unsigned long long*)masks, (double2*)workspace);
+  ++g_launches;
+  dense_expect_final_kernel<<<(count + 127) / 128, 128, 0, st>>>((const double2*)workspace, nblk,
+                                                                  ny, count, (double2*)out);
+  ++g_launches;
+  return launch_status();
+}
+
+int32_t bmps_dense_prob_tree(const double* amps, int32_t n, double* tree, void* stream) {
+  if (!amps || !tree || n < 1 || n > kDenseMaxQubits) return BMPS_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  dense_tree_leaves_kernel<<<dense_grid(1ull << n), 256, 0, st>>>((const double2*)amps, n, tree);
+  ++g_launches;
+  for (int k = n - 1; k >= 0; --k) {
+    dense_tree_level_kernel<<<dense_grid(1ull << k), 256, 0, st>>>(tree, k);
+    ++g_launches;
+  }
+  return launch_status();
+}
+
+int32_t bmps_dense_sample(const double* tree, int32_t n, const double* uniforms, int32_t shots,
+                          uint64_t* out, void* stream) {
+  if (shots == 0) return BMPS_OK;
+  if (!tree || !uniforms || !out || n < 1 || n > kDenseMaxQubits || shots < 0) return BMPS_E_ARG;
+  dense_sample_kernel<<<(shots + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+      tree, n, uniforms, shots, (unsigned long long*)out);
   ++g_launches;
   return launch_status();
 }

@@ -1,4 +1,4 @@
-"""VQE energies and the one-parameter sweep driver on the MPS backend.
+"""VQE energies and the one-parameter sweep driver on the MPS and dense backends.
 
 Restates ``R:src/mpsqvm/vqe.py``: E = sum_k c_k <P_k> summed left to right in
 term order (analytic, ``:87-89``), or with ``shots`` each non-identity term
@@ -6,8 +6,8 @@ estimated from the parity of samples of the basis-rotated state (``:40-67``,
 ``:90-97``) with the reference's per-term generator ``default_rng([seed, k])``.
 The GPU path differs only in scheduling: every grid point (and, with shots,
 every (grid point, term) state) of a ``sweep`` is one state of a shared
-``MpsBatch`` run in the same launches, instead of one ``run_program`` per
-point. Sampling consumes the same uniforms in the same order as
+``MpsBatch`` (``backend="mps"``) or ``DenseBatch`` (``backend="dense"``) run in
+the same launches, instead of one ``run_program`` per point. Sampling consumes the same uniforms in the same order as
 ``MpsState.sample`` (``mps.py:206-237``), so counts are identical.
 """
 
@@ -18,7 +18,8 @@ from math import pi, sqrt
 
 import numpy as np
 
-from .backends import simulate_batch
+from .backends import BACKENDS, simulate_batch
+from .dense import DenseBatch
 from .ir import GateKind, Instruction, bind_parameters, flatten, num_qubits
 from .policy import TruncationPolicy
 
@@ -77,9 +78,14 @@ def _basis_rotations(pauli: str) -> list[Instruction]:
 
 
 def _check_backend(backend: str) -> None:
-    if backend != "mps":
-        raise ValueError(f"unknown backend {backend!r}; expected one of ('mps',) "
-                         "(the dense oracle is out of scope for this framework)")
+    if backend not in BACKENDS:
+        raise ValueError(f"unknown backend {backend!r}; expected one of {BACKENDS}")
+
+
+def _simulate(programs, n: int, backend: str, policy, device):
+    if backend == "dense":
+        return DenseBatch(len(programs), n, device=device).run(programs)
+    return simulate_batch(programs, n, policy, device=device)
 
 
 def _parity_value(counts: dict[str, int], support: list[int], shots: int) -> float:
@@ -107,7 +113,7 @@ def grid_energies(ansatz, thetas, hamiltonian, backend: str = "mps",
         paulis = [p for _, p in terms]
         coeffs = [c for c, _ in terms]
         for a in range(0, len(programs), _MAX_STATES_PER_BATCH):
-            batch = simulate_batch(programs[a:a + _MAX_STATES_PER_BATCH], n, policy, device=device)
+            batch = _simulate(programs[a:a + _MAX_STATES_PER_BATCH], n, backend, policy, device)
             out.extend(float(e) for e in batch_energies(batch, paulis, coeffs))
         return out
     # sampled: one state per (grid point, non-identity term)
@@ -117,7 +123,7 @@ def grid_energies(ansatz, thetas, hamiltonian, backend: str = "mps",
     for a in range(0, len(jobs), _MAX_STATES_PER_BATCH):
         chunk = jobs[a:a + _MAX_STATES_PER_BATCH]
         progs = [programs[v] + _basis_rotations(terms[k][1]) for v, k in chunk]
-        batch = simulate_batch(progs, n, policy, device=device)
+        batch = _simulate(progs, n, backend, policy, device)
         for s, (v, k) in enumerate(chunk):
             rng = np.random.default_rng([0 if seed is None else seed, k])
             counts = batch.sample(s, shots, rng)
