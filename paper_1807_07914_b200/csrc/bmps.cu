@@ -35,6 +35,7 @@ int g_gram_cache = 1;      // cross visits reuse rotated intra-block Grams
 int g_block_w2 = 32;       // block-mode panel width (32 or 64 columns)
 int g_double_qr = 1;       // second QR of R^H before the Jacobi (preconditioned items)
 int g_jac_per_sm = 0;      // dynamic Jacobi CTAs per SM (0: occupancy maximum)
+int g_col_sort = 1;        // descending-norm column order ahead of the first QR (double-QR items)
 
 // ---------------------------------------------------------------------------
 // init: product state |0...0> (mps.py:55-66)
@@ -517,6 +518,7 @@ int32_t bmps_set_param(const char* name, double value) {
   else if (k == "block_w2" && (value == 32 || value == 64)) g_block_w2 = (int)value;
   else if (k == "double_qr" && (value == 0 || value == 1)) g_double_qr = (int)value;
   else if (k == "jac_per_sm" && value >= 0 && value <= 8) g_jac_per_sm = (int)value;
+  else if (k == "col_sort" && (value == 0 || value == 1)) g_col_sort = (int)value;
   else return BMPS_E_ARG;
   return BMPS_OK;
 }
@@ -584,10 +586,16 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   const int tpd = (dim_bound + 31) / 32;
   theta_kernel<<<dim3(tpd * tpd, nitems), 256, kThetaSmem, st>>>(
       sv, items, (const double2*)gates, ws.meta, ws.M0, ws.X, ws.mat_stride, tpd, g_qr_min_cols,
-      g_double_qr);
+      g_double_qr, g_col_sort);
   ++g_launches;
   int32_t rc = launch_status();
   if (rc) return rc;
+  const int cmax0 = 2 * dim_bound;
+  if (g_col_sort && g_double_qr && cmax0 >= g_qr_min_cols) {
+    dq_colsort_kernel<<<nitems, 512, 0, st>>>(ws.meta, ws.M0, ws.X, ws.mat_stride);
+    ++g_launches;
+    if ((rc = launch_status())) return rc;
+  }
 
   // K3a Householder QR preconditioner (items with c >= qr_min_cols)
   const int cmax = 2 * dim_bound;

@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* ite
                                                     const double2* gates, ItemMeta* meta,
                                                     double2* M0, double2* X, size_t mat_stride,
                                                     int tiles_per_dim, int qr_min_cols,
-                                                    int double_qr) {
+                                                    int double_qr, int col_sort) {
   __shared__ __align__(16) double2 sA[kKC][kLds];
   __shared__ __align__(16) double2 sB[kKC][kLds];
   __shared__ double2 sG[16];
@@ -123,6 +123,10 @@ __global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* ite
   __syncthreads();
   double2* m0p = M0 + (size_t)item * mat_stride;
   double2* xp = X + (size_t)item * mat_stride;
+  // double-QR items get their working copy from dq_colsort_kernel (columns in
+  // descending-norm order), the others straight from here
+  const int ccols = orient == 0 ? 2 * dr : 2 * dl;
+  const bool write_x = !(col_sort && double_qr && ccols >= qr_min_cols);
   double fro = 0.0;
   for (int idx = tid; idx < 32 * 32; idx += 256) {
     // orient 0 writes (2l+a) contiguous -> l fastest; orient 1 writes (b*dr+r) -> r fastest
@@ -147,7 +151,7 @@ __global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* ite
         v = cconj(v);
       }
       m0p[off] = v;
-      xp[off] = v;
+      if (write_x) xp[off] = v;
       fro += cabs2(v);
     }
   }
