@@ -21,6 +21,7 @@ the reference's own einsum/LAPACK calls) on a bounded sample of the same step.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -48,6 +49,13 @@ def nominal_update_flops(dl: int, dm: int, dr: int, keep: int) -> float:
     m, n = 2 * dl, 2 * dr
     p, q = min(m, n), max(m, n)
     return 32.0 * dl * dm * dr + 128.0 * dl * dr + 4.0 * (14.0 * q * p * p + 8.0 * p ** 3)
+
+
+def svd_flops(dl: int, dr: int) -> float:
+    """SURVEY.md §8(d) F_svd: Golub-Kahan thin SVD with U1 and V, x4 for complex."""
+    m, n = 2 * dl, 2 * dr
+    p, q = min(m, n), max(m, n)
+    return 4.0 * (14.0 * q * p * p + 8.0 * p ** 3)
 
 
 def update_bytes(dl: int, dm: int, dr: int, keep: int) -> float:
@@ -250,6 +258,11 @@ def main() -> None:
         batch.execute(plans[k], mode=args.mode)
     batch.check_status()
     barrier()
+    # live device time of the dominant stage (K3, the SVD) from CUDA events the
+    # library records on its launch stream around that stage of every update batch
+    svd_ms, svd_n = ctypes.c_double(0.0), ctypes.c_int32(0)
+    lib.bmps_svd_time(ctypes.byref(svd_ms), ctypes.byref(svd_n))
+    lib.bmps_set_param(b"time_svd", 1.0)
     l0 = lib.bmps_launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -260,6 +273,9 @@ def main() -> None:
         e1.record(stream)
         barrier()
     launches = int(lib.bmps_launch_count() - l0)
+    lib.bmps_set_param(b"time_svd", 0.0)
+    lib.bmps_svd_time(ctypes.byref(svd_ms), ctypes.byref(svd_n))
+    svd_launch_ms = svd_ms.value / max(svd_n.value, 1)
     ms = e0.elapsed_time(e1)
     batch.check_status()
     sw = batch.last_sweeps(int(upd[total_steps - 1]))
@@ -302,7 +318,10 @@ def main() -> None:
     line = None
     if rank == 0:
         f_upd = nominal_update_flops(CHI, CHI, CHI, CHI)
-        achieved = f_upd * value / world / 1e12   # per GPU
+        f_svd = svd_flops(CHI, CHI)
+        step_achieved = f_upd * value / world / 1e12   # per GPU, whole update
+        upd_per_launch = n_upd / max(svd_n.value, 1)
+        achieved = f_svd * upd_per_launch / (svd_launch_ms / 1e3) / 1e12
         prof = {}
         tp = ROOT / "profiles" / "r01_traffic.json"
         if tp.exists():
@@ -318,15 +337,25 @@ def main() -> None:
                        "chi256_pairs_per_replica": [len(f) for f in full],
                        "l2": "inputs larger than L2 (states + workspace > 126 MB), no flush",
                        "parallelism": f"dp{world} (independent replicas)"},
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+            "roofline": {"bound": "tensor",
+                         "kernel": "K3 SVD stage (column sort + double Householder QR + block Jacobi "
+                                   "+ Q1 epilogue), one launch sequence per bulk layer",
+                         "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
-                         "traffic": prof.get("dram_bytes_per_update"),
-                         "traffic_unit": "DRAM bytes per chi=256 update (ncu capture, profiles/r01_traffic.json)",
-                         "executed_fp64_tflops": (prof["fp64_tensor_flops_per_update"] * value / world / 1e12
-                                                  if prof else None),
-                         "basis": "nominal SURVEY §8(d) flops per chi=256 update "
-                                  f"({f_upd:.4g}) x updates / device step time; peak = measured "
-                                  "FP64 cuBLAS ZGEMM (MEASURED_PEAKS.json has no FP64 entry)",
+                         "traffic": (prof["svd_dram_bytes_per_update"] * upd_per_launch
+                                     if "svd_dram_bytes_per_update" in prof else None),
+                         "traffic_unit": "DRAM bytes per K3 launch sequence (ncu launch list, "
+                                         "profiles/r01_traffic.json, per update x updates per launch)",
+                         "algorithmic_flops_per_launch": f_svd * upd_per_launch,
+                         "svd_launch_ms": svd_launch_ms, "svd_share_of_step": svd_ms.value / ms,
+                         "basis": f"F_svd = 4(14 q p^2 + 8 p^3) = {f_svd:.4g} flop per chi=256 update "
+                                  "(SURVEY §8(d), Golub-Kahan count, not Jacobi's executed work) x "
+                                  "updates per launch / live CUDA-event time of the stage; peak = "
+                                  "measured FP64 (cuBLAS ZGEMM 4096^3 / DMMA probe, tools/fp64_peaks.py; "
+                                  "MEASURED_PEAKS.json has no FP64 entry)",
+                         "executed_fp64_tensor_flops_per_update": prof.get("fp64_tensor_flops_per_update"),
+                         "step": {"achieved": step_achieved, "frac": step_achieved / FP64_PEAK_TFLOPS,
+                                  "basis": f"whole update F = {f_upd:.4g} flop x updates / step time"},
                          "nominal_bytes_per_update": update_bytes(CHI, CHI, CHI, CHI)},
             "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),

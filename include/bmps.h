@@ -57,6 +57,13 @@ typedef struct bmps_policy {
   int32_t relative;  /* TruncationPolicy.relative (mps.py:35) */
 } bmps_policy;
 
+/* Device time of the SVD stage (column sort + QR preconditioner + Jacobi +
+ * double-QR epilogue) summed over the bmps_apply_2q calls made since the last
+ * call, measured with CUDA events on the calls' streams while the tunable
+ * "time_svd" is 1 (bench.py's roofline of the dominant kernel). Synchronises
+ * on the recorded events; resets the accumulator. */
+int32_t bmps_svd_time(double* total_ms, int32_t* count);
+
 /* ABI version and a human-readable message for a return/status code. */
 int32_t bmps_version(void);
 const char* bmps_status_string(int32_t code);

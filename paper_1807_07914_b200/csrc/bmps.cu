@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "bmps.h"
 #include "bmps_dense.cuh"
@@ -36,6 +37,23 @@ int g_block_w2 = 32;       // block-mode panel width (32 or 64 columns)
 int g_double_qr = 1;       // second QR of R^H before the Jacobi (preconditioned items)
 int g_jac_per_sm = 0;      // dynamic Jacobi CTAs per SM (0: occupancy maximum)
 int g_col_sort = 1;        // descending-norm column order ahead of the first QR (double-QR items)
+int g_time_svd = 0;        // record CUDA events around the SVD stage (bmps_svd_time)
+
+// CUDA-event pairs bracketing the SVD stage (K3: column sort, QR preconditioner,
+// Jacobi, double-QR epilogue) of each bmps_apply_2q call while g_time_svd is set.
+struct SvdTimer {
+  std::vector<cudaEvent_t> ev;  // 2 per recorded call
+  size_t used = 0;
+  cudaEvent_t next() {
+    if (used == ev.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev.push_back(e);
+    }
+    return ev[used++];
+  }
+};
+SvdTimer g_svd_timer;
 
 // ---------------------------------------------------------------------------
 // init: product state |0...0> (mps.py:55-66)
@@ -519,7 +537,25 @@ int32_t bmps_set_param(const char* name, double value) {
   else if (k == "double_qr" && (value == 0 || value == 1)) g_double_qr = (int)value;
   else if (k == "jac_per_sm" && value >= 0 && value <= 8) g_jac_per_sm = (int)value;
   else if (k == "col_sort" && (value == 0 || value == 1)) g_col_sort = (int)value;
+  else if (k == "time_svd" && (value == 0 || value == 1)) g_time_svd = (int)value;
   else return BMPS_E_ARG;
+  return BMPS_OK;
+}
+
+int32_t bmps_svd_time(double* total_ms, int32_t* count) {
+  if (!total_ms || !count) return BMPS_E_ARG;
+  double t = 0.0;
+  const int n = (int)(g_svd_timer.used / 2);
+  for (int i = 0; i < n; ++i) {
+    float ms = 0.f;
+    cudaEventSynchronize(g_svd_timer.ev[2 * i + 1]);
+    if (cudaEventElapsedTime(&ms, g_svd_timer.ev[2 * i], g_svd_timer.ev[2 * i + 1]) != cudaSuccess)
+      return BMPS_E_LAUNCH;
+    t += ms;
+  }
+  g_svd_timer.used = 0;
+  *total_ms = t;
+  *count = n;
   return BMPS_OK;
 }
 
@@ -590,6 +626,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   ++g_launches;
   int32_t rc = launch_status();
   if (rc) return rc;
+  if (g_time_svd) cudaEventRecord(g_svd_timer.next(), st);
   const int cmax0 = 2 * dim_bound;
   if (g_col_sort && g_double_qr && cmax0 >= g_qr_min_cols) {
     dq_colsort_kernel<<<nitems, 512, 0, st>>>(ws.meta, ws.M0, ws.X, ws.mat_stride);
@@ -772,6 +809,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
     if ((rc = launch_status())) return rc;
   }
 
+  if (g_time_svd) cudaEventRecord(g_svd_timer.next(), st);
   // K4 finalize + split
   finalize_kernel<<<nitems, 512, 0, st>>>(sv, items, ws.meta, ws.X, ws.Y, ws.mat_stride, ws.sig,
                                           ws.perm, ws.sig_stride, policy.cutoff, policy.max_bond,

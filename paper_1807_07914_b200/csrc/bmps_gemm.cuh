@@ -59,8 +59,9 @@ BMPS_DEV void gemm_load_chunk(const Op& op, double2 (*sA)[kLds], double2 (*sB)[k
   }
 }
 
-// acc[mi][ni][kZ3]: warp tile 32 x 16 = 4 x 2 DMMA tiles (zmma3 accumulators, read by z3_get).
-BMPS_DEV void gemm_mma_chunk(double (&acc)[4][2][kZ3], const double2 (*sA)[kLds],
+// acc[mi][ni][4]: warp tile 32 x 16 = 4 x 2 DMMA tiles; (re0, re1, im0, im1). The 4-product
+// form here: 8 tiles x 6 accumulators of the 3-product form cost occupancy (measured slower).
+BMPS_DEV void gemm_mma_chunk(double (&acc)[4][2][4], const double2 (*sA)[kLds],
                              const double2 (*sB)[kLds], int wm, int wn, int lane) {
   const int kr = lane & 3, rc = lane >> 2;
 #pragma unroll
@@ -73,7 +74,7 @@ BMPS_DEV void gemm_mma_chunk(double (&acc)[4][2][kZ3], const double2 (*sA)[kLds]
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni) zmma3(acc[mi][ni], a[mi], b[ni]);
+      for (int ni = 0; ni < 2; ++ni) zmma(acc[mi][ni], a[mi], b[ni]);
   }
 }
 
@@ -87,13 +88,13 @@ __global__ void __launch_bounds__(256) gemm_kernel(Op op) {
   if (m0 >= M || n0 >= N) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 2, wn = warp & 3;
-  double acc[4][2][kZ3];
+  double acc[4][2][4];
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
-      for (int q = 0; q < kZ3; ++q) acc[mi][ni][q] = 0.0;
+      for (int q = 0; q < 4; ++q) acc[mi][ni][q] = 0.0;
   for (int k0 = 0; k0 < K; k0 += kKC) {
     gemm_load_chunk(op, sA, sB, M, N, K, m0, n0, k0, tid);
     __syncthreads();
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(256) gemm_kernel(Op op) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int i = m0 + wm * 32 + mi * 8 + rr, j = n0 + wn * 16 + ni * 8 + cc + h;
-        if (i < M && j < N) op.store(i, j, z3_get(acc[mi][ni], h));
+        if (i < M && j < N) op.store(i, j, make_double2(acc[mi][ni][h], acc[mi][ni][2 + h]));
       }
 }
 

@@ -95,13 +95,13 @@ __global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* ite
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 2, wn = warp & 3;
   if (tid < 16) sG[tid] = gates[(size_t)item * 16 + tid];
-  double acc[4][2][kZ3];
+  double acc[4][2][4];
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
-      for (int q = 0; q < kZ3; ++q) acc[mi][ni][q] = 0.0;
+      for (int q = 0; q < 4; ++q) acc[mi][ni][q] = 0.0;
   for (int k0 = 0; k0 < K; k0 += kKC) {
     gemm_load_chunk(op, sA, sB, M, N, K, m0, n0, k0, tid);
     __syncthreads();
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* ite
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int i = wm * 32 + mi * 8 + rr, j = wn * 16 + ni * 8 + cc + h;
-          sC[i * kThetaLdc + j] = z3_get(acc[mi][ni], h);
+          sC[i * kThetaLdc + j] = make_double2(acc[mi][ni][h], acc[mi][ni][2 + h]);
         }
   }
   __syncthreads();

@@ -9,7 +9,7 @@ h = rows[hi]
 data = rows[hi + 1:]
 ki, mi, ni, ui = (h.index(x) for x in ('Kernel Name', 'Metric Value', 'Metric Name', 'Metric Unit'))
 SC = {'nsecond': 1e-6, 'ns': 1e-6, 'usecond': 1e-3, 'us': 1e-3, 'msecond': 1.0, 'ms': 1.0,
-      'second': 1e3, 's': 1e3, 'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9}
+      'second': 1e3, 's': 1e3, 'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9, '': 1, 'inst': 1}
 agg = collections.defaultdict(lambda: collections.defaultdict(float))
 cnt = collections.Counter()
 for r in data:

@@ -21,3 +21,4 @@ e1.record(); torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStop()
 b.check_status()
 print("step ms", e0.elapsed_time(e1) / a.steps)
+print("updates", sum(1 for k in range(a.steps) for p in [bench.bulk_layer(k + 1, r, full[r]) for r in range(R)] for op in p if len(op.qubits) == 2))
