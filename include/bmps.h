@@ -45,6 +45,8 @@ extern "C" {
 #define BMPS_E_ARG -1
 #define BMPS_E_LAUNCH -2
 #define BMPS_E_WORKSPACE -3
+#define BMPS_PLAN_E_SITE -10       /* planner: site out of range (mps.py:161-163) */
+#define BMPS_PLAN_E_SAME_SITE -11  /* planner: two-qubit gate on one site (mps.py:146-147) */
 /* per-state numerical status (status[] words) */
 #define BMPS_S_OK 0
 #define BMPS_S_SVD_FAILED 1        /* mps.py:117-118 "SVD failed on bond q" */
@@ -209,6 +211,23 @@ int32_t bmps_dense_prob_tree(const double* amps, int32_t n, double* tree, void* 
  * qubit per shot in qubit order), out uint64 [shots] basis indices. */
 int32_t bmps_dense_sample(const double* tree, int32_t n, const double* uniforms, int32_t shots,
                           uint64_t* out, void* stream);
+
+/* ---- host-side program planner (engine.compile_batch; no device work) ------
+ * Input: the ops of nprogs programs concatenated (MEASUREs already dropped),
+ * program p = ops [prog_off[p], prog_off[p+1]) for state prog_state[p];
+ * arity 1/2, sites q1 (and q2 for arity 2, any order, any distance).
+ * Output per EXPANDED op (SWAP routing of mps.py:138-157 applied, in program
+ * order): state, arity, site (the left site of a two-site op), x_src = source
+ * op index (>= 0), -i-2 for source op i applied as SWAP.G.SWAP (q1 > q2), -1
+ * for a routing SWAP; x_layer = ASAP layer within the program; x_rec = the
+ * op's record index (two-site ops numbered in program order across the batch)
+ * or -1. On BMPS_PLAN_E_* *err_op is the offending source op. */
+int64_t bmps_plan_expanded_count(const int8_t* arity, const int32_t* q1, const int32_t* q2,
+                                 int64_t nops);
+int32_t bmps_plan_build(int32_t nprogs, const int64_t* prog_off, const int32_t* prog_state,
+                        const int8_t* arity, const int32_t* q1, const int32_t* q2, int32_t n,
+                        int32_t* x_state, int8_t* x_arity, int32_t* x_site, int64_t* x_src,
+                        int32_t* x_layer, int64_t* x_rec, int64_t* err_op);
 
 #ifdef __cplusplus
 }

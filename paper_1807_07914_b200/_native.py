@@ -18,6 +18,8 @@ BMPS_S_OK = 0
 BMPS_S_SVD_FAILED = 1
 BMPS_S_ALL_TRUNCATED = 2
 BMPS_S_CAPACITY = 3
+BMPS_PLAN_E_SITE = -10
+BMPS_PLAN_E_SAME_SITE = -11
 
 
 class BmpsPolicy(ctypes.Structure):
@@ -48,6 +50,8 @@ _SIGNATURES = {
     "bmps_sample": ([_P, _P, _P, _I, _I, _I, _P, _P, _I, _P, _P], _I),
     "bmps_env_transfer": ([_P, _P, _P, _I, _I, _I, _P, _P, _P, _I, _P, _L, _P, _L, _P, _I, _P], _I),
     "bmps_env_close": ([_P, _I, _I, _P, _P, _P, _L, _P, _L, _I, _P, _P], _I),
+    "bmps_plan_expanded_count": ([_P, _P, _P, _L], _L),
+    "bmps_plan_build": ([_I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P], _I),
     "bmps_dense_init": ([_P, _I, _I, _P], _I),
     "bmps_dense_apply_1q": ([_P, _I, _I, _P, _P], _I),
     "bmps_dense_apply_2q": ([_P, _I, _I, _I, _P, _P], _I),

@@ -10,7 +10,7 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SOURCES = [PKG / "csrc" / "bmps.cu"]
+SOURCES = [PKG / "csrc" / "bmps.cu", PKG / "csrc" / "bmps_plan.cpp"]
 DEPS = SOURCES + sorted((PKG / "csrc").glob("*.cuh")) + [ROOT / "include" / "bmps.h"]
 OUT = PKG / "libbmps.so"
 

@@ -111,7 +111,7 @@ def test_workload_generators_deterministic():
 
 def _header_functions():
     text = (ROOT / "include" / "bmps.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int32_t|size_t|uint64_t|const char\*)\s+(bmps_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int32_t|int64_t|size_t|uint64_t|const char\*)\s+(bmps_\w+)\(", text, re.M)))
 
 
 def test_library_exports_every_header_symbol():
@@ -168,3 +168,54 @@ def test_reference_instruction_objects_are_accepted():
             np.testing.assert_array_equal(gate_matrix(o), ref_gate_matrix(o))
     finally:
         sys.path.remove(ref_src)
+
+
+def _python_plan(programs, n):
+    """compile_batch restated with the Python lowering/layering (the readable spec)."""
+    lay_l, st_l, ar_l, site_l, mat_l, rec_l, ranges, rb = [], [], [], [], [], [], [], 0
+    for s, prog in enumerate(programs):
+        ar, st, mats = lower_program(prog, n)
+        lay = asap_layers(ar, st, n)
+        two = ar == 2
+        rec = np.full(len(ar), -1, dtype=np.int64)
+        n2 = int(two.sum())
+        rec[two] = rb + np.arange(n2)
+        if n2:
+            ranges.append((s, rb, n2))
+        rb += n2
+        lay_l.append(lay); st_l.append(np.full(len(ar), s, np.int32)); ar_l.append(ar)
+        site_l.append(st); mat_l.extend(mats); rec_l.append(rec)
+    layer, state, ar = np.concatenate(lay_l), np.concatenate(st_l), np.concatenate(ar_l)
+    site, rec = np.concatenate(site_l), np.concatenate(rec_l)
+    order = np.argsort(layer, kind="stable")
+    one, two = order[ar[order] == 1], order[ar[order] == 2]
+    return dict(n_layers=int(layer.max()) + 1,
+                items1=np.stack([state[one], site[one]], 1), items2=np.stack([state[two], site[two]], 1),
+                gates1=np.array([mat_l[i] for i in one]).reshape(-1, 2, 2),
+                gates2=np.array([mat_l[i] for i in two]).reshape(-1, 4, 4),
+                logidx2=rec[two], ranges=np.array(ranges).reshape(-1, 3))
+
+
+def test_native_planner_matches_python_lowering_bit_for_bit():
+    rng = np.random.default_rng(11)
+    progs = [random_program(9, 150, rng) for _ in range(12)] + [[]]
+    progs += [[MatrixGate(haar_unitary(rng), (5, 2)), Instruction(GateKind.RZ, (3,), (0.25,)),
+               MatrixGate(haar_unitary(rng, 2), (1,)), Instruction(GateKind.MEASURE, (0,), (), 0)]]
+    progs += [brick_circuit(9, 6, rng, haar_prob=0.5)]
+    ref = _python_plan(progs, 9)
+    plan = compile_batch(progs, 9)
+    assert plan.n_layers == ref["n_layers"]
+    for key in ("items1", "items2", "logidx2", "ranges"):
+        np.testing.assert_array_equal(getattr(plan, key), ref[key], err_msg=key)
+    for key in ("gates1", "gates2"):   # identical bits, not just close
+        np.testing.assert_array_equal(getattr(plan, key).view(np.uint64), ref[key].view(np.uint64),
+                                      err_msg=key)
+
+
+def test_native_planner_errors_match_reference_messages():
+    with pytest.raises(ValueError, match="site 7 out of range for 6 qubits"):
+        compile_batch([[Instruction(GateKind.X, (1,))], [Instruction(GateKind.CNOT, (2, 7))]], 6)
+    with pytest.raises(ValueError, match="distinct"):
+        compile_batch([[Instruction(GateKind.CZ, (3, 3))]], 6)
+    with pytest.raises(ValueError, match="not unitary"):
+        compile_batch([[MatrixGate(np.ones((2, 2)), (0,))]], 2)
