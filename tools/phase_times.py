@@ -2,7 +2,7 @@
 import ctypes, sys, shutil, numpy as np, torch
 sys.path.insert(0, '.')
 from paper_1807_07914_b200 import _native
-_native.LIB_PATH = __import__('pathlib').Path('tools/libbmps_timers.so')
+_native.LIB_PATH = __import__('pathlib').Path(__import__('os').environ.get('TIMERS_LIB', 'tools/libbmps_timers.so'))
 lib = _native.load()
 import bench
 from paper_1807_07914_b200 import MpsBatch, TruncationPolicy, compile_batch
