@@ -598,7 +598,7 @@ template <int W2>
 BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, double noise2,
                         double fro, bool full, int max_inner, bool resident, double2* sG,
                         double2* sQ, double2* sP, RotShared& rs, JacStage& st, bool tma,
-                        double2* gcache = nullptr) {
+                        double2* gcache = nullptr, bool inner_regs = false) {
   using C = JacCfg<W2>;
   BMPS_TICK(tv0);
   const int nch = (r + C::RC - 1) / C::RC;
@@ -975,7 +975,9 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? BMPS_JAC_MINB : 1) jacobi_dy
     double2* gc = args.gcache ? args.gcache + (size_t)i * args.gcache_stride : nullptr;
     const bool dirty = jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, rho == 0, args.max_inner,
                                      false, sG, sQ, sP, rs, st, args.tma, gc);
-    __threadfence();
+    // release: the CTA barrier orders every thread's panel / Gram-cache stores before
+    // thread 0's GPU-scope fence, which is cumulative (the CUTLASS semaphore pattern);
+    // one fence per visit instead of a MEMBAR.GPU stall in all 256 threads
     __syncthreads();
     if (threadIdx.x == 0) {
       if (dirty) atomicOr(&sc->dirty, 1);
