@@ -205,7 +205,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--replicas", type=int, default=8)
+    ap.add_argument("--replicas", type=int, default=16)
     ap.add_argument("--ref-updates", type=int, default=2)
     ap.add_argument("--mode", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -398,6 +398,26 @@ def main() -> None:
             torch.cuda.synchronize()
             line["cfg3_full_circuit"] = {"s": g0.elapsed_time(g1) / 1e3,
                                          "circuits_per_s": 1e3 / g0.elapsed_time(g1)}
+            # BASELINE config 4's circuits/s (a 256-circuit slice of the 1024; the
+            # public batched path incl. host planning: simulate_batch + <Z0 Z31> +
+            # 16 amplitudes per circuit, one D2H of the results)
+            del b3
+            n4 = 256
+            w4 = W.config4(circuits=n4)
+            from paper_1807_07914_b200 import simulate_batch
+            torch.cuda.synchronize()
+            t4 = time.perf_counter()
+            b4 = simulate_batch(w4.programs, w4.n, TruncationPolicy(w4.cutoff, w4.max_bond))
+            zz = b4.expectations(np.arange(n4, dtype=np.int32), w4.paulis * n4)
+            am = b4.amplitudes(np.repeat(np.arange(n4, dtype=np.int32), 16),
+                               [x for bs in w4.bitstrings for x in bs])
+            torch.cuda.synchronize()
+            dt4 = time.perf_counter() - t4
+            line["cfg4_circuits"] = {"circuits": n4, "s": dt4, "circuits_per_s": n4 / dt4,
+                                     "path": "simulate_batch (host planning included) + "
+                                             "expectations + amplitudes, wall clock",
+                                     "outputs": int(zz.size + am.size)}
+            del b4
         if not args.no_cpu_baseline and world == 1:
             gam = batch.site_tensors(0)
             lam = batch.bond_vectors(0)
