@@ -33,7 +33,7 @@ int g_jacobi_mode = 4;     // block-mode Jacobi: 1 persistent CTA/item, 2 round 
 int g_cluster_size = 8;
 int g_tma_staging = 0;     // 1: Jacobi panels staged by TMA bulk copies instead of cp.async
 int g_gram_cache = 1;      // cross visits reuse rotated intra-block Grams
-int g_block_w2 = 32;       // block-mode panel width (32 or 64 columns)
+int g_block_w2 = 32;       // block-mode panel width: 16, 32, 64 columns, or 0 = auto (16 / 32)
 int g_double_qr = 1;       // second QR of R^H before the Jacobi (preconditioned items)
 int g_jac_per_sm = 0;      // dynamic Jacobi CTAs per SM (0: occupancy maximum)
 int g_col_sort = 1;        // descending-norm column order ahead of the first QR (double-QR items)
@@ -481,6 +481,8 @@ void set_attrs() {
                        (int)JacCfg<32>::kSmem);
   cudaFuncSetAttribute(jacobi_dynamic_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)JacCfg<64>::kSmem);
+  cudaFuncSetAttribute(jacobi_dynamic_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)JacCfg<16>::kSmem);
   g_attrs_set = true;
 }
 
@@ -533,7 +535,8 @@ int32_t bmps_set_param(const char* name, double value) {
   else if (k == "cluster_size" && value >= 1 && value <= 16) g_cluster_size = (int)value;
   else if (k == "tma_staging" && (value == 0 || value == 1)) g_tma_staging = (int)value;
   else if (k == "gram_cache" && (value == 0 || value == 1)) g_gram_cache = (int)value;
-  else if (k == "block_w2" && (value == 32 || value == 64)) g_block_w2 = (int)value;
+  else if (k == "block_w2" && (value == 0 || value == 16 || value == 32 || value == 64))
+    g_block_w2 = (int)value;
   else if (k == "double_qr" && (value == 0 || value == 1)) g_double_qr = (int)value;
   else if (k == "jac_per_sm" && value >= 0 && value <= 8) g_jac_per_sm = (int)value;
   else if (k == "col_sort" && (value == 0 || value == 1)) g_col_sort = (int)value;
@@ -701,34 +704,49 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       cudaMemsetAsync(ws.sched, 0, sizeof(JacSched) * (size_t)nitems, st);
       init_active_kernel<<<1, 32, 0, st>>>(ws.counter, nitems);
       ++g_launches;
-      static int n_slots[2] = {0, 0};
-      const int wi = g_block_w2 == 64 ? 1 : 0;
-      if (!n_slots[wi]) {
-        int per_sm = 0;
-        if (wi)
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_dynamic_kernel<64>, 256,
-                                                        JacCfg<64>::kSmem);
-        else
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_dynamic_kernel<32>, 256,
-                                                        JacCfg<32>::kSmem);
-        int dev = 0, sms = kNumSMs;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        n_slots[wi] = std::max(1, per_sm) * sms;
-      }
-      int slots = n_slots[wi];
+      // panel width by the tunable (default 32). 16 (8-column blocks) quadruples the
+      // visits per round for small batches, but each visit keeps most of a 32-wide
+      // visit's latency: one cfg3 brick layer (16 items) ran 36 -> 41 ms, so the auto
+      // mode (0: 16 when nitems x visits < CTA slots) is off by default
+      static int n_slots[3] = {0, 0, 0};
+      auto slots_of = [&](int wi) {
+        if (!n_slots[wi]) {
+          int per_sm = 0;
+          if (wi == 2)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_dynamic_kernel<64>, 256,
+                                                          JacCfg<64>::kSmem);
+          else if (wi == 1)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_dynamic_kernel<32>, 256,
+                                                          JacCfg<32>::kSmem);
+          else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_dynamic_kernel<16>, 256,
+                                                          JacCfg<16>::kSmem);
+          int dev = 0, sms = kNumSMs;
+          cudaGetDevice(&dev);
+          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+          n_slots[wi] = std::max(1, per_sm) * sms;
+        }
+        return n_slots[wi];
+      };
+      int wi = g_block_w2 == 64 ? 2 : g_block_w2 == 16 ? 0 : 1;
+      if (g_block_w2 == 0) wi = (long long)nitems * (nbmax / 2) < slots_of(1) ? 0 : 1;
+      int slots = slots_of(wi);
       if (g_jac_per_sm > 0) {
         int dev = 0, sms = kNumSMs;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         slots = std::min(slots, g_jac_per_sm * sms);
       }
-      const int vis = wi ? std::max(1, (cmax + 63) / 64) : nbmax / 2;
+      const int vis = wi == 2 ? std::max(1, (cmax + 63) / 64)
+                    : wi == 1 ? nbmax / 2
+                              : (cmax + 15) / 16;
       const int grid = std::min(slots, nitems * vis);
-      if (wi)
+      if (wi == 2)
         jacobi_dynamic_kernel<64><<<grid, 256, JacCfg<64>::kSmem, st>>>(ja);
-      else
+      else if (wi == 1)
         jacobi_dynamic_kernel<32><<<grid, 256, JacCfg<32>::kSmem, st>>>(ja);
+      else
+        jacobi_dynamic_kernel<16><<<grid, 256, JacCfg<16>::kSmem, st>>>(ja);
       ++g_launches;
       if ((rc = launch_status())) return rc;
     } else if (cl_mode == 1) {

@@ -289,7 +289,7 @@ BMPS_DEV void jac_gram_chunk(double (&acc)[JacCfg<W2>::GT + 1][kZ3], const doubl
       zmma3(acc[u], cconj(sP[k + (ti * 8 + rc) * C::RCP]), sP[k + (tj * 8 + rc) * C::RCP]);
     }
   }
-  if (C::GREM) {
+  if (C::GREM && warp / C::GSPLIT < C::GREM) {
     int ti, tj;
     upper_tile<C::NT>(8 * C::GT + warp / C::GSPLIT, ti, tj);
     const int part = warp % C::GSPLIT;
@@ -360,9 +360,10 @@ BMPS_DEV void jac_gram_chunk_cross(double (&acc)[JacCfg<W2>::GT + 1][kZ3], const
       }
     }
   } else {
-    const int t = warp >> 1, part = warp & 1;
+    constexpr int KS = CT < 8 ? 8 / CT : 1;   // warps sharing one tile (k-split)
+    const int t = warp / KS, part = warp % KS;
     const int ti = t / NTc, tj = NTc + t % NTc;
-    const int k0 = part * nk4 / 2, k1 = (part + 1) * nk4 / 2;
+    const int k0 = part * nk4 / KS, k1 = (part + 1) * nk4 / KS;
     for (int k4 = k0; k4 < k1; ++k4) {
       const int k = k4 * 4 + kr;
       zmma3(acc[0], cconj(sP[k + (ti * 8 + rc) * C::RCP]), sP[k + (tj * 8 + rc) * C::RCP]);
@@ -402,9 +403,11 @@ BMPS_DEV void jac_gram_store_cross(const double (&acc)[JacCfg<W2>::GT + 1][kZ3],
   for (int h = 0; h < 2; ++h)
     scratch[warp * 64 + rr * 8 + cc + h] = z3_get(acc[0], h);
   __syncthreads();
+  constexpr int KS = CT < 8 ? 8 / CT : 1;
   for (int idx = threadIdx.x; idx < CT * 64; idx += blockDim.x) {
     const int t = idx / 64, e = idx % 64;
-    const double2 v = cadd(scratch[(2 * t) * 64 + e], scratch[(2 * t + 1) * 64 + e]);
+    double2 v = scratch[(KS * t) * 64 + e];
+    for (int k = 1; k < KS; ++k) v = cadd(v, scratch[(KS * t + k) * 64 + e]);
     const int i = (t / NTc) * 8 + e / 8, j = w + (t % NTc) * 8 + e % 8;
     sG[i + j * C::LDGG] = v;
     sG[j + i * C::LDGG] = cconj(v);
@@ -646,8 +649,11 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
   }
   BMPS_TICK(tv1);
   BMPS_ACC(0, tv0, tv1);
-  if (cross_gram) jac_gram_store_cross<W2>(gacc, sG, sQ, cI, cJ);
-  else jac_gram_store<W2>(gacc, sG, sQ);
+  // k-split partials need 8 warps x 64 complex: Q's space, or (W2 = 16) staging buffer 1,
+  // whose last chunk every warp has consumed by now
+  double2* scratch = W2 * C::LDG >= 512 ? sQ : sP + C::BUF;
+  if (cross_gram) jac_gram_store_cross<W2>(gacc, sG, scratch, cI, cJ);
+  else jac_gram_store<W2>(gacc, sG, scratch);
   __syncthreads();
   const bool staged = nch == 1;  // single chunk still in buffer 0 from the Gram pass
   // prefetch the first apply chunk so its load overlaps the inner sweep
@@ -751,7 +757,7 @@ BMPS_DEV void jac_load_resident(double2* sP, const double2* X, int r, int c) {
 }
 
 template <int W2>
-__global__ void __launch_bounds__(256, (W2 == 32) ? BMPS_JAC_MINB : 1) jacobi_kernel(JacArgs args) {
+__global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_kernel(JacArgs args) {
   using C = JacCfg<W2>;
   extern __shared__ __align__(16) double2 jsm[];
   double2* sQ = jsm;
@@ -881,7 +887,7 @@ __global__ void __launch_bounds__(256, (W2 == 32) ? BMPS_JAC_MINB : 1) jacobi_ke
 // re-probe -- so there is no deadlock, no host polling and no per-round
 // launch, and stragglers' rounds overlap other items' work.
 template <int W2>
-__global__ void __launch_bounds__(256, (W2 == 32) ? BMPS_JAC_MINB : 1) jacobi_dynamic_kernel(JacArgs args) {
+__global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dynamic_kernel(JacArgs args) {
   using C = JacCfg<W2>;
   extern __shared__ __align__(16) double2 jsm[];
   double2* sQ = jsm;
