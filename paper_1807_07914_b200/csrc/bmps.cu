@@ -38,6 +38,7 @@ int g_double_qr = 1;       // second QR of R^H before the Jacobi (preconditioned
 int g_jac_per_sm = 0;      // dynamic Jacobi CTAs per SM (0: occupancy maximum)
 int g_col_sort = 1;        // descending-norm column order ahead of the first QR (double-QR items)
 int g_time_svd = 0;        // record CUDA events around the SVD stage (bmps_svd_time)
+int g_pair_skip = 1;       // dynamic Jacobi: skip cross visits of provably clean block pairs
 
 // CUDA-event pairs bracketing the SVD stage (K3: column sort, QR preconditioner,
 // Jacobi, double-QR epilogue) of each bmps_apply_2q call while g_time_svd is set.
@@ -408,6 +409,9 @@ struct Ws {
   JacSched* sched;
   double2* gcache;
   size_t gcache_stride;
+  int* pairlog;
+  int nbcap;
+  size_t pairlog_stride;
   size_t mat_stride;
   size_t aux_stride;
   int maxp;
@@ -446,6 +450,10 @@ size_t ws_layout(int cap, int nitems, char* base, Ws* ws) {
                                         (size_t)((2 * cap + 31) / 32 + 1) * 1024);
   const size_t o_gc = off;
   off = align256(off + sizeof(double2) * gcache_stride * nitems);
+  const int nbcap = (2 * cap + 7) / 8 + 1;   // blocks of the narrowest panel (8 columns), even
+  const size_t pairlog_stride = (size_t)nbcap + (size_t)nbcap * nbcap;
+  const size_t o_pl = off;
+  off = align256(off + sizeof(int) * pairlog_stride * nitems);
   if (ws && base) {
     ws->meta = (ItemMeta*)(base + o_meta);
     ws->sig = (double*)(base + o_sig);
@@ -459,6 +467,9 @@ size_t ws_layout(int cap, int nitems, char* base, Ws* ws) {
     ws->sched = (JacSched*)(base + o_sched);
     ws->gcache = (double2*)(base + o_gc);
     ws->gcache_stride = gcache_stride;
+    ws->pairlog = (int*)(base + o_pl);
+    ws->nbcap = nbcap;
+    ws->pairlog_stride = pairlog_stride;
     ws->aux_stride = aux_stride;
     ws->maxp = maxp;
     ws->mat_stride = mat_stride;
@@ -541,6 +552,7 @@ int32_t bmps_set_param(const char* name, double value) {
   else if (k == "jac_per_sm" && value >= 0 && value <= 8) g_jac_per_sm = (int)value;
   else if (k == "col_sort" && (value == 0 || value == 1)) g_col_sort = (int)value;
   else if (k == "time_svd" && (value == 0 || value == 1)) g_time_svd = (int)value;
+  else if (k == "pair_skip" && (value == 0 || value == 1)) g_pair_skip = (int)value;
   else return BMPS_E_ARG;
   return BMPS_OK;
 }
@@ -688,6 +700,8 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   ja.tma = g_tma_staging;
   ja.gcache = g_gram_cache ? ws.gcache : nullptr;
   ja.gcache_stride = ws.gcache_stride;
+  ja.pairlog = g_pair_skip ? ws.pairlog : nullptr;
+  ja.nbcap = ws.nbcap;
   const int explicit_mode = mode & 7;  // 0 = library default (g_jacobi_mode)
   if (cmax <= 64) {
     ja.persistent = 1;
@@ -702,6 +716,8 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
     const int cl_mode = explicit_mode == 0 ? g_jacobi_mode : explicit_mode;
     if (cl_mode == 4) {
       cudaMemsetAsync(ws.sched, 0, sizeof(JacSched) * (size_t)nitems, st);
+      if (g_pair_skip)
+        cudaMemsetAsync(ws.pairlog, 0xff, sizeof(int) * ws.pairlog_stride * (size_t)nitems, st);
       init_active_kernel<<<1, 32, 0, st>>>(ws.counter, nitems);
       ++g_launches;
       // panel width by the tunable (default 32). 16 (8-column blocks) quadruples the

@@ -87,6 +87,10 @@ struct JacArgs {
   int tma;           // stage panels with TMA bulk copies (else cp.async)
   double2* gcache;   // per item: rotated 16x16 intra-block Grams (nullptr: off)
   size_t gcache_stride;
+  int* pairlog;      // per item: [nbcap] last rotation round of each block, then
+                     // [nbcap x nbcap] round of the last clean check of each block pair
+                     // (-1: none / rotated since); nullptr: no skipping
+  int nbcap;
 };
 
 struct RotShared {
@@ -979,8 +983,30 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dy
     int I, J;
     tourney_pair(nb, rho, v, I, J);
     double2* gc = args.gcache ? args.gcache + (size_t)i * args.gcache_stride : nullptr;
-    const bool dirty = jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, rho == 0, args.max_inner,
-                                     false, sG, sQ, sP, rs, st, args.tma, gc);
+    // Exact skip of a cross visit whose outcome is known: the pair was checked clean
+    // at round lc and neither block has been rotated since, so its columns -- hence
+    // its Gram and the rotation test -- are bit-for-bit what they were (most visits
+    // of the last sweeps of an item)
+    int* last_rot = args.pairlog ? args.pairlog + (size_t)i * (args.nbcap + args.nbcap * args.nbcap)
+                                 : nullptr;
+    int* last_chk = last_rot ? last_rot + args.nbcap + I * args.nbcap + J : nullptr;
+    bool skip = false;
+    if (last_rot && rho > 0) {
+      const int lc = *((volatile int*)last_chk);
+      skip = lc >= 0 && *((volatile int*)(last_rot + I)) < lc && *((volatile int*)(last_rot + J)) < lc;
+    }
+    const bool dirty = skip ? false
+                            : jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, rho == 0,
+                                            args.max_inner, false, sG, sQ, sP, rs, st, args.tma, gc);
+    if (last_rot && !skip && threadIdx.x == 0) {
+      if (dirty) {
+        last_rot[I] = (int)rnd;
+        last_rot[J] = (int)rnd;
+        *last_chk = -1;
+      } else {
+        *last_chk = (int)rnd;
+      }
+    }
     // release: the CTA barrier orders every thread's panel / Gram-cache stores before
     // thread 0's GPU-scope fence, which is cumulative (the CUTLASS semaphore pattern);
     // one fence per visit instead of a MEMBAR.GPU stall in all 256 threads
