@@ -483,6 +483,8 @@ void set_attrs() {
   if (g_attrs_set) return;
   cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
   cudaFuncSetAttribute(qr_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQrUpdateSmem);
+  cudaFuncSetAttribute(qr_panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(sizeof(double2) * kQrNb * kQrPanelSmemRows));
   cudaFuncSetAttribute(dq_apply_q1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQ1Smem);
   cudaFuncSetAttribute(jacobi_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)JacCfg<32>::kSmem);
@@ -666,7 +668,12 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       qa.second = second;
       for (int p = 0; p < npanels; ++p) {
         qa.panel = p;
-        qr_panel_kernel<<<nitems, 512, 0, st>>>(qa);
+        // rows of this panel: the first QR works on r x c (r <= 2 dim_bound), the second on c x c
+        const int prow = cmax - p * kQrNb;
+        if (prow <= kQrPanelSmemRows)
+          qr_panel_kernel<true><<<nitems, 512, sizeof(double2) * kQrNb * prow, st>>>(qa);
+        else
+          qr_panel_kernel<false><<<nitems, 512, 0, st>>>(qa);
         ++g_launches;
         const int trail = cmax - (p + 1) * kQrNb;
         if (trail > 0) {

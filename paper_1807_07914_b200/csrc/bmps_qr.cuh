@@ -102,9 +102,17 @@ BMPS_DEV double block_sum(double v, double* red) {
   return t;
 }
 
+// SMEM = true: the panel's rows [j0, r) are staged in shared memory for the
+// factorization (every column step then costs shared-memory instead of L2
+// round trips: ~4x faster for these latency-bound launches); the arithmetic and
+// its order are identical to the global-memory version. Used when
+// (r - j0) x kQrNb x 16 B fits (kQrPanelSmemRows).
+constexpr int kQrPanelSmemRows = 384;   // 384 x 32 x 16 B + 33 KB static <= 227 KB
+template <bool SMEM>
 __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
   __shared__ double red[16];
   __shared__ double2 s_S[kQrNb][kQrNb];
+  extern __shared__ __align__(16) double2 spanel[];
   const int item = blockIdx.x;
   const ItemMeta* m = a.meta + item;
   double2* A;
@@ -117,8 +125,20 @@ __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
   const int j1 = min(j0 + kQrNb, c);
   double2* T = qr_tslot(a, tau);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ldp = r - j0;   // staged column k holds rows j0.. at spanel[(k - j0) * ldp]
+  if (SMEM) {
+    for (int idx = tid; idx < (j1 - j0) * ldp; idx += blockDim.x) {
+      const int kk = idx / ldp, i = idx % ldp;
+      spanel[idx] = A[(size_t)(j0 + kk) * r + j0 + i];
+    }
+    __syncthreads();
+  }
+  // column k of the panel, indexed by global row (>= j0)
+  auto colp = [&](int k) -> double2* {
+    return SMEM ? spanel + (size_t)(k - j0) * ldp - j0 : A + (size_t)k * r;
+  };
   for (int k = j0; k < j1; ++k) {
-    double2* col = A + (size_t)k * r;
+    double2* col = colp(k);
     double s = 0.0;
     for (int i = k + 1 + tid; i < r; i += blockDim.x) s += cabs2(col[i]);
     const double xnorm2 = block_sum(s, red);
@@ -143,7 +163,7 @@ __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
     __syncthreads();
     // apply P_k = I - conj(tau) v v^H to panel columns k+1 .. j1-1 (one warp per column)
     for (int jj = k + 1 + warp; jj < j1 && (t.x != 0.0 || t.y != 0.0); jj += blockDim.x >> 5) {
-      double2* cj = A + (size_t)jj * r;
+      double2* cj = colp(jj);
       double2 w = lane == 0 ? cj[k] : make_double2(0.0, 0.0);
       for (int i = k + 1 + lane; i < r; i += 32) w = cfma(cconj(col[i]), cj[i], w);
 #pragma unroll
@@ -154,6 +174,13 @@ __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
       const double2 f = cmul(cconj(t), w);
       if (lane == 0) cj[k] = csub(cj[k], f);
       for (int i = k + 1 + lane; i < r; i += 32) cj[i] = csub(cj[i], cmul(col[i], f));
+    }
+    __syncthreads();
+  }
+  if (SMEM) {
+    for (int idx = tid; idx < (j1 - j0) * ldp; idx += blockDim.x) {
+      const int kk = idx / ldp, i = idx % ldp;
+      A[(size_t)(j0 + kk) * r + j0 + i] = spanel[idx];
     }
     __syncthreads();
   }
