@@ -670,7 +670,9 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
         qa.panel = p;
         // rows of this panel: the first QR works on r x c (r <= 2 dim_bound), the second on c x c
         const int prow = cmax - p * kQrNb;
-        if (prow <= kQrPanelSmemRows)
+        // shared-memory panels run one CTA per SM (up to 229 KB): worth it while the
+        // batch fits one wave, or when the panel is small enough for two per SM
+        if (prow <= kQrPanelSmemRows && (nitems <= kNumSMs || prow <= 150))
           qr_panel_kernel<true><<<nitems, 512, sizeof(double2) * kQrNb * prow, st>>>(qa);
         else
           qr_panel_kernel<false><<<nitems, 512, 0, st>>>(qa);
