@@ -162,6 +162,28 @@ int32_t bmps_env_transfer(const double* gamma, const double* lam, const int32_t*
                           int64_t in_stride, double* env_out, int64_t out_stride, double* scratch,
                           int32_t count, void* stream);
 
+/* MpsState.expectation_pauli (mps.py:188-204) for a batch of (state, string)
+ * items at small bonds (cap <= 32), fused: item i sweeps sites lo[i]..hi[i] (its
+ * first / last non-identity site; hi < lo for an all-identity string) from the
+ * cached left environment L_lo and closes with R_{hi+1} (R_lo if hi < lo).
+ * Environments are complex128 [U][n+1][cap][cap] with env_stride = (n+1)*cap*cap
+ * complex elements per environment set; env_idx[i] selects the set of item i;
+ * codes uint8 [count][n] (I=0 X=1 Y=2 Z=3); out complex128 [count]. */
+int32_t bmps_pauli_sweep(const double* gamma, const double* lam, const int32_t* dims, int32_t S,
+                         int32_t n, int32_t cap, const int32_t* state_idx, const int32_t* env_idx,
+                         const uint8_t* codes, const int32_t* lo, const int32_t* hi,
+                         const double* env_l, const double* env_r, int64_t env_stride,
+                         int32_t count, double* out, void* stream);
+
+/* All identity environments of `count` states in one launch (small bonds,
+ * cap <= 32): direction 0 fills L_1..L_n, direction 1 R_{n-1}..R_0, of env
+ * complex128 [count][n+1][cap][cap] (env_stride = (n+1)*cap*cap complex
+ * elements; the caller sets L_0 / R_n = [[1]] and zero padding). The
+ * identity-Pauli case of the transfers above, kept in shared memory. */
+int32_t bmps_env_sweep(const double* gamma, const double* lam, const int32_t* dims, int32_t S,
+                       int32_t n, int32_t cap, const int32_t* states, int32_t count,
+                       int32_t direction, double* env, int64_t env_stride, void* stream);
+
 /* <E_left, R_right> contraction: out[i] = sum_{r,q} L_i[r,q] * R_i[r,q] over
  * the dims[s][b_i] x dims[s][b_i] leading block (complex128 out); L_i at
  * env_l + i*l_stride, R_i at env_r + i*r_stride (complex elements). */

@@ -384,6 +384,157 @@ __global__ void __launch_bounds__(256) env_close_kernel(const int* dims, int n, 
   if (threadIdx.x == 0) out[it] = red[0];
 }
 
+// Fused Pauli-string sweep for small bonds (cap <= kSweepCap): one CTA per
+// (state, string) item walks the string's support lo..hi with the environment
+// resident in shared memory and closes it against the cached right environment
+// R_{hi+1}: the same contraction as the K5 GEMM pair (mps.py:196-204 reassociated:
+// F = E (O T), E' = T^H F, T = Gamma lambda), in one launch for every string instead
+// of three launches plus gathers per site. CUDA-core FP64: the blocks are at most
+// 32 x 64 x 32, far below a DMMA tile's worth of reuse.
+constexpr int kSweepCap = 32;
+__global__ void __launch_bounds__(256) pauli_sweep_kernel(StateView sv, const int* state_idx,
+                                                          const int* env_idx,
+                                                          const unsigned char* codes,
+                                                          const int* lo, const int* hi,
+                                                          const double2* lenv,
+                                                          const double2* renv,
+                                                          size_t env_stride, double2* out) {
+  extern __shared__ __align__(16) double2 ssw[];
+  double2* sE = ssw;                                 // [kSweepCap][kSweepCap]
+  double2* sF = sE + kSweepCap * kSweepCap;          // [2 kSweepCap][kSweepCap]
+  double2* sT = sF + 2 * kSweepCap * kSweepCap;      // [2 kSweepCap][kSweepCap]
+  __shared__ double2 red[8];
+  const int it = blockIdx.x, tid = threadIdx.x, n = sv.n, cap = sv.cap;
+  const int s = state_idx[it];
+  const int* d = sv.dimv(s);
+  const int l0 = lo[it], h0 = hi[it];
+  const size_t ebase = (size_t)env_idx[it] * env_stride;
+  {
+    const int D = d[l0];
+    const double2* L = lenv + ebase + (size_t)l0 * cap * cap;
+    for (int idx = tid; idx < D * D; idx += blockDim.x)
+      sE[(idx / D) * kSweepCap + idx % D] = L[(size_t)(idx / D) * cap + idx % D];
+  }
+  __syncthreads();
+  for (int k = l0; k <= h0; ++k) {
+    const int dl = d[k], dr = d[k + 1], op = codes[(size_t)it * n + k];
+    const double2* g = sv.site(s, k);
+    const double* lam = sv.bond(s, k + 1);
+    for (int idx = tid; idx < 2 * dl * dr; idx += blockDim.x) {
+      const int row = idx / dr, q = idx % dr;   // row = 2b + t
+      sT[row * kSweepCap + q] = cscale(g[(size_t)row * cap + q], lam[q]);
+    }
+    __syncthreads();
+    // F[(a,s), q] = sum_b E[a,b] (O T)[b,s,q]
+    for (int idx = tid; idx < 2 * dl * dr; idx += blockDim.x) {
+      const int as = idx / dr, q = idx % dr, a = as >> 1, so = as & 1;
+      const int t = (op == 1 || op == 2) ? so ^ 1 : so;
+      double2 acc = make_double2(0.0, 0.0);
+      for (int b = 0; b < dl; ++b) acc = cfma(sE[a * kSweepCap + b], sT[(2 * b + t) * kSweepCap + q], acc);
+      if (op == 2) acc = so == 0 ? make_double2(acc.y, -acc.x) : make_double2(-acc.y, acc.x);  // -i, +i
+      else if (op == 3 && so == 1) acc = make_double2(-acc.x, -acc.y);
+      sF[as * kSweepCap + q] = acc;
+    }
+    __syncthreads();
+    // E'[r,q] = sum_{(a,s)} conj(T[(a,s), r]) F[(a,s), q]
+    for (int idx = tid; idx < dr * dr; idx += blockDim.x) {
+      const int r = idx / dr, q = idx % dr;
+      double2 acc = make_double2(0.0, 0.0);
+      for (int as = 0; as < 2 * dl; ++as)
+        acc = cfma(cconj(sT[as * kSweepCap + r]), sF[as * kSweepCap + q], acc);
+      sE[r * kSweepCap + q] = acc;
+    }
+    __syncthreads();
+  }
+  const int bond = h0 >= l0 ? h0 + 1 : l0;
+  const int D = d[bond];
+  const double2* R = renv + ebase + (size_t)bond * cap * cap;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int idx = tid; idx < D * D; idx += blockDim.x) {
+    const int i = idx / D, j = idx % D;
+    acc = cfma(sE[i * kSweepCap + j], R[(size_t)i * cap + j], acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+  }
+  if ((tid & 31) == 0) red[tid >> 5] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double2 t = red[0];
+    for (int w = 1; w < 8; ++w) t = cadd(t, red[w]);
+    out[it] = t;
+  }
+}
+
+// All identity environments of a state in one CTA (small bonds, cap <= kSweepCap):
+// direction 0 writes L_1..L_n from L_0 = [[1]] (E' = T^H (E T)), direction 1 writes
+// R_{n-1}..R_0 from R_n = [[1]] (R' = conj(T) (T R^T)^T) -- the identity-Pauli case
+// of K5, with the environment kept in shared memory across the whole chain.
+__global__ void __launch_bounds__(256) env_sweep_kernel(StateView sv, const int* states,
+                                                        int direction, double2* env,
+                                                        size_t env_stride) {
+  extern __shared__ __align__(16) double2 ssw[];
+  double2* sE = ssw;
+  double2* sF = sE + kSweepCap * kSweepCap;
+  double2* sT = sF + 2 * kSweepCap * kSweepCap;
+  const int it = blockIdx.x, tid = threadIdx.x, n = sv.n, cap = sv.cap;
+  const int s = states[it];
+  const int* d = sv.dimv(s);
+  double2* e = env + (size_t)it * env_stride;
+  if (tid == 0) sE[0] = make_double2(1.0, 0.0);
+  __syncthreads();
+  for (int step = 0; step < n; ++step) {
+    const int k = direction == 0 ? step : n - 1 - step;
+    const int dl = d[k], dr = d[k + 1];
+    const double2* g = sv.site(s, k);
+    const double* lam = sv.bond(s, k + 1);
+    for (int idx = tid; idx < 2 * dl * dr; idx += blockDim.x) {
+      const int row = idx / dr, q = idx % dr;
+      sT[row * kSweepCap + q] = cscale(g[(size_t)row * cap + q], lam[q]);
+    }
+    __syncthreads();
+    if (direction == 0) {
+      for (int idx = tid; idx < 2 * dl * dr; idx += blockDim.x) {   // F[(a,s),q] = sum_b E[a,b] T[(b,s),q]
+        const int as = idx / dr, q = idx % dr, a = as >> 1, so = as & 1;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int b = 0; b < dl; ++b) acc = cfma(sE[a * kSweepCap + b], sT[(2 * b + so) * kSweepCap + q], acc);
+        sF[as * kSweepCap + q] = acc;
+      }
+      __syncthreads();
+      double2* out = e + (size_t)(k + 1) * cap * cap;
+      for (int idx = tid; idx < dr * dr; idx += blockDim.x) {       // E'[r,q] = sum conj(T[as,r]) F[as,q]
+        const int r = idx / dr, q = idx % dr;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int as = 0; as < 2 * dl; ++as)
+          acc = cfma(cconj(sT[as * kSweepCap + r]), sF[as * kSweepCap + q], acc);
+        sE[r * kSweepCap + q] = acc;
+        out[(size_t)r * cap + q] = acc;
+      }
+    } else {
+      for (int idx = tid; idx < 2 * dl * dr; idx += blockDim.x) {   // F[(b,s),r] = sum_q T[(b,s),q] R[r,q]
+        const int bs = idx / dr, r = idx % dr;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int q = 0; q < dr; ++q) acc = cfma(sT[bs * kSweepCap + q], sE[r * kSweepCap + q], acc);
+        sF[bs * kSweepCap + r] = acc;
+      }
+      __syncthreads();
+      double2* out = e + (size_t)k * cap * cap;
+      for (int idx = tid; idx < dl * dl; idx += blockDim.x) {       // R'[a,b] = sum_{s,r} conj(T[(a,s),r]) F[(b,s),r]
+        const int a = idx / dl, b = idx % dl;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int so = 0; so < 2; ++so)
+          for (int r = 0; r < dr; ++r)
+            acc = cfma(cconj(sT[(2 * a + so) * kSweepCap + r]), sF[(2 * b + so) * kSweepCap + r], acc);
+        sE[a * kSweepCap + b] = acc;
+        out[(size_t)a * cap + b] = acc;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void init_active_kernel(int* active, int nitems) {
   if (threadIdx.x == 0) *active = nitems;
 }
@@ -989,6 +1140,48 @@ int32_t bmps_env_transfer(const double* gamma, const double* lam, const int32_t*
     gemm_kernel<EnvR2><<<dim3(t1, t1, count), 256, 0, st>>>(g2);
     ++g_launches;
   }
+  return launch_status();
+}
+
+int32_t bmps_pauli_sweep(const double* gamma, const double* lam, const int32_t* dims, int32_t S,
+                         int32_t n, int32_t cap, const int32_t* state_idx, const int32_t* env_idx,
+                         const uint8_t* codes, const int32_t* lo, const int32_t* hi,
+                         const double* env_l, const double* env_r, int64_t env_stride,
+                         int32_t count, double* out, void* stream) {
+  if (count == 0) return BMPS_OK;
+  if (count < 0 || S < 1 || n < 1 || cap < 1 || cap > kSweepCap || !env_l || !env_r || !out)
+    return BMPS_E_ARG;
+  StateView sv = make_view((double*)gamma, (double*)lam, (int32_t*)dims, n, cap);
+  constexpr size_t smem = sizeof(double2) * 5 * kSweepCap * kSweepCap;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(pauli_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  pauli_sweep_kernel<<<count, 256, smem, (cudaStream_t)stream>>>(
+      sv, state_idx, env_idx, codes, lo, hi, (const double2*)env_l, (const double2*)env_r,
+      (size_t)env_stride, (double2*)out);
+  ++g_launches;
+  return launch_status();
+}
+
+int32_t bmps_env_sweep(const double* gamma, const double* lam, const int32_t* dims, int32_t S,
+                       int32_t n, int32_t cap, const int32_t* states, int32_t count,
+                       int32_t direction, double* env, int64_t env_stride, void* stream) {
+  if (count == 0) return BMPS_OK;
+  if (count < 0 || S < 1 || n < 1 || cap < 1 || cap > kSweepCap || !env ||
+      (direction != 0 && direction != 1))
+    return BMPS_E_ARG;
+  StateView sv = make_view((double*)gamma, (double*)lam, (int32_t*)dims, n, cap);
+  constexpr size_t smem = sizeof(double2) * 5 * kSweepCap * kSweepCap;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(env_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  env_sweep_kernel<<<count, 256, smem, (cudaStream_t)stream>>>(sv, states, direction,
+                                                               (double2*)env, (size_t)env_stride);
+  ++g_launches;
   return launch_status();
 }
 

@@ -29,10 +29,11 @@ import torch
 
 from . import _native
 from .gates import SWAP_MATRIX, check_unitary, gate_matrix
-from .hamiltonian import encode_pauli
+from .hamiltonian import encode_paulis
 from .policy import TruncationPolicy
 
 MAX_CAP = 1024
+SWEEP_CAP = 32          # fused Pauli-string sweep (bmps_pauli_sweep) up to this bond capacity
 _RECORD = _native.RECORD_BYTES
 RECORD_DTYPE = np.dtype([("err", "<f8"), ("dl", "<i4"), ("dm", "<i4"), ("dr", "<i4"),
                          ("keep", "<i4"), ("status", "<i4"), ("site", "<i4")])
@@ -642,6 +643,12 @@ class MpsBatch:
         else:
             env[:, n, 0, 0] = 1.0
             steps = range(n - 1, -1, -1)
+        if cap <= SWEEP_CAP:
+            rc = self.lib.bmps_env_sweep(_ptr(self.gamma), _ptr(self.lam), _ptr(self.dims), self.S, n,
+                                         cap, sidx.data_ptr(), ns, direction, env.data_ptr(), stride,
+                                         _stream())
+            _native.check(rc, "bmps_env_sweep")
+            return env
         for k in steps:
             site = torch.full((ns,), k, dtype=torch.int32, device=self.device)
             src, dst = (k, k + 1) if direction == 0 else (k + 1, k)
@@ -660,11 +667,7 @@ class MpsBatch:
         """
         n = self.n
         state_idx = np.asarray(state_idx, dtype=np.int32)
-        codes = np.zeros((len(paulis), n), dtype=np.uint8)
-        for i, p in enumerate(paulis):
-            if len(p) != n:
-                raise ValueError(f"Pauli string length {len(p)} != qubit count {n}")
-            codes[i] = encode_pauli(p)
+        codes = encode_paulis(paulis, n)
         self.check_status()
         npairs = len(paulis)
         if npairs == 0:
@@ -683,6 +686,22 @@ class MpsBatch:
             lo[:] = 0
             hi[:] = n - 1
         out = np.empty(npairs, dtype=np.complex128)
+        if use_env and cap <= SWEEP_CAP:
+            # small bonds: every string in one fused sweep launch (bmps_pauli_sweep)
+            stride = (n + 1) * cap * cap
+            res = torch.empty(npairs, dtype=torch.complex128, device=dev)
+            args = [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in
+                    (state_idx, inv.astype(np.int32), codes, lo, hi)]
+            rc = self.lib.bmps_pauli_sweep(
+                _ptr(self.gamma), _ptr(self.lam), _ptr(self.dims), self.S, n, cap,
+                *(a.data_ptr() for a in args), Lenv.data_ptr(), Renv.data_ptr(), stride, npairs,
+                res.data_ptr(), _stream())
+            _native.check(rc, "bmps_pauli_sweep")
+            out[:] = res.cpu().numpy()
+            bad = np.abs(out.imag) > 1e-10
+            if bad.any():
+                raise RuntimeError(f"expectation has imaginary residue {out.imag[bad][0]:.3e}")
+            return out.real.copy()
         chunk = self._env_chunk()
         for c0 in range(0, npairs, chunk):
             c1 = min(npairs, c0 + chunk)

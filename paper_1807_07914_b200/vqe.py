@@ -38,14 +38,12 @@ def batch_energies(batch, paulis, coeffs, states=None) -> np.ndarray:
     nt = len(paulis)
     sidx = np.repeat(states.astype(np.int32), nt)
     vals = batch.expectations(sidx, list(paulis) * len(states)).reshape(len(states), nt)
-    coeffs = [float(c) for c in coeffs]
-    out = np.empty(len(states))
-    for v in range(len(states)):
-        acc = 0  # python sum order, as vqe.py:89
-        for c, e in zip(coeffs, vals[v]):
-            acc = acc + c * float(e)
-        out[v] = acc
-    return out
+    coeffs = np.asarray([float(c) for c in coeffs], dtype=np.float64)
+    if nt == 0:
+        return np.zeros(len(states))
+    # the reference's left-to-right Python sum (vqe.py:89): np.add.accumulate is
+    # sequential, so the result is bit-identical to the scalar loop
+    return np.add.accumulate(coeffs[None, :] * vals, axis=1)[:, -1].copy()
 
 
 @dataclass(frozen=True)
