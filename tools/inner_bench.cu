@@ -46,6 +46,8 @@ __device__ int inner_var(double2* sG, double2* sQ, RotShared& rs, double tol, do
     sQ[i + j * C::LDG] = make_double2(i == j ? 1.0 : 0.0, 0.0);
   }
   int any = 0;
+  int pq_q = (int)((sqrtf(8.0f * (float)tid + 1.0f) - 1.0f) * 0.5f);
+  const int pq_p = tid - pq_q * (pq_q + 1) / 2;
   for (int rho = 0; rho < w; ++rho) {
     int act = 0;
     if (tid < w) {
@@ -62,20 +64,29 @@ __device__ int inner_var(double2* sG, double2* sQ, RotShared& rs, double tol, do
     if (nact == 0) continue;
     if (MODE & 1) {
       for (int idx = tid; idx < w * (w + 1) / 2; idx += blockDim.x) {
-        const int q = (int)((sqrtf(8.0f * (float)idx + 1.0f) - 1.0f) * 0.5f);
-        const int p = idx - q * (q + 1) / 2;
+        const int q = (MODE & 256) ? pq_q : (int)((sqrtf(8.0f * (float)idx + 1.0f) - 1.0f) * 0.5f);
+        const int p = (MODE & 256) ? pq_p : idx - q * (q + 1) / 2;
         if (!(MODE & 16) && !(rs.act[p] | rs.act[q])) continue;
         const int ip = (MODE & 32) ? p : rs.i[p], jp = (MODE & 32) ? w + (p + rho) % w : rs.j[p];
         const int iq = (MODE & 32) ? q : rs.i[q], jq = (MODE & 32) ? w + (q + rho) % w : rs.j[q];
         const double cp = rs.c[p], sp = rs.s[p], cq = rs.c[q], sq = rs.s[q];
         const double2 sep = rs.se[p], cep = rs.ce[p], seq = rs.se[q], ceq = rs.ce[q];
-        const double2 g00 = sG[ip + iq * C::LDGG], g01 = sG[ip + jq * C::LDGG];
-        const double2 g10 = sG[jp + iq * C::LDGG], g11 = sG[jp + jq * C::LDGG];
+        double2 g00, g01, g10, g11;
+        if (MODE & 64) {
+          g00 = make_double2(ip, iq); g01 = make_double2(ip, jq); g10 = make_double2(jp, iq); g11 = make_double2(jp, jq);
+        } else {
+          g00 = sG[ip + iq * C::LDGG]; g01 = sG[ip + jq * C::LDGG];
+          g10 = sG[jp + iq * C::LDGG]; g11 = sG[jp + jq * C::LDGG];
+        }
         const double2 r00 = cmsc(g00, cq, seq, g01), r01 = cmac(g00, sq, ceq, g01);
         const double2 r10 = cmsc(g10, cq, seq, g11), r11 = cmac(g10, sq, ceq, g11);
         double2 n00 = cms(r00, cp, sep, r10), n01 = cms(r01, cp, sep, r11);
         double2 n10 = cma(r00, sp, cep, r10), n11 = cma(r01, sp, cep, r11);
         if (MODE & 8) { n00 = g00; n01 = g01; n10 = g10; n11 = g11; }
+        if (MODE & 128) {
+          if (n00.x == 12345.0 && n01.y == 1.0 && n10.x == 3.0 && n11.y == 2.0) sG[0] = n00;
+          continue;
+        }
         sG[ip + iq * C::LDGG] = n00; sG[ip + jq * C::LDGG] = n01;
         sG[jp + iq * C::LDGG] = n10; sG[jp + jq * C::LDGG] = n11;
         if (!(MODE & 4) && p != q) {
@@ -147,8 +158,9 @@ int main() {
   cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost); cudaMemcpy(&n, dn, 4, cudaMemcpyDeviceToHost);
   printf("cross inner sweep: %.0f cycles per sweep, %.0f per round (16 rounds), rotations/sweep %d\n",
          (double)c / reps, (double)c / reps / 16, n / reps);
-  const char* names[9] = {"rotations only", "+G", "+Q", "+G+Q", "G nomirror", "G nomath", "G noact", "G arith idx", "G all three"};
-  for (int mode = 0; mode < 9; ++mode) {
+  const char* names[13] = {"rotations only", "+G", "+Q", "+G+Q", "G nomirror", "G nomath", "G noact", "G arith idx", "G all three",
+                           "G noloads", "G nostores", "G pq hoisted", "G nold nost"};
+  for (int mode = 0; mode < 13; ++mode) {
     if (mode == 0) var_kernel<32, 0><<<1, 256>>>(dG, reps, dc, dn);
     if (mode == 1) var_kernel<32, 1><<<1, 256>>>(dG, reps, dc, dn);
     if (mode == 2) var_kernel<32, 2><<<1, 256>>>(dG, reps, dc, dn);
@@ -158,6 +170,10 @@ int main() {
     if (mode == 6) var_kernel<32, 1 | 16><<<1, 256>>>(dG, reps, dc, dn);
     if (mode == 7) var_kernel<32, 1 | 32><<<1, 256>>>(dG, reps, dc, dn);
     if (mode == 8) var_kernel<32, 1 | 4 | 16 | 32><<<1, 256>>>(dG, reps, dc, dn);
+    if (mode == 9) var_kernel<32, 1 | 64><<<1, 256>>>(dG, reps, dc, dn);
+    if (mode == 10) var_kernel<32, 1 | 128><<<1, 256>>>(dG, reps, dc, dn);
+    if (mode == 11) var_kernel<32, 1 | 256><<<1, 256>>>(dG, reps, dc, dn);
+    if (mode == 12) var_kernel<32, 1 | 64 | 128><<<1, 256>>>(dG, reps, dc, dn);
     cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost); cudaMemcpy(&n, dn, 4, cudaMemcpyDeviceToHost);
     printf("variant %-15s: %.0f cycles per round (rot/sweep %d)\n", names[mode], (double)c / reps / 16, n / reps);
   }
