@@ -66,6 +66,11 @@ typedef struct bmps_policy {
  * on the recorded events; resets the accumulator. */
 int32_t bmps_svd_time(double* total_ms, int32_t* count);
 
+/* Development aid (no reference counterpart): point the warp-specialised Jacobi
+ * kernel's per-CTA progress words at pinned host memory (16 int32 per CTA); only in
+ * builds with -DBMPS_WS_TRACE, BMPS_E_ARG otherwise. */
+int32_t bmps_debug_set_trace(void* host_pinned);
+
 /* ABI version and a human-readable message for a return/status code. */
 int32_t bmps_version(void);
 const char* bmps_status_string(int32_t code);
@@ -79,8 +84,9 @@ int32_t bmps_set_param(const char* name, double value);
 uint64_t bmps_launch_count(void);
 
 /* Development aid: cumulative cycles of the Jacobi phases (Gram pass, inner
- * sweep, apply pass, visit count) in a -DBMPS_PHASE_TIMERS build; returns
- * BMPS_E_ARG in normal builds. out4 is a host array of 4 uint64. */
+ * sweep, apply pass, visit counts, warp-specialised waits) in a
+ * -DBMPS_PHASE_TIMERS build; returns BMPS_E_ARG in normal builds. out4 is a host
+ * array of 16 uint64. */
 int32_t bmps_phase_cycles(uint64_t* out4);
 
 /* MpsState.__init__ (mps.py:55-66): |0...0>, unit boundary bonds, stats reset. */

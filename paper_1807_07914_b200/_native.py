@@ -40,6 +40,7 @@ _SIGNATURES = {
     "bmps_launch_count": ([], ctypes.c_uint64),
     "bmps_phase_cycles": ([_P], _I),
     "bmps_svd_time": ([_P, _P], _I),
+    "bmps_debug_set_trace": ([_P], _I),
     "bmps_init_product": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P], _I),
     "bmps_apply_1q": ([_P, _P, _I, _I, _I, _P, _P, _I, _P], _I),
     "bmps_apply_2q_workspace_bytes": ([_I, _I], _SZ),
@@ -72,7 +73,8 @@ _lib = None
 # library defaults of the bmps_set_param tunables (csrc/bmps.cu)
 DEFAULT_PARAMS = {"tol_factor": 4.0, "max_sweeps": 60, "max_inner": 1, "qr_min_cols": 65,
                   "jacobi_mode": 4, "cluster_size": 8, "tma_staging": 0, "gram_cache": 1,
-                  "block_w2": 32, "double_qr": 1, "jac_per_sm": 0, "col_sort": 1, "time_svd": 0, "pair_skip": 1}
+                  "block_w2": 32, "double_qr": 1, "jac_per_sm": 0, "col_sort": 1, "time_svd": 0, "pair_skip": 1,
+                  "jac_ws": 0}
 
 
 def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:

@@ -35,6 +35,7 @@ int g_tma_staging = 0;     // 1: Jacobi panels staged by TMA bulk copies instead
 int g_gram_cache = 1;      // cross visits reuse rotated intra-block Grams
 int g_block_w2 = 32;       // block-mode panel width: 16, 32, 64 columns, or 0 = auto (16 / 32)
 int g_double_qr = 1;       // second QR of R^H before the Jacobi (preconditioned items)
+int g_jac_ws = 0;          // warp-specialised dynamic Jacobi (W2 = 32); measured slower, opt-in
 int g_jac_per_sm = 0;      // dynamic Jacobi CTAs per SM (0: occupancy maximum)
 int g_col_sort = 1;        // descending-norm column order ahead of the first QR (double-QR items)
 int g_time_svd = 0;        // record CUDA events around the SVD stage (bmps_svd_time)
@@ -647,6 +648,8 @@ void set_attrs() {
                        (int)JacCfg<64>::kSmem);
   cudaFuncSetAttribute(jacobi_dynamic_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)JacCfg<16>::kSmem);
+  cudaFuncSetAttribute(jacobi_ws_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)WsCfg<32>::kSmem);
   g_attrs_set = true;
 }
 
@@ -680,7 +683,7 @@ uint64_t bmps_launch_count(void) { return g_launches; }
 // Development aid: cumulative Jacobi phase cycles (builds with -DBMPS_PHASE_TIMERS only).
 int32_t bmps_phase_cycles(uint64_t* out4) {
 #ifdef BMPS_PHASE_TIMERS
-  cudaMemcpyFromSymbol(out4, g_phase_cycles, 8 * sizeof(unsigned long long));
+  cudaMemcpyFromSymbol(out4, g_phase_cycles, 16 * sizeof(unsigned long long));
   return BMPS_OK;
 #else
   (void)out4;
@@ -703,11 +706,26 @@ int32_t bmps_set_param(const char* name, double value) {
     g_block_w2 = (int)value;
   else if (k == "double_qr" && (value == 0 || value == 1)) g_double_qr = (int)value;
   else if (k == "jac_per_sm" && value >= 0 && value <= 8) g_jac_per_sm = (int)value;
+  else if (k == "jac_ws" && (value == 0 || value == 1)) g_jac_ws = (int)value;
   else if (k == "col_sort" && (value == 0 || value == 1)) g_col_sort = (int)value;
   else if (k == "time_svd" && (value == 0 || value == 1)) g_time_svd = (int)value;
   else if (k == "pair_skip" && (value == 0 || value == 1)) g_pair_skip = (int)value;
   else return BMPS_E_ARG;
   return BMPS_OK;
+}
+
+// Development aid: per-CTA progress words of the warp-specialised Jacobi kernel
+// written to pinned host memory (builds with -DBMPS_WS_TRACE only).
+int32_t bmps_debug_set_trace(void* host_pinned) {
+#ifdef BMPS_WS_TRACE
+  void* dptr = nullptr;
+  if (host_pinned && cudaHostGetDevicePointer(&dptr, host_pinned, 0) != cudaSuccess) return BMPS_E_ARG;
+  cudaMemcpyToSymbol(g_ws_trace, &dptr, sizeof(void*));
+  return BMPS_OK;
+#else
+  (void)host_pinned;
+  return BMPS_E_ARG;
+#endif
 }
 
 int32_t bmps_svd_time(double* total_ms, int32_t* count) {
@@ -884,11 +902,14 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       // visits per round for small batches, but each visit keeps most of a 32-wide
       // visit's latency: one cfg3 brick layer (16 items) ran 36 -> 41 ms, so the auto
       // mode (0: 16 when nitems x visits < CTA slots) is off by default
-      static int n_slots[3] = {0, 0, 0};
+      static int n_slots[4] = {0, 0, 0, 0};
       auto slots_of = [&](int wi) {
         if (!n_slots[wi]) {
           int per_sm = 0;
-          if (wi == 2)
+          if (wi == 3)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_ws_kernel<32>, kWsThreads,
+                                                          WsCfg<32>::kSmem);
+          else if (wi == 2)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_dynamic_kernel<64>, 256,
                                                           JacCfg<64>::kSmem);
           else if (wi == 1)
@@ -906,7 +927,8 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       };
       int wi = g_block_w2 == 64 ? 2 : g_block_w2 == 16 ? 0 : 1;
       if (g_block_w2 == 0) wi = (long long)nitems * (nbmax / 2) < slots_of(1) ? 0 : 1;
-      int slots = slots_of(wi);
+      const bool ws_mode = wi == 1 && g_jac_ws;
+      int slots = slots_of(ws_mode ? 3 : wi);
       if (g_jac_per_sm > 0) {
         int dev = 0, sms = kNumSMs;
         cudaGetDevice(&dev);
@@ -917,7 +939,9 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
                     : wi == 1 ? nbmax / 2
                               : (cmax + 15) / 16;
       const int grid = std::min(slots, nitems * vis);
-      if (wi == 2)
+      if (ws_mode)
+        jacobi_ws_kernel<32><<<grid, kWsThreads, WsCfg<32>::kSmem, st>>>(ja);
+      else if (wi == 2)
         jacobi_dynamic_kernel<64><<<grid, 256, JacCfg<64>::kSmem, st>>>(ja);
       else if (wi == 1)
         jacobi_dynamic_kernel<32><<<grid, 256, JacCfg<32>::kSmem, st>>>(ja);

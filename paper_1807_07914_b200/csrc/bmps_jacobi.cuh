@@ -25,19 +25,36 @@
 
 namespace bmps {
 
+#ifndef BMPS_REGQ
+#define BMPS_REGQ 1   // register-resident Q in the cross rounds of the inner sweep
+#endif
+
 #ifndef BMPS_JAC_MINB
 #define BMPS_JAC_MINB 4   // resident Jacobi CTAs per SM the register budget is sized for
 #endif
 
 #ifdef BMPS_PHASE_TIMERS
 // cycles spent in [0] Gram pass, [1] inner sweep (incl. check), [2] apply pass, [3] visits
-__device__ unsigned long long g_phase_cycles[8];
+__device__ unsigned long long g_phase_cycles[16];
 #define BMPS_TICK(var) const long long var = clock64()
 #define BMPS_ACC(slot, t0, t1) \
   if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[slot], (unsigned long long)((t1) - (t0)))
+#define WS_ACC(lead, slot, t0, t1) \
+  if (threadIdx.x == (lead)) atomicAdd(&g_phase_cycles[slot], (unsigned long long)((t1) - (t0)))
 #else
+#define WS_ACC(lead, slot, t0, t1)
 #define BMPS_TICK(var)
 #define BMPS_ACC(slot, t0, t1)
+#endif
+
+#ifdef BMPS_WS_TRACE
+// development aid: per-CTA progress words in pinned host memory (readable while a
+// kernel hangs), set by bmps_debug_set_trace
+__device__ volatile int* g_ws_trace;
+#define WS_TR(slot, val) \
+  do { if (g_ws_trace) g_ws_trace[blockIdx.x * 16 + (slot)] = (int)(val); } while (0)
+#else
+#define WS_TR(slot, val) do { } while (0)
 #endif
 
 template <int W2>
@@ -98,6 +115,39 @@ struct RotShared {
   double2 e[32];
   double2 se[32], ce[32];   // s e, c e
   int i[32], j[32], act[32];
+};
+
+// Thread groups a Jacobi phase runs on. CtaGrp: the whole CTA (classic kernels,
+// barrier 0). NamedGrp: a warp-aligned subset synchronised on its own named
+// barrier (warp-specialised kernel: math warps and rotation warps).
+struct CtaGrp {
+  static constexpr int kN = 256;   // block size of every classic Jacobi launch
+  BMPS_DEV static int tid() { return (int)threadIdx.x; }
+  BMPS_DEV static int n() { return (int)blockDim.x; }
+  BMPS_DEV static void sync() { __syncthreads(); }
+  BMPS_DEV static int count(int p) { return __syncthreads_count(p); }
+};
+template <int BASE, int N, int ID>
+struct NamedGrp {
+  static constexpr int kN = N;
+  BMPS_DEV static int tid() { return (int)threadIdx.x - BASE; }
+  BMPS_DEV static constexpr int n() { return N; }
+  // __barrier_sync_count is a convergent intrinsic: the compiler reconverges the warp
+  // before it (an inline-asm bar.sync after a divergent loop exit can be reached by a
+  // split warp, which deadlocks or faults)
+  BMPS_DEV static void sync() { __barrier_sync_count(ID, N); }
+  // number of group threads with p != 0 (ballot per warp, one word per warp)
+  BMPS_DEV static int count(int p) {
+    __shared__ int s_w[N / 32];
+    const unsigned bal = __ballot_sync(0xffffffffu, p != 0);
+    if ((threadIdx.x & 31) == 0) s_w[tid() >> 5] = __popc(bal);
+    sync();
+    int r = 0;
+#pragma unroll
+    for (int k = 0; k < N / 32; ++k) r += s_w[k];
+    sync();
+    return r;
+  }
 };
 
 // ---- TMA bulk copies (cp.async.bulk) with mbarrier completion -------------
@@ -307,7 +357,7 @@ BMPS_DEV void jac_gram_chunk(double (&acc)[JacCfg<W2>::GT + 1][kZ3], const doubl
 
 // Scatter the Gram accumulators into sG (both triangles); scratch holds the
 // k-split partials of the leftover tiles (8 warps x 64 complex).
-template <int W2>
+template <int W2, class G = CtaGrp>
 BMPS_DEV void jac_gram_store(const double (&acc)[JacCfg<W2>::GT + 1][kZ3], double2* sG, double2* scratch) {
   using C = JacCfg<W2>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -328,8 +378,8 @@ BMPS_DEV void jac_gram_store(const double (&acc)[JacCfg<W2>::GT + 1][kZ3], doubl
 #pragma unroll
     for (int h = 0; h < 2; ++h)
       scratch[warp * 64 + rr * 8 + cc + h] = z3_get(acc[C::GT], h);
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < C::GREM * 64; idx += blockDim.x) {
+    G::sync();
+    for (int idx = G::tid(); idx < C::GREM * 64; idx += G::n()) {
       const int t = idx / 64, e = idx % 64;
       double2 v = make_double2(0.0, 0.0);
       for (int p = 0; p < C::GSPLIT; ++p) v = cadd(v, scratch[(t * C::GSPLIT + p) * 64 + e]);
@@ -376,14 +426,14 @@ BMPS_DEV void jac_gram_chunk_cross(double (&acc)[JacCfg<W2>::GT + 1][kZ3], const
 }
 
 // sG <- [[cache_I, G_IJ], [G_IJ^H, cache_J]] (scratch: 8 warps x 64 partials).
-template <int W2>
+template <int W2, class G = CtaGrp>
 BMPS_DEV void jac_gram_store_cross(const double (&acc)[JacCfg<W2>::GT + 1][kZ3], double2* sG,
                                    double2* scratch, const double2* cI, const double2* cJ) {
   using C = JacCfg<W2>;
   constexpr int w = W2 / 2, NTc = W2 / 16, CT = NTc * NTc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rr = lane >> 2, cc = (lane & 3) * 2;
-  for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
+  for (int idx = G::tid(); idx < w * w; idx += G::n()) {
     const int i = idx % w, j = idx / w;
     sG[i + j * C::LDGG] = cI[i + j * w];
     sG[(w + i) + (w + j) * C::LDGG] = cJ[i + j * w];
@@ -406,9 +456,9 @@ BMPS_DEV void jac_gram_store_cross(const double (&acc)[JacCfg<W2>::GT + 1][kZ3],
 #pragma unroll
   for (int h = 0; h < 2; ++h)
     scratch[warp * 64 + rr * 8 + cc + h] = z3_get(acc[0], h);
-  __syncthreads();
+  G::sync();
   constexpr int KS = CT < 8 ? 8 / CT : 1;
-  for (int idx = threadIdx.x; idx < CT * 64; idx += blockDim.x) {
+  for (int idx = G::tid(); idx < CT * 64; idx += G::n()) {
     const int t = idx / 64, e = idx % 64;
     double2 v = scratch[(KS * t) * 64 + e];
     for (int k = 1; k < KS; ++k) v = cadd(v, scratch[(KS * t + k) * 64 + e]);
@@ -418,11 +468,11 @@ BMPS_DEV void jac_gram_store_cross(const double (&acc)[JacCfg<W2>::GT + 1][kZ3],
   }
 }
 
-template <int W2>
+template <int W2, class G = CtaGrp>
 BMPS_DEV void jac_cache_store(const double2* sG, double2* cI, double2* cJ) {
   using C = JacCfg<W2>;
   constexpr int w = W2 / 2;
-  for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
+  for (int idx = G::tid(); idx < w * w; idx += G::n()) {
     const int i = idx % w, j = idx / w;
     cI[i + j * w] = sG[i + j * C::LDGG];
     cJ[i + j * w] = sG[(w + i) + (w + j) * C::LDGG];
@@ -502,21 +552,43 @@ BMPS_DEV void inner_pair(bool full, int rho, int p, int& i, int& j) {
 
 // One (or more) cyclic Jacobi sweeps on the W2 x W2 Gram, accumulating Q.
 // Returns the number of rotations of the first sweep (block-uniform).
-template <int W2>
+template <int W2, class G = CtaGrp>
 BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, double noise2,
                        double fro, bool full, int max_inner) {
   using C = JacCfg<W2>;
   constexpr int w = W2 / 2;
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < W2 * W2; idx += blockDim.x) {
-    const int i = idx % W2, j = idx / W2;
-    sQ[i + j * C::LDG] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+  const int tid = G::tid();
+  // Cross sweeps keep Q in registers: thread (warp gw, lane) owns row `lane` of the
+  // I-block columns p = gw*PP .. gw*PP+PP-1 and of the J-block columns they are
+  // paired with (w + (p + rho) mod w). Between rounds the partners advance by one
+  // pair: a register move inside the thread, one shared exchange with the next
+  // warp (sQ is free until the end). After the w cross rounds the pairing is back
+  // to the identity and Q is written out.
+  constexpr int NW = G::kN / 32;
+  constexpr bool kRegQ = BMPS_REGQ && W2 == 32 && w % NW == 0;
+  constexpr int PP = kRegQ ? w / NW : 1;
+  const bool regq = kRegQ && !full;
+  const int lane = tid & 31, gw = tid >> 5;
+  double2 qi[PP], qj[PP];
+  if (regq) {
+#pragma unroll
+    for (int u = 0; u < PP; ++u) {
+      const int p = gw * PP + u;
+      qi[u] = make_double2(lane == p ? 1.0 : 0.0, 0.0);
+      qj[u] = make_double2(lane == w + p ? 1.0 : 0.0, 0.0);
+    }
+  } else {
+    for (int idx = tid; idx < W2 * W2; idx += G::n()) {
+      const int i = idx % W2, j = idx / W2;
+      sQ[i + j * C::LDG] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+    }
   }
   int first = 0;
   const int rounds = full ? W2 - 1 : w;
   for (int it = 0; it < max_inner; ++it) {
     int any = 0;
     for (int rho = 0; rho < rounds; ++rho) {
+      if (threadIdx.x == 0) WS_TR(12, it * 1000 + rho);
       BMPS_TICK(tr0);
       int act = 0;
       if (tid < w) {
@@ -540,15 +612,15 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
         rs.se[tid] = cscale(e, s);
         rs.ce[tid] = cscale(e, c);
       }
-      const int nact = __syncthreads_count(act);
+      const int nact = G::count(act);
       BMPS_TICK(tr1);
       BMPS_ACC(4, tr0, tr1);
       BMPS_ACC(6, 0, 1);
       any += nact;
-      if (nact == 0) continue;
+      if (nact == 0 && !regq) continue;
       // G <- J^H G J as independent 2x2 blocks (p <= q computed, (q, p) mirrored);
       // Q <- Q J
-      for (int idx = tid; idx < w * (w + 1) / 2; idx += blockDim.x) {
+      for (int idx = tid; idx < (nact ? w * (w + 1) / 2 : 0); idx += G::n()) {
         const int q = (int)((sqrtf(8.0f * (float)idx + 1.0f) - 1.0f) * 0.5f);
         const int p = idx - q * (q + 1) / 2;
         if (!(rs.act[p] | rs.act[q])) continue;  // identity on both sides
@@ -578,7 +650,25 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
           sG[jq + jp * C::LDGG] = cconj(n11);
         }
       }
-      for (int idx = tid; idx < W2 * w; idx += blockDim.x) {
+      if (regq) {
+#pragma unroll
+        for (int u = 0; u < PP; ++u) {
+          const int p = gw * PP + u;
+          if (rs.act[p]) {
+            const double2 ni = cmsc(qi[u], rs.c[p], rs.se[p], qj[u]);
+            const double2 nj = cmac(qi[u], rs.s[p], rs.ce[p], qj[u]);
+            qi[u] = ni;
+            qj[u] = nj;
+          }
+        }
+        sQ[gw * 32 + lane] = qj[0];
+#pragma unroll
+        for (int u = 0; u + 1 < PP; ++u) qj[u] = qj[u + 1];
+        G::sync();
+        qj[PP - 1] = sQ[((gw + 1) % NW) * 32 + lane];
+        continue;
+      }
+      for (int idx = tid; idx < W2 * w; idx += G::n()) {
         const int k = idx % W2, q = idx / W2;
         if (!rs.act[q]) continue;
         const int iq = rs.i[q], jq = rs.j[q];
@@ -587,12 +677,21 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
         sQ[k + iq * C::LDG] = cmsc(qi, cq, rs.se[q], qj);
         sQ[k + jq * C::LDG] = cmac(qi, sq, rs.ce[q], qj);
       }
-      __syncthreads();
+      G::sync();
       BMPS_TICK(tr2);
       BMPS_ACC(5, tr1, tr2);
     }
     if (it == 0) first = any;
     if (!any) break;
+  }
+  if (regq) {
+    G::sync();   // every thread has taken its last exchange value
+#pragma unroll
+    for (int u = 0; u < PP; ++u) {
+      const int p = gw * PP + u;
+      sQ[lane + p * C::LDG] = qi[u];
+      sQ[lane + (w + p) * C::LDG] = qj[u];
+    }
   }
   return first;
 }
@@ -601,7 +700,7 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
 // `resident`, the whole panel (r <= RC) already sits in buffer 0 and is
 // neither loaded nor stored here. W2 = 32 streams the panel with TMA bulk
 // copies (double buffered, mbarrier completion); W2 = 64 with cp.async.
-template <int W2>
+template <int W2, class G = CtaGrp>
 BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, double noise2,
                         double fro, bool full, int max_inner, bool resident, double2* sG,
                         double2* sQ, double2* sP, RotShared& rs, JacStage& st, bool tma,
@@ -622,19 +721,19 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
   if (resident) {
     jac_gram_chunk<W2>(gacc, sP, r);
   } else if (bulk) {
-    __syncthreads();
+    G::sync();
     jac_issue_bulk<W2>(sP, st, 0, X, r, c, 0, I, J);
     for (int k = 0; k < nch; ++k) {
       const int b = k & 1;
       if (k + 1 < nch) jac_issue_bulk<W2>(sP + (b ^ 1) * C::BUF, st, b ^ 1, X, r, c, (k + 1) * C::RC, I, J);
       jac_wait_bulk(st, b);
-      __syncthreads();
+      G::sync();
       if (cross_gram) jac_gram_chunk_cross<W2>(gacc, sP + b * C::BUF, min(C::RC, r - k * C::RC));
       else jac_gram_chunk<W2>(gacc, sP + b * C::BUF, min(C::RC, r - k * C::RC));
-      __syncthreads();
+      G::sync();
     }
   } else {
-    __syncthreads();
+    G::sync();
     jac_issue_chunk<W2>(sP, X, r, c, 0, I, J);
     for (int k = 0; k < nch; ++k) {
       double2* cur = sP + (k % C::NBUF) * C::BUF;
@@ -644,10 +743,10 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
       } else {
         cp_async_wait<0>();
       }
-      __syncthreads();
+      G::sync();
       if (cross_gram) jac_gram_chunk_cross<W2>(gacc, cur, min(C::RC, r - k * C::RC));
       else jac_gram_chunk<W2>(gacc, cur, min(C::RC, r - k * C::RC));
-      __syncthreads();
+      G::sync();
       if (C::NBUF == 1 && k + 1 < nch) jac_issue_chunk<W2>(sP, X, r, c, (k + 1) * C::RC, I, J);
     }
   }
@@ -656,9 +755,9 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
   // k-split partials need 8 warps x 64 complex: Q's space, or (W2 = 16) staging buffer 1,
   // whose last chunk every warp has consumed by now
   double2* scratch = W2 * C::LDG >= 512 ? sQ : sP + C::BUF;
-  if (cross_gram) jac_gram_store_cross<W2>(gacc, sG, scratch, cI, cJ);
-  else jac_gram_store<W2>(gacc, sG, scratch);
-  __syncthreads();
+  if (cross_gram) jac_gram_store_cross<W2, G>(gacc, sG, scratch, cI, cJ);
+  else jac_gram_store<W2, G>(gacc, sG, scratch);
+  G::sync();
   const bool staged = nch == 1;  // single chunk still in buffer 0 from the Gram pass
   // prefetch the first apply chunk so its load overlaps the inner sweep
   if (!resident && !staged) {
@@ -670,7 +769,7 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
   {
     constexpr int w = W2 / 2;
     const int npairs = full ? W2 * W2 : w * w;
-    for (int idx = threadIdx.x; idx < npairs && !need; idx += blockDim.x) {
+    for (int idx = G::tid(); idx < npairs && !need; idx += G::n()) {
       int i, j;
       if (full) {
         i = idx % W2;
@@ -684,13 +783,13 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
                           noise2, fro);
     }
   }
-  const int nrot = __syncthreads_or(need) ? jac_inner<W2>(sG, sQ, rs, tol, noise2, fro, full, max_inner)
+  const int nrot = (G::count(need) != 0) ? jac_inner<W2, G>(sG, sQ, rs, tol, noise2, fro, full, max_inner)
                                           : 0;
   BMPS_TICK(tv2);
   BMPS_ACC(1, tv1, tv2);
   BMPS_ACC(3, 0, 1);
-  if (gcache != nullptr && !resident && (full || nrot > 0)) jac_cache_store<W2>(sG, cI, cJ);
-  if (C::G_IN_BUF) __syncthreads();  // sG (buffer 1) is read before the apply refills it
+  if (gcache != nullptr && !resident && (full || nrot > 0)) jac_cache_store<W2, G>(sG, cI, cJ);
+  if (C::G_IN_BUF) G::sync();  // sG (buffer 1) is read before the apply refills it
   if (nrot == 0) {
     if (!resident && !staged) {
       if (bulk) jac_wait_bulk(st, 0);
@@ -701,9 +800,9 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
   double aacc[C::AT][kZ3];
   if (resident) {
     jac_apply_mma<W2>(aacc, sP, sQ);
-    __syncthreads();
+    G::sync();
     jac_apply_writeback<W2>(aacc, sP);
-    __syncthreads();
+    G::sync();
     return true;
   }
   if (bulk) {
@@ -715,16 +814,16 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
         if (r - row1 < C::RC || panel_col<W2>(W2 - 1, I, J) >= c) {
           // the issue zero-fills: the bulk store out of that buffer must be done reading
           if ((threadIdx.x >> 5) == 0) bulk_wait_read0();
-          __syncthreads();
+          G::sync();
         }
         jac_issue_bulk<W2>(sP + (b ^ 1) * C::BUF, st, b ^ 1, X, r, c, row1, I, J);
       }
       if (!staged) jac_wait_bulk(st, b);
-      __syncthreads();
+      G::sync();
       jac_apply_mma<W2>(aacc, cur, sQ);
-      __syncthreads();
+      G::sync();
       jac_apply_writeback<W2>(aacc, cur);
-      __syncthreads();
+      G::sync();
       jac_store_bulk<W2>(cur, X, r, c, k * C::RC, I, J);
     }
     jac_flush_bulk();
@@ -742,10 +841,10 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
         cp_async_wait<0>();
       }
     }
-    __syncthreads();
+    G::sync();
     jac_apply_mma<W2>(aacc, cur, sQ);
     jac_apply_store_global<W2>(aacc, X, r, c, k * C::RC, I, J);
-    __syncthreads();  // every warp is done reading `cur` before it is refilled
+    G::sync();  // every warp is done reading `cur` before it is refilled
     if (C::NBUF == 1 && !staged && k + 1 < nch) jac_issue_chunk<W2>(sP, X, r, c, (k + 1) * C::RC, I, J);
   }
   BMPS_TICK(tv3);
@@ -753,11 +852,11 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
   return true;
 }
 
-template <int W2>
+template <int W2, class G = CtaGrp>
 BMPS_DEV void jac_load_resident(double2* sP, const double2* X, int r, int c) {
   jac_issue_chunk<W2>(sP, X, r, c, 0, 0, 1);
   cp_async_wait<0>();
-  __syncthreads();
+  G::sync();
 }
 
 template <int W2>
@@ -1043,6 +1142,522 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dy
     }
     __syncthreads();
   }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-specialised dynamic kernel (default for W2 = 32).
+//
+// A visit is Gram -> inner (Gram-space) sweep -> apply. The inner sweep is a
+// chain of latency-bound rounds that leaves the tensor pipe idle, so the CTA
+// is split into 8 math warps (Gram / apply on DMMA, cp.async staging) and 4
+// rotation warps (inner sweep). Visits are software-pipelined two deep: while
+// the rotation warps sweep the Gram of visit k, the math warps form the Gram of
+// visit k+1 and then apply visit k's rotations, so the inner sweep runs under
+// the tensor work. Two Gram buffers and two Q buffers hand visits back and
+// forth through named barriers (GF[b]: Gram b full, math arrives / rotation
+// waits; QF[b]: Q b full, rotation arrives / math waits; the alternation makes
+// the "empty" signals implicit). Claiming, exact visit skipping and round
+// bookkeeping are those of jacobi_dynamic_kernel.
+constexpr int kWsMath = 256, kWsRot = 128, kWsPair = kWsMath + kWsRot, kWsSched = kWsPair;
+constexpr int kWsThreads = kWsPair + 32;   // + one scheduler warp
+using WsMath = NamedGrp<0, kWsMath, 1>;
+using WsRot = NamedGrp<kWsMath, kWsRot, 2>;
+// GF / QF hand-offs between the math and rotation warps (384 threads; the
+// scheduler warp does not take part). The waiting side uses the convergent
+// intrinsic; the arriving side calls it right after a barrier of its own group
+// (converged, straight-line).
+BMPS_DEV void ws_arrive(int id) {
+  if (id == 3) asm volatile("bar.arrive 3, %0;\n" ::"n"(kWsPair) : "memory");
+  else if (id == 4) asm volatile("bar.arrive 4, %0;\n" ::"n"(kWsPair) : "memory");
+  else if (id == 5) asm volatile("bar.arrive 5, %0;\n" ::"n"(kWsPair) : "memory");
+  else asm volatile("bar.arrive 6, %0;\n" ::"n"(kWsPair) : "memory");
+}
+BMPS_DEV void ws_wait(int id) {
+  if (id == 3) __barrier_sync_count(3, kWsPair);
+  else if (id == 4) __barrier_sync_count(4, kWsPair);
+  else if (id == 5) __barrier_sync_count(5, kWsPair);
+  else __barrier_sync_count(6, kWsPair);
+}
+constexpr int kWsGf = 3, kWsQf = 5;   // named barrier ids GF[0..1], QF[0..1]
+
+
+
+template <int W2>
+struct WsCfg {
+  using C = JacCfg<W2>;
+  static constexpr int QSZ = W2 * C::LDG;    // one Q buffer (complex elements)
+  static constexpr int GSZ = W2 * C::LDGG;   // one Gram buffer
+  static constexpr size_t kSmem = (size_t)(2 * QSZ + 2 * GSZ + 2 * C::BUF) * sizeof(double2);
+};
+
+// Visit handed from the math warps to the rotation warps (and nrot back).
+struct WsVisit {
+  double tol, noise2, fro;
+  double2* cI;
+  double2* cJ;
+  int full, stop, nrot, pad;
+};
+
+// Round bookkeeping of a finished visit (one thread): the pair log for exact
+// skipping, the item's dirty flag, and -- for the last visit of a round -- the
+// opening of the next round or the end of the item (as in jacobi_dynamic_kernel).
+template <int W2>
+BMPS_DEV void jac_complete(const JacArgs& args, int i, unsigned rnd, int I, int J, bool dirty,
+                           bool skipped) {
+  constexpr int w = W2 / 2;
+  ItemMeta* m = args.meta + i;
+  int nb = (m->c + w - 1) / w;
+  nb += nb & 1;
+  const int rounds = nb - 1;
+  const int sweep = (int)(rnd / (unsigned)rounds), rho = (int)(rnd % (unsigned)rounds);
+  JacSched* sc = args.sched + i;
+  if (args.pairlog && !skipped) {
+    int* last_rot = args.pairlog + (size_t)i * (args.nbcap + args.nbcap * args.nbcap);
+    int* last_chk = last_rot + args.nbcap + I * args.nbcap + J;
+    if (dirty) {
+      last_rot[I] = (int)rnd;
+      last_rot[J] = (int)rnd;
+      *last_chk = -1;
+    } else {
+      *last_chk = (int)rnd;
+    }
+  }
+  if (dirty) atomicOr(&sc->dirty, 1);
+  __threadfence();
+  const int d = atomicAdd(&sc->done, 1);
+  if (d == nb / 2 - 1) {
+    sc->done = 0;
+    bool finished = false;
+    if (rho == rounds - 1) {
+      const int dsw = atomicAdd(&sc->dirty, 0);
+      if (!dsw) {
+        m->sweeps = sweep;
+        finished = true;
+      } else if (sweep + 1 >= args.max_sweeps) {
+        m->sweeps = sweep + 1;
+        m->status = BMPS_S_SVD_FAILED;
+        finished = true;
+      } else {
+        sc->dirty = 0;
+      }
+    }
+    __threadfence();
+    if (finished) {
+      m->conv = 1;
+      atomicSub(args.active, 1);
+    } else {
+      atomicExch(&sc->ticket, (unsigned long long)(rnd + 1) << 32);
+    }
+  }
+}
+
+// Claim the next visit (one thread). Visits whose outcome is known (pair checked
+// clean, neither block rotated since) are completed on the spot and the claim
+// goes on. Returns the item (v, rnd set), -1 if nothing is claimable right now,
+// -2 once every item has converged.
+template <int W2>
+BMPS_DEV int ws_claim(const JacArgs& args, int& cursor, int& v_out, unsigned& rnd_out) {
+  constexpr int w = W2 / 2;
+  const int nitems = args.nitems;
+  for (;;) {
+    if (*((volatile int*)args.active) <= 0) return -2;
+    int got = -1;
+    for (int probe = 0; probe < nitems; ++probe) {
+      const int i = (cursor + probe) % nitems;
+      JacSched* sc = args.sched + i;
+      if (((volatile ItemMeta*)args.meta)[i].conv) continue;
+      const int c = args.meta[i].c;
+      int nb = (c + w - 1) / w;
+      nb += nb & 1;
+      const unsigned nbv = (unsigned)(nb / 2);
+      const unsigned long long peek = *((volatile unsigned long long*)&sc->ticket);
+      if ((unsigned)(peek & 0xffffffffull) >= nbv) continue;
+      const unsigned long long old = atomicAdd(&sc->ticket, 1ull);
+      const unsigned v = (unsigned)(old & 0xffffffffull);
+      if (v >= nbv) continue;
+      got = i;
+      v_out = (int)v;
+      rnd_out = (unsigned)(old >> 32);
+      cursor = i;
+      break;
+    }
+    __threadfence();
+    if (got < 0) return -1;
+    if (args.pairlog) {
+      const int c = args.meta[got].c;
+      int nb = (c + w - 1) / w;
+      nb += nb & 1;
+      const int rounds = nb - 1, rho = (int)(rnd_out % (unsigned)rounds);
+      if (nb > 2 && rho > 0) {
+        int I, J;
+        tourney_pair(nb, rho, v_out, I, J);
+        const int* last_rot = args.pairlog + (size_t)got * (args.nbcap + args.nbcap * args.nbcap);
+        const int lc = *((volatile const int*)(last_rot + args.nbcap + I * args.nbcap + J));
+        if (lc >= 0 && *((volatile const int*)(last_rot + I)) < lc &&
+            *((volatile const int*)(last_rot + J)) < lc) {
+          jac_complete<W2>(args, got, rnd_out, I, J, false, true);
+          continue;
+        }
+      }
+    }
+    return got;
+  }
+}
+
+BMPS_DEV void cp_async_wait_n(int n) {
+  if (n <= 0) cp_async_wait<0>();
+  else if (n == 1) cp_async_wait<1>();
+  else if (n == 2) cp_async_wait<2>();
+  else cp_async_wait<3>();
+}
+
+// Staging ring of the warp-specialised visit phases: slots 0, 1 are the staging
+// buffers, slots 2, 3 borrow whichever Q / Gram buffers are idle in that phase
+// (all hold >= one RCP x W2 chunk).
+struct WsRing {
+  double2* s0;
+  double2* s2;
+  double2* s3;
+  int depth;
+  template <int W2>
+  BMPS_DEV double2* slot(int k) const {
+    return k < 2 ? s0 + k * JacCfg<W2>::BUF : (k == 2 ? s2 : s3);
+  }
+};
+
+// Gram of the panel (I, J) into sG (math warps), chunks streamed through a
+// depth-deep cp.async ring (depth - 1 chunks in flight). Cross visits form only
+// G_IJ and take the rotated intra-block Grams from the cache.
+template <int W2>
+BMPS_DEV void ws_gram(const double2* X, int r, int c, int I, int J, bool cross, double2* sG,
+                      const WsRing& ring, double2* scratch, const double2* cI, const double2* cJ) {
+  using C = JacCfg<W2>;
+  const int nch = (r + C::RC - 1) / C::RC;
+  const int D = ring.depth;
+  double gacc[C::GT + 1][kZ3];
+#pragma unroll
+  for (int u = 0; u < C::GT + 1; ++u)
+#pragma unroll
+    for (int q = 0; q < kZ3; ++q) gacc[u][q] = 0.0;
+  for (int k = 0; k < D - 1 && k < nch; ++k)
+    jac_issue_chunk<W2>(ring.slot<W2>(k), X, r, c, k * C::RC, I, J);
+  for (int k = 0; k < nch; ++k) {
+    const double2* cur = ring.slot<W2>(k % D);
+    const int nxt = k + D - 1;
+    if (nxt < nch) jac_issue_chunk<W2>(ring.slot<W2>(nxt % D), X, r, c, nxt * C::RC, I, J);
+    cp_async_wait_n(min(nch - 1, nxt) - k);
+    WsMath::sync();
+    if (cross) jac_gram_chunk_cross<W2>(gacc, cur, min(C::RC, r - k * C::RC));
+    else jac_gram_chunk<W2>(gacc, cur, min(C::RC, r - k * C::RC));
+    WsMath::sync();
+  }
+  if (cross) jac_gram_store_cross<W2, WsMath>(gacc, sG, scratch, cI, cJ);
+  else jac_gram_store<W2, WsMath>(gacc, sG, scratch);
+}
+
+// Wait for the rotation warps' verdict on a visit and apply its Q (math warps).
+// The first chunks are requested before the wait so their loads overlap the tail
+// of the inner sweep. Returns the rotation count.
+template <int W2>
+BMPS_DEV int ws_finish(double2* X, int r, int c, int I, int J, const double2* sQ, const WsRing& ring,
+                       int pb, const WsVisit* wv) {
+  using C = JacCfg<W2>;
+  const int nch = (r + C::RC - 1) / C::RC;
+  const int D = ring.depth;
+  for (int k = 0; k < D - 1 && k < nch; ++k)
+    jac_issue_chunk<W2>(ring.slot<W2>(k), X, r, c, k * C::RC, I, J);
+  BMPS_TICK(fw0);
+  ws_wait(kWsQf + pb);
+  BMPS_TICK(fw1);
+  WS_ACC(0, 1, fw0, fw1);
+  const int nrot = ((volatile const WsVisit*)wv)[pb].nrot;
+  if (nrot == 0) {
+    cp_async_wait<0>();
+    return 0;
+  }
+  double aacc[C::AT][kZ3];
+  for (int k = 0; k < nch; ++k) {
+    const double2* cur = ring.slot<W2>(k % D);
+    const int nxt = k + D - 1;
+    if (nxt < nch) jac_issue_chunk<W2>(ring.slot<W2>(nxt % D), X, r, c, nxt * C::RC, I, J);
+    cp_async_wait_n(min(nch - 1, nxt) - k);
+    WsMath::sync();
+    jac_apply_mma<W2>(aacc, cur, sQ);
+    jac_apply_store_global<W2>(aacc, X, r, c, k * C::RC, I, J);
+    WsMath::sync();
+  }
+  BMPS_TICK(fw2);
+  WS_ACC(0, 2, fw1, fw2);
+  return nrot;
+}
+
+// Claim ring (scheduler -> math) and completion ring (math -> scheduler) in
+// shared memory, single producer / single consumer, polled with volatile flags.
+struct WsClaim {
+  int item, v, flag, pad;
+  unsigned rnd, pad2;
+};
+struct WsDone {
+  int item, I, J, dirty, flag, pad;
+  unsigned rnd, pad2;
+};
+constexpr int kWsRing = 2;
+#ifndef BMPS_WS_GRAM_DEPTH
+#define BMPS_WS_GRAM_DEPTH 4
+#endif
+#ifndef BMPS_WS_APPLY_DEPTH
+#define BMPS_WS_APPLY_DEPTH 2
+#endif
+constexpr int kWsGramDepth = BMPS_WS_GRAM_DEPTH, kWsApplyDepth = BMPS_WS_APPLY_DEPTH;
+
+template <int W2>
+__global__ void __launch_bounds__(kWsThreads, 2) jacobi_ws_kernel(JacArgs args) {
+  using C = JacCfg<W2>;
+  using WC = WsCfg<W2>;
+  constexpr int w = W2 / 2;
+  extern __shared__ __align__(16) double2 jsm[];
+  double2* sQ0 = jsm;                    // Q[0], Q[1]
+  double2* sG0 = sQ0 + 2 * WC::QSZ;      // G[0], G[1]
+  double2* sP = sG0 + 2 * WC::GSZ;       // two staging buffers
+  __shared__ RotShared rs_rot, rs_math;
+  __shared__ WsVisit wv[2];
+  __shared__ WsClaim claims[kWsRing];
+  __shared__ WsDone dones[kWsRing];
+  __shared__ int s_item, s_v;
+  __shared__ unsigned s_round;
+  __shared__ unsigned long long jbar[2];
+  if (threadIdx.x < kWsRing) {
+    claims[threadIdx.x].flag = 0;
+    dones[threadIdx.x].flag = 0;
+  }
+  if (threadIdx.x == 0) wv[0].stop = wv[1].stop = 0;
+  __syncthreads();
+
+  if (threadIdx.x >= kWsSched) {
+    // ---- scheduler warp (lane 0): claims visits ahead of the math warps, completes
+    // skippable visits, and does the round bookkeeping of finished visits ----
+    if (threadIdx.x != kWsSched) return;
+    volatile WsClaim* vc = claims;
+    volatile WsDone* vd = dones;
+    int cursor = blockIdx.x % args.nitems;
+    int cs = 0, ds = 0;
+    for (;;) {
+      // finished visits first: they may open the rounds the next claim needs
+      while (vd[ds].flag) {
+        __threadfence_block();
+        jac_complete<W2>(args, vd[ds].item, vd[ds].rnd, vd[ds].I, vd[ds].J, vd[ds].dirty != 0, false);
+        vd[ds].flag = 0;
+        ds = (ds + 1) % kWsRing;
+      }
+      if (vc[cs].flag) {       // ring full: the math warps are busy
+        __nanosleep(256);
+        continue;
+      }
+      int v = 0;
+      unsigned rnd = 0;
+      const int it = ws_claim<W2>(args, cursor, v, rnd);
+      if (it == -1) {
+        // nothing claimable: tell the math warps once (they finish their pending
+        // visit, whose completion may open a round), then back off
+        vc[cs].item = -1;
+        __threadfence_block();
+        vc[cs].flag = 1;
+        cs = (cs + 1) % kWsRing;
+        __nanosleep(1000);
+        cursor = (cursor + 1) % args.nitems;
+        continue;
+      }
+      vc[cs].item = it;
+      vc[cs].v = v;
+      vc[cs].rnd = rnd;
+      __threadfence_block();
+      vc[cs].flag = 1;
+      cs = (cs + 1) % kWsRing;
+      if (it == -2) return;
+    }
+  }
+
+  if (threadIdx.x >= kWsMath) {
+    // ---- rotation warps: inner sweeps, in visit order ----
+    for (int b = 0;; b ^= 1) {
+      BMPS_TICK(rw0);
+      ws_wait(kWsGf + b);
+      BMPS_TICK(rw1);
+      WS_ACC(kWsMath, 4, rw0, rw1);
+      const volatile WsVisit& v = wv[b];
+      if (v.stop) break;
+      double2* sG = sG0 + b * WC::GSZ;
+      double2* sQ = sQ0 + b * WC::QSZ;
+      const bool full = v.full;
+      const double tol = v.tol, noise2 = v.noise2, fro = v.fro;
+      double2* cI = v.cI;
+      double2* cJ = v.cJ;
+      int need = 0;
+      const int npairs = full ? W2 * W2 : w * w;
+      for (int idx = WsRot::tid(); idx < npairs && !need; idx += kWsRot) {
+        int i, j;
+        if (full) {
+          i = idx % W2;
+          j = idx / W2;
+          if (i >= j) continue;
+        } else {
+          i = idx % w;
+          j = w + idx / w;
+        }
+        need = jacobi_needs(sG[i + i * C::LDGG].x, sG[j + j * C::LDGG].x, sG[i + j * C::LDGG], tol,
+                            noise2, fro);
+      }
+      const int nrot = WsRot::count(need) != 0
+                           ? jac_inner<W2, WsRot>(sG, sQ, rs_rot, tol, noise2, fro, full, args.max_inner)
+                           : 0;
+      if (cI != nullptr && (full || nrot > 0)) jac_cache_store<W2, WsRot>(sG, cI, cJ);
+      if (WsRot::tid() == 0) wv[b].nrot = nrot;
+      WsRot::sync();
+      BMPS_TICK(rw2);
+      WS_ACC(kWsMath, 5, rw1, rw2);
+      WS_ACC(kWsMath, 6, 0, 1);
+      ws_arrive(kWsQf + b);
+    }
+    return;
+  }
+
+  // ---- math warps: Gram, apply ----
+  JacStage st{jbar, 0u};   // unused (no TMA staging here)
+  const int mt = threadIdx.x;
+  int b = 0;               // buffer pair of the next new visit
+  int cs = 0, ds = 0;      // claim / completion ring slots
+  bool pend = false;       // a visit is with the rotation warps (buffer b ^ 1)
+  int p_item = 0, p_I = 0, p_J = 0, p_r = 0, p_c = 0;
+  unsigned p_rnd = 0;
+  double2* p_X = nullptr;
+  // finish the pending visit and hand its completion to the scheduler warp
+  auto finish_pending = [&]() {
+    // apply ring: staging buffers + the pending visit's Gram buffer (the rotation
+    // warps are done with it once QF is passed; loads issued before that only
+    // target the staging buffers, depth 3 -> slots 0, 1 first)
+    const WsRing aring{sP, sG0 + (b ^ 1) * WC::GSZ, nullptr, kWsApplyDepth};
+    ws_finish<W2>(p_X, p_r, p_c, p_I, p_J, sQ0 + (b ^ 1) * WC::QSZ, aring, b ^ 1, wv);
+    if (mt == 0) {
+      volatile WsDone* vd = dones;
+      while (vd[ds].flag) __nanosleep(64);
+      vd[ds].item = p_item;
+      vd[ds].I = p_I;
+      vd[ds].J = p_J;
+      vd[ds].rnd = p_rnd;
+      vd[ds].dirty = wv[b ^ 1].nrot > 0;
+      __threadfence();     // the visit's panel (all math threads, ordered by the apply's
+                           // last barrier) and Gram-cache stores before the completion
+      vd[ds].flag = 1;
+    }
+    ds = (ds + 1) % kWsRing;
+  };
+  for (;;) {
+    BMPS_TICK(cw0);
+    if (mt == 0) {
+      volatile WsClaim* vc = claims;
+      while (!vc[cs].flag) { }
+      __threadfence_block();
+      s_item = vc[cs].item;
+      s_v = vc[cs].v;
+      s_round = vc[cs].rnd;
+      __threadfence_block();
+      vc[cs].flag = 0;
+    }
+    cs = (cs + 1) % kWsRing;
+    WsMath::sync();
+    const int i = s_item, v = s_v;
+    const unsigned rnd = s_round;
+    WsMath::sync();
+    BMPS_TICK(cw1);
+    if (i >= 0) { WS_ACC(0, 7, cw0, cw1); } else { WS_ACC(0, 8, cw0, cw1); WS_ACC(0, 9, 0, 1); }
+    if (i < 0) {
+      if (pend) {
+        finish_pending();
+        pend = false;
+      }
+      if (i == -2) break;
+      continue;
+    }
+    ItemMeta* m = args.meta + i;
+    const int r = m->jrows, c = m->c;
+    double2* X = (m->dq ? args.Z : m->precond ? args.Y : args.X) + (size_t)i * args.mat_stride;
+    int nb = (c + w - 1) / w;
+    nb += nb & 1;
+    const double tol = args.tol_factor * sqrt((double)r) * kEps;
+    const double noise2 = kNoiseRel * kNoiseRel * m->fro2;
+    const double fro = sqrt(m->fro2);
+    double2* sG = sG0 + b * WC::GSZ;
+    double2* sQ = sQ0 + b * WC::QSZ;
+    if (nb == 2) {
+      // single panel: the math warps iterate the whole item (buffer pair b is free)
+      const bool resident = r <= C::RC;
+      if (resident) jac_load_resident<W2, WsMath>(sP, X, r, c);
+      int sweep = 0;
+      bool clean = false;
+      for (; sweep < args.max_sweeps; ++sweep) {
+        if (!jac_visit<W2, WsMath>(X, r, c, 0, 1, tol, noise2, fro, true, 64, resident, sG, sQ, sP, rs_math,
+                                   st, false)) {
+          clean = true;
+          break;
+        }
+      }
+      if (resident) {
+        WsMath::sync();
+        jac_store_chunk<W2>(sP, X, r, c, 0, 0, 1);
+      }
+      WsMath::sync();
+      if (mt == 0) {
+        __threadfence();
+        m->sweeps = sweep;
+        if (!clean) m->status = BMPS_S_SVD_FAILED;
+        __threadfence();
+        m->conv = 1;
+        atomicSub(args.active, 1);
+      }
+      WsMath::sync();
+      continue;
+    }
+    const int rounds = nb - 1;
+    const int rho = (int)(rnd % (unsigned)rounds);
+    int I, J;
+    tourney_pair(nb, rho, v, I, J);
+    double2* gc = args.gcache ? args.gcache + (size_t)i * args.gcache_stride : nullptr;
+    double2* cI = gc ? gc + (size_t)I * w * w : nullptr;
+    double2* cJ = gc ? gc + (size_t)J * w * w : nullptr;
+    const bool full = rho == 0;
+    if (mt == 0) {
+      wv[b].tol = tol;
+      wv[b].noise2 = noise2;
+      wv[b].fro = fro;
+      wv[b].cI = cI;
+      wv[b].cJ = cJ;
+      wv[b].full = full;
+      wv[b].stop = 0;
+    }
+    // Q[b] is free (its last apply finished before this point): scratch for the
+    // k-split Gram partials
+    BMPS_TICK(gw0);
+    const WsRing gring{sP, sQ, sG, kWsGramDepth};
+    ws_gram<W2>(X, r, c, I, J, gc != nullptr && !full, sG, gring, sQ, cI, cJ);
+    WsMath::sync();
+    BMPS_TICK(gw1);
+    WS_ACC(0, 0, gw0, gw1);
+    WS_ACC(0, 3, 0, 1);
+    ws_arrive(kWsGf + b);
+    if (pend) finish_pending();
+    pend = true;
+    p_item = i;
+    p_I = I;
+    p_J = J;
+    p_r = r;
+    p_c = c;
+    p_rnd = rnd;
+    p_X = X;
+    b ^= 1;
+  }
+  if (mt == 0) wv[b].stop = 1;
+  WsMath::sync();
+  ws_arrive(kWsGf + b);
 }
 
 }  // namespace bmps
