@@ -696,6 +696,16 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, doub
   return first;
 }
 
+#ifndef BMPS_GRAM_RING3
+#define BMPS_GRAM_RING3 1
+#endif
+// Slot k % 3 of the Gram pass's staging ring: buffers 0, 1, then the Q buffer.
+template <int W2>
+BMPS_DEV double2* jac_ring3(double2* sP, double2* sQ, int k) {
+  const int m = k % 3;
+  return m == 2 ? sQ : sP + m * JacCfg<W2>::BUF;
+}
+
 // One block-pair visit; returns true if any rotation was applied. If
 // `resident`, the whole panel (r <= RC) already sits in buffer 0 and is
 // neither loaded nor stored here. W2 = 32 streams the panel with TMA bulk
@@ -732,6 +742,23 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
       else jac_gram_chunk<W2>(gacc, sP + b * C::BUF, min(C::RC, r - k * C::RC));
       G::sync();
     }
+  } else if (BMPS_GRAM_RING3 && C::NBUF == 2 && W2 * C::LDG >= C::BUF) {
+    // three-slot ring (staging buffers 0, 1 and sQ, idle until the inner sweep):
+    // two chunks in flight, one barrier per chunk -- the Gram pass reads the panel
+    // from HBM and is latency-bound with a single chunk in flight
+    G::sync();   // earlier users of the buffers are done
+    jac_issue_chunk<W2>(jac_ring3<W2>(sP, sQ, 0), X, r, c, 0, I, J);
+    if (nch > 1) jac_issue_chunk<W2>(jac_ring3<W2>(sP, sQ, 1), X, r, c, C::RC, I, J);
+    for (int k = 0; k < nch; ++k) {
+      if (k + 1 < nch) cp_async_wait<1>();
+      else cp_async_wait<0>();
+      G::sync();   // chunk k visible to all; every warp is done with chunk k - 1's slot
+      if (k + 2 < nch) jac_issue_chunk<W2>(jac_ring3<W2>(sP, sQ, k + 2), X, r, c, (k + 2) * C::RC, I, J);
+      const double2* cur = jac_ring3<W2>(sP, sQ, k);
+      if (cross_gram) jac_gram_chunk_cross<W2>(gacc, cur, min(C::RC, r - k * C::RC));
+      else jac_gram_chunk<W2>(gacc, cur, min(C::RC, r - k * C::RC));
+    }
+    G::sync();   // the Gram store reuses buffer 1 / sQ
   } else {
     G::sync();
     jac_issue_chunk<W2>(sP, X, r, c, 0, I, J);

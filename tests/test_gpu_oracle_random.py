@@ -150,3 +150,40 @@ def test_double_qr_preconditioning_matches_oracle(dq, chi, cutoff):
         _compare(prog, 14, cutoff, chi, seed=chi)
     finally:
         lib.bmps_set_param(b"double_qr", float(_native.DEFAULT_PARAMS["double_qr"]))
+
+
+@pytest.mark.parametrize("chi,cutoff", [(48, 1e-10), (128, 0.0), (128, 1e-10)])
+def test_warp_specialised_jacobi_matches_oracle(chi, cutoff):
+    """jac_ws=1: math / rotation / scheduler warps with a two-deep visit pipeline
+    (single-panel items run by the math warps alone) give the oracle's results."""
+    from paper_1807_07914_b200 import _native
+    lib = _native.load()
+    assert lib.bmps_set_param(b"jac_ws", 1.0) == 0
+    try:
+        prog = brick_circuit(14, 14, np.random.default_rng(500 + chi))
+        _compare(prog, 14, cutoff, chi, seed=chi + 1)
+    finally:
+        lib.bmps_set_param(b"jac_ws", float(_native.DEFAULT_PARAMS["jac_ws"]))
+
+
+def test_warp_specialised_jacobi_bulk_layer_spectra():
+    """jac_ws=1 on a batch of chi=256 updates (the bench workload's shape): bond
+    spectra and keep counts equal the default kernel's (1e-10 of the largest)."""
+    from paper_1807_07914_b200 import _native, MpsBatch, TruncationPolicy
+    lib = _native.load()
+    rng = np.random.default_rng(11)
+    progs = [brick_circuit(18, 12, rng) for _ in range(3)]
+    out = []
+    for ws in (0.0, 1.0):
+        assert lib.bmps_set_param(b"jac_ws", ws) == 0
+        try:
+            b = MpsBatch(3, 18, TruncationPolicy(1e-10, 256))
+            b.run(progs)
+            b.check_status()
+            out.append((b.host_dims(), [b.bond_vectors(s) for s in range(3)]))
+        finally:
+            lib.bmps_set_param(b"jac_ws", float(_native.DEFAULT_PARAMS["jac_ws"]))
+    assert (out[0][0] == out[1][0]).all()
+    for s in range(3):
+        for la, lb in zip(out[0][1][s], out[1][1][s]):
+            assert np.max(np.abs(la - lb)) <= 1e-10 * max(la.max(), 1.0)
