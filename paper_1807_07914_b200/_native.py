@@ -74,7 +74,7 @@ _lib = None
 DEFAULT_PARAMS = {"tol_factor": 4.0, "max_sweeps": 60, "max_inner": 1, "qr_min_cols": 65,
                   "jacobi_mode": 4, "cluster_size": 8, "tma_staging": 0, "gram_cache": 1,
                   "block_w2": 32, "double_qr": 1, "jac_per_sm": 0, "col_sort": 1, "time_svd": 0, "pair_skip": 1,
-                  "jac_ws": 0}
+                  "jac_ws": 0, "jac_cluster": -1}
 
 
 def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:

@@ -35,6 +35,7 @@ int g_tma_staging = 0;     // 1: Jacobi panels staged by TMA bulk copies instead
 int g_gram_cache = 1;      // cross visits reuse rotated intra-block Grams
 int g_block_w2 = 32;       // block-mode panel width: 16, 32, 64 columns, or 0 = auto (16 / 32)
 int g_double_qr = 1;       // second QR of R^H before the Jacobi (preconditioned items)
+int g_jac_cluster = -1;    // row-split cluster Jacobi: -1 auto (small batches), 0 off, 2 / 4 CTAs
 int g_jac_ws = 0;          // warp-specialised dynamic Jacobi (W2 = 32); measured slower, opt-in
 int g_jac_per_sm = 0;      // dynamic Jacobi CTAs per SM (0: occupancy maximum)
 int g_col_sort = 1;        // descending-norm column order ahead of the first QR (double-QR items)
@@ -650,6 +651,10 @@ void set_attrs() {
                        (int)JacCfg<16>::kSmem);
   cudaFuncSetAttribute(jacobi_ws_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)WsCfg<32>::kSmem);
+  cudaFuncSetAttribute(jacobi_cluster_kernel<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)ClCfg<32>::kSmem);
+  cudaFuncSetAttribute(jacobi_cluster_kernel<32, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)ClCfg<32>::kSmem);
   g_attrs_set = true;
 }
 
@@ -707,6 +712,8 @@ int32_t bmps_set_param(const char* name, double value) {
   else if (k == "double_qr" && (value == 0 || value == 1)) g_double_qr = (int)value;
   else if (k == "jac_per_sm" && value >= 0 && value <= 8) g_jac_per_sm = (int)value;
   else if (k == "jac_ws" && (value == 0 || value == 1)) g_jac_ws = (int)value;
+  else if (k == "jac_cluster" && (value == -1 || value == 0 || value == 2 || value == 4))
+    g_jac_cluster = (int)value;
   else if (k == "col_sort" && (value == 0 || value == 1)) g_col_sort = (int)value;
   else if (k == "time_svd" && (value == 0 || value == 1)) g_time_svd = (int)value;
   else if (k == "pair_skip" && (value == 0 || value == 1)) g_pair_skip = (int)value;
@@ -929,6 +936,27 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       if (g_block_w2 == 0) wi = (long long)nitems * (nbmax / 2) < slots_of(1) ? 0 : 1;
       const bool ws_mode = wi == 1 && g_jac_ws;
       int slots = slots_of(ws_mode ? 3 : wi);
+      // small batches: one visit per cluster of CTAs (row split), see jacobi_cluster_kernel
+      // (auto: when a round's visits fit the clusters that are co-resident; a visit
+      // on a cluster of CS CTAs finishes sooner, but CS x fewer visits are in flight)
+      int csize = 0;
+      int cl_per_sm = 0, n_sms = kNumSMs;
+      if (wi == 1 && !g_tma_staging && g_jac_cluster != 0) {
+        static int cl_occ = 0;
+        if (!cl_occ) {
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cl_occ, jacobi_cluster_kernel<32, 4>, 256,
+                                                        ClCfg<32>::kSmem);
+          cl_occ = std::max(cl_occ, 1);
+        }
+        cl_per_sm = cl_occ;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
+        const long long vis_round = (long long)nitems * (nbmax / 2);
+        if (g_jac_cluster > 0) csize = g_jac_cluster;
+        else if (vis_round <= (long long)cl_per_sm * n_sms / 4) csize = 4;
+        else if (vis_round <= (long long)cl_per_sm * n_sms / 2) csize = 2;
+      }
       if (g_jac_per_sm > 0) {
         int dev = 0, sms = kNumSMs;
         cudaGetDevice(&dev);
@@ -939,7 +967,27 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
                     : wi == 1 ? nbmax / 2
                               : (cmax + 15) / 16;
       const int grid = std::min(slots, nitems * vis);
-      if (ws_mode)
+      if (csize > 0) {
+        const int nclusters = std::max(1, std::min(nitems * (nbmax / 2), cl_per_sm * n_sms / csize));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(nclusters * csize, 1, 1);
+        cfg.blockDim = dim3(256, 1, 1);
+        cfg.dynamicSmemBytes = ClCfg<32>::kSmem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = csize;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const cudaError_t e = csize == 4 ? cudaLaunchKernelEx(&cfg, jacobi_cluster_kernel<32, 4>, ja)
+                                         : cudaLaunchKernelEx(&cfg, jacobi_cluster_kernel<32, 2>, ja);
+        if (e != cudaSuccess) {
+          fprintf(stderr, "libbmps: cluster Jacobi launch failed: %s\n", cudaGetErrorString(e));
+          return BMPS_E_LAUNCH;
+        }
+      } else if (ws_mode)
         jacobi_ws_kernel<32><<<grid, kWsThreads, WsCfg<32>::kSmem, st>>>(ja);
       else if (wi == 2)
         jacobi_dynamic_kernel<64><<<grid, 256, JacCfg<64>::kSmem, st>>>(ja);

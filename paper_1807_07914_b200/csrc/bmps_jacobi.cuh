@@ -26,7 +26,7 @@
 namespace bmps {
 
 #ifndef BMPS_REGQ
-#define BMPS_REGQ 1   // register-resident Q in the cross rounds of the inner sweep
+#define BMPS_REGQ 0   // register-resident Q in the cross rounds of the inner sweep (measured neutral, spills)
 #endif
 
 #ifndef BMPS_JAC_MINB
@@ -1685,6 +1685,216 @@ __global__ void __launch_bounds__(kWsThreads, 2) jacobi_ws_kernel(JacArgs args) 
   if (mt == 0) wv[b].stop = 1;
   WsMath::sync();
   ws_arrive(kWsGf + b);
+}
+
+// ---------------------------------------------------------------------------
+// Row-split cluster kernel (small batches: one circuit's brick layer).
+//
+// With few items the dynamic kernel cannot fill the GPU, and an item's ~9 x 31
+// rounds run back to back at the latency of one visit (16 chunks of Gram pass,
+// 16 inner rounds, 16 chunks of apply on one CTA). Here a thread-block cluster
+// of CS CTAs works one visit: CTA k streams rows [k*rs, (k+1)*rs) of the panel,
+// forms its partial Gram, the partials are summed through distributed shared
+// memory in rank order (every CTA gets the bit-identical G), every CTA runs the
+// same inner sweep (same G, same code -> the same Q, no broadcast), and applies
+// Q to its own rows. Claiming, exact skipping and round bookkeeping are those of
+// the dynamic kernel (rank 0 of the cluster).
+template <int W2>
+struct ClCfg {
+  using C = JacCfg<W2>;
+  static constexpr int PSZ = W2 * C::LDGG;   // partial Gram buffer
+  static constexpr size_t kSmem = (size_t)(W2 * C::LDG + C::NBUF * C::BUF + PSZ) * sizeof(double2);
+};
+
+// Partial Gram over rows [row0, row1) (chunk-aligned), three-slot ring as in jac_visit.
+template <int W2>
+BMPS_DEV void cl_gram_rows(double (&gacc)[JacCfg<W2>::GT + 1][kZ3], const double2* X, int r, int c,
+                           int I, int J, bool cross, double2* sP, double2* sQ, int row0, int row1) {
+  using C = JacCfg<W2>;
+  const int nch = (row1 - row0 + C::RC - 1) / C::RC;
+#pragma unroll
+  for (int u = 0; u < C::GT + 1; ++u)
+#pragma unroll
+    for (int q = 0; q < kZ3; ++q) gacc[u][q] = 0.0;
+  __syncthreads();
+  if (nch > 0) jac_issue_chunk<W2>(jac_ring3<W2>(sP, sQ, 0), X, r, c, row0, I, J);
+  if (nch > 1) jac_issue_chunk<W2>(jac_ring3<W2>(sP, sQ, 1), X, r, c, row0 + C::RC, I, J);
+  for (int k = 0; k < nch; ++k) {
+    if (k + 1 < nch) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    __syncthreads();
+    if (k + 2 < nch)
+      jac_issue_chunk<W2>(jac_ring3<W2>(sP, sQ, k + 2), X, r, c, row0 + (k + 2) * C::RC, I, J);
+    const double2* cur = jac_ring3<W2>(sP, sQ, k);
+    const int nrows = min(C::RC, row1 - (row0 + k * C::RC));
+    if (cross) jac_gram_chunk_cross<W2>(gacc, cur, nrows);
+    else jac_gram_chunk<W2>(gacc, cur, nrows);
+  }
+  __syncthreads();
+}
+
+// P <- P Q over rows [row0, row1) (chunk-aligned), cp.async double buffering.
+template <int W2>
+BMPS_DEV void cl_apply_rows(double2* X, int r, int c, int I, int J, const double2* sQ, double2* sP,
+                            int row0, int row1) {
+  using C = JacCfg<W2>;
+  const int nch = (row1 - row0 + C::RC - 1) / C::RC;
+  if (nch <= 0) return;
+  double aacc[C::AT][kZ3];
+  jac_issue_chunk<W2>(sP, X, r, c, row0, I, J);
+  for (int k = 0; k < nch; ++k) {
+    double2* cur = sP + (k & 1) * C::BUF;
+    if (k + 1 < nch) {
+      jac_issue_chunk<W2>(sP + ((k + 1) & 1) * C::BUF, X, r, c, row0 + (k + 1) * C::RC, I, J);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    jac_apply_mma<W2>(aacc, cur, sQ);
+    jac_apply_store_global<W2>(aacc, X, r, c, row0 + k * C::RC, I, J);
+    __syncthreads();
+  }
+}
+
+template <int W2, int CS>
+__global__ void __launch_bounds__(256, 3) jacobi_cluster_kernel(JacArgs args) {
+  namespace cg = cooperative_groups;
+  using C = JacCfg<W2>;
+  using CC = ClCfg<W2>;
+  constexpr int w = W2 / 2;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  extern __shared__ __align__(16) double2 jsm[];
+  double2* sQ = jsm;
+  double2* sP = sQ + W2 * C::LDG;
+  double2* sG = C::G_IN_BUF ? sP + C::BUF : nullptr;   // W2 = 32 only
+  double2* sPart = sP + C::NBUF * C::BUF;
+  __shared__ RotShared rs;
+  __shared__ int c_item, c_v;
+  __shared__ unsigned c_round;
+  __shared__ unsigned long long jbar[2];
+  JacStage st{jbar, 0u};
+  const double2* rPart[CS];
+#pragma unroll
+  for (int k = 0; k < CS; ++k) rPart[k] = cl.map_shared_rank(sPart, k);
+  const int* r_item = cl.map_shared_rank(&c_item, 0);
+  const int* r_v = cl.map_shared_rank(&c_v, 0);
+  const unsigned* r_round = cl.map_shared_rank(&c_round, 0);
+  const int tid = threadIdx.x;
+  int cursor = (int)(blockIdx.x / CS) % args.nitems;
+  for (;;) {
+    if (rank == 0 && tid == 0) {
+      int v = 0;
+      unsigned rnd = 0;
+      int it;
+      while ((it = ws_claim<W2>(args, cursor, v, rnd)) == -1) {
+        __nanosleep(1000);
+        cursor = (cursor + 1) % args.nitems;
+      }
+      c_item = it;
+      c_v = v;
+      c_round = rnd;
+    }
+    cl.sync();
+    const int i = *r_item, v = *r_v;
+    const unsigned rnd = *r_round;
+    cl.sync();   // rank 0 may overwrite the claim only after every CTA has read it
+    if (i < 0) break;
+    ItemMeta* m = args.meta + i;
+    const int r = m->jrows, c = m->c;
+    double2* X = (m->dq ? args.Z : m->precond ? args.Y : args.X) + (size_t)i * args.mat_stride;
+    int nb = (c + w - 1) / w;
+    nb += nb & 1;
+    const double tol = args.tol_factor * sqrt((double)r) * kEps;
+    const double noise2 = kNoiseRel * kNoiseRel * m->fro2;
+    const double fro = sqrt(m->fro2);
+    if (nb == 2) {
+      // single panel: rank 0 iterates the item alone (small; the others move on)
+      if (rank == 0) {
+        const bool resident = r <= C::RC;
+        if (resident) jac_load_resident<W2>(sP, X, r, c);
+        int sweep = 0;
+        bool clean = false;
+        for (; sweep < args.max_sweeps; ++sweep) {
+          if (!jac_visit<W2>(X, r, c, 0, 1, tol, noise2, fro, true, 64, resident, sG, sQ, sP, rs, st, false)) {
+            clean = true;
+            break;
+          }
+        }
+        if (resident) {
+          __syncthreads();
+          jac_store_chunk<W2>(sP, X, r, c, 0, 0, 1);
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+          m->sweeps = sweep;
+          if (!clean) m->status = BMPS_S_SVD_FAILED;
+          __threadfence();
+          m->conv = 1;
+          atomicSub(args.active, 1);
+        }
+        __syncthreads();
+      }
+      continue;
+    }
+    const int rounds = nb - 1;
+    const int rho = (int)(rnd % (unsigned)rounds);
+    int I, J;
+    tourney_pair(nb, rho, v, I, J);
+    const bool full = rho == 0;
+    double2* gc = args.gcache ? args.gcache + (size_t)i * args.gcache_stride : nullptr;
+    double2* cI = gc ? gc + (size_t)I * w * w : nullptr;
+    double2* cJ = gc ? gc + (size_t)J * w * w : nullptr;
+    const bool cross = gc != nullptr && !full;
+    // chunk-aligned row range of this rank
+    const int rs_rows = ((r + C::RC - 1) / C::RC + CS - 1) / CS * C::RC;
+    const int row0 = min(r, rank * rs_rows), row1 = min(r, row0 + rs_rows);
+    double gacc[C::GT + 1][kZ3];
+    cl_gram_rows<W2>(gacc, X, r, c, I, J, cross, sP, sQ, row0, row1);
+    if (cross) jac_gram_store_cross<W2>(gacc, sPart, sQ, cI, cJ);
+    else jac_gram_store<W2>(gacc, sPart, sQ);
+    cl.sync();   // every rank's partial Gram is in place
+    for (int idx = tid; idx < W2 * W2; idx += blockDim.x) {
+      const int a = idx % W2, b2 = idx / W2;
+      const int e = a + b2 * C::LDGG;
+      if (cross && ((a < w) == (b2 < w))) {
+        sG[e] = sPart[e];        // rotated intra-block Gram from the cache (same in every rank)
+      } else {
+        double2 acc = rPart[0][e];
+#pragma unroll
+        for (int k = 1; k < CS; ++k) acc = cadd(acc, rPart[k][e]);
+        sG[e] = acc;
+      }
+    }
+    cl.sync();   // partials consumed (the next visit rewrites them); sG complete in every rank
+    int need = 0;
+    {
+      const int npairs = full ? W2 * W2 : w * w;
+      for (int idx = tid; idx < npairs && !need; idx += blockDim.x) {
+        int a, b2;
+        if (full) {
+          a = idx % W2;
+          b2 = idx / W2;
+          if (a >= b2) continue;
+        } else {
+          a = idx % w;
+          b2 = w + idx / w;
+        }
+        need = jacobi_needs(sG[a + a * C::LDGG].x, sG[b2 + b2 * C::LDGG].x, sG[a + b2 * C::LDGG], tol,
+                            noise2, fro);
+      }
+    }
+    const int nrot = __syncthreads_or(need) ? jac_inner<W2>(sG, sQ, rs, tol, noise2, fro, full, args.max_inner)
+                                            : 0;
+    if (rank == 0 && gc != nullptr && (full || nrot > 0)) jac_cache_store<W2>(sG, cI, cJ);
+    __syncthreads();   // sG (staging buffer 1) is read before the apply refills it
+    if (nrot > 0) cl_apply_rows<W2>(X, r, c, I, J, sQ, sP, row0, row1);
+    __threadfence();
+    cl.sync();         // every rank's panel rows (and rank 0's cache) are written
+    if (rank == 0 && tid == 0) jac_complete<W2>(args, i, rnd, I, J, nrot > 0, false);
+  }
 }
 
 }  // namespace bmps
