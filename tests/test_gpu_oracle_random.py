@@ -187,3 +187,18 @@ def test_warp_specialised_jacobi_bulk_layer_spectra():
     for s in range(3):
         for la, lb in zip(out[0][1][s], out[1][1][s]):
             assert np.max(np.abs(la - lb)) <= 1e-10 * max(la.max(), 1.0)
+
+
+@pytest.mark.parametrize("csize", [0, 2, 4])
+@pytest.mark.parametrize("chi,cutoff", [(64, 1e-10), (128, 0.0)])
+def test_row_split_cluster_jacobi_matches_oracle(csize, chi, cutoff):
+    """jac_cluster: each visit's panel rows split over a 2- or 4-CTA cluster (partial
+    Grams summed through distributed shared memory), or off (0)."""
+    from paper_1807_07914_b200 import _native
+    lib = _native.load()
+    assert lib.bmps_set_param(b"jac_cluster", float(csize)) == 0
+    try:
+        prog = brick_circuit(14, 14, np.random.default_rng(900 + chi + csize))
+        _compare(prog, 14, cutoff, chi, seed=chi + csize)
+    finally:
+        lib.bmps_set_param(b"jac_cluster", float(_native.DEFAULT_PARAMS["jac_cluster"]))
