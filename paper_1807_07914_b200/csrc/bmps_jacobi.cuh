@@ -1034,6 +1034,7 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dy
   int cursor = blockIdx.x % nitems;
   volatile int* active = args.active;
   while (*active > 0) {
+    BMPS_TICK(dc0);
     if (threadIdx.x == 0) {
       s_item = -1;
       for (int probe = 0; probe < nitems; ++probe) {
@@ -1059,6 +1060,8 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dy
     }
     __syncthreads();
     const int i = s_item;
+    BMPS_TICK(dc1);
+    if (i >= 0) { WS_ACC(0, 10, dc0, dc1); WS_ACC(0, 11, 0, 1); } else { WS_ACC(0, 12, dc0, dc1); }
     if (i < 0) {
       if (threadIdx.x == 0) __nanosleep(2000);
       __syncthreads();
@@ -1121,6 +1124,7 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dy
       const int lc = *((volatile int*)last_chk);
       skip = lc >= 0 && *((volatile int*)(last_rot + I)) < lc && *((volatile int*)(last_rot + J)) < lc;
     }
+    if (skip) { WS_ACC(0, 13, 0, 1); }
     const bool dirty = skip ? false
                             : jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, rho == 0,
                                             args.max_inner, false, sG, sQ, sP, rs, st, args.tma, gc);
