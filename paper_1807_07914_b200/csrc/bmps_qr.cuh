@@ -108,6 +108,11 @@ BMPS_DEV double block_sum(double v, double* red) {
 // its order are identical to the global-memory version. Used when
 // (r - j0) x kQrNb x 16 B fits (kQrPanelSmemRows).
 constexpr int kQrPanelSmemRows = 384;   // 384 x 32 x 16 B + 33 KB static <= 227 KB
+#ifndef BMPS_QR_PANEL_U
+#define BMPS_QR_PANEL_U 4
+#endif
+// row strides per batch of the per-column loops (4 measured best of 4 / 8 / 16)
+constexpr int kQrPanelU = BMPS_QR_PANEL_U;
 template <bool SMEM>
 __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
   __shared__ double red[16];
@@ -140,6 +145,7 @@ __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
   for (int k = j0; k < j1; ++k) {
     double2* col = colp(k);
     double s = 0.0;
+#pragma unroll 4
     for (int i = k + 1 + tid; i < r; i += blockDim.x) s += cabs2(col[i]);
     const double xnorm2 = block_sum(s, red);
     const double2 alpha = col[k];
@@ -155,6 +161,7 @@ __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
       scale = make_double2(d.x * inv, -d.y * inv);
     }
     __syncthreads();
+#pragma unroll 4
     for (int i = k + 1 + tid; i < r; i += blockDim.x) col[i] = cmul(col[i], scale);
     if (tid == 0) {
       col[k] = make_double2(beta, 0.0);
@@ -164,8 +171,30 @@ __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
     // apply P_k = I - conj(tau) v v^H to panel columns k+1 .. j1-1 (one warp per column)
     for (int jj = k + 1 + warp; jj < j1 && (t.x != 0.0 || t.y != 0.0); jj += blockDim.x >> 5) {
       double2* cj = colp(jj);
-      double2 w = lane == 0 ? cj[k] : make_double2(0.0, 0.0);
-      for (int i = k + 1 + lane; i < r; i += 32) w = cfma(cconj(col[i]), cj[i], w);
+      // four row strides per iteration, loads issued together (tall panels run from
+      // L2: one dependent round trip per stride otherwise); interleaved partial sums
+      constexpr int U = kQrPanelU;
+      double2 wp[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) wp[u] = make_double2(0.0, 0.0);
+      if (lane == 0) wp[0] = cj[k];
+      int i = k + 1 + lane;
+      for (; i + 32 * (U - 1) < r; i += 32 * U) {
+        double2 av[U], bv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          av[u] = col[i + 32 * u];
+          bv[u] = cj[i + 32 * u];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) wp[u] = cfma(cconj(av[u]), bv[u], wp[u]);
+      }
+      for (; i < r; i += 32) wp[0] = cfma(cconj(col[i]), cj[i], wp[0]);
+#pragma unroll
+      for (int h = U / 2; h > 0; h >>= 1)
+#pragma unroll
+        for (int u = 0; u < h; ++u) wp[u] = cadd(wp[u], wp[u + h]);
+      double2 w = wp[0];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         w.x += __shfl_xor_sync(0xffffffffu, w.x, o);
@@ -173,7 +202,18 @@ __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
       }
       const double2 f = cmul(cconj(t), w);
       if (lane == 0) cj[k] = csub(cj[k], f);
-      for (int i = k + 1 + lane; i < r; i += 32) cj[i] = csub(cj[i], cmul(col[i], f));
+      i = k + 1 + lane;
+      for (; i + 32 * (U - 1) < r; i += 32 * U) {
+        double2 av[U], bv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          av[u] = col[i + 32 * u];
+          bv[u] = cj[i + 32 * u];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) cj[i + 32 * u] = csub(bv[u], cmul(av[u], f));
+      }
+      for (; i < r; i += 32) cj[i] = csub(cj[i], cmul(col[i], f));
     }
     __syncthreads();
   }
@@ -193,17 +233,32 @@ __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
     const int kr = lane & 3, rc = lane >> 2;
     const int ti = warp >> 2, tj = warp & 3;   // 512 threads: 16 warps cover 4 x 4 tiles
     const bool own = ti < kQrNb / 8 && tj < kQrNb / 8;
-    for (int rb = j0; rb < r; rb += 32) {
-      for (int i = tid; i < 32 * kQrNb; i += blockDim.x) {
-        const int row = i % 32, p = i / 32;
-        const int gr = rb + row, k = j0 + p;
-        double2 v = make_double2(0.0, 0.0);
-        if (p < nbp && gr < r) {
-          if (gr == k) v = make_double2(1.0, 0.0);
-          else if (gr > k) v = A[(size_t)k * r + gr];
-        }
-        sVc[row][p] = v;
+    // chunk loader: element i of the 32-row chunk at rb (each thread owns the same
+    // elements of every chunk: 32 x kQrNb <= 2 x 512); the next chunk is loaded into
+    // registers while the current one is multiplied
+    constexpr int kPer = (32 * kQrNb + 511) / 512;
+    auto vload = [&](int rb, int u) -> double2 {
+      const int i = tid + u * 512;
+      const int row = i % 32, p = i / 32;
+      const int gr = rb + row, k = j0 + p;
+      double2 v = make_double2(0.0, 0.0);
+      if (i < 32 * kQrNb && p < nbp && gr < r) {
+        if (gr == k) v = make_double2(1.0, 0.0);
+        else if (gr > k) v = A[(size_t)k * r + gr];
       }
+      return v;
+    };
+    double2 vnext[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) vnext[u] = vload(j0, u);
+    for (int rb = j0; rb < r; rb += 32) {
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int i = tid + u * 512;
+        if (i < 32 * kQrNb) sVc[i % 32][i / 32] = vnext[u];
+      }
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) vnext[u] = rb + 32 < r ? vload(rb + 32, u) : make_double2(0.0, 0.0);
       __syncthreads();
       if (own) {
 #pragma unroll
