@@ -152,6 +152,9 @@ BMPS_DEV bool jacobi_needs(double a, double b, double2 g, double tol, double noi
   return cabs2(g) > thr * thr * lo;
 }
 
+#ifndef BMPS_ROT32
+#define BMPS_ROT32 0   // FP32 rotation angles: parity-green, throughput-neutral (measured), off
+#endif
 BMPS_DEV bool jacobi_rotation(double a, double b, double2 g, double tol, double noise2, double fro,
                               double& c, double& s, double2& e) {
   const double lo = fmin(a, b), hi = fmax(a, b);
@@ -166,6 +169,40 @@ BMPS_DEV bool jacobi_rotation(double a, double b, double2 g, double tol, double 
   // (zeta = delta / 2|g|, t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2))), with
   // c^2 + s^2 = 1 by construction; the rotation chain is ~40% shorter, which is
   // what the inner sweep waits on (the FP64 pipe is shared with other CTAs' DMMA).
+#if BMPS_ROT32
+  // Angle in FP32 (the FP32 pipe is not shared with the DMMA of other CTAs), then an
+  // FP64 renormalisation so the transform stays unitary to FP64 rounding: c, s and e
+  // are scaled by 1/sqrt(c^2 + s^2) and 1/|e| with the series 1 - d/2 + 3d^2/8
+  // (|d| ~ 1e-7, remainder ~1e-21). The 2x2 Gram is first scaled by a power of two
+  // (exact) so hi is O(1); a pair whose scaled |g|^2 leaves the FP32 range takes the
+  // FP64 path below. (numpy model on harvested cfg3 theta: same sweep count, sigma
+  // error 9e-14 vs 3e-14 relative.)
+  {
+    const int eh = (int)((__double_as_longlong(hi) >> 52) & 0x7ff);
+    const double sc = __longlong_as_double((long long)(2046 - eh) << 52);   // 2^(1023 - eh)
+    // delta in FP64 first: nearly equal column norms cancel catastrophically in FP32
+    const float df = (float)((b - a) * sc);
+    const float gxf = (float)(g.x * sc), gyf = (float)(g.y * sc);
+    const float g2f = fmaf(gxf, gxf, gyf * gyf);
+    if (g2f > 1e-30f) {
+      const float rrf = rsqrtf(fmaf(df, df, 4.0f * g2f));
+      const float c2f = fmaf(0.5f * fabsf(df), rrf, 0.5f);
+      const float rcf = rsqrtf(c2f);
+      const float rgf = rsqrtf(g2f);
+      const double c0 = (double)(c2f * rcf);
+      const double s0 = (double)((g2f * rgf) * rrf * rcf);
+      const double ex = (double)(gxf * rgf), ey = (double)(gyf * rgf);
+      const double d = fma(c0, c0, s0 * s0) - 1.0;
+      const double n = fma(d, fma(d, 0.375, -0.5), 1.0);
+      const double de = fma(ex, ex, ey * ey) - 1.0;
+      const double ne = fma(de, fma(de, 0.375, -0.5), 1.0);
+      c = c0 * n;
+      s = df < 0.0f ? -(s0 * n) : s0 * n;
+      e = make_double2(ex * ne, ey * ne);
+      return true;
+    }
+  }
+#endif
   const double rg = g2 > 1e-290 ? fast_rsqrt(g2) : rsqrt(g2);   // 1 / |g|, off the chain
   const double delta = b - a;
   const double rho2 = fma(delta, delta, 4.0 * g2);
