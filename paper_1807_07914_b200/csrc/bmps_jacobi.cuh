@@ -438,8 +438,8 @@ BMPS_DEV void jac_gram_store_cross(const double (&acc)[JacCfg<W2>::GT + 1][kZ3],
     sG[i + j * C::LDGG] = cI[i + j * w];
     sG[(w + i) + (w + j) * C::LDGG] = cJ[i + j * w];
   }
-  if (CT >= 8) {
-    constexpr int TPW = CT >= 8 ? CT / 8 : 1;
+  if constexpr (CT >= 8) {
+    constexpr int TPW = CT / 8;
 #pragma unroll
     for (int u = 0; u < TPW; ++u) {
       const int t = warp * TPW + u, ti = t / NTc, tj = NTc + t % NTc;
@@ -451,20 +451,20 @@ BMPS_DEV void jac_gram_store_cross(const double (&acc)[JacCfg<W2>::GT + 1][kZ3],
         sG[j + i * C::LDGG] = cconj(v);
       }
     }
-    return;
-  }
+  } else {
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
-    scratch[warp * 64 + rr * 8 + cc + h] = z3_get(acc[0], h);
-  G::sync();
-  constexpr int KS = CT < 8 ? 8 / CT : 1;
-  for (int idx = G::tid(); idx < CT * 64; idx += G::n()) {
-    const int t = idx / 64, e = idx % 64;
-    double2 v = scratch[(KS * t) * 64 + e];
-    for (int k = 1; k < KS; ++k) v = cadd(v, scratch[(KS * t + k) * 64 + e]);
-    const int i = (t / NTc) * 8 + e / 8, j = w + (t % NTc) * 8 + e % 8;
-    sG[i + j * C::LDGG] = v;
-    sG[j + i * C::LDGG] = cconj(v);
+    for (int h = 0; h < 2; ++h)
+      scratch[warp * 64 + rr * 8 + cc + h] = z3_get(acc[0], h);
+    G::sync();
+    constexpr int KS = 8 / CT;
+    for (int idx = G::tid(); idx < CT * 64; idx += G::n()) {
+      const int t = idx / 64, e = idx % 64;
+      double2 v = scratch[(KS * t) * 64 + e];
+      for (int k = 1; k < KS; ++k) v = cadd(v, scratch[(KS * t + k) * 64 + e]);
+      const int i = (t / NTc) * 8 + e / 8, j = w + (t % NTc) * 8 + e % 8;
+      sG[i + j * C::LDGG] = v;
+      sG[j + i * C::LDGG] = cconj(v);
+    }
   }
 }
 
