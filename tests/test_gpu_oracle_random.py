@@ -202,3 +202,39 @@ def test_row_split_cluster_jacobi_matches_oracle(csize, chi, cutoff):
         _compare(prog, 14, cutoff, chi, seed=chi + csize)
     finally:
         lib.bmps_set_param(b"jac_cluster", float(_native.DEFAULT_PARAMS["jac_cluster"]))
+
+
+def _theta(gammas, lams, q):
+    """Gauge-invariant two-site tensor lam_{q-1} G_q lam_q G_{q+1} lam_{q+1} (mps.py:105-109)."""
+    n = len(gammas)
+    lam_l = lams[q - 1] if q > 0 else np.ones(1)
+    lam_r = lams[q + 1] if q + 1 < n - 1 else np.ones(1)
+    return np.einsum("l,lsm,m,mtr,r->lstr", lam_l, gammas[q], lams[q], gammas[q + 1], lam_r, optimize=True)
+
+
+def test_chi256_updates_on_cfg3_steady_state_match_oracle():
+    """The bench's unit of work at full size: chi = 256 CNOT updates (512 x 512 theta,
+    keep 256 of 512) on a GPU-evolved cfg3 state (50 qubits, 25 layers), against the
+    oracle applied to the same tensors: new bond vector and the two-site tensor."""
+    import bench
+    from paper_1807_07914_b200.ir import GateKind, Instruction
+    st = mps_run(bench.prefix_program(1003, 25), bench.N_QUBITS, TruncationPolicy(bench.CUTOFF, bench.CHI))
+    gam, lam = st.site_tensors, st.bond_vectors
+    sites = [q for q in range(10, 38, 9) if len(lam[q - 1]) == len(lam[q]) == len(lam[q + 1]) == 256]
+    assert sites, "no all-256 site pair in the steady state"
+    o = OracleMps(bench.N_QUBITS, bench.CUTOFF, bench.CHI)
+    o.gammas = [g.copy() for g in gam]
+    o.lams = [v.copy() for v in lam]
+    cnot = oracle_gate_matrix(Instruction(GateKind.CNOT, (0, 1)))
+    err0 = st.trunc_error_sq
+    for q in sites:
+        st.apply_two_qubit_adjacent(cnot, q)
+        o.apply_2q(cnot, q)
+    gam2, lam2 = st.site_tensors, st.bond_vectors
+    for q in sites:
+        assert len(lam2[q]) == len(o.lams[q]) == 256
+        assert_scaled_close(lam2[q], o.lams[q], RTOL, f"lambda bond {q}")
+        assert_scaled_close(_theta(gam2, lam2, q).ravel(), _theta(o.gammas, o.lams, q).ravel(), RTOL,
+                            f"theta sites {q},{q + 1}")
+    d_err = st.trunc_error_sq - err0
+    assert abs(d_err - o.trunc_error_sq) <= 1e-10 * max(1.0, o.trunc_error_sq)
