@@ -848,7 +848,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
         const int prow = cmax - p * kQrNb;
         // shared-memory panels run one CTA per SM (up to 229 KB): worth it while the
         // batch fits one wave, or when the panel is small enough for two per SM
-        if (prow <= kQrPanelSmemRows && (nitems <= kNumSMs || prow <= 150))
+        if (prow <= kQrPanelSmemRows && (nitems <= kNumSMs || prow <= 150 * 32 / kQrNb))
           qr_panel_kernel<true><<<nitems, 512, sizeof(double2) * kQrNb * prow, st>>>(qa);
         else
           qr_panel_kernel<false><<<nitems, 512, 0, st>>>(qa);

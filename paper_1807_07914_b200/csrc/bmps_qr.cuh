@@ -107,7 +107,7 @@ BMPS_DEV double block_sum(double v, double* red) {
 // round trips: ~4x faster for these latency-bound launches); the arithmetic and
 // its order are identical to the global-memory version. Used when
 // (r - j0) x kQrNb x 16 B fits (kQrPanelSmemRows).
-constexpr int kQrPanelSmemRows = 384;   // 384 x 32 x 16 B + 33 KB static <= 227 KB
+constexpr int kQrPanelSmemRows = 384 * 32 / kQrNb;   // 384 x 32 x 16 B + 33 KB static <= 227 KB
 #ifndef BMPS_QR_PANEL_U
 #define BMPS_QR_PANEL_U 4
 #endif
