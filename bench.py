@@ -313,7 +313,42 @@ def main() -> None:
     f1.record(stream)
     barrier()
     e2e_ms = max(f0.elapsed_time(f1), 1e3 * (time.perf_counter() - t_w0))
-    e2e_value = sum(n_updates(p) for p in e2e_steps) / (e2e_ms / 1e3)
+    # whole job like `value`: updates of all ranks over the slowest rank's time
+    e2e_t = torch.tensor([e2e_ms, float(sum(n_updates(p) for p in e2e_steps))], dtype=torch.float64,
+                         device="cuda")
+    if world > 1:
+        e2e_max = e2e_t[:1].clone()
+        dist.all_reduce(e2e_max, op=dist.ReduceOp.MAX)
+        dist.all_reduce(e2e_t)
+        e2e_t[0] = e2e_max[0]
+    e2e_value = float(e2e_t[1].item()) / (float(e2e_t[0].item()) / 1e3)
+
+    # BASELINE config 4's circuits/s, sharded by circuit: a 256 x N-circuit
+    # job, circuits dealt round-robin to the N ranks (weak scaling), the public batched
+    # path incl. host planning: simulate_batch + <Z0 Z31> + 16 amplitudes per circuit and
+    # one D2H of the results; wall clock between barriers (= the slowest rank)
+    cfg4 = None
+    if not args.no_circuit:
+        from paper_1807_07914_b200 import workloads as W
+        from paper_1807_07914_b200 import simulate_batch
+        per_rank = 256
+        n4 = per_rank * world
+        mine = list(range(rank, n4, world))
+        w4 = W.config4(circuits=n4, indices=mine)
+        barrier()
+        t4 = time.perf_counter()
+        b4 = simulate_batch(w4.programs, w4.n, TruncationPolicy(w4.cutoff, w4.max_bond))
+        zz = b4.expectations(np.arange(len(mine), dtype=np.int32), w4.paulis * len(mine))
+        am = b4.amplitudes(np.repeat(np.arange(len(mine), dtype=np.int32), 16),
+                           [x for bs in w4.bitstrings for x in bs])
+        barrier()
+        dt4 = time.perf_counter() - t4
+        cfg4 = {"circuits": n4, "s": dt4, "circuits_per_s": n4 / dt4, "scaling": "weak",
+                "circuits_per_gpu": per_rank,
+                "path": "simulate_batch (host planning included) + expectations + amplitudes, "
+                        "wall clock between barriers",
+                "outputs": int(zz.size + am.size) * world}
+        del b4
 
     line = None
     if rank == 0:
@@ -398,26 +433,9 @@ def main() -> None:
             torch.cuda.synchronize()
             line["cfg3_full_circuit"] = {"s": g0.elapsed_time(g1) / 1e3,
                                          "circuits_per_s": 1e3 / g0.elapsed_time(g1)}
-            # BASELINE config 4's circuits/s (a 256-circuit slice of the 1024; the
-            # public batched path incl. host planning: simulate_batch + <Z0 Z31> +
-            # 16 amplitudes per circuit, one D2H of the results)
             del b3
-            n4 = 256
-            w4 = W.config4(circuits=n4)
-            from paper_1807_07914_b200 import simulate_batch
-            torch.cuda.synchronize()
-            t4 = time.perf_counter()
-            b4 = simulate_batch(w4.programs, w4.n, TruncationPolicy(w4.cutoff, w4.max_bond))
-            zz = b4.expectations(np.arange(n4, dtype=np.int32), w4.paulis * n4)
-            am = b4.amplitudes(np.repeat(np.arange(n4, dtype=np.int32), 16),
-                               [x for bs in w4.bitstrings for x in bs])
-            torch.cuda.synchronize()
-            dt4 = time.perf_counter() - t4
-            line["cfg4_circuits"] = {"circuits": n4, "s": dt4, "circuits_per_s": n4 / dt4,
-                                     "path": "simulate_batch (host planning included) + "
-                                             "expectations + amplitudes, wall clock",
-                                     "outputs": int(zz.size + am.size)}
-            del b4
+        if cfg4 is not None:
+            line["cfg4_circuits"] = cfg4
         if not args.no_cpu_baseline and world == 1:
             gam = batch.site_tensors(0)
             lam = batch.bond_vectors(0)

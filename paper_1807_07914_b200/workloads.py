@@ -126,10 +126,16 @@ def config3(seed: int = 1003) -> Workload:
     return Workload("cfg3", n, [prog], 1e-10, 256, [], paulis, meta={"seed": seed, "depth": 40})
 
 
-def config4(seed: int = 1004, circuits: int = 1024, cutoff: float = 1e-4) -> Workload:
-    """cfg4: independent 32-qubit depth-24 circuits, chi_max 64, cutoff 1e-4 (reference default)."""
+def config4(seed: int = 1004, circuits: int = 1024, cutoff: float = 1e-4, indices=None) -> Workload:
+    """cfg4: independent 32-qubit depth-24 circuits, chi_max 64, cutoff 1e-4 (reference default).
+
+    ``indices`` builds only those circuits of the ``circuits``-circuit set (a rank's shard);
+    circuit i depends on (seed, i) only.
+    """
     n = 32
     children = np.random.SeedSequence(seed).spawn(circuits)
+    if indices is not None:
+        children = [children[i] for i in indices]
     progs, bits = [], []
     for child in children:
         rc, rb = [np.random.default_rng(s) for s in child.spawn(2)]
