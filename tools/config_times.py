@@ -3,7 +3,7 @@ import json, sys, time
 import numpy as np
 import torch
 sys.path.insert(0, '.')
-from paper_1807_07914_b200 import MpsBatch, TruncationPolicy, compile_batch
+from paper_1807_07914_b200 import MpsBatch, TruncationPolicy, compile_batch, simulate_batch
 from paper_1807_07914_b200 import workloads as W
 from paper_1807_07914_b200.vqe import batch_energies
 
@@ -18,8 +18,7 @@ for name in [w for w in which for _ in range(2)]:   # second run of each config 
     pol = TruncationPolicy(w.cutoff, w.max_bond)
     S = len(w.programs)
     def evolve():
-        b = MpsBatch(S, w.n, pol)
-        b.execute(compile_batch(w.programs, w.n))
+        b = simulate_batch(w.programs, w.n, pol)   # public batched path (chunked planning)
         b.check_status()
         return b
     b, t_ev = timed(evolve)
