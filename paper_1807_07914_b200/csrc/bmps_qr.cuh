@@ -286,8 +286,14 @@ __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
 // of kQrRB stream through two cp.async stages (zero-filled beyond r / the chunk),
 // and the first block of the second pass is in flight during the T product.
 constexpr int kQrRB = 16;
-constexpr int kQrLdA = kQrChunk + 1;
-constexpr int kQrLdV = kQrNb + 1;
+// row strides in 16-byte elements: = 2 mod 8 makes the DMMA fragment loads of the k
+// loops (lanes: k = 4 consecutive rows x 2 consecutive columns) conflict-free
+// (+1 padding gave 2-way conflicts); pass 2's V fragments stay 2-way
+#ifndef BMPS_QR_PAD
+#define BMPS_QR_PAD 2
+#endif
+constexpr int kQrLdA = kQrChunk + BMPS_QR_PAD;
+constexpr int kQrLdV = kQrNb + BMPS_QR_PAD;
 constexpr int kQrStage = kQrRB * (kQrLdV + kQrLdA);
 constexpr size_t kWyApplySmem =
     (size_t)(2 * kQrStage + kQrNb * kQrLdA + kQrNb * kQrNb) * sizeof(double2);
