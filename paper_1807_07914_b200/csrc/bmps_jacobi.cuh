@@ -25,6 +25,9 @@
 
 namespace bmps {
 
+#ifndef BMPS_WARP_CLAIM
+#define BMPS_WARP_CLAIM 1   // warp-cooperative visit claims in the dynamic kernel
+#endif
 #ifndef BMPS_REGQ
 #define BMPS_REGQ 0   // register-resident Q in the cross rounds of the inner sweep (measured neutral, spills)
 #endif
@@ -1035,11 +1038,61 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dy
   volatile int* active = args.active;
   while (*active > 0) {
     BMPS_TICK(dc0);
+#if BMPS_WARP_CLAIM
+    // warp 0 probes 32 items per round trip (lane l: item cursor + base + l), ballots
+    // the ones with unclaimed visits and tries them in probe order; a claim used to
+    // scan ~10 exhausted items one dependent load at a time (~7k cycles per visit)
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      int got = -1, gv = 0;
+      unsigned grnd = 0;
+      for (int base = 0; base < nitems && got < 0; base += 32) {
+        const int probe = base + lane;
+        const int i = (cursor + probe) % nitems;
+        WS_ACC(0, 14, 0, min(32, nitems - base));   // probes (timer builds)
+        bool cand = false;
+        unsigned nbv = 0;
+        if (probe < nitems && !((volatile ItemMeta*)args.meta)[i].conv) {
+          int nb = (args.meta[i].c + w - 1) / w;
+          nb += nb & 1;
+          nbv = (unsigned)(nb / 2);
+          const unsigned long long peek = *((volatile unsigned long long*)&args.sched[i].ticket);
+          cand = (unsigned)(peek & 0xffffffffull) < nbv;
+        }
+        unsigned mask = __ballot_sync(0xffffffffu, cand);
+        while (mask) {
+          const int l = __ffs(mask) - 1;
+          int ok = 0;
+          unsigned long long old = 0;
+          if (lane == l) {
+            old = atomicAdd(&args.sched[i].ticket, 1ull);
+            ok = (unsigned)(old & 0xffffffffull) < nbv;
+          }
+          if (__shfl_sync(0xffffffffu, ok, l)) {
+            got = __shfl_sync(0xffffffffu, i, l);
+            old = __shfl_sync(0xffffffffu, old, l);
+            gv = (int)(old & 0xffffffffull);
+            grnd = (unsigned)(old >> 32);
+            break;
+          }
+          mask &= mask - 1;
+        }
+      }
+      if (got >= 0) cursor = got;
+      if (lane == 0) {
+        s_item = got;
+        s_v = gv;
+        s_round = grnd;
+        __threadfence();
+      }
+    }
+#else
     if (threadIdx.x == 0) {
       s_item = -1;
       for (int probe = 0; probe < nitems; ++probe) {
         const int i = (cursor + probe) % nitems;
         JacSched* sc = args.sched + i;
+        WS_ACC(0, 14, 0, 1);   // probes (timer builds)
         if (args.meta[i].conv) continue;
         const int c = args.meta[i].c;
         int nb = (c + w - 1) / w;
@@ -1058,6 +1111,7 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dy
       }
       __threadfence();
     }
+#endif
     __syncthreads();
     const int i = s_item;
     BMPS_TICK(dc1);
