@@ -22,7 +22,12 @@ namespace bmps {
 
 constexpr int kTile = 64;
 constexpr int kKC = 16;
-constexpr int kLds = kTile + 1;   // padded row of the k-major staging tiles
+// padded row of the k-major staging tiles, in 16-byte elements (2 would make the DMMA
+// fragment loads conflict-free but the k-major operand stores 2-way: measured no gain)
+#ifndef BMPS_GEMM_PAD
+#define BMPS_GEMM_PAD 1
+#endif
+constexpr int kLds = kTile + BMPS_GEMM_PAD;
 
 template <class Op>
 BMPS_DEV void gemm_load_chunk(const Op& op, double2 (*sA)[kLds], double2 (*sB)[kLds], int M,
