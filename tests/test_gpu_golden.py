@@ -110,3 +110,17 @@ def test_cfg5():
     for k, v in enumerate(lam):
         head = g["lam_head"][k][: min(8, len(v))]
         assert_scaled_close(v[: len(head)], head, RTOL, f"cfg5 lambda head bond {k}")
+
+
+@pytest.mark.parametrize("param,value", [("jac_cluster", 4.0), ("jac_cluster", 2.0), ("jac_ws", 1.0)])
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg5"])
+def test_golden_under_jacobi_variants(cfg, param, value):
+    """The config-scale goldens (cfg3: chi 256, cfg5: chi 1024) through the row-split
+    cluster kernel forced on every layer and through the warp-specialised kernel."""
+    from paper_1807_07914_b200 import _native
+    lib = _native.load()
+    assert lib.bmps_set_param(param.encode(), value) == 0
+    try:
+        (test_cfg3 if cfg == "cfg3" else test_cfg5)()
+    finally:
+        lib.bmps_set_param(param.encode(), float(_native.DEFAULT_PARAMS[param]))
