@@ -110,33 +110,105 @@ __global__ void __launch_bounds__(256) apply1q_kernel(StateView sv, const int* i
 
 // ---------------------------------------------------------------------------
 // K6: <bits|psi> = [1] T_0[:, b_0, :] ... T_{n-1}[:, b_{n-1}, :] (mps.py:172-179),
-// T_k = Gamma_k lam_{k+1}. One CTA per bitstring, vector in shared memory.
+// T_k = Gamma_k lam_{k+1}. A CTA takes a group of up to kAmpGroup consecutive
+// bitstrings; when they belong to one state (the usual call: a state's bitstrings
+// listed together) every Gamma element is loaded once for the whole group (both
+// physical slices, each bitstring picks its own), which divides the L2 traffic of
+// this L2-bound kernel by the group size. Each bitstring's row sum runs over l in
+// order, as in the one-bitstring-per-CTA form, so results do not depend on the
+// grouping. Mixed-state groups are walked one bitstring at a time.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) amplitude_kernel(StateView sv, const int* state_idx,
-                                                        const unsigned char* bits, double2* out) {
-  extern __shared__ __align__(16) double2 vbuf[];  // 2 * cap
-  const int it = blockIdx.x, s = state_idx[it], n = sv.n, cap = sv.cap;
+#ifndef BMPS_AMP_GROUP
+#define BMPS_AMP_GROUP 4
+#endif
+constexpr int kAmpGroup = BMPS_AMP_GROUP;
+
+BMPS_DEV void amplitude_group(const StateView& sv, int s, const unsigned char* const* bb, int nb,
+                              double2* vbuf, double2* out_first) {
+  const int n = sv.n, cap = sv.cap, tid = threadIdx.x;
   const int* d = sv.dimv(s);
-  const unsigned char* bb = bits + (size_t)it * n;
-  double2* cur = vbuf;
-  double2* nxt = vbuf + cap;
-  if (threadIdx.x == 0) cur[0] = make_double2(1.0, 0.0);
+  double2* cur = vbuf;                      // [nb][cap]
+  double2* nxt = vbuf + (size_t)nb * cap;   // [nb][cap]
+  if (tid < nb) cur[(size_t)tid * cap] = make_double2(1.0, 0.0);
   __syncthreads();
   for (int k = 0; k < n; ++k) {
-    const int dl = d[k], dr = d[k + 1], b = bb[k];
-    const double2* t = sv.site(s, k) + (size_t)b * cap;
+    const int dl = d[k], dr = d[k + 1];
+    const double2* t = sv.site(s, k);
     const double* lam = sv.bond(s, k + 1);
-    for (int r = threadIdx.x; r < dr; r += blockDim.x) {
-      double2 acc = make_double2(0.0, 0.0);
-      for (int l = 0; l < dl; ++l) acc = cfma(cur[l], t[(size_t)(2 * l) * cap + r], acc);
-      nxt[r] = cscale(acc, lam[r]);
+    int drp = 1;
+    while (drp < dr) drp <<= 1;
+    // ng thread groups share the bitstrings (group q takes j = q, q + ng, ...)
+    const int ng = drp >= (int)blockDim.x ? 1 : min(nb, (int)blockDim.x / drp);
+    const int q = tid / drp;
+    unsigned mask = 0;   // bit j: bitstring q + j*ng reads slice 1
+#pragma unroll
+    for (int j = 0; j < kAmpGroup; ++j) {
+      const int jj = q + j * ng;
+      if (jj < nb && bb[jj][k]) mask |= 1u << j;
+    }
+    for (int r = (ng > 1 ? tid % drp : tid); r < dr && q < ng; r += (ng > 1 ? dr + 1 : (int)blockDim.x)) {
+      double2 acc[kAmpGroup];
+#pragma unroll
+      for (int j = 0; j < kAmpGroup; ++j) acc[j] = make_double2(0.0, 0.0);
+      // four rows per step, their loads issued together (memory-level parallelism)
+      int l = 0;
+      for (; l + 4 <= dl; l += 4) {
+        double2 t0[4], t1[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          t0[u] = t[(size_t)(2 * (l + u)) * cap + r];
+          t1[u] = t[(size_t)(2 * (l + u) + 1) * cap + r];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int j = 0; j < kAmpGroup; ++j) {
+            const int jj = q + j * ng;
+            if (jj < nb)
+              acc[j] = cfma(cur[(size_t)jj * cap + l + u], (mask >> j) & 1u ? t1[u] : t0[u], acc[j]);
+          }
+      }
+      for (; l < dl; ++l) {
+        const double2 t0 = t[(size_t)(2 * l) * cap + r];
+        const double2 t1 = t[(size_t)(2 * l + 1) * cap + r];
+#pragma unroll
+        for (int j = 0; j < kAmpGroup; ++j) {
+          const int jj = q + j * ng;
+          if (jj < nb) acc[j] = cfma(cur[(size_t)jj * cap + l], (mask >> j) & 1u ? t1 : t0, acc[j]);
+        }
+      }
+      const double lr = lam[r];
+#pragma unroll
+      for (int j = 0; j < kAmpGroup; ++j) {
+        const int jj = q + j * ng;
+        if (jj < nb) nxt[(size_t)jj * cap + r] = cscale(acc[j], lr);
+      }
     }
     __syncthreads();
     double2* tmp = cur;
     cur = nxt;
     nxt = tmp;
   }
-  if (threadIdx.x == 0) out[it] = cur[0];
+  if (tid < nb) out_first[tid] = cur[(size_t)tid * cap];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) amplitude_kernel(StateView sv, const int* state_idx,
+                                                        const unsigned char* bits, int count, int group,
+                                                        double2* out) {
+  extern __shared__ __align__(16) double2 vbuf[];  // 2 * group * cap
+  const int i0 = blockIdx.x * group, nb = min(group, count - i0);
+  const int s = state_idx[i0];
+  bool same = true;
+  for (int j = 1; j < nb; ++j) same &= state_idx[i0 + j] == s;
+  const unsigned char* bb[kAmpGroup];
+#pragma unroll
+  for (int j = 0; j < kAmpGroup; ++j) bb[j] = bits + (size_t)(i0 + min(j, nb - 1)) * sv.n;
+  if (same) {
+    amplitude_group(sv, s, bb, nb, vbuf, out + i0);
+  } else {
+    for (int j = 0; j < nb; ++j) amplitude_group(sv, state_idx[i0 + j], bb + j, 1, vbuf, out + i0 + j);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1146,8 +1218,16 @@ int32_t bmps_amplitudes(const double* gamma, const double* lam, const int32_t* d
   if (count == 0) return BMPS_OK;
   if (count < 0 || S < 1 || n < 1 || cap < 1) return BMPS_E_ARG;
   StateView sv = make_view((double*)gamma, (double*)lam, (int32_t*)dims, n, cap);
-  amplitude_kernel<<<count, 256, 2 * cap * sizeof(double2), (cudaStream_t)stream>>>(
-      sv, state_idx, bits, (double2*)out);
+  // bitstrings per CTA: up to kAmpGroup, vectors (2 x group x cap) within 32 KB
+  const int group = max(1, min(kAmpGroup, 1024 / cap));
+  const size_t smem = 2 * (size_t)group * cap * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(amplitude_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10);
+    attr = true;
+  }
+  amplitude_kernel<<<(count + group - 1) / group, 256, smem, (cudaStream_t)stream>>>(
+      sv, state_idx, bits, count, group, (double2*)out);
   ++g_launches;
   return launch_status();
 }
