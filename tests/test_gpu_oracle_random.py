@@ -238,3 +238,24 @@ def test_chi256_updates_on_cfg3_steady_state_match_oracle():
                             f"theta sites {q},{q + 1}")
     d_err = st.trunc_error_sq - err0
     assert abs(d_err - o.trunc_error_sq) <= 1e-10 * max(1.0, o.trunc_error_sq)
+
+
+@pytest.mark.parametrize("count", [1, 3, 7, 29])
+def test_batched_amplitudes_mixed_states(count):
+    """bmps_amplitudes groups consecutive same-state bitstrings per CTA; interleaved
+    states (mixed groups) and ragged counts must give the oracle's amplitudes and be
+    bit-identical to one call per bitstring."""
+    n, S = 8, 3
+    rng = np.random.default_rng(40 + count)
+    progs = [brick_circuit(n, 6, np.random.default_rng(100 + s)) for s in range(S)]
+    b = MpsBatch(S, n, TruncationPolicy(0.0, 8))
+    b.run(progs)
+    b.check_status()
+    refs = [oracle_run(p, n, 0.0, 8, True) for p in progs]
+    states = rng.integers(0, S, count).astype(np.int32)
+    states[: min(count, 2)] = 0   # at least one same-state run when count > 1
+    bits = random_bitstrings(n, count, rng)
+    got = b.amplitudes(states, bits)
+    assert_scaled_close(got, [refs[s].amplitude(x) for s, x in zip(states, bits)], RTOL, "amplitudes")
+    one = np.array([b.amplitudes(states[i:i + 1], bits[i:i + 1])[0] for i in range(count)])
+    assert np.array_equal(got, one)
