@@ -28,6 +28,9 @@ namespace bmps {
 #ifndef BMPS_WARP_CLAIM
 #define BMPS_WARP_CLAIM 1   // warp-cooperative visit claims in the dynamic kernel
 #endif
+#ifndef BMPS_CLAIM_SLEEP_NS
+#define BMPS_CLAIM_SLEEP_NS 2000   // dynamic Jacobi: back-off of a CTA that found no open visit
+#endif
 #ifndef BMPS_REGQ
 #define BMPS_REGQ 0   // register-resident Q in the cross rounds of the inner sweep (measured neutral, spills)
 #endif
@@ -1117,7 +1120,7 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dy
     BMPS_TICK(dc1);
     if (i >= 0) { WS_ACC(0, 10, dc0, dc1); WS_ACC(0, 11, 0, 1); } else { WS_ACC(0, 12, dc0, dc1); }
     if (i < 0) {
-      if (threadIdx.x == 0) __nanosleep(2000);
+      if (threadIdx.x == 0) __nanosleep(BMPS_CLAIM_SLEEP_NS);
       __syncthreads();
       cursor = (cursor + 1) % nitems;
       continue;
