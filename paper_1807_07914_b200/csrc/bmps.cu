@@ -118,10 +118,17 @@ __global__ void __launch_bounds__(256) apply1q_kernel(StateView sv, const int* i
 // order, as in the one-bitstring-per-CTA form, so results do not depend on the
 // grouping. Mixed-state groups are walked one bitstring at a time.
 // ---------------------------------------------------------------------------
+#ifndef BMPS_AMP_VEC
+#define BMPS_AMP_VEC 2048   // group x cap bound (vector buffers 2 x 16 B x BMPS_AMP_VEC)
+#endif
 #ifndef BMPS_AMP_GROUP
-#define BMPS_AMP_GROUP 4
+#define BMPS_AMP_GROUP 8
 #endif
 constexpr int kAmpGroup = BMPS_AMP_GROUP;
+#ifndef BMPS_AMP_UNROLL
+#define BMPS_AMP_UNROLL 4
+#endif
+constexpr int kAmpUnroll = BMPS_AMP_UNROLL;
 
 BMPS_DEV void amplitude_group(const StateView& sv, int s, const unsigned char* const* bb, int nb,
                               double2* vbuf, double2* out_first) {
@@ -150,17 +157,17 @@ BMPS_DEV void amplitude_group(const StateView& sv, int s, const unsigned char* c
       double2 acc[kAmpGroup];
 #pragma unroll
       for (int j = 0; j < kAmpGroup; ++j) acc[j] = make_double2(0.0, 0.0);
-      // four rows per step, their loads issued together (memory-level parallelism)
+      // BMPS_AMP_UNROLL rows per step, their loads issued together (memory-level parallelism)
       int l = 0;
-      for (; l + 4 <= dl; l += 4) {
-        double2 t0[4], t1[4];
+      for (; l + kAmpUnroll <= dl; l += kAmpUnroll) {
+        double2 t0[kAmpUnroll], t1[kAmpUnroll];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kAmpUnroll; ++u) {
           t0[u] = t[(size_t)(2 * (l + u)) * cap + r];
           t1[u] = t[(size_t)(2 * (l + u) + 1) * cap + r];
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < kAmpUnroll; ++u)
 #pragma unroll
           for (int j = 0; j < kAmpGroup; ++j) {
             const int jj = q + j * ng;
@@ -1218,12 +1225,12 @@ int32_t bmps_amplitudes(const double* gamma, const double* lam, const int32_t* d
   if (count == 0) return BMPS_OK;
   if (count < 0 || S < 1 || n < 1 || cap < 1) return BMPS_E_ARG;
   StateView sv = make_view((double*)gamma, (double*)lam, (int32_t*)dims, n, cap);
-  // bitstrings per CTA: up to kAmpGroup, vectors (2 x group x cap) within 32 KB
-  const int group = max(1, min(kAmpGroup, 1024 / cap));
+  // bitstrings per CTA: up to kAmpGroup, vectors (2 x group x cap) within 32 x BMPS_AMP_VEC bytes
+  const int group = max(1, min(kAmpGroup, BMPS_AMP_VEC / cap));
   const size_t smem = 2 * (size_t)group * cap * sizeof(double2);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(amplitude_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10);
+    cudaFuncSetAttribute(amplitude_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * BMPS_AMP_VEC);
     attr = true;
   }
   amplitude_kernel<<<(count + group - 1) / group, 256, smem, (cudaStream_t)stream>>>(
