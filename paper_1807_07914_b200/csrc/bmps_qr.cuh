@@ -285,7 +285,10 @@ __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
 // above) stored below the diagonal of Vm (ld r). Both products on DMMA; row blocks
 // of kQrRB stream through two cp.async stages (zero-filled beyond r / the chunk),
 // and the first block of the second pass is in flight during the T product.
-constexpr int kQrRB = 16;
+#ifndef BMPS_QR_RB
+#define BMPS_QR_RB 8   // rows per staged block of the WY apply
+#endif
+constexpr int kQrRB = BMPS_QR_RB;
 // row strides in 16-byte elements: = 2 mod 8 makes the DMMA fragment loads of the k
 // loops (lanes: k = 4 consecutive rows x 2 consecutive columns) conflict-free
 // (+1 padding gave 2-way conflicts); pass 2's V fragments stay 2-way
