@@ -297,25 +297,32 @@ constexpr int kQrRB = BMPS_QR_RB;
 #endif
 constexpr int kQrLdA = kQrChunk + BMPS_QR_PAD;
 constexpr int kQrLdV = kQrNb + BMPS_QR_PAD;
-constexpr int kQrStage = kQrRB * (kQrLdV + kQrLdA);
-constexpr size_t kWyApplySmem =
-    (size_t)(2 * kQrStage + kQrNb * kQrLdA + kQrNb * kQrNb) * sizeof(double2);
-constexpr size_t kQrUpdateSmem = kWyApplySmem;
+#ifndef BMPS_QR_Q1_RB
+#define BMPS_QR_Q1_RB 16   // row block of the Q1 epilogue's WY apply (measured: 16 beats 8 there)
+#endif
+constexpr int kQ1RB = BMPS_QR_Q1_RB;
+BMPS_HOSTDEV constexpr int qr_stage(int rb) { return rb * (kQrLdV + kQrLdA); }
+BMPS_HOSTDEV constexpr size_t wy_apply_smem(int rb) {
+  return (size_t)(2 * qr_stage(rb) + kQrNb * kQrLdA + kQrNb * kQrNb) * sizeof(double2);
+}
+constexpr int kQrStage = qr_stage(kQrRB);
+constexpr size_t kQrUpdateSmem = wy_apply_smem(kQrRB);
 
+template <int RB>
 BMPS_DEV void wy_issue(double2* smem, int b, const double2* Vm, const double2* A, int r, int j0,
                        int nbp, int c0, int nc) {
-  double2* sV = smem + (b & 1) * kQrStage;
-  double2* sA = sV + kQrRB * kQrLdV;
-  const int rb = j0 + b * kQrRB;
-  for (int i = threadIdx.x; i < kQrRB * kQrNb; i += blockDim.x) {
-    const int row = i % kQrRB, p = i / kQrRB;
+  double2* sV = smem + (b & 1) * qr_stage(RB);
+  double2* sA = sV + RB * kQrLdV;
+  const int rb = j0 + b * RB;
+  for (int i = threadIdx.x; i < RB * kQrNb; i += blockDim.x) {
+    const int row = i % RB, p = i / RB;
     const int gr = rb + row, k = j0 + p;
     double2* dst = sV + row * kQrLdV + p;
     if (p < nbp && gr > k && gr < r) cp_async16(dst, Vm + (size_t)k * r + gr, true);
     else *dst = make_double2(p < nbp && gr == k ? 1.0 : 0.0, 0.0);
   }
-  for (int i = threadIdx.x; i < kQrRB * kQrChunk; i += blockDim.x) {
-    const int row = i % kQrRB, q = i / kQrRB;
+  for (int i = threadIdx.x; i < RB * kQrChunk; i += blockDim.x) {
+    const int row = i % RB, q = i / RB;
     const int gr = rb + row;
     const bool ok = gr < r && q < nc;
     cp_async16(sA + row * kQrLdA + q, ok ? A + (size_t)(c0 + q) * r + gr : A, ok);
@@ -323,14 +330,14 @@ BMPS_DEV void wy_issue(double2* smem, int b, const double2* Vm, const double2* A
   cp_async_commit();
 }
 
-template <bool TH>
+template <bool TH, int RB>
 BMPS_DEV void wy_apply(double2* smem, const double2* Vm, double2* A, int r, int j0, int nbp,
                        int c0, int nc) {
-  double2* sW = smem + 2 * kQrStage;  // [kQrNb][kQrLdA]
+  double2* sW = smem + 2 * qr_stage(RB);  // [kQrNb][kQrLdA]
   const double2* sT = sW + kQrNb * kQrLdA;  // [kQrNb][kQrNb], filled by the caller
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kr = lane & 3, rc = lane >> 2;
-  const int nblk = (r - j0 + kQrRB - 1) / kQrRB;
+  const int nblk = (r - j0 + RB - 1) / RB;
   // pass 1: W = V^H A; warp -> W row tile warp / kWPR, kNU column tiles
   double acc[kNU][kZ3];
 #pragma unroll
@@ -338,19 +345,19 @@ BMPS_DEV void wy_apply(double2* smem, const double2* Vm, double2* A, int r, int 
 #pragma unroll
     for (int q = 0; q < kZ3; ++q) acc[u][q] = 0.0;
   const int tr = warp / kWPR, tc0 = (warp % kWPR) * kNU;
-  wy_issue(smem, 0, Vm, A, r, j0, nbp, c0, nc);
+  wy_issue<RB>(smem, 0, Vm, A, r, j0, nbp, c0, nc);
   for (int b = 0; b < nblk; ++b) {
     if (b + 1 < nblk) {
-      wy_issue(smem, b + 1, Vm, A, r, j0, nbp, c0, nc);
+      wy_issue<RB>(smem, b + 1, Vm, A, r, j0, nbp, c0, nc);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double2* sV = smem + (b & 1) * kQrStage;
-    const double2* sA = sV + kQrRB * kQrLdV;
+    const double2* sV = smem + (b & 1) * qr_stage(RB);
+    const double2* sA = sV + RB * kQrLdV;
 #pragma unroll
-    for (int k4 = 0; k4 < kQrRB / 4; ++k4) {
+    for (int k4 = 0; k4 < RB / 4; ++k4) {
       const int k = k4 * 4 + kr;
       const double2 av = cconj(sV[k * kQrLdV + tr * 8 + rc]);
 #pragma unroll
@@ -358,7 +365,7 @@ BMPS_DEV void wy_apply(double2* smem, const double2* Vm, double2* A, int r, int 
     }
     __syncthreads();
   }
-  wy_issue(smem, 0, Vm, A, r, j0, nbp, c0, nc);  // pass 2's first block, in flight below
+  wy_issue<RB>(smem, 0, Vm, A, r, j0, nbp, c0, nc);  // pass 2's first block, in flight below
 #pragma unroll
   for (int u = 0; u < kNU; ++u)
 #pragma unroll
@@ -384,19 +391,19 @@ BMPS_DEV void wy_apply(double2* smem, const double2* Vm, double2* A, int r, int 
     const int idx = tid + u * 256;
     sW[(idx / kQrChunk) * kQrLdA + idx % kQrChunk] = wt[u];
   }
-  // pass 2: A -= V W; a kQrRB x kQrChunk block = (kQrRB / 8) x kCT tiles, kOU per warp
-  constexpr int kOU = (kQrRB / 8) * kCT / 8;   // output column tiles per warp
+  // pass 2: A -= V W; a RB x kQrChunk block = (RB / 8) x kCT tiles, kOU per warp
+  constexpr int kOU = (RB / 8) * kCT / 8;   // output column tiles per warp
   const int orow = warp / (kCT / kOU), oc0 = (warp % (kCT / kOU)) * kOU;
   for (int b = 0; b < nblk; ++b) {
     if (b + 1 < nblk) {
-      wy_issue(smem, b + 1, Vm, A, r, j0, nbp, c0, nc);
+      wy_issue<RB>(smem, b + 1, Vm, A, r, j0, nbp, c0, nc);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double2* sV = smem + (b & 1) * kQrStage;
-    const double2* sA = sV + kQrRB * kQrLdV;
+    const double2* sV = smem + (b & 1) * qr_stage(RB);
+    const double2* sA = sV + RB * kQrLdV;
     double oacc[kOU][kZ3];
 #pragma unroll
     for (int u = 0; u < kOU; ++u)
@@ -409,7 +416,7 @@ BMPS_DEV void wy_apply(double2* smem, const double2* Vm, double2* A, int r, int 
 #pragma unroll
       for (int u = 0; u < kOU; ++u) zmma3(oacc[u], av, sW[k * kQrLdA + (oc0 + u) * 8 + rc]);
     }
-    const int rb = j0 + b * kQrRB;
+    const int rb = j0 + b * RB;
 #pragma unroll
     for (int u = 0; u < kOU; ++u)
 #pragma unroll
@@ -442,7 +449,7 @@ __global__ void __launch_bounds__(256) qr_update_kernel(QrArgs a) {
   double2* sT = qsm + 2 * kQrStage + kQrNb * kQrLdA;
   const double2* T = qr_tslot(a, tauw);
   for (int i = threadIdx.x; i < kQrNb * kQrNb; i += blockDim.x) sT[i] = T[i];
-  wy_apply<true>(qsm, A, A, r, j0, nbp, c0, min(kQrChunk, c - c0));
+  wy_apply<true, kQrRB>(qsm, A, A, r, j0, nbp, c0, min(kQrChunk, c - c0));
 }
 
 // Y = R^H (c x c, ld c): Y[i][j] = conj(R[j][i]) for j <= i, else 0.
@@ -602,11 +609,11 @@ __global__ void __launch_bounds__(512) dq_sort_kernel(ItemMeta* meta, const doub
 // L[:, 0:keep] <- (I - V T V^H) L for the panel's Householder block (V from the
 // first QR, stored below the diagonal of X; T rebuilt from tau1). Called for the
 // panels in reverse order so that L <- H_1 ... H_c L = Q1 L.
-constexpr size_t kQ1Smem = kWyApplySmem;
+constexpr size_t kQ1Smem = wy_apply_smem(kQ1RB);
 
 __global__ void __launch_bounds__(256) dq_apply_q1_kernel(QrArgs a) {
   extern __shared__ __align__(16) double2 qsm[];
-  double2* sT = qsm + 2 * kQrStage + kQrNb * kQrLdA;  // [kQrNb][kQrNb]
+  double2* sT = qsm + 2 * qr_stage(kQ1RB) + kQrNb * kQrLdA;  // [kQrNb][kQrNb]
   const int item = blockIdx.y;
   const ItemMeta* m = a.meta + item;
   if (!m->dq || !m->msel || m->status) return;
@@ -622,7 +629,7 @@ __global__ void __launch_bounds__(256) dq_apply_q1_kernel(QrArgs a) {
   double2* Lm = a.Y + (size_t)item * a.mat_stride;
   for (int i = threadIdx.x; i < kQrNb * kQrNb; i += blockDim.x) sT[i] = T[i];  // T1 of this panel
   __syncthreads();
-  wy_apply<false>(qsm, V, Lm, r, j0, nbp, c0, min(kQrChunk, keep - c0));
+  wy_apply<false, kQ1RB>(qsm, V, Lm, r, j0, nbp, c0, min(kQrChunk, keep - c0));
 }
 
 }  // namespace bmps

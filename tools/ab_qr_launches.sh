@@ -1,5 +1,6 @@
 #!/bin/bash
 # per-kernel launch-list time of one 16-replica bench step for the in-tree lib and tools/variants/*.so
+shopt -s nullglob
 cp paper_1807_07914_b200/libbmps.so /tmp/cur.so
 one() {
   ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \

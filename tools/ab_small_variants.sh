@@ -1,4 +1,5 @@
 #!/bin/bash
+shopt -s nullglob
 cp paper_1807_07914_b200/libbmps.so /tmp/cur.so
 ./tools/sweep_small.sh tol_factor=4 | sed 's/^/current: /'
 for v in tools/variants/*.so; do
