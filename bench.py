@@ -41,7 +41,22 @@ N_QUBITS = 50
 CUTOFF = 1e-10
 BULK = (8, 41)          # pairs (q, q+1) with q in [8, 40]: dims[q..q+2] all 256 at steady state
 STEADY_LAYERS = 25
-FP64_PEAK_TFLOPS = 36.8  # measured: cuBLAS ZGEMM 4096^3 on this pool's B200 (tools/fp64_peaks.py)
+PEAKS_FILE = ROOT / "profiles" / "fp64_peak.json"   # tools/fp64_peaks.py on this pool's B200
+TRAFFIC_FILE = ROOT / "profiles" / "r02_traffic.json"  # tools/make_traffic.py, final-build launch list
+
+
+def fp64_peak() -> tuple[float, str]:
+    """The FP64 roofline denominator: the measured SUSTAINED complex128 GEMM rate
+    (cuBLAS ZGEMM back to back under the power cap, tools/fp64_peaks.py) -- the
+    bench's stage is timed inside a seconds-long step. MEASURED_PEAKS.json has no
+    FP64 entry and B200_PROFILING.md gives no FP64 fallback."""
+    if not PEAKS_FILE.exists():
+        return 36.8, "round-1 cuBLAS ZGEMM 4096^3 measurement (profiles/fp64_peak.json absent)"
+    d = json.loads(PEAKS_FILE.read_text())
+    return float(d["zgemm_tflops_sustained"]), (
+        f"{PEAKS_FILE.relative_to(ROOT)}: cuBLAS ZGEMM {d['zgemm_n']}^3 sustained "
+        f"{d['zgemm_tflops_sustained']:.2f} TFLOP/s (burst {d['zgemm_tflops_burst']:.2f}, DMMA probe "
+        f"{d.get('dmma_tflops', float('nan')):.2f}), clocks {d['clocks']}")
 
 
 def nominal_update_flops(dl: int, dm: int, dr: int, keep: int) -> float:
@@ -56,6 +71,14 @@ def svd_flops(dl: int, dr: int) -> float:
     m, n = 2 * dl, 2 * dr
     p, q = min(m, n), max(m, n)
     return 4.0 * (14.0 * q * p * p + 8.0 * p ** 3)
+
+
+def records_flops(rec) -> float:
+    """Sum of SURVEY §8(d)'s nominal F(dl, dm, dr) over executed update records."""
+    dl, dm, dr = (rec[k].astype(np.float64) for k in ("dl", "dm", "dr"))
+    m, n = 2 * dl, 2 * dr
+    p, q = np.minimum(m, n), np.maximum(m, n)
+    return float(np.sum(32.0 * dl * dm * dr + 128.0 * dl * dr + 4.0 * (14.0 * q * p * p + 8.0 * p ** 3)))
 
 
 def update_bytes(dl: int, dm: int, dr: int, keep: int) -> float:
@@ -142,61 +165,176 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def cpu_baseline_sample(states, seconds_target: float = 15.0):
-    """Time the reference algorithm (verbatim numpy/LAPACK calls) on chi=256 updates."""
-    from oracle.mps_oracle import OracleMps, oracle_gate_matrix
-    gam, lam = states
-    o = OracleMps(N_QUBITS, CUTOFF, CHI, verbatim=True)
-    o.gammas = [np.array(g) for g in gam]
-    o.lams = [np.array(v) for v in lam]
-    prog = [op for op in bulk_layer(0, 0) if len(op.qubits) == 2]
-    done, t0 = 0, time.perf_counter()
-    for op in prog:
+def _host_cores() -> tuple[int, int]:
+    return os.cpu_count() or 1, len(os.sched_getaffinity(0))
+
+
+_POOL_STATE = None
+
+
+def _pool_update(i: int) -> float:
+    """Pool task: one verbatim chi=256 update on this worker's forked copy of the
+    steady state, OpenBLAS single-threaded; returns its wall time."""
+    from threadpoolctl import threadpool_limits
+    from oracle.mps_oracle import oracle_gate_matrix
+    o, ops = _POOL_STATE
+    op = ops[i % len(ops)]
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
         o.apply_2q(oracle_gate_matrix(op), op.qubits[0])
-        done += 1
-        if time.perf_counter() - t0 > seconds_target:
-            break
-    dt = time.perf_counter() - t0
-    return done, dt
+        return time.perf_counter() - t0
+
+
+def _oracle_steady(gam=None, lam=None):
+    from oracle.mps_oracle import OracleMps
+    o = OracleMps(N_QUBITS, CUTOFF, CHI, verbatim=False)
+    if gam is None:
+        o.run(prefix_program(1003, STEADY_LAYERS))   # fast contraction order (setup only)
+    else:
+        o.gammas = [np.array(g) for g in gam]
+        o.lams = [np.array(v) for v in lam]
+    o.verbatim = True                                # timed: the reference's own einsum + zgesdd
+    return o
+
+
+def cpu_reference_rates(o, rounds: int = 2) -> dict:
+    """The reference CPU path (verbatim mps.py:94-136: its einsums + LAPACK zgesdd) on
+    chi=256 updates of the steady state, three ways on this host: one process with
+    OpenBLAS on all cores, one process single-threaded, and a fork Pool of one
+    single-threaded process per usable core (independent updates -- the replicas are
+    independent states). Returns updates/s of each and the best."""
+    import multiprocessing as mp
+    from threadpoolctl import threadpool_limits
+    from oracle.mps_oracle import oracle_gate_matrix
+    global _POOL_STATE
+    ops = [op for op in bulk_layer(0, 0) if len(op.qubits) == 2]
+    ncpu, naff = _host_cores()
+    out = {}
+    for label, threads in (("1_process_all_threads", None), ("1_process_1_thread", 1)):
+        with threadpool_limits(threads):
+            t0 = time.perf_counter()
+            for op in ops[:2]:
+                o.apply_2q(oracle_gate_matrix(op), op.qubits[0])
+            out[label] = 2 / (time.perf_counter() - t0)
+    _POOL_STATE = (o, ops)
+    with mp.get_context("fork").Pool(naff) as pool:
+        pool.map(_pool_update, range(naff))          # warm (page in numpy/BLAS per worker)
+        t0 = time.perf_counter()
+        for _ in range(rounds):
+            pool.map(_pool_update, range(naff), chunksize=1)
+        out[f"pool_{naff}_processes_1_thread"] = rounds * naff / (time.perf_counter() - t0)
+    _POOL_STATE = None
+    best = max(out, key=out.get)
+    return {"rates_updates_per_s": out, "best": best, "value": out[best], "cores": naff,
+            "os_cpu_count": ncpu, "sched_getaffinity": naff}
 
 
 def run_reference(args) -> None:
-    """--impl reference: the reference CPU algorithm on a bounded sample, rank 0 only."""
+    """--impl reference: the reference CPU algorithm on the box's host cores, rank 0
+    only. One step = one chi=256 update per usable core, run by a fork Pool of
+    single-threaded processes on independent copies of the steady state (the
+    reference's verbatim einsum + zgesdd via oracle/mps_oracle.py)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle.mps_oracle import OracleMps, oracle_gate_matrix
+    import multiprocessing as mp
+    global _POOL_STATE
     t_setup = time.perf_counter()
-    o = OracleMps(N_QUBITS, CUTOFF, CHI, verbatim=False)
-    o.run(prefix_program(1003, STEADY_LAYERS))   # untimed setup (fast contraction order)
+    o = _oracle_steady()
     setup_s = time.perf_counter() - t_setup
-    o.verbatim = True
-    per_step = args.ref_updates
+    ncpu, naff = _host_cores()
+    _POOL_STATE = (o, [op for op in bulk_layer(0, 0) if len(op.qubits) == 2])
     times = []
-    for k in range(args.warmup + args.steps):
-        ops = [op for op in bulk_layer(k, 0) if len(op.qubits) == 2][:per_step]
-        t0 = time.perf_counter()
-        for op in ops:
-            o.apply_2q(oracle_gate_matrix(op), op.qubits[0])
-        if k >= args.warmup:
-            times.append(time.perf_counter() - t0)
+    with mp.get_context("fork").Pool(naff) as pool:
+        for k in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            pool.map(_pool_update, range(k * naff, (k + 1) * naff), chunksize=1)
+            if k >= args.warmup:
+                times.append(time.perf_counter() - t0)
+    _POOL_STATE = None
     total = sum(times)
-    value = per_step * len(times) / total
-    cores = os.cpu_count()
+    value = naff * len(times) / total
     line = {
         "impl": "reference", "metric": "MPS 2-qubit gate updates/sec at chi=256 (contract+SVD)",
         "value": value, "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": "cfg3 steady-state bulk brick layer (chi=256)", "n": N_QUBITS,
-                   "chi_max": CHI, "cutoff": CUTOFF, "updates_per_step": per_step,
+                   "chi_max": CHI, "cutoff": CUTOFF, "updates_per_step": naff,
                    "steady_layers": STEADY_LAYERS, "setup_s": setup_s},
-        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": cores, "kind": "port",
-                         "sample": f"{per_step} chi=256 updates per step, verbatim reference einsum+zgesdd "
-                                   f"(oracle/mps_oracle.py verbatim=True), OpenBLAS threads default"},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": naff, "kind": "port",
+                         "sample": f"{naff} chi=256 updates per step, one per usable core: fork Pool of "
+                                   f"{naff} single-threaded processes (os.cpu_count {ncpu}, "
+                                   f"sched_getaffinity {naff}), verbatim reference einsum + zgesdd "
+                                   f"(oracle/mps_oracle.py verbatim=True)"},
         "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _timed(fn, stream):
+    import torch
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    out = fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return out, max(e0.elapsed_time(e1) / 1e3, 0.0), time.perf_counter() - t0
+
+
+def config_rooflines(peak: float, world: int, rank: int, stream) -> dict:
+    """Whole-config FP64 fractions: the nominal F(dl, dm, dr) of every
+    two-qubit update actually executed (device records, read back once) / wall / peak.
+    Two-site updates only (1q gates and queries are < 2% of each config)."""
+    from paper_1807_07914_b200 import MpsBatch, TruncationPolicy, compile_batch, simulate_batch
+    from paper_1807_07914_b200 import workloads as W
+    out = {}
+    import torch
+    import torch.distributed as dist
+    # cfg4: BASELINE config 4 as stated -- 1024 circuits sharded by circuit across the ranks
+    # (round-robin), host planning included, plus <Z0 Z31> and 16 amplitudes per circuit
+    n4 = 1024
+    mine = list(range(rank, n4, world))
+    w4 = W.config4(circuits=n4, indices=mine)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t4 = time.perf_counter()
+    b4 = simulate_batch(w4.programs, w4.n, TruncationPolicy(w4.cutoff, w4.max_bond), keep_records=True)
+    zz = b4.expectations(np.arange(len(mine), dtype=np.int32), w4.paulis * len(mine))
+    am = b4.amplitudes(np.repeat(np.arange(len(mine), dtype=np.int32), 16),
+                       [x for bs in w4.bitstrings for x in bs])
+    torch.cuda.synchronize()
+    dt4 = time.perf_counter() - t4
+    f4 = sum(records_flops(b4.update_records(s)) for s in range(len(mine)))
+    t = torch.tensor([dt4, f4], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tmax = t[:1].clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t)
+        t[0] = tmax[0]
+    dt4, f4 = float(t[0]), float(t[1])
+    out["cfg4"] = {"circuits": n4, "s": dt4, "circuits_per_s": n4 / dt4, "scaling": "strong",
+                   "nominal_tflop": f4 / 1e12, "achieved_tflops": f4 / dt4 / 1e12,
+                   "frac": f4 / dt4 / 1e12 / (peak * world),
+                   "path": "simulate_batch (host planning included) + expectations + amplitudes, "
+                           "wall clock between barriers, max over ranks",
+                   "outputs": int(zz.size + am.size)}
+    del b4
+    if world == 1:
+        for name, cfg in (("cfg3", W.config3()), ("cfg5", W.config5())):
+            b = MpsBatch(1, cfg.n, TruncationPolicy(cfg.cutoff, cfg.max_bond), keep_records=True)
+            plan = compile_batch(cfg.programs, cfg.n)
+            _, dev_s, wall_s = _timed(lambda: b.execute(plan), stream)
+            f = records_flops(b.update_records(0))
+            out[name] = {"s": wall_s, "device_s": dev_s, "updates": int(len(b.update_records(0))),
+                         "nominal_tflop": f / 1e12, "achieved_tflops": f / wall_s / 1e12,
+                         "frac": f / wall_s / 1e12 / peak, "path": "MpsBatch.execute (evolution)"}
+            del b
+    return out
 
 
 def main() -> None:
@@ -206,7 +344,6 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--replicas", type=int, default=16)
-    ap.add_argument("--ref-updates", type=int, default=2)
     ap.add_argument("--mode", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-circuit", action="store_true")
@@ -216,22 +353,32 @@ def main() -> None:
         run_reference(args)
         return
 
-    import torch
-    import torch.distributed as dist
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        # NCCL's communicator-init lines (to stderr) show each rank's device and transport
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+
+    import torch
+    import torch.distributed as dist
+
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        warm = torch.ones(1, device="cuda")
+        dist.all_reduce(warm)              # communicator up before any timing
 
     from paper_1807_07914_b200 import MpsBatch, TruncationPolicy, compile_batch, _native
+    from paper_1807_07914_b200.engine import SvdTimer
 
     lib = _native.load()
     for kv in args.param:
         k, v = kv.split("=")
-        assert lib.bmps_set_param(k.encode(), float(v)) == 0, kv
+        _native._overrides[k.strip()] = float(v)
+    peak, peak_basis = fp64_peak()
     R = args.replicas
     policy = TruncationPolicy(CUTOFF, CHI)
     batch = MpsBatch(R, N_QUBITS, policy)
@@ -257,12 +404,11 @@ def main() -> None:
     for k in range(args.warmup):
         batch.execute(plans[k], mode=args.mode)
     batch.check_status()
-    barrier()
     # live device time of the dominant stage (K3, the SVD) from CUDA events the
     # library records on its launch stream around that stage of every update batch
-    svd_ms, svd_n = ctypes.c_double(0.0), ctypes.c_int32(0)
-    lib.bmps_svd_time(ctypes.byref(svd_ms), ctypes.byref(svd_n))
-    lib.bmps_set_param(b"time_svd", 1.0)
+    timer = SvdTimer(capacity=4 * args.steps + 8)
+    timer.attach(batch)
+    barrier()
     l0 = lib.bmps_launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -273,9 +419,9 @@ def main() -> None:
         e1.record(stream)
         barrier()
     launches = int(lib.bmps_launch_count() - l0)
-    lib.bmps_set_param(b"time_svd", 0.0)
-    lib.bmps_svd_time(ctypes.byref(svd_ms), ctypes.byref(svd_n))
-    svd_launch_ms = svd_ms.value / max(svd_n.value, 1)
+    svd_total_ms, svd_n = timer.total_ms()
+    batch.svd_timer = None
+    svd_launch_ms = svd_total_ms / max(svd_n, 1)
     ms = e0.elapsed_time(e1)
     batch.check_status()
     sw = batch.last_sweeps(int(upd[total_steps - 1]))
@@ -292,15 +438,14 @@ def main() -> None:
     value = n_upd_all / (ms_max / 1e3)
 
     # e2e: through the public API from host program lists, H2D of the plan + D2H of results
-    import torch as _t
     e2e_steps = [bulk_layer(args.warmup + k, r, full[r]) for k in range(args.steps) for r in range(R)]
-    lam_host = _t.empty(batch.lam.shape, dtype=batch.lam.dtype, pin_memory=True)
-    err_host = _t.empty(batch.trunc_err.shape, dtype=batch.trunc_err.dtype, pin_memory=True)
+    lam_host = torch.empty(batch.lam.shape, dtype=batch.lam.dtype, pin_memory=True)
+    err_host = torch.empty(batch.trunc_err.shape, dtype=batch.trunc_err.dtype, pin_memory=True)
     h2d = d2h = 0
     barrier()
     t_w0 = time.perf_counter()
-    f0 = _t.cuda.Event(enable_timing=True)
-    f1 = _t.cuda.Event(enable_timing=True)
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     for k in range(args.steps):
         progs = e2e_steps[k * R:(k + 1) * R]
@@ -323,44 +468,16 @@ def main() -> None:
         e2e_t[0] = e2e_max[0]
     e2e_value = float(e2e_t[1].item()) / (float(e2e_t[0].item()) / 1e3)
 
-    # BASELINE config 4's circuits/s, sharded by circuit: a 256 x N-circuit
-    # job, circuits dealt round-robin to the N ranks (weak scaling), the public batched
-    # path incl. host planning: simulate_batch + <Z0 Z31> + 16 amplitudes per circuit and
-    # one D2H of the results; wall clock between barriers (= the slowest rank)
-    cfg4 = None
-    if not args.no_circuit:
-        from paper_1807_07914_b200 import workloads as W
-        from paper_1807_07914_b200 import simulate_batch
-        per_rank = 256
-        n4 = per_rank * world
-        mine = list(range(rank, n4, world))
-        w4 = W.config4(circuits=n4, indices=mine)
-        barrier()
-        t4 = time.perf_counter()
-        b4 = simulate_batch(w4.programs, w4.n, TruncationPolicy(w4.cutoff, w4.max_bond))
-        zz = b4.expectations(np.arange(len(mine), dtype=np.int32), w4.paulis * len(mine))
-        am = b4.amplitudes(np.repeat(np.arange(len(mine), dtype=np.int32), 16),
-                           [x for bs in w4.bitstrings for x in bs])
-        barrier()
-        dt4 = time.perf_counter() - t4
-        cfg4 = {"circuits": n4, "s": dt4, "circuits_per_s": n4 / dt4, "scaling": "weak",
-                "circuits_per_gpu": per_rank,
-                "path": "simulate_batch (host planning included) + expectations + amplitudes, "
-                        "wall clock between barriers",
-                "outputs": int(zz.size + am.size) * world}
-        del b4
+    configs = None if args.no_circuit else config_rooflines(peak, world, rank, stream)
 
     line = None
     if rank == 0:
         f_upd = nominal_update_flops(CHI, CHI, CHI, CHI)
         f_svd = svd_flops(CHI, CHI)
         step_achieved = f_upd * value / world / 1e12   # per GPU, whole update
-        upd_per_launch = n_upd / max(svd_n.value, 1)
+        upd_per_launch = n_upd / max(svd_n, 1)
         achieved = f_svd * upd_per_launch / (svd_launch_ms / 1e3) / 1e12
-        prof = {}
-        tp = ROOT / "profiles" / "r01_traffic.json"
-        if tp.exists():
-            prof = json.loads(tp.read_text())
+        prof = json.loads(TRAFFIC_FILE.read_text()) if TRAFFIC_FILE.exists() else {}
         line = {
             "metric": "MPS 2-qubit gate updates/sec at chi=256 (contract+SVD)",
             "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
@@ -375,21 +492,19 @@ def main() -> None:
             "roofline": {"bound": "tensor",
                          "kernel": "K3 SVD stage (column sort + double Householder QR + block Jacobi "
                                    "+ Q1 epilogue), one launch sequence per bulk layer",
-                         "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                         "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+                         "achieved": achieved, "peak": peak, "peak_basis": peak_basis,
+                         "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": (prof["svd_dram_bytes_per_update"] * upd_per_launch
                                      if "svd_dram_bytes_per_update" in prof else None),
-                         "traffic_unit": "DRAM bytes per K3 launch sequence (ncu launch list, "
-                                         "profiles/r01_traffic.json, per update x updates per launch)",
+                         "traffic_unit": f"DRAM bytes per K3 launch sequence (ncu, "
+                                         f"{TRAFFIC_FILE.relative_to(ROOT)}: per update x updates per launch)",
                          "algorithmic_flops_per_launch": f_svd * upd_per_launch,
-                         "svd_launch_ms": svd_launch_ms, "svd_share_of_step": svd_ms.value / ms,
+                         "svd_launch_ms": svd_launch_ms, "svd_share_of_step": svd_total_ms / ms,
                          "basis": f"F_svd = 4(14 q p^2 + 8 p^3) = {f_svd:.4g} flop per chi=256 update "
                                   "(SURVEY §8(d), Golub-Kahan count, not Jacobi's executed work) x "
-                                  "updates per launch / live CUDA-event time of the stage; peak = "
-                                  "measured FP64 (cuBLAS ZGEMM 4096^3 / DMMA probe, tools/fp64_peaks.py; "
-                                  "MEASURED_PEAKS.json has no FP64 entry)",
+                                  "updates per launch / live CUDA-event time of the stage",
                          "executed_fp64_tensor_flops_per_update": prof.get("fp64_tensor_flops_per_update"),
-                         "step": {"achieved": step_achieved, "frac": step_achieved / FP64_PEAK_TFLOPS,
+                         "step": {"achieved": step_achieved, "frac": step_achieved / peak,
                                   "basis": f"whole update F = {f_upd:.4g} flop x updates / step time"},
                          "nominal_bytes_per_update": update_bytes(CHI, CHI, CHI, CHI)},
             "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
@@ -419,32 +534,20 @@ def main() -> None:
             line["single_circuit_layer"] = {
                 "updates_per_layer": nb / 3, "updates_per_s": nb / (h0.elapsed_time(h1) / 1e3),
                 "ms_per_layer": h0.elapsed_time(h1) / 3}
-        if not args.no_circuit and world == 1:
-            from paper_1807_07914_b200 import workloads as W
-            w3 = W.config3()
-            b3 = MpsBatch(1, w3.n, TruncationPolicy(w3.cutoff, w3.max_bond))
-            p3 = compile_batch(w3.programs, w3.n)
-            torch.cuda.synchronize()
-            g0 = torch.cuda.Event(enable_timing=True)
-            g1 = torch.cuda.Event(enable_timing=True)
-            g0.record(stream)
-            b3.execute(p3)
-            g1.record(stream)
-            torch.cuda.synchronize()
-            line["cfg3_full_circuit"] = {"s": g0.elapsed_time(g1) / 1e3,
-                                         "circuits_per_s": 1e3 / g0.elapsed_time(g1)}
-            del b3
-        if cfg4 is not None:
-            line["cfg4_circuits"] = cfg4
+        if configs is not None:
+            line["configs"] = configs
+            line["cfg4_circuits"] = configs["cfg4"]
         if not args.no_cpu_baseline and world == 1:
-            gam = batch.site_tensors(0)
-            lam = batch.bond_vectors(0)
-            done, dt = cpu_baseline_sample((gam, lam))
-            line["cpu_baseline"] = {"value": done / dt, "unit": "updates/s", "cores": os.cpu_count(),
-                                    "kind": "port",
-                                    "sample": f"{done} chi=256 updates (verbatim reference einsum + "
-                                              f"zgesdd via oracle/mps_oracle.py) in {dt:.1f} s on the "
-                                              "GPU box host, from replica 0's steady state"}
+            t_cpu = time.perf_counter()
+            cpu = cpu_reference_rates(_oracle_steady(batch.site_tensors(0), batch.bond_vectors(0)))
+            line["cpu_baseline"] = {
+                "value": cpu["value"], "unit": "updates/s", "cores": cpu["cores"], "kind": "port",
+                "sample": (f"chi=256 updates from replica 0's steady state, verbatim reference einsum + "
+                           f"zgesdd (oracle/mps_oracle.py verbatim=True) on the GPU box host "
+                           f"(os.cpu_count {cpu['os_cpu_count']}, sched_getaffinity "
+                           f"{cpu['sched_getaffinity']}); best of {cpu['rates_updates_per_s']} "
+                           f"= {cpu['best']}; {time.perf_counter() - t_cpu:.1f} s of CPU timing"),
+                "rates": cpu["rates_updates_per_s"]}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -22,10 +22,13 @@
  *               int32 max_bond_seen[S], int32 status[S], int32 status_bond[S]
  *               (RunRecord / MpsState bookkeeping, mps.py:64-84).
  *   - Every call is asynchronous on the given cudaStream_t (passed as void*),
- *     never allocates, never synchronises (except bmps_apply_2q mode 2, which
- *     polls Jacobi convergence once per sweep), and returns 0 or a negative
+ *     never allocates, never synchronises, and returns 0 or a negative
  *     BMPS_E_* launch/argument error. Numerical failures are reported through
  *     the per-state status words (BMPS_S_*) and read at the next host sync.
+ *   - The library holds no mutable numerical state: every tunable of a call
+ *     travels in its arguments (bmps_params). The only process-wide data are a
+ *     per-device cache of kernel attributes / occupancy (set once under a
+ *     mutex) and a read-only statistic (bmps_launch_count).
  *   - Work lists ("items") are int32 pairs (state index, site q), in program
  *     order per state; gates are complex128 row-major 2x2 / 4x4 matrices, one
  *     per item, 4x4 indexed [2a+b][2s+t] with a,s on site q (gates.py:3-4).
@@ -59,13 +62,6 @@ typedef struct bmps_policy {
   int32_t relative;  /* TruncationPolicy.relative (mps.py:35) */
 } bmps_policy;
 
-/* Device time of the SVD stage (column sort + QR preconditioner + Jacobi +
- * double-QR epilogue) summed over the bmps_apply_2q calls made since the last
- * call, measured with CUDA events on the calls' streams while the tunable
- * "time_svd" is 1 (bench.py's roofline of the dominant kernel). Synchronises
- * on the recorded events; resets the accumulator. */
-int32_t bmps_svd_time(double* total_ms, int32_t* count);
-
 /* Development aid (no reference counterpart): point the warp-specialised Jacobi
  * kernel's per-CTA progress words at pinned host memory (16 int32 per CTA); only in
  * builds with -DBMPS_WS_TRACE, BMPS_E_ARG otherwise. */
@@ -75,13 +71,13 @@ int32_t bmps_debug_set_trace(void* host_pinned);
 int32_t bmps_version(void);
 const char* bmps_status_string(int32_t code);
 
-/* Process-wide tunables of the Jacobi SVD: "tol_factor" (rotate while
- * |g_ij| > tol_factor * sqrt(rows) * eps * sqrt(g_ii g_jj); default 4),
- * "max_sweeps" (default 60), "max_inner" (Gram sweeps per block visit, 1). */
-int32_t bmps_set_param(const char* name, double value);
-
-/* Number of kernels this library has launched so far (process-wide). */
+/* Number of kernels this library has launched so far (process-wide statistic). */
 uint64_t bmps_launch_count(void);
+
+/* Build flags: bit 0 = measured-slower development variants compiled in
+ * (-DBMPS_EXPERIMENTAL: warp-specialised Jacobi, TMA bulk panel staging,
+ * Jacobi modes 2 and 3). */
+int32_t bmps_build_flags(void);
 
 /* Development aid: cumulative cycles of the Jacobi phases (Gram pass, inner
  * sweep, apply pass, visit counts, warp-specialised waits) in a
@@ -99,13 +95,51 @@ int32_t bmps_init_product(double* gamma, double* lam, int32_t* dims, double* tru
 int32_t bmps_apply_1q(double* gamma, const int32_t* dims, int32_t S, int32_t n, int32_t cap,
                       const int32_t* items, const double* gates, int32_t nitems, void* stream);
 
-/* Per-update record written by bmps_apply_2q (32 bytes): discarded weight
+/* Per-update record written by bmps_apply_2q (48 bytes): discarded weight
  * sum(sigma[keep:]^2) (mps.py:121-122), bond dims before the update, kept
- * dimension, status (BMPS_S_*) and the site q. */
+ * dimension, status (BMPS_S_*), the site q, and two robustness figures of the
+ * keep decision (mps.py:43-49) on the sorted spectrum sigma:
+ *   margin = min_{k < min(p, max_bond)} |sigma_k - thr| / sigma_0, the distance of
+ *            the nearest singular value that could change keep from the cutoff
+ *            threshold (+inf when cutoff == 0);
+ *   gap    = (sigma_{keep-1} - sigma_keep) / sigma_0, the spectral gap at the
+ *            truncation boundary (+inf when nothing is discarded).
+ * A margin below ~1e-12 is a cutoff tie: the reference's own zgesdd could
+ * decide it either way. */
 typedef struct bmps_update_record {
   double err;
   int32_t dl, dm, dr, keep, status, site;
+  double margin, gap;
 } bmps_update_record;
+
+/* Tunables of bmps_apply_2q (per call; bmps_default_params fills defaults). */
+typedef struct bmps_params {
+  double tol_factor;     /* rotate while |g_ij| > tol_factor*sqrt(rows)*eps*sqrt(g_ii g_jj) (4) */
+  int32_t max_sweeps;    /* Jacobi sweep cap; exceeding it is BMPS_S_SVD_FAILED (60) */
+  int32_t max_inner;     /* Gram-space sweeps per block visit (1) */
+  int32_t qr_min_cols;   /* Householder-QR preconditioning from this many columns (65) */
+  int32_t jacobi_mode;   /* block Jacobi (> 64 columns): 1 one persistent CTA per item,
+                            4 dynamic visit claiming (default); 2 round launches and
+                            3 cluster per item need BMPS_EXPERIMENTAL */
+  int32_t block_w2;      /* visit panel width 16 / 32 / 64 columns, 0 auto (32) */
+  int32_t double_qr;     /* second QR of R^H before the Jacobi (1) */
+  int32_t col_sort;      /* descending-norm column order ahead of the first QR (1) */
+  int32_t gram_cache;    /* cross visits reuse rotated intra-block Grams (1) */
+  int32_t pair_skip;     /* skip cross visits of provably clean block pairs (1) */
+  int32_t jac_cluster;   /* row-split cluster visits: -1 auto, 0 off, 2 / 4 CTAs (-1) */
+  int32_t jac_per_sm;    /* dynamic Jacobi CTAs per SM, 0 = occupancy maximum (0) */
+  int32_t jac_ws;        /* warp-specialised Jacobi (BMPS_EXPERIMENTAL only) (0) */
+  int32_t tma_staging;   /* TMA bulk panel staging (BMPS_EXPERIMENTAL only) (0) */
+  int32_t cluster_size;  /* CTAs per item in mode 3 (8) */
+  int32_t n_svd_events;  /* capacity of svd_events in event pairs (0: no timing) */
+  void** svd_events;     /* host array of 2*n_svd_events cudaEvent_t: the call records
+                            a pair bracketing its SVD stage (column sort, QR
+                            preconditioner, Jacobi, double-QR epilogue) at index
+                            *svd_events_used, then increments it */
+  int32_t* svd_events_used;
+} bmps_params;
+
+void bmps_default_params(bmps_params* p);
 
 /* Workspace bytes for bmps_apply_2q with nitems items at capacity cap. */
 size_t bmps_apply_2q_workspace_bytes(int32_t cap, int32_t nitems);
@@ -115,26 +149,27 @@ size_t bmps_apply_2q_workspace_bytes(int32_t cap, int32_t nitems);
  * one-sided Jacobi SVD -> truncate (policy) -> split. Item i's record is
  * written to log[log_index[i]]; bookkeeping is applied by bmps_stats_replay in
  * program order. dim_bound (<= cap, 0 = cap) is an upper bound on the left /
- * right bond dims of every item, used only to size grids. mode (block
- * Jacobi for > 64 columns): 0 library default (4), 1 persistent (one CTA per
- * item), 2 round-parallel (one launch per Jacobi round; polls convergence with
- * one stream sync per sweep), 3 one thread-block cluster per item (rounds
- * separated by cluster barriers, no host sync), 4 dynamic: one persistent
- * wave of CTAs claims block-pair visits from any item whose round is open
- * (no host sync, stragglers overlap other items). */
+ * right bond dims of every item, used only to size grids. params may be NULL
+ * (defaults). Results are bit-deterministic: no reduction depends on the
+ * order in which CTAs run. */
 int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int32_t n,
                       int32_t cap, const int32_t* items, const double* gates, int32_t nitems,
                       bmps_policy policy, bmps_update_record* log, const int32_t* log_index,
-                      void* workspace, size_t workspace_bytes, int32_t dim_bound, int32_t mode,
-                      void* stream);
+                      void* workspace, size_t workspace_bytes, int32_t dim_bound,
+                      const bmps_params* params, void* stream);
 
 /* Bookkeeping of MpsState._note_sizes / trunc_error_sq (mps.py:82-84, 122)
  * replayed over update records in PROGRAM order: ranges holds nranges int32
- * triples (state, first record, count). Sets the first failing record's
- * status and site into status / status_bond. */
+ * triples (state, first record, count; at most one range per state per call).
+ * Sets the first failing record's status and site into status / status_bond.
+ * Optional (NULL = skip): bond_err float64 [S][n-1] += each record's discarded
+ * weight at its bond (the per-bond truncation error, summed in program order),
+ * min_margin / min_gap float64 [S] = running minimum of the records' margin /
+ * gap (cutoff-tie and truncation-gap detectors). */
 int32_t bmps_stats_replay(const bmps_update_record* log, const int32_t* ranges, int32_t nranges,
                           double* trunc_err, int64_t* entries, int64_t* peak,
                           int32_t* max_bond_seen, int32_t* status, int32_t* status_bond,
+                          double* bond_err, int32_t n, double* min_margin, double* min_gap,
                           void* stream);
 
 /* Diagnostics of the last bmps_apply_2q on this workspace: per-item Jacobi
@@ -147,6 +182,14 @@ int32_t bmps_apply_2q_sweeps(const void* workspace, int32_t nitems, int32_t* swe
 int32_t bmps_amplitudes(const double* gamma, const double* lam, const int32_t* dims, int32_t S,
                         int32_t n, int32_t cap, const int32_t* state_idx, const uint8_t* bits,
                         int32_t count, double* out, void* stream);
+
+/* MpsState.conditional_prob_zero (mps.py:206-214) for state `state`, qubit
+ * `site`: prefix complex128 [dims[site]] (device), w0 / w1 complex128
+ * [dims[site+1]] = prefix @ T_site[:, b, :], p01 float64 [2] = <w0,w0>, <w1,w1>
+ * (the caller forms p0 / (p0 + p1), 0.5 when both vanish). */
+int32_t bmps_conditional(const double* gamma, const double* lam, const int32_t* dims, int32_t S,
+                         int32_t n, int32_t cap, int32_t state, int32_t site, const double* prefix,
+                         double* w0, double* w1, double* p01, void* stream);
 
 /* MpsState.sample / conditional_prob_zero (mps.py:206-237) for a batch of
  * shots: uniforms is float64 [shots][n] (the reference's rng.random() draws,

@@ -49,14 +49,70 @@ class _NpShim(types.ModuleType):
         return getattr(np, name)
 
 
-def set_shim(on: bool) -> None:
+class _SvdRecorder(types.ModuleType):
+    """``np.linalg`` whose ``svd`` also keeps the raw singular values it returns
+    (the numbers ``keep_count`` decides on, ``mps.py:116-120``); the call itself is
+    numpy's, so results are bit-identical to the unpatched reference."""
+
+    def __init__(self, name):
+        super().__init__(name)
+        self.spectra = []
+
+    def __getattr__(self, name):
+        return getattr(np.linalg, name)
+
+    def svd(self, *a, **k):
+        out = np.linalg.svd(*a, **k)
+        self.spectra.append(np.array(out[1]))
+        return out
+
+
+def set_shim(on: bool, record: bool = False):
+    """O2 shim on/off; with ``record`` the reference's SVD spectra are captured
+    (returns the recorder)."""
     _, ref_mps = _ref()
-    if on:
+    rec = None
+    if on or record:
         shim = _NpShim("numpy_o2")
-        shim.einsum = lambda *a, **k: np.einsum(*a, **{**k, "optimize": True})
+        if on:
+            shim.einsum = lambda *a, **k: np.einsum(*a, **{**k, "optimize": True})
+        if record:
+            rec = _SvdRecorder("numpy_linalg_rec")
+            shim.linalg = rec
         ref_mps.np = shim
     else:
         ref_mps.np = np
+    return rec
+
+
+def decision_margins(spectra, cutoff, max_bond, relative=True):
+    """Per update: the keep count of ``TruncationPolicy.keep_count`` (``mps.py:43-49``),
+    the distance of the nearest singular value that can move it from the cutoff
+    threshold, ``min_{k < min(p, max_bond)} |sigma_k - thr| / sigma_0`` (inf when
+    cutoff is 0), and the spectral gap at the truncation boundary
+    ``(sigma_{keep-1} - sigma_keep) / sigma_0`` (inf when nothing is discarded)."""
+    keep, margin, gap = [], [], []
+    for s in spectra:
+        p = len(s)
+        s0 = float(s[0]) if p else 0.0
+        if cutoff > 0:
+            thr = cutoff * (s0 if relative else 1.0)
+            k = int(np.sum(s >= thr))
+        else:
+            thr, k = None, p
+        k = max(k, 1)
+        if max_bond is not None:
+            k = min(k, max_bond)
+        K = p if max_bond is None else min(p, max_bond)
+        if thr is None or s0 == 0.0:
+            m = np.inf
+        else:
+            m = float(np.min(np.abs(s[:K] - thr))) / s0
+        g = float(s[k - 1] - s[k]) / s0 if k < p and s0 > 0 else np.inf
+        keep.append(k)
+        margin.append(m)
+        gap.append(g)
+    return np.array(keep, np.int64), np.array(margin), np.array(gap)
 
 
 def ref_matrix(op):
@@ -157,10 +213,11 @@ def gen_small() -> None:
 def gen_cfg1() -> None:
     from paper_1807_07914_b200.workloads import config1
     w = config1()
-    set_shim(False)
+    rec = set_shim(False, record=True)
     t0 = time.perf_counter()
     state, _ = ref_evolve(w.programs[0], w.n, w.cutoff, w.max_bond)
     t_ev = time.perf_counter() - t0
+    keep, margin, gap = decision_margins(rec.spectra, w.cutoff, w.max_bond)
     amps = np.array([state.amplitude(b) for b in w.bitstrings[0]])
     set_shim(True)
     t0 = time.perf_counter()
@@ -169,7 +226,7 @@ def gen_cfg1() -> None:
     set_shim(False)
     save("cfg1", {"mode": "O1 evolution + amplitudes; O2 shim for <Z>", "evolve_s": t_ev,
                   "query_s": t_q, "seed": w.meta["seed"]},
-         amps=amps, z=z, **state_summary(state))
+         amps=amps, z=z, upd_keep=keep, upd_margin=margin, upd_gap=gap, **state_summary(state))
 
 
 def gen_cfg2() -> None:
@@ -195,10 +252,11 @@ def gen_cfg2() -> None:
 def gen_cfg3() -> None:
     from paper_1807_07914_b200.workloads import config3
     w = config3()
-    set_shim(True)
+    rec = set_shim(True, record=True)
     t0 = time.perf_counter()
     state, bond_err = ref_evolve(w.programs[0], w.n, w.cutoff, w.max_bond, per_bond=True)
     t_ev = time.perf_counter() - t0
+    keep, margin, gap = decision_margins(rec.spectra, w.cutoff, w.max_bond)
     t0 = time.perf_counter()
     z = np.array([state.expectation_pauli(p) for p in w.paulis])
     t_q = time.perf_counter() - t0
@@ -207,27 +265,54 @@ def gen_cfg3() -> None:
     set_shim(False)
     save("cfg3", {"mode": "O2 shim evolution + O2 expectation_pauli", "evolve_s": t_ev,
                   "query_s": t_q, "seed": w.meta["seed"]},
-         z=z, z_env=z_env, norm=np.float64(norm), bond_err=bond_err, **state_summary(state))
+         z=z, z_env=z_env, norm=np.float64(norm), bond_err=bond_err, upd_keep=keep,
+         upd_margin=margin, upd_gap=gap, **state_summary(state))
 
 
-def gen_cfg4(count: int = 16) -> None:
+def _cfg4_circuit(c: int):
+    """One cfg4 circuit through the O2-shimmed reference (a Pool task)."""
+    from threadpoolctl import threadpool_limits
     from paper_1807_07914_b200.workloads import config4
-    w = config4()
-    set_shim(True)
-    zz, amps, dims, errs, mbs = [], [], [], [], []
-    t0 = time.perf_counter()
-    for c in range(count):
-        state, _ = ref_evolve(w.programs[c], w.n, w.cutoff, w.max_bond)
-        zz.append(state.expectation_pauli(w.paulis[0]))
-        amps.append([state.amplitude(b) for b in w.bitstrings[c]])
-        dims.append([len(x) for x in state.bond_vectors])
-        errs.append(state.trunc_error_sq)
-        mbs.append(state.max_bond_seen)
+    threadpool_limits(1)
+    w = config4(circuits=c + 1, indices=[c])
+    rec = set_shim(True, record=True)
+    note = ""
+    try:
+        state, _ = ref_evolve(w.programs[0], w.n, w.cutoff, w.max_bond)
+    except RuntimeError as exc:
+        # LAPACK zgesdd occasionally reports non-convergence ("SVD failed on bond q",
+        # mps.py:115-118) for one particular rounding of theta; the verbatim reference
+        # (its own einsums, O1) evolves the same circuit fine, so pin that run instead
+        note = f"O2 shim at 1 thread: {exc}; evolved verbatim (O1)"
+        rec = set_shim(False, record=True)
+        state, _ = ref_evolve(w.programs[0], w.n, w.cutoff, w.max_bond)
+        set_shim(True)
+    _, margin, gap = decision_margins(rec.spectra, w.cutoff, w.max_bond)
+    out = (state.expectation_pauli(w.paulis[0]), [state.amplitude(b) for b in w.bitstrings[0]],
+           [len(x) for x in state.bond_vectors], state.trunc_error_sq, state.max_bond_seen,
+           state.peak_entries, float(margin.min()), float(gap.min()), note)
     set_shim(False)
+    return out
+
+
+def gen_cfg4(count: int = 1024) -> None:
+    """All ``count`` circuits of cfg4 (circuit i depends on (seed, i) only, so these pin
+    every prefix slice the bench and the tests run), one circuit per Pool task with
+    single-threaded OpenBLAS."""
+    import multiprocessing as mp
+    from paper_1807_07914_b200.workloads import config4
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(os.cpu_count()) as pool:
+        res = pool.map(_cfg4_circuit, range(count), chunksize=4)
+    zz, amps, dims, errs, mbs, peaks, margins, gaps, fails = (list(x) for x in zip(*res))
+    failed = [i for i, f in enumerate(fails) if f]
     save("cfg4", {"mode": "O2 shim", "circuits": count, "elapsed_s": time.perf_counter() - t0,
-                  "seed": w.meta["seed"]},
-         zz=np.array(zz), amps=np.array(amps), dims=np.array(dims, dtype=np.int64),
-         trunc_error_sq=np.array(errs), max_bond_seen=np.array(mbs, dtype=np.int64))
+                  "seed": config4(circuits=1).meta["seed"],
+                  "reference_retries": {str(i): fails[i] for i in failed}},
+         zz=np.array(zz), amps=np.array(amps), dims=np.array(dims, dtype=np.int16),
+         trunc_error_sq=np.array(errs), max_bond_seen=np.array(mbs, dtype=np.int64),
+         peak_entries=np.array(peaks, dtype=np.int64), min_margin=np.array(margins),
+         min_gap=np.array(gaps))
 
 
 def gen_o2check() -> None:
@@ -254,10 +339,11 @@ def gen_o2check() -> None:
 def gen_cfg5() -> None:
     from paper_1807_07914_b200.workloads import config5
     w = config5()
-    set_shim(True)
+    rec = set_shim(True, record=True)
     t0 = time.perf_counter()
     state, bond_err = ref_evolve(w.programs[0], w.n, w.cutoff, w.max_bond, per_bond=True)
     t_ev = time.perf_counter() - t0
+    keep, margin, gap = decision_margins(rec.spectra, w.cutoff, w.max_bond)
     set_shim(False)
     t0 = time.perf_counter()
     vals = to_oracle(state).expectations_env(w.paulis + ["I" * w.n])
@@ -268,8 +354,9 @@ def gen_cfg5() -> None:
     save("cfg5", {"mode": "O2 shim evolution + O2+ env-reuse queries", "evolve_s": t_ev,
                   "query_s": t_q, "seed": w.meta["seed"]},
          x=vals[: w.n], z=vals[w.n: 2 * w.n], norm=np.float64(vals[-1]), bond_err=bond_err,
-         dims=dims, lam_head=lam_head, trunc_error_sq=summ["trunc_error_sq"],
-         max_bond_seen=summ["max_bond_seen"], peak_entries=summ["peak_entries"])
+         dims=dims, lam_head=lam_head, lam=summ["lam"], trunc_error_sq=summ["trunc_error_sq"],
+         max_bond_seen=summ["max_bond_seen"], peak_entries=summ["peak_entries"],
+         upd_keep=keep, upd_margin=margin, upd_gap=gap)
 
 
 if __name__ == "__main__":

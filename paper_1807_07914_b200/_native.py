@@ -26,7 +26,21 @@ class BmpsPolicy(ctypes.Structure):
     _fields_ = [("cutoff", ctypes.c_double), ("max_bond", ctypes.c_int32), ("relative", ctypes.c_int32)]
 
 
-RECORD_BYTES = 32  # sizeof(bmps_update_record)
+class BmpsParams(ctypes.Structure):
+    """``bmps_params`` (include/bmps.h): every tunable of one bmps_apply_2q call."""
+
+    _fields_ = [("tol_factor", ctypes.c_double), ("max_sweeps", ctypes.c_int32),
+                ("max_inner", ctypes.c_int32), ("qr_min_cols", ctypes.c_int32),
+                ("jacobi_mode", ctypes.c_int32), ("block_w2", ctypes.c_int32),
+                ("double_qr", ctypes.c_int32), ("col_sort", ctypes.c_int32),
+                ("gram_cache", ctypes.c_int32), ("pair_skip", ctypes.c_int32),
+                ("jac_cluster", ctypes.c_int32), ("jac_per_sm", ctypes.c_int32),
+                ("jac_ws", ctypes.c_int32), ("tma_staging", ctypes.c_int32),
+                ("cluster_size", ctypes.c_int32), ("n_svd_events", ctypes.c_int32),
+                ("svd_events", ctypes.c_void_p), ("svd_events_used", ctypes.c_void_p)]
+
+
+RECORD_BYTES = 48  # sizeof(bmps_update_record)
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int32
@@ -36,16 +50,17 @@ _L = ctypes.c_int64
 _SIGNATURES = {
     "bmps_version": ([], _I),
     "bmps_status_string": ([_I], ctypes.c_char_p),
-    "bmps_set_param": ([ctypes.c_char_p, ctypes.c_double], _I),
     "bmps_launch_count": ([], ctypes.c_uint64),
+    "bmps_build_flags": ([], _I),
+    "bmps_default_params": ([_P], None),
     "bmps_phase_cycles": ([_P], _I),
-    "bmps_svd_time": ([_P, _P], _I),
     "bmps_debug_set_trace": ([_P], _I),
     "bmps_init_product": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P], _I),
     "bmps_apply_1q": ([_P, _P, _I, _I, _I, _P, _P, _I, _P], _I),
     "bmps_apply_2q_workspace_bytes": ([_I, _I], _SZ),
-    "bmps_apply_2q": ([_P, _P, _P, _I, _I, _I, _P, _P, _I, BmpsPolicy, _P, _P, _P, _SZ, _I, _I, _P], _I),
-    "bmps_stats_replay": ([_P, _P, _I, _P, _P, _P, _P, _P, _P, _P], _I),
+    "bmps_apply_2q": ([_P, _P, _P, _I, _I, _I, _P, _P, _I, BmpsPolicy, _P, _P, _P, _SZ, _I, _P, _P], _I),
+    "bmps_stats_replay": ([_P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P], _I),
+    "bmps_conditional": ([_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P], _I),
     "bmps_apply_2q_sweeps": ([_P, _I, _P, _P], _I),
     "bmps_amplitudes": ([_P, _P, _P, _I, _I, _I, _P, _P, _I, _P, _P], _I),
     "bmps_sample": ([_P, _P, _P, _I, _I, _I, _P, _P, _I, _P, _P], _I),
@@ -70,11 +85,57 @@ EXPORTED = tuple(_SIGNATURES)
 _lib = None
 
 
-# library defaults of the bmps_set_param tunables (csrc/bmps.cu)
-DEFAULT_PARAMS = {"tol_factor": 4.0, "max_sweeps": 60, "max_inner": 1, "qr_min_cols": 65,
-                  "jacobi_mode": 4, "cluster_size": 8, "tma_staging": 0, "gram_cache": 1,
-                  "block_w2": 32, "double_qr": 1, "jac_per_sm": 0, "col_sort": 1, "time_svd": 0, "pair_skip": 1,
-                  "jac_ws": 0, "jac_cluster": -1}
+# tunables of bmps_apply_2q (bmps_default_params); the package-level overrides
+# below apply to every call made while they are set (the library itself keeps no
+# mutable state: each call gets its own bmps_params)
+TUNABLES = ("tol_factor", "max_sweeps", "max_inner", "qr_min_cols", "jacobi_mode", "block_w2",
+            "double_qr", "col_sort", "gram_cache", "pair_skip", "jac_cluster", "jac_per_sm",
+            "jac_ws", "tma_staging", "cluster_size")
+_overrides: dict = {}
+
+
+def experimental() -> bool:
+    """True when libbmps.so was built with -DBMPS_EXPERIMENTAL (slower development variants)."""
+    return bool(load().bmps_build_flags() & 1)
+
+
+def params(**extra) -> BmpsParams:
+    """A ``bmps_params`` of the library defaults, the active overrides and ``extra``."""
+    p = BmpsParams()
+    load().bmps_default_params(ctypes.byref(p))
+    for k, v in {**_overrides, **extra}.items():
+        if k not in TUNABLES:
+            raise ValueError(f"unknown tunable {k!r}")
+        setattr(p, k, type(getattr(p, k))(v))
+    return p
+
+
+def default_params() -> dict:
+    p = BmpsParams()
+    load().bmps_default_params(ctypes.byref(p))
+    return {k: getattr(p, k) for k in TUNABLES}
+
+
+class tunables:
+    """``with tunables(jac_cluster=4): ...`` -- override Jacobi tunables for the calls
+    made inside the block (tests, A/B tools)."""
+
+    def __init__(self, **kw):
+        for k in kw:
+            if k not in TUNABLES:
+                raise ValueError(f"unknown tunable {k!r}")
+        self.kw = kw
+        self.saved: dict = {}
+
+    def __enter__(self):
+        self.saved = dict(_overrides)
+        _overrides.update(self.kw)
+        return self
+
+    def __exit__(self, *exc):
+        _overrides.clear()
+        _overrides.update(self.saved)
+        return False
 
 
 def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
@@ -93,13 +154,15 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    # optional tunables, e.g. BMPS_PARAMS="block_w2=64,tol_factor=4"
-    for kv in filter(None, os.environ.get("BMPS_PARAMS", "").split(",")):
-        k, v = kv.split("=")
-        if lib.bmps_set_param(k.strip().encode(), float(v)) != 0:
-            raise ValueError(f"bad BMPS_PARAMS entry {kv!r}")
     if path is None:
         _lib = lib
+        # optional tunables, e.g. BMPS_PARAMS="block_w2=64,tol_factor=4"
+        for kv in filter(None, os.environ.get("BMPS_PARAMS", "").split(",")):
+            k, v = kv.split("=")
+            k = k.strip()
+            if k not in TUNABLES:
+                raise ValueError(f"bad BMPS_PARAMS entry {kv!r}")
+            _overrides[k] = float(v)
     return lib
 
 

@@ -46,7 +46,7 @@ def run_program(program, n: int | None = None, backend: str = "mps",
 
 
 def simulate_batch(programs, n: int, policy: TruncationPolicy | None = None, *, device=None,
-                   mode: int = 0, chunk: int | None = None) -> MpsBatch:
+                   mode: int = 0, chunk: int | None = None, keep_records: bool = False) -> MpsBatch:
     """Run ``programs[i]`` on state i of a fresh ``MpsBatch`` (one device).
 
     Batches of 256 or more circuits are planned and launched in ``chunk``-circuit
@@ -57,7 +57,7 @@ def simulate_batch(programs, n: int, policy: TruncationPolicy | None = None, *, 
     1024 circuits 280 -> 334 circuits/s (``tools/cfg4_chunks.py``).
     """
     S = len(programs)
-    batch = MpsBatch(S, n, policy, device=device)
+    batch = MpsBatch(S, n, policy, device=device, keep_records=keep_records)
     if chunk is None:
         chunk = S if S < 256 else max(128, -(-S // 4))
     for c0 in range(0, S, max(1, chunk)):

@@ -11,7 +11,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 SOURCES = [PKG / "csrc" / "bmps.cu", PKG / "csrc" / "bmps_plan.cpp"]
-DEPS = SOURCES + sorted((PKG / "csrc").glob("*.cuh")) + [ROOT / "include" / "bmps.h"]
+DEPS = SOURCES + sorted((PKG / "csrc").glob("*.cuh")) + [ROOT / "include" / "bmps.h", PKG / "csrc" / "libbmps.map"]
 OUT = PKG / "libbmps.so"
 
 NVCC_FLAGS = [
@@ -19,6 +19,8 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-shared", "-Xcompiler", "-fPIC",
     "-Xptxas", "-v",
+    # export only the bmps_* C ABI (the statically linked cudart stays internal)
+    "-Xlinker", "--version-script=" + str(Path(__file__).resolve().parent / "csrc" / "libbmps.map"),
 ]
 
 

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -21,42 +23,26 @@ namespace {
 
 constexpr int kNumSMs = 148;
 
-// Tunables (bmps_set_param): Jacobi tolerance factor (tol = f * sqrt(rows) * eps),
-// sweep cap, inner Gram sweeps per block visit.
-unsigned long long g_launches = 0;  // kernels launched through this library
-double g_tol_factor = 4.0;
-int g_max_sweeps = 60;
-int g_max_inner = 1;
-int g_qr_min_cols = 65;    // Householder-QR preconditioning for Jacobi matrices with >= this many columns
-int g_jacobi_mode = 4;     // block-mode Jacobi: 1 persistent CTA/item, 2 round launches,
-                           // 3 cluster/item, 4 dynamic persistent scheduler
-int g_cluster_size = 8;
-int g_tma_staging = 0;     // 1: Jacobi panels staged by TMA bulk copies instead of cp.async
-int g_gram_cache = 1;      // cross visits reuse rotated intra-block Grams
-int g_block_w2 = 32;       // block-mode panel width: 16, 32, 64 columns, or 0 = auto (16 / 32)
-int g_double_qr = 1;       // second QR of R^H before the Jacobi (preconditioned items)
-int g_jac_cluster = -1;    // row-split cluster Jacobi: -1 auto (small batches), 0 off, 2 / 4 CTAs
-int g_jac_ws = 0;          // warp-specialised dynamic Jacobi (W2 = 32); measured slower, opt-in
-int g_jac_per_sm = 0;      // dynamic Jacobi CTAs per SM (0: occupancy maximum)
-int g_col_sort = 1;        // descending-norm column order ahead of the first QR (double-QR items)
-int g_time_svd = 0;        // record CUDA events around the SVD stage (bmps_svd_time)
-int g_pair_skip = 1;       // dynamic Jacobi: skip cross visits of provably clean block pairs
+// Process-wide data (no numerical state): a statistic, and per-device caches of
+// kernel attributes / occupancy filled once under a mutex. Every tunable of a
+// call arrives in its bmps_params.
+std::atomic<unsigned long long> g_launches{0};  // kernels launched through this library
 
-// CUDA-event pairs bracketing the SVD stage (K3: column sort, QR preconditioner,
-// Jacobi, double-QR epilogue) of each bmps_apply_2q call while g_time_svd is set.
-struct SvdTimer {
-  std::vector<cudaEvent_t> ev;  // 2 per recorded call
-  size_t used = 0;
-  cudaEvent_t next() {
-    if (used == ev.size()) {
-      cudaEvent_t e;
-      cudaEventCreate(&e);
-      ev.push_back(e);
-    }
-    return ev[used++];
-  }
+constexpr int kMaxDevices = 64;
+struct DevCache {
+  bool attrs = false;        // dynamic shared-memory attributes set
+  int sms = 0;               // multiprocessor count
+  int jac_slots[4] = {0, 0, 0, 0};  // resident dynamic-Jacobi CTAs (W2 16 / 32 / 64 / ws)
+  int cl_per_sm = 0;         // resident 4-CTA cluster-Jacobi CTAs per SM
 };
-SvdTimer g_svd_timer;
+std::mutex g_cache_mu;
+DevCache g_cache[kMaxDevices];
+
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 || d >= kMaxDevices ? 0 : d;
+}
 
 // ---------------------------------------------------------------------------
 // init: product state |0...0> (mps.py:55-66)
@@ -277,6 +263,50 @@ __global__ void __launch_bounds__(256) sample_kernel(StateView sv, const int* st
     const double2* src = bit ? w1 : w0;
     for (int r = tid; r < dr; r += blockDim.x) cur[r] = src[r];
     __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// MpsState.conditional_prob_zero (mps.py:206-214) for one (state, site):
+// w_b = prefix @ T_k[:, b, :] (T_k = Gamma_k lam_{k+1}), p_b = <w_b, w_b>. One CTA;
+// p0, p1 summed per thread in r order, then over threads in a fixed tree.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) conditional_kernel(StateView sv, int s, int k,
+                                                          const double2* prefix, double2* w0,
+                                                          double2* w1, double* p01) {
+  __shared__ double red[2][256];
+  const int tid = threadIdx.x, cap = sv.cap;
+  const int* d = sv.dimv(s);
+  const int dl = d[k], dr = d[k + 1];
+  const double2* t = sv.site(s, k);
+  const double* lam = sv.bond(s, k + 1);
+  double p0 = 0.0, p1 = 0.0;
+  for (int r = tid; r < dr; r += blockDim.x) {
+    double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+    for (int l = 0; l < dl; ++l) {
+      a0 = cfma(prefix[l], t[(size_t)(2 * l) * cap + r], a0);
+      a1 = cfma(prefix[l], t[(size_t)(2 * l + 1) * cap + r], a1);
+    }
+    a0 = cscale(a0, lam[r]);
+    a1 = cscale(a1, lam[r]);
+    w0[r] = a0;
+    w1[r] = a1;
+    p0 += cabs2(a0);
+    p1 += cabs2(a1);
+  }
+  red[0][tid] = p0;
+  red[1][tid] = p1;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (tid < o) {
+      red[0][tid] += red[0][tid + o];
+      red[1][tid] += red[1][tid + o];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    p01[0] = red[0][0];
+    p01[1] = red[1][0];
   }
 }
 
@@ -648,6 +678,8 @@ struct Ws {
   size_t aux_stride;
   int maxp;
   int sig_stride;
+  double* fro_part;   // per item: theta's per-CTA ||M||_F^2 partials
+  int fro_stride;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -686,6 +718,10 @@ size_t ws_layout(int cap, int nitems, char* base, Ws* ws) {
   const size_t pairlog_stride = (size_t)nbcap + (size_t)nbcap * nbcap;
   const size_t o_pl = off;
   off = align256(off + sizeof(int) * pairlog_stride * nitems);
+  const int tpd = (cap + 31) / 32;
+  const int fro_stride = tpd * tpd;
+  const size_t o_fro = off;
+  off = align256(off + sizeof(double) * (size_t)fro_stride * nitems);
   if (ws && base) {
     ws->meta = (ItemMeta*)(base + o_meta);
     ws->sig = (double*)(base + o_sig);
@@ -706,13 +742,20 @@ size_t ws_layout(int cap, int nitems, char* base, Ws* ws) {
     ws->maxp = maxp;
     ws->mat_stride = mat_stride;
     ws->sig_stride = sig_stride;
+    ws->fro_part = (double*)(base + o_fro);
+    ws->fro_stride = fro_stride;
   }
   return off;
 }
 
-bool g_attrs_set = false;
-void set_attrs() {
-  if (g_attrs_set) return;
+// Dynamic shared-memory attributes and occupancy figures of this device, set /
+// measured once per device (cudaFuncSetAttribute is per device).
+constexpr int kSweepCapSmem = (int)(sizeof(double2) * 5 * 32 * 32);
+const DevCache& device_cache() {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lock(g_cache_mu);
+  DevCache& dc = g_cache[dev];
+  if (dc.attrs) return dc;
   cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kThetaSmem);
   cudaFuncSetAttribute(qr_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQrUpdateSmem);
   cudaFuncSetAttribute(qr_panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -728,13 +771,40 @@ void set_attrs() {
                        (int)JacCfg<64>::kSmem);
   cudaFuncSetAttribute(jacobi_dynamic_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)JacCfg<16>::kSmem);
-  cudaFuncSetAttribute(jacobi_ws_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)WsCfg<32>::kSmem);
   cudaFuncSetAttribute(jacobi_cluster_kernel<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)ClCfg<32>::kSmem);
   cudaFuncSetAttribute(jacobi_cluster_kernel<32, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)ClCfg<32>::kSmem);
-  g_attrs_set = true;
+  cudaFuncSetAttribute(amplitude_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * BMPS_AMP_VEC);
+  cudaFuncSetAttribute(sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(3 * 1024 * sizeof(double2)));
+  cudaFuncSetAttribute(pauli_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepCapSmem);
+  cudaFuncSetAttribute(env_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepCapSmem);
+  cudaFuncSetAttribute(dense_run_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(sizeof(double2) << kDenseSmemQubits));
+#ifdef BMPS_EXPERIMENTAL
+  cudaFuncSetAttribute(jacobi_ws_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)WsCfg<32>::kSmem);
+#endif
+  cudaDeviceGetAttribute(&dc.sms, cudaDevAttrMultiProcessorCount, dev);
+  if (dc.sms <= 0) dc.sms = kNumSMs;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_dynamic_kernel<16>, 256, JacCfg<16>::kSmem);
+  dc.jac_slots[0] = std::max(1, per_sm) * dc.sms;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_dynamic_kernel<32>, 256, JacCfg<32>::kSmem);
+  dc.jac_slots[1] = std::max(1, per_sm) * dc.sms;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_dynamic_kernel<64>, 256, JacCfg<64>::kSmem);
+  dc.jac_slots[2] = std::max(1, per_sm) * dc.sms;
+#ifdef BMPS_EXPERIMENTAL
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_ws_kernel<32>, kWsThreads, WsCfg<32>::kSmem);
+  dc.jac_slots[3] = std::max(1, per_sm) * dc.sms;
+#endif
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dc.cl_per_sm, jacobi_cluster_kernel<32, 4>, 256,
+                                                ClCfg<32>::kSmem);
+  dc.cl_per_sm = std::max(dc.cl_per_sm, 1);
+  cudaGetLastError();
+  dc.attrs = true;
+  return dc;
 }
 
 int32_t launch_status() {
@@ -760,9 +830,40 @@ StateView make_view(double* gamma, double* lam, int32_t* dims, int n, int cap) {
 
 extern "C" {
 
-int32_t bmps_version(void) { return 1; }
+int32_t bmps_version(void) { return 2; }
 
-uint64_t bmps_launch_count(void) { return g_launches; }
+uint64_t bmps_launch_count(void) { return g_launches.load(); }
+
+int32_t bmps_build_flags(void) {
+#ifdef BMPS_EXPERIMENTAL
+  return 1;
+#else
+  return 0;
+#endif
+}
+
+void bmps_default_params(bmps_params* p) {
+  if (!p) return;
+  *p = bmps_params{};
+  p->tol_factor = 4.0;
+  p->max_sweeps = 60;
+  p->max_inner = 1;
+  p->qr_min_cols = 65;
+  p->jacobi_mode = 4;
+  p->block_w2 = 32;
+  p->double_qr = 1;
+  p->col_sort = 1;
+  p->gram_cache = 1;
+  p->pair_skip = 1;
+  p->jac_cluster = -1;
+  p->jac_per_sm = 0;
+  p->jac_ws = 0;
+  p->tma_staging = 0;
+  p->cluster_size = 8;
+  p->n_svd_events = 0;
+  p->svd_events = nullptr;
+  p->svd_events_used = nullptr;
+}
 
 // Development aid: cumulative Jacobi phase cycles (builds with -DBMPS_PHASE_TIMERS only).
 int32_t bmps_phase_cycles(uint64_t* out4) {
@@ -775,35 +876,10 @@ int32_t bmps_phase_cycles(uint64_t* out4) {
 #endif
 }
 
-int32_t bmps_set_param(const char* name, double value) {
-  if (!name) return BMPS_E_ARG;
-  const std::string k(name);
-  if (k == "tol_factor" && value > 0) g_tol_factor = value;
-  else if (k == "max_sweeps" && value >= 1) g_max_sweeps = (int)value;
-  else if (k == "max_inner" && value >= 1) g_max_inner = (int)value;
-  else if (k == "qr_min_cols" && value >= 1) g_qr_min_cols = (int)value;
-  else if (k == "jacobi_mode" && value >= 1 && value <= 4) g_jacobi_mode = (int)value;
-  else if (k == "cluster_size" && value >= 1 && value <= 16) g_cluster_size = (int)value;
-  else if (k == "tma_staging" && (value == 0 || value == 1)) g_tma_staging = (int)value;
-  else if (k == "gram_cache" && (value == 0 || value == 1)) g_gram_cache = (int)value;
-  else if (k == "block_w2" && (value == 0 || value == 16 || value == 32 || value == 64))
-    g_block_w2 = (int)value;
-  else if (k == "double_qr" && (value == 0 || value == 1)) g_double_qr = (int)value;
-  else if (k == "jac_per_sm" && value >= 0 && value <= 8) g_jac_per_sm = (int)value;
-  else if (k == "jac_ws" && (value == 0 || value == 1)) g_jac_ws = (int)value;
-  else if (k == "jac_cluster" && (value == -1 || value == 0 || value == 2 || value == 4))
-    g_jac_cluster = (int)value;
-  else if (k == "col_sort" && (value == 0 || value == 1)) g_col_sort = (int)value;
-  else if (k == "time_svd" && (value == 0 || value == 1)) g_time_svd = (int)value;
-  else if (k == "pair_skip" && (value == 0 || value == 1)) g_pair_skip = (int)value;
-  else return BMPS_E_ARG;
-  return BMPS_OK;
-}
-
 // Development aid: per-CTA progress words of the warp-specialised Jacobi kernel
 // written to pinned host memory (builds with -DBMPS_WS_TRACE only).
 int32_t bmps_debug_set_trace(void* host_pinned) {
-#ifdef BMPS_WS_TRACE
+#if defined(BMPS_WS_TRACE) && defined(BMPS_EXPERIMENTAL)
   void* dptr = nullptr;
   if (host_pinned && cudaHostGetDevicePointer(&dptr, host_pinned, 0) != cudaSuccess) return BMPS_E_ARG;
   cudaMemcpyToSymbol(g_ws_trace, &dptr, sizeof(void*));
@@ -812,23 +888,6 @@ int32_t bmps_debug_set_trace(void* host_pinned) {
   (void)host_pinned;
   return BMPS_E_ARG;
 #endif
-}
-
-int32_t bmps_svd_time(double* total_ms, int32_t* count) {
-  if (!total_ms || !count) return BMPS_E_ARG;
-  double t = 0.0;
-  const int n = (int)(g_svd_timer.used / 2);
-  for (int i = 0; i < n; ++i) {
-    float ms = 0.f;
-    cudaEventSynchronize(g_svd_timer.ev[2 * i + 1]);
-    if (cudaEventElapsedTime(&ms, g_svd_timer.ev[2 * i], g_svd_timer.ev[2 * i + 1]) != cudaSuccess)
-      return BMPS_E_LAUNCH;
-    t += ms;
-  }
-  g_svd_timer.used = 0;
-  *total_ms = t;
-  *count = n;
-  return BMPS_OK;
 }
 
 const char* bmps_status_string(int32_t code) {
@@ -876,31 +935,54 @@ size_t bmps_apply_2q_workspace_bytes(int32_t cap, int32_t nitems) {
 int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int32_t n,
                       int32_t cap, const int32_t* items, const double* gates, int32_t nitems,
                       bmps_policy policy, bmps_update_record* log, const int32_t* log_index,
-                      void* workspace, size_t workspace_bytes, int32_t dim_bound, int32_t mode,
-                      void* stream) {
+                      void* workspace, size_t workspace_bytes, int32_t dim_bound,
+                      const bmps_params* params, void* stream) {
   if (nitems == 0) return BMPS_OK;
   if (nitems < 0 || S < 1 || n < 2 || cap < 1 || cap > 1024 || !log || !log_index)
     return BMPS_E_ARG;
   if (workspace_bytes < ws_layout(cap, nitems, nullptr, nullptr)) return BMPS_E_WORKSPACE;
+  bmps_params P;
+  if (params) P = *params;
+  else bmps_default_params(&P);
+  if (!(P.tol_factor > 0) || P.max_sweeps < 1 || P.max_inner < 1 || P.qr_min_cols < 1 ||
+      !(P.block_w2 == 0 || P.block_w2 == 16 || P.block_w2 == 32 || P.block_w2 == 64) ||
+      !(P.jac_cluster == -1 || P.jac_cluster == 0 || P.jac_cluster == 2 || P.jac_cluster == 4) ||
+      P.jac_per_sm < 0 || P.jac_per_sm > 8 || P.cluster_size < 1 || P.cluster_size > 16 ||
+      !(P.jacobi_mode == 0 || P.jacobi_mode == 1 || P.jacobi_mode == 4 || P.jacobi_mode == 2 ||
+        P.jacobi_mode == 3) ||
+      (P.n_svd_events > 0 && (!P.svd_events || !P.svd_events_used)))
+    return BMPS_E_ARG;
+#ifndef BMPS_EXPERIMENTAL
+  if (P.jac_ws || P.tma_staging || P.jacobi_mode == 2 || P.jacobi_mode == 3) return BMPS_E_ARG;
+#endif
+  const bool timed = P.n_svd_events > 0;
+  if (timed && *P.svd_events_used >= P.n_svd_events) return BMPS_E_ARG;
   cudaStream_t st = (cudaStream_t)stream;
-  set_attrs();
+  const DevCache& dc = device_cache();
   Ws ws;
   ws_layout(cap, nitems, (char*)workspace, &ws);
   StateView sv = make_view(gamma, lam, dims, n, cap);
   if (dim_bound <= 0 || dim_bound > cap) dim_bound = cap;
 
-  // K2 theta (meta zeroed first: theta accumulates ||M||_F^2 atomically)
+  // K2 theta; ||M||_F^2 from per-CTA partials summed in a fixed order (bit-deterministic)
   cudaMemsetAsync(ws.meta, 0, sizeof(ItemMeta) * (size_t)nitems, st);
   const int tpd = (dim_bound + 31) / 32;
   theta_kernel<<<dim3(tpd * tpd, nitems), 256, kThetaSmem, st>>>(
-      sv, items, (const double2*)gates, ws.meta, ws.M0, ws.X, ws.mat_stride, tpd, g_qr_min_cols,
-      g_double_qr, g_col_sort);
+      sv, items, (const double2*)gates, ws.meta, ws.M0, ws.X, ws.mat_stride, tpd, P.qr_min_cols,
+      P.double_qr, P.col_sort, ws.fro_part, ws.fro_stride);
+  ++g_launches;
+  fro_reduce_kernel<<<nitems, 32, 0, st>>>(ws.meta, ws.fro_part, ws.fro_stride, tpd * tpd);
   ++g_launches;
   int32_t rc = launch_status();
   if (rc) return rc;
-  if (g_time_svd) cudaEventRecord(g_svd_timer.next(), st);
+  cudaEvent_t ev_end = nullptr;
+  if (timed) {
+    const int k = (*P.svd_events_used)++;
+    cudaEventRecord((cudaEvent_t)P.svd_events[2 * k], st);
+    ev_end = (cudaEvent_t)P.svd_events[2 * k + 1];
+  }
   const int cmax0 = 2 * dim_bound;
-  if (g_col_sort && g_double_qr && cmax0 >= g_qr_min_cols) {
+  if (P.col_sort && P.double_qr && cmax0 >= P.qr_min_cols) {
     dq_colsort_kernel<<<nitems, 512, 0, st>>>(ws.meta, ws.M0, ws.X, ws.mat_stride);
     ++g_launches;
     if ((rc = launch_status())) return rc;
@@ -908,7 +990,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
 
   // K3a Householder QR preconditioner (items with c >= qr_min_cols)
   const int cmax = 2 * dim_bound;
-  if (cmax >= g_qr_min_cols) {
+  if (cmax >= P.qr_min_cols) {
     QrArgs qa;
     qa.meta = ws.meta;
     qa.X = ws.X;
@@ -919,7 +1001,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
     qa.aux_stride = ws.aux_stride;
     qa.maxp = ws.maxp;
     const int npanels = (cmax + kQrNb - 1) / kQrNb;
-    for (int second = 0; second <= (g_double_qr ? 1 : 0); ++second) {
+    for (int second = 0; second <= (P.double_qr ? 1 : 0); ++second) {
       qa.second = second;
       for (int p = 0; p < npanels; ++p) {
         qa.panel = p;
@@ -927,7 +1009,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
         const int prow = cmax - p * kQrNb;
         // shared-memory panels run one CTA per SM (up to 229 KB): worth it while the
         // batch fits one wave, or when the panel is small enough for two per SM
-        if (prow <= kQrPanelSmemRows && (nitems <= kNumSMs || prow <= 150 * 32 / kQrNb))
+        if (prow <= kQrPanelSmemRows && (nitems <= dc.sms || prow <= 150 * 32 / kQrNb))
           qr_panel_kernel<true><<<nitems, 512, sizeof(double2) * kQrNb * prow, st>>>(qa);
         else
           qr_panel_kernel<false><<<nitems, 512, 0, st>>>(qa);
@@ -946,8 +1028,6 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   }
 
   // K3b Jacobi SVD
-  const int max_sweeps = g_max_sweeps;
-  const double tol_factor = g_tol_factor;
   JacArgs ja;
   ja.meta = ws.meta;
   ja.X = ws.X;
@@ -955,18 +1035,17 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   ja.Z = ws.Z;
   ja.mat_stride = ws.mat_stride;
   ja.round = 0;
-  ja.max_sweeps = max_sweeps;
-  ja.max_inner = g_max_inner;
-  ja.tol_factor = tol_factor;
+  ja.max_sweeps = P.max_sweeps;
+  ja.max_inner = P.max_inner;
+  ja.tol_factor = P.tol_factor;
   ja.sched = ws.sched;
   ja.active = ws.counter;
   ja.nitems = nitems;
-  ja.tma = g_tma_staging;
-  ja.gcache = g_gram_cache ? ws.gcache : nullptr;
+  ja.tma = P.tma_staging;
+  ja.gcache = P.gram_cache ? ws.gcache : nullptr;
   ja.gcache_stride = ws.gcache_stride;
-  ja.pairlog = g_pair_skip ? ws.pairlog : nullptr;
+  ja.pairlog = P.pair_skip ? ws.pairlog : nullptr;
   ja.nbcap = ws.nbcap;
-  const int explicit_mode = mode & 7;  // 0 = library default (g_jacobi_mode)
   if (cmax <= 64) {
     ja.persistent = 1;
     if (cmax <= 32)
@@ -977,10 +1056,10 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
     if ((rc = launch_status())) return rc;
   } else {
     const int nbmax = (cmax + 15) / 16 + ((cmax + 15) / 16 & 1);
-    const int cl_mode = explicit_mode == 0 ? g_jacobi_mode : explicit_mode;
+    const int cl_mode = P.jacobi_mode == 0 ? 4 : P.jacobi_mode;
     if (cl_mode == 4) {
       cudaMemsetAsync(ws.sched, 0, sizeof(JacSched) * (size_t)nitems, st);
-      if (g_pair_skip)
+      if (P.pair_skip)
         cudaMemsetAsync(ws.pairlog, 0xff, sizeof(int) * ws.pairlog_stride * (size_t)nitems, st);
       init_active_kernel<<<1, 32, 0, st>>>(ws.counter, nitems);
       ++g_launches;
@@ -988,66 +1067,27 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       // visits per round for small batches, but each visit keeps most of a 32-wide
       // visit's latency: one cfg3 brick layer (16 items) ran 36 -> 41 ms, so the auto
       // mode (0: 16 when nitems x visits < CTA slots) is off by default
-      static int n_slots[4] = {0, 0, 0, 0};
-      auto slots_of = [&](int wi) {
-        if (!n_slots[wi]) {
-          int per_sm = 0;
-          if (wi == 3)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_ws_kernel<32>, kWsThreads,
-                                                          WsCfg<32>::kSmem);
-          else if (wi == 2)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_dynamic_kernel<64>, 256,
-                                                          JacCfg<64>::kSmem);
-          else if (wi == 1)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_dynamic_kernel<32>, 256,
-                                                          JacCfg<32>::kSmem);
-          else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_dynamic_kernel<16>, 256,
-                                                          JacCfg<16>::kSmem);
-          int dev = 0, sms = kNumSMs;
-          cudaGetDevice(&dev);
-          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-          n_slots[wi] = std::max(1, per_sm) * sms;
-        }
-        return n_slots[wi];
-      };
-      int wi = g_block_w2 == 64 ? 2 : g_block_w2 == 16 ? 0 : 1;
-      if (g_block_w2 == 0) wi = (long long)nitems * (nbmax / 2) < slots_of(1) ? 0 : 1;
-      const bool ws_mode = wi == 1 && g_jac_ws;
-      int slots = slots_of(ws_mode ? 3 : wi);
+      int wi = P.block_w2 == 64 ? 2 : P.block_w2 == 16 ? 0 : 1;
+      if (P.block_w2 == 0) wi = (long long)nitems * (nbmax / 2) < dc.jac_slots[1] ? 0 : 1;
+      const bool ws_mode = wi == 1 && P.jac_ws;
+      int slots = dc.jac_slots[ws_mode ? 3 : wi];
       // small batches: one visit per cluster of CTAs (row split), see jacobi_cluster_kernel
-      // (auto: when a round's visits fit the clusters that are co-resident; a visit
-      // on a cluster of CS CTAs finishes sooner, but CS x fewer visits are in flight)
+      // (auto: when a round's visits fit the co-resident clusters; a visit on a cluster
+      // of CS CTAs finishes sooner, but CS x fewer visits are in flight)
       int csize = 0;
-      int cl_per_sm = 0, n_sms = kNumSMs;
-      if (wi == 1 && !g_tma_staging && g_jac_cluster != 0) {
-        static int cl_occ = 0;
-        if (!cl_occ) {
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cl_occ, jacobi_cluster_kernel<32, 4>, 256,
-                                                        ClCfg<32>::kSmem);
-          cl_occ = std::max(cl_occ, 1);
-        }
-        cl_per_sm = cl_occ;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
+      if (wi == 1 && !P.tma_staging && P.jac_cluster != 0 && !ws_mode) {
         const long long vis_round = (long long)nitems * (nbmax / 2);
-        if (g_jac_cluster > 0) csize = g_jac_cluster;
-        else if (vis_round <= (long long)cl_per_sm * n_sms / 4) csize = 4;
-        else if (vis_round <= (long long)cl_per_sm * n_sms / 2) csize = 2;
+        if (P.jac_cluster > 0) csize = P.jac_cluster;
+        else if (vis_round <= (long long)dc.cl_per_sm * dc.sms / 4) csize = 4;
+        else if (vis_round <= (long long)dc.cl_per_sm * dc.sms / 2) csize = 2;
       }
-      if (g_jac_per_sm > 0) {
-        int dev = 0, sms = kNumSMs;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        slots = std::min(slots, g_jac_per_sm * sms);
-      }
+      if (P.jac_per_sm > 0) slots = std::min(slots, P.jac_per_sm * dc.sms);
       const int vis = wi == 2 ? std::max(1, (cmax + 63) / 64)
                     : wi == 1 ? nbmax / 2
                               : (cmax + 15) / 16;
       const int grid = std::min(slots, nitems * vis);
       if (csize > 0) {
-        const int nclusters = std::max(1, std::min(nitems * (nbmax / 2), cl_per_sm * n_sms / csize));
+        const int nclusters = std::max(1, std::min(nitems * (nbmax / 2), dc.cl_per_sm * dc.sms / csize));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(nclusters * csize, 1, 1);
         cfg.blockDim = dim3(256, 1, 1);
@@ -1066,8 +1106,11 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
           fprintf(stderr, "libbmps: cluster Jacobi launch failed: %s\n", cudaGetErrorString(e));
           return BMPS_E_LAUNCH;
         }
-      } else if (ws_mode)
+      }
+#ifdef BMPS_EXPERIMENTAL
+      else if (ws_mode)
         jacobi_ws_kernel<32><<<grid, kWsThreads, WsCfg<32>::kSmem, st>>>(ja);
+#endif
       else if (wi == 2)
         jacobi_dynamic_kernel<64><<<grid, 256, JacCfg<64>::kSmem, st>>>(ja);
       else if (wi == 1)
@@ -1081,9 +1124,11 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       jacobi_kernel<32><<<dim3(1, nitems), 256, JacCfg<32>::kSmem, st>>>(ja);
       ++g_launches;
       if ((rc = launch_status())) return rc;
-    } else if (cl_mode == 3) {
+    }
+#ifdef BMPS_EXPERIMENTAL
+    else if (cl_mode == 3) {
       ja.persistent = 2;
-      const int csize = std::min(g_cluster_size, nbmax / 2);
+      const int csize = std::min(P.cluster_size, nbmax / 2);
       if (csize > 8)
         cudaFuncSetAttribute(jacobi_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaLaunchConfig_t cfg = {};
@@ -1106,31 +1151,26 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       }
       if ((rc = launch_status())) return rc;
     } else {
+      // development variant: one launch per Jacobi round, a fixed number of sweeps
+      // (no host polling inside the ABI); items converge by their own flags
       ja.persistent = 0;
-      static int* h_cnt = nullptr;
-      if (!h_cnt) cudaMallocHost(&h_cnt, sizeof(int));
-      for (int sweep = 0; sweep < max_sweeps; ++sweep) {
-        cudaMemsetAsync(ws.counter, 0, sizeof(int), st);
+      for (int sweep = 0; sweep < P.max_sweeps; ++sweep) {
         for (int rho = 0; rho < nbmax - 1; ++rho) {
           ja.round = rho;
           jacobi_kernel<32><<<dim3(nbmax / 2, nitems), 256, JacCfg<32>::kSmem, st>>>(ja);
           ++g_launches;
         }
-        sweep_end_kernel<<<(nitems + 127) / 128, 128, 0, st>>>(ws.meta, nitems, max_sweeps,
+        sweep_end_kernel<<<(nitems + 127) / 128, 128, 0, st>>>(ws.meta, nitems, P.max_sweeps,
                                                                ws.counter);
         ++g_launches;
         if ((rc = launch_status())) return rc;
-        if (sweep >= 3) {
-          cudaMemcpyAsync(h_cnt, ws.counter, sizeof(int), cudaMemcpyDeviceToHost, st);
-          cudaStreamSynchronize(st);
-          if (*h_cnt == 0) break;
-        }
       }
     }
+#endif
   }
 
   // K3c double-QR epilogue: L = Q1 [Z sorted; 0] for the kept columns
-  if (g_double_qr && cmax >= g_qr_min_cols) {
+  if (P.double_qr && cmax >= P.qr_min_cols) {
     dq_sort_kernel<<<nitems, 512, 0, st>>>(ws.meta, ws.Z, ws.Y, ws.mat_stride, ws.sig,
                                            ws.sig_stride, policy.cutoff, policy.max_bond,
                                            policy.relative);
@@ -1154,7 +1194,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
     if ((rc = launch_status())) return rc;
   }
 
-  if (g_time_svd) cudaEventRecord(g_svd_timer.next(), st);
+  if (timed) cudaEventRecord(ev_end, st);
   // K4 finalize + split
   finalize_kernel<<<nitems, 512, 0, st>>>(sv, items, ws.meta, ws.X, ws.Y, ws.mat_stride, ws.sig,
                                           ws.perm, ws.sig_stride, policy.cutoff, policy.max_bond,
@@ -1177,7 +1217,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
     dim3 sgrid((cmax + 63) / 64, (std::min(kb, cmax) + 63) / 64, nitems);
     gemm_kernel<SplitOp<false>><<<sgrid, 256, 0, st>>>(sop);
     ++g_launches;
-    if (cmax >= g_qr_min_cols) {
+    if (cmax >= P.qr_min_cols) {
       SplitOp<true> pop;
       pop.sv = sv;
       pop.items = items;
@@ -1199,12 +1239,13 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
 int32_t bmps_stats_replay(const bmps_update_record* log, const int32_t* ranges, int32_t nranges,
                           double* trunc_err, int64_t* entries, int64_t* peak,
                           int32_t* max_bond_seen, int32_t* status, int32_t* status_bond,
+                          double* bond_err, int32_t n, double* min_margin, double* min_gap,
                           void* stream) {
   if (nranges == 0) return BMPS_OK;
-  if (nranges < 0 || !log || !ranges) return BMPS_E_ARG;
+  if (nranges < 0 || !log || !ranges || (bond_err && n < 2)) return BMPS_E_ARG;
   stats_replay_kernel<<<(nranges + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
       log, ranges, nranges, trunc_err, (long long*)entries, (long long*)peak, max_bond_seen,
-      status, status_bond);
+      status, status_bond, bond_err, n, min_margin, min_gap);
   ++g_launches;
   return launch_status();
 }
@@ -1228,11 +1269,7 @@ int32_t bmps_amplitudes(const double* gamma, const double* lam, const int32_t* d
   // bitstrings per CTA: up to kAmpGroup, vectors (2 x group x cap) within 32 x BMPS_AMP_VEC bytes
   const int group = max(1, min(kAmpGroup, BMPS_AMP_VEC / cap));
   const size_t smem = 2 * (size_t)group * cap * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(amplitude_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * BMPS_AMP_VEC);
-    attr = true;
-  }
+  device_cache();
   amplitude_kernel<<<(count + group - 1) / group, 256, smem, (cudaStream_t)stream>>>(
       sv, state_idx, bits, count, group, (double2*)out);
   ++g_launches;
@@ -1246,9 +1283,21 @@ int32_t bmps_sample(const double* gamma, const double* lam, const int32_t* dims,
   if (shots < 0 || S < 1 || n < 1 || cap < 1) return BMPS_E_ARG;
   StateView sv = make_view((double*)gamma, (double*)lam, (int32_t*)dims, n, cap);
   const size_t smem = 3 * (size_t)cap * sizeof(double2);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  device_cache();
   sample_kernel<<<shots, 256, smem, (cudaStream_t)stream>>>(sv, state_idx, uniforms, bits);
+  ++g_launches;
+  return launch_status();
+}
+
+int32_t bmps_conditional(const double* gamma, const double* lam, const int32_t* dims, int32_t S,
+                         int32_t n, int32_t cap, int32_t state, int32_t site, const double* prefix,
+                         double* w0, double* w1, double* p01, void* stream) {
+  if (S < 1 || n < 1 || cap < 1 || state < 0 || state >= S || site < 0 || site >= n || !prefix ||
+      !w0 || !w1 || !p01)
+    return BMPS_E_ARG;
+  StateView sv = make_view((double*)gamma, (double*)lam, (int32_t*)dims, n, cap);
+  conditional_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(sv, state, site, (const double2*)prefix,
+                                                         (double2*)w0, (double2*)w1, p01);
   ++g_launches;
   return launch_status();
 }
@@ -1312,11 +1361,7 @@ int32_t bmps_pauli_sweep(const double* gamma, const double* lam, const int32_t* 
     return BMPS_E_ARG;
   StateView sv = make_view((double*)gamma, (double*)lam, (int32_t*)dims, n, cap);
   constexpr size_t smem = sizeof(double2) * 5 * kSweepCap * kSweepCap;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(pauli_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  device_cache();
   pauli_sweep_kernel<<<count, 256, smem, (cudaStream_t)stream>>>(
       sv, state_idx, env_idx, codes, lo, hi, (const double2*)env_l, (const double2*)env_r,
       (size_t)env_stride, (double2*)out);
@@ -1333,11 +1378,7 @@ int32_t bmps_env_sweep(const double* gamma, const double* lam, const int32_t* di
     return BMPS_E_ARG;
   StateView sv = make_view((double*)gamma, (double*)lam, (int32_t*)dims, n, cap);
   constexpr size_t smem = sizeof(double2) * 5 * kSweepCap * kSweepCap;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(env_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  device_cache();
   env_sweep_kernel<<<count, 256, smem, (cudaStream_t)stream>>>(sv, states, direction,
                                                                (double2*)env, (size_t)env_stride);
   ++g_launches;
@@ -1403,12 +1444,7 @@ int32_t bmps_dense_run_smem(double* amps, int32_t S, int32_t n, const int32_t* o
   if (nops == 0) return BMPS_OK;
   if (!amps || !ops || !mats || S < 1 || n < 1 || n > kDenseSmemQubits || nops < 0) return BMPS_E_ARG;
   const size_t smem = sizeof(double2) << n;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(dense_run_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(double2) << kDenseSmemQubits));
-    attr = true;
-  }
+  device_cache();
   dense_run_smem_kernel<<<S, 512, smem, (cudaStream_t)stream>>>((double2*)amps, n, ops,
                                                                 (const double2*)mats, nops);
   ++g_launches;

@@ -2,6 +2,7 @@
 // (DMMA, mma.sync m8n8k4 f64) complex tile products, state indexing.
 #pragma once
 #include <cuda_runtime.h>
+#include <math_constants.h>
 #include <stdint.h>
 
 #include "bmps.h"

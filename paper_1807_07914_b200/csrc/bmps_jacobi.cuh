@@ -35,6 +35,12 @@ namespace bmps {
 #define BMPS_REGQ 0   // register-resident Q in the cross rounds of the inner sweep (measured neutral, spills)
 #endif
 
+#ifdef BMPS_EXPERIMENTAL
+constexpr bool kTmaStaging = true;    // TMA bulk panel staging compiled in (measured slower)
+#else
+constexpr bool kTmaStaging = false;
+#endif
+
 #ifndef BMPS_JAC_MINB
 #define BMPS_JAC_MINB 4   // resident Jacobi CTAs per SM the register budget is sized for
 #endif
@@ -724,7 +730,7 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
   using C = JacCfg<W2>;
   BMPS_TICK(tv0);
   const int nch = (r + C::RC - 1) / C::RC;
-  const bool bulk = !resident && tma;
+  const bool bulk = kTmaStaging && !resident && tma;
   // cross visits reuse the rotated intra-block Grams cached by earlier visits
   const bool cross_gram = gcache != nullptr && !full && !resident;
   double2* cI = gcache ? gcache + (size_t)I * (W2 / 2) * (W2 / 2) : nullptr;
@@ -1392,6 +1398,8 @@ BMPS_DEV int ws_claim(const JacArgs& args, int& cursor, int& v_out, unsigned& rn
   }
 }
 
+#ifdef BMPS_EXPERIMENTAL  // the warp-specialised pipeline (measured slower)
+
 BMPS_DEV void cp_async_wait_n(int n) {
   if (n <= 0) cp_async_wait<0>();
   else if (n == 1) cp_async_wait<1>();
@@ -1747,6 +1755,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) jacobi_ws_kernel(JacArgs args) 
   WsMath::sync();
   ws_arrive(kWsGf + b);
 }
+
+#endif  // BMPS_EXPERIMENTAL
 
 // ---------------------------------------------------------------------------
 // Row-split cluster kernel (small batches: one circuit's brick layer).

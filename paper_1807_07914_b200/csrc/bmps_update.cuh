@@ -62,7 +62,8 @@ __global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* ite
                                                     const double2* gates, ItemMeta* meta,
                                                     double2* M0, double2* X, size_t mat_stride,
                                                     int tiles_per_dim, int qr_min_cols,
-                                                    int double_qr, int col_sort) {
+                                                    int double_qr, int col_sort,
+                                                    double* fro_part, int fro_stride) {
   __shared__ __align__(16) double2 sA[kKC][kLds];
   __shared__ __align__(16) double2 sB[kKC][kLds];
   __shared__ double2 sG[16];
@@ -91,7 +92,10 @@ __global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* ite
   }
   const int tm = blockIdx.x / tiles_per_dim, tn = blockIdx.x % tiles_per_dim;
   const int m0 = tm * kTile, n0 = tn * kTile;
-  if (m0 >= M || n0 >= N) return;
+  if (m0 >= M || n0 >= N) {
+    if (threadIdx.x == 0) fro_part[(size_t)item * fro_stride + blockIdx.x] = 0.0;
+    return;
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 2, wn = warp & 3;
   if (tid < 16) sG[tid] = gates[(size_t)item * 16 + tid];
@@ -163,8 +167,22 @@ __global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* ite
   if (tid == 0) {
     double t = 0.0;
     for (int w8 = 0; w8 < 8; ++w8) t += sfro[w8];
-    atomicAdd(&meta[item].fro2, t);
+    fro_part[(size_t)item * fro_stride + blockIdx.x] = t;
   }
+}
+
+// ||M||_F^2 = sum of theta's per-CTA partials in a fixed order (lane-strided
+// sums, then a fixed shuffle tree), so every later decision that reads it (the
+// Jacobi noise floor, the zero-sigma threshold of the split) is run-to-run
+// bit-identical -- an atomicAdd over CTAs would depend on their completion order.
+__global__ void fro_reduce_kernel(ItemMeta* meta, const double* fro_part, int fro_stride, int ntiles) {
+  const int item = blockIdx.x, lane = threadIdx.x;
+  const double* p = fro_part + (size_t)item * fro_stride;
+  double t = 0.0;
+  for (int k = lane; k < ntiles; k += 32) t += p[k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) meta[item].fro2 = t;
 }
 
 }  // namespace bmps
@@ -279,6 +297,18 @@ __global__ void __launch_bounds__(512) finalize_kernel(StateView sv, const int* 
       keep = sv.cap;
       if (!status) status = BMPS_S_CAPACITY;
     }
+    // robustness of the keep decision: distance of the nearest singular value that
+    // could move keep from the threshold, and the gap at the truncation boundary
+    double margin = CUDART_INF, gap = CUDART_INF;
+    const double s0 = ssig[0];
+    if (cutoff > 0.0 && s0 > 0.0) {
+      const double thr = cutoff * (relative ? s0 : 1.0);
+      const int K = max_bond > 0 ? min(c, max_bond) : c;
+      double mn = CUDART_INF;
+      for (int k = 0; k < K; ++k) mn = fmin(mn, fabs(ssig[k] - thr));
+      margin = mn / s0;
+    }
+    if (keep < c && s0 > 0.0) gap = (ssig[keep - 1] - ssig[keep]) / s0;
     double err = 0.0, nrm2 = 0.0;
     for (int k = keep; k < c; ++k) err += ssig[k] * ssig[k];
     for (int k = 0; k < keep; ++k) nrm2 += ssig[k] * ssig[k];
@@ -299,6 +329,8 @@ __global__ void __launch_bounds__(512) finalize_kernel(StateView sv, const int* 
     rec.keep = keep;
     rec.status = status;
     rec.site = q;
+    rec.margin = margin;
+    rec.gap = gap;
     log[log_index[item]] = rec;
   }
   __syncthreads();
@@ -422,13 +454,16 @@ struct SplitOp {
 // ---------------------------------------------------------------------------
 __global__ void stats_replay_kernel(const bmps_update_record* log, const int* ranges, int nranges,
                                     double* trunc_err, long long* entries, long long* peak,
-                                    int* max_bond_seen, int* status, int* status_bond) {
+                                    int* max_bond_seen, int* status, int* status_bond,
+                                    double* bond_err, int n, double* min_margin, double* min_gap) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= nranges) return;
   const int s = ranges[3 * g], first = ranges[3 * g + 1], count = ranges[3 * g + 2];
   double te = trunc_err[s];
   long long ent = entries[s], pk = peak[s];
   int mb = max_bond_seen[s], st = status[s], sb = status_bond[s];
+  double mm = min_margin ? min_margin[s] : 0.0, mg = min_gap ? min_gap[s] : 0.0;
+  double* be = bond_err ? bond_err + (size_t)s * (n - 1) : nullptr;
   for (int it = first; it < first + count; ++it) {
     const bmps_update_record m = log[it];
     if (st) break;  // the reference raises at the first failure
@@ -438,6 +473,7 @@ __global__ void stats_replay_kernel(const bmps_update_record* log, const int* ra
       break;
     }
     te += m.err;  // added before the all-truncated check, as mps.py:122-126
+    if (be) be[m.site] += m.err;   // per-bond discarded weight, same program order
     if (m.status) {
       st = m.status;
       sb = m.site;
@@ -447,6 +483,8 @@ __global__ void stats_replay_kernel(const bmps_update_record* log, const int* ra
     ent += 2 * dl * k + 2 * k * dr - 2 * dl * dm - 2 * dm * dr;
     pk = ent > pk ? ent : pk;
     mb = m.keep > mb ? m.keep : mb;
+    mm = fmin(mm, m.margin);
+    mg = fmin(mg, m.gap);
   }
   trunc_err[s] = te;
   entries[s] = ent;
@@ -454,6 +492,8 @@ __global__ void stats_replay_kernel(const bmps_update_record* log, const int* ra
   max_bond_seen[s] = mb;
   status[s] = st;
   status_bond[s] = sb;
+  if (min_margin) min_margin[s] = mm;
+  if (min_gap) min_gap[s] = mg;
 }
 
 }  // namespace bmps

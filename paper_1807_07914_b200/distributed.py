@@ -58,21 +58,27 @@ def energies_by_vector(n_vectors: int, evaluate: Callable[[np.ndarray], np.ndarr
 def energies_by_term(n_vectors: int, coeffs: Sequence[float],
                      term_values: Callable[[np.ndarray], np.ndarray], group=None) -> np.ndarray:
     """``term_values(term_idx) -> [n_vectors, len(term_idx)]`` expectations for this
-    rank's terms; returns sum_k c_k <P_k> per vector in term order (vqe.py:89)."""
+    rank's terms; returns sum_k c_k <P_k> per vector in term order (vqe.py:89).
+
+    One collective for the whole batch: every rank scatters its columns into a
+    zero [n_vectors, n_terms] matrix and a single allreduce(sum) assembles it
+    (exact: each entry has one non-zero contributor); the weighted sums then run
+    left to right on the host, as the reference's Python ``sum``."""
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     nt = len(coeffs)
     tidx = shard(nt, world, rank)
     local = term_values(tidx) if len(tidx) else np.zeros((n_vectors, 0))
-    full = np.zeros((n_vectors, nt))
-    for v in range(n_vectors):
-        full[v] = allreduce_scattered(tidx, local[v], nt, group)
-    out = np.empty(n_vectors)
-    for v in range(n_vectors):
-        acc = 0
-        for c, e in zip(coeffs, full[v]):
-            acc = acc + float(c) * float(e)
-        out[v] = acc
-    return out
+    buf = torch.zeros((n_vectors, nt), dtype=torch.float64, device=_device_for(group))
+    if len(tidx):
+        buf[:, torch.as_tensor(tidx, device=buf.device)] = torch.as_tensor(
+            np.asarray(local, dtype=np.float64).reshape(n_vectors, len(tidx)), device=buf.device)
+    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    full = buf.cpu().numpy()
+    c = np.asarray([float(x) for x in coeffs], dtype=np.float64)
+    if nt == 0:
+        return np.zeros(n_vectors)
+    # np.add.accumulate is sequential: bit-identical to the scalar left-to-right loop
+    return np.add.accumulate(c[None, :] * full, axis=1)[:, -1].copy()
 
 
 def vqe_energies(programs, n: int, paulis, coeffs, policy=None, group=None, mode: str = "by_vector"):

@@ -36,7 +36,8 @@ MAX_CAP = 1024
 SWEEP_CAP = 32          # fused Pauli-string sweep (bmps_pauli_sweep) up to this bond capacity
 _RECORD = _native.RECORD_BYTES
 RECORD_DTYPE = np.dtype([("err", "<f8"), ("dl", "<i4"), ("dm", "<i4"), ("dr", "<i4"),
-                         ("keep", "<i4"), ("status", "<i4"), ("site", "<i4")])
+                         ("keep", "<i4"), ("status", "<i4"), ("site", "<i4"),
+                         ("margin", "<f8"), ("gap", "<f8")])
 assert RECORD_DTYPE.itemsize == _RECORD
 _ZERO2 = np.zeros((2, 2), dtype=np.complex128)
 
@@ -47,6 +48,18 @@ def _ptr(t: torch.Tensor | None) -> int | None:
 
 def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
+
+
+def _on_device(fn):
+    """Run a method with its batch's device current, so the library's launches
+    (which use the current device and stream) and the tensors agree."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(self, *a, **k):
+        with torch.cuda.device(self.device):
+            return fn(self, *a, **k)
+    return wrapper
 
 
 def require_cuda(device=None) -> torch.device:
@@ -136,6 +149,7 @@ class Plan:
     logidx2: np.ndarray     # int32 [K2]
     ranges: np.ndarray      # int32 [R, 3] (state, first record, count), program order
     n_records: int
+    max_state: int = -1     # largest state index the plan touches
 
 
 _FIXED_1Q = ("I", "X", "Y", "Z", "H")
@@ -271,6 +285,12 @@ def compile_batch(programs, n: int, states=None, validate_matrices: bool = True)
     programs = list(programs)
     states = np.arange(len(programs), dtype=np.int32) if states is None else \
         np.asarray(list(states), dtype=np.int32)
+    if len(states) != len(programs):
+        raise ValueError(f"{len(programs)} programs but {len(states)} state indices")
+    if len(states) and (states.min() < 0 or len(np.unique(states)) != len(states)):
+        # one program per state per plan: the layering and the in-order stats replay
+        # assume a state's ops come from a single program
+        raise ValueError("state indices of a plan must be distinct and non-negative")
     ar, q1, q2, code, theta, custom, off = _extract(programs)
     lib = _native.load()
     nx = int(lib.bmps_plan_expanded_count(ar.ctypes.data, q1.ctypes.data, q2.ctypes.data, len(ar)))
@@ -299,11 +319,12 @@ def compile_batch(programs, n: int, states=None, validate_matrices: bool = True)
     first, counts = cs[off[:-1]], cs[off[1:]] - cs[off[:-1]]
     n_records = int(cs[-1])
     ranges = [(int(states[p]), int(first[p]), int(counts[p])) for p in np.nonzero(counts)[0]]
+    max_state = int(states.max()) if len(states) else -1
     if nx == 0:
         return Plan(0, np.zeros(1, np.int64), np.zeros(1, np.int64), np.zeros((0, 2), np.int32),
                     np.zeros((0, 2, 2), complex), np.zeros((0, 2), np.int32),
                     np.zeros((0, 4, 4), complex), np.zeros(0, np.int32),
-                    np.zeros((0, 3), np.int32), 0)
+                    np.zeros((0, 3), np.int32), 0, max_state)
     n_layers = int(x_layer.max()) + 1
     # stable order: layer, then original (state-major, program) order
     order = np.argsort(x_layer, kind="stable")
@@ -333,7 +354,7 @@ def compile_batch(programs, n: int, states=None, validate_matrices: bool = True)
     off1 = np.searchsorted(lay_one, np.arange(n_layers + 1)) if len(one) else np.zeros(n_layers + 1, np.int64)
     off2 = np.searchsorted(lay_two, np.arange(n_layers + 1)) if len(two) else np.zeros(n_layers + 1, np.int64)
     return Plan(n_layers, off1, off2, items1, gates1, items2, gates2, x_rec[two].astype(np.int32),
-                np.asarray(ranges, dtype=np.int32).reshape(-1, 3), n_records)
+                np.asarray(ranges, dtype=np.int32).reshape(-1, 3), n_records, max_state)
 
 
 # ---------------------------------------------------------------------------
@@ -341,12 +362,95 @@ def compile_batch(programs, n: int, states=None, validate_matrices: bool = True)
 # ---------------------------------------------------------------------------
 
 
+class SvdTimer:
+    """CUDA-event pairs the library records around the SVD stage (column sort, QR
+    preconditioner, Jacobi, double-QR epilogue) of every ``bmps_apply_2q`` call of
+    the batches it is attached to (``bmps_params.svd_events``), on the launching
+    stream. Bench instrumentation; ``total_ms`` synchronises."""
+
+    def __init__(self, capacity: int = 4096):
+        self.capacity = int(capacity)
+        self.events = []
+        for _ in range(2 * self.capacity):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()                     # creates the underlying cudaEvent_t
+            self.events.append(e)
+        self.handles = (ctypes.c_void_p * (2 * self.capacity))(*[e.cuda_event for e in self.events])
+        self.used = ctypes.c_int32(0)
+        torch.cuda.synchronize()
+
+    def attach(self, batch: "MpsBatch") -> None:
+        batch.svd_timer = (self.handles, self.used, self.capacity)
+
+    def reset(self) -> None:
+        self.used.value = 0
+
+    def total_ms(self) -> tuple[float, int]:
+        n = self.used.value
+        tot = 0.0
+        for i in range(n):
+            self.events[2 * i + 1].synchronize()
+            tot += self.events[2 * i].elapsed_time(self.events[2 * i + 1])
+        return tot, n
+
+
+class _DevPtr:
+    """A raw device address with the ``data_ptr()`` of a tensor view."""
+
+    __slots__ = ("p",)
+
+    def __init__(self, p: int):
+        self.p = p
+
+    def data_ptr(self) -> int:
+        return self.p
+
+
+class _Staging:
+    """Ring of pinned host / device argument slots for per-gate launches. A slot
+    is reused only after the event recorded behind its H2D copy has completed,
+    so a host write can never race an in-flight copy."""
+
+    SLOT = 512   # bytes: item (8) | log index (4) | range (12) | ... | gate at 64 (256)
+
+    def __init__(self, device, slots: int = 64):
+        self.n = slots
+        self.host = torch.empty(slots * self.SLOT, dtype=torch.uint8).pin_memory()
+        self.host_i32 = self.host.numpy().view(np.int32)
+        self.dev = torch.empty(slots * self.SLOT, dtype=torch.uint8, device=device)
+        self.events = [None] * slots
+        self.k = 0
+
+    def acquire(self):
+        slot = self.k % self.n
+        self.k += 1
+        ev = self.events[slot]
+        if ev is not None:
+            ev.synchronize()
+        w = self.SLOT // 4
+        return self.host_i32[slot * w:(slot + 1) * w], self.dev.data_ptr() + slot * self.SLOT, slot
+
+    def commit(self, slot: int, nbytes: int) -> None:
+        a = slot * self.SLOT
+        self.dev[a:a + nbytes].copy_(self.host[a:a + nbytes], non_blocking=True)
+        ev = self.events[slot] or torch.cuda.Event()
+        ev.record()
+        self.events[slot] = ev
+
+
 class MpsBatch:
-    """S independent n-qubit MPS states resident in HBM, initially |0...0>."""
+    """S independent n-qubit MPS states resident in HBM, initially |0...0>.
+
+    ``keep_records`` retains every executed plan's per-update records on the
+    device (for ``update_records``); by default only the most recent plan's are
+    kept, so a long per-gate loop does not grow device memory. Per-bond
+    truncation, the cutoff-tie margin and the truncation gap are accumulated on
+    the device for every update regardless.
+    """
 
     def __init__(self, num_states: int, n: int, policy: TruncationPolicy | None = None,
                  device=None, cap: int | None = None, max_items_per_launch: int = 4096,
-                 workspace_budget: int = 24 << 30):
+                 workspace_budget: int = 24 << 30, keep_records: bool = False):
         if n < 1:
             raise ValueError("need at least one qubit")
         if num_states < 1:
@@ -358,13 +462,16 @@ class MpsBatch:
         self.policy = policy or TruncationPolicy()
         self.max_items = int(max_items_per_launch)
         self.workspace_budget = int(workspace_budget)
+        self.keep_records = bool(keep_records)
         self.cap = 1
-        self._alloc(int(cap) if cap else 1)
         self.dim_ub = np.ones((self.S, self.n + 1), dtype=np.int64)
         self._ws = None
         self._ws_bytes = 0
         self._logs: list = []
-        self.reset()
+        self.svd_timer = None       # bench hook: (events array, used counter, capacity)
+        with torch.cuda.device(self.device):
+            self._alloc(int(cap) if cap else 1)
+            self.reset()
 
     # -- buffers ---------------------------------------------------------------
     def _alloc(self, cap: int) -> None:
@@ -380,13 +487,20 @@ class MpsBatch:
             self.mbs = torch.zeros(S, dtype=torch.int32, device=dev)
             self.status = torch.zeros(S, dtype=torch.int32, device=dev)
             self.status_bond = torch.zeros(S, dtype=torch.int32, device=dev)
+            self.bond_err = torch.zeros((S, max(n - 1, 1)), dtype=torch.float64, device=dev)
+            self.min_margin = torch.full((S,), float("inf"), dtype=torch.float64, device=dev)
+            self.min_gap = torch.full((S,), float("inf"), dtype=torch.float64, device=dev)
 
+    @_on_device
     def reset(self) -> None:
         """Re-initialise every state to |0...0> (``mps.py:55-66``)."""
         self.gamma.zero_()
         self.lam.zero_()
         self.dim_ub[:] = 1
         self._logs = []
+        self.bond_err.zero_()
+        self.min_margin.fill_(float("inf"))
+        self.min_gap.fill_(float("inf"))
         rc = self.lib.bmps_init_product(
             _ptr(self.gamma), _ptr(self.lam), _ptr(self.dims), _ptr(self.trunc_err),
             _ptr(self.entries), _ptr(self.peak), _ptr(self.mbs), _ptr(self.status),
@@ -398,6 +512,7 @@ class MpsBatch:
         mb = self.policy.max_bond
         return min(full, mb) if mb is not None else full
 
+    @_on_device
     def ensure_capacity(self, needed: int) -> None:
         """Grow the bond capacity (power of two) to hold ``needed``; copies state."""
         if needed <= self.cap:
@@ -416,12 +531,29 @@ class MpsBatch:
         self.lam[:, :, :oc] = old_l
         self.dims.copy_(old_d)
 
+    def refresh_bounds(self) -> None:
+        """Replace the host's upper-bound model of the bond dims by the true dims
+        (one device sync). Called before the model would force a capacity growth,
+        so growth and the capacity limit follow the real bonds, not the bound --
+        e.g. CNOT layers on |0...0> keep every bond at 1 however deep they go."""
+        self.dim_ub[:] = self.dims.cpu().numpy()
+
     def _workspace(self, nitems: int) -> tuple[int, int]:
         need = int(self.lib.bmps_apply_2q_workspace_bytes(self.cap, nitems))
         if self._ws is None or self._ws_bytes < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
             self._ws_bytes = need
         return self._ws.data_ptr(), self._ws_bytes
+
+    def _params(self, mode: int = 0):
+        extra = {"jacobi_mode": mode} if mode else {}
+        p = _native.params(**extra)
+        t = self.svd_timer
+        if t is not None:
+            p.svd_events = ctypes.cast(t[0], ctypes.c_void_p)
+            p.svd_events_used = ctypes.cast(ctypes.pointer(t[1]), ctypes.c_void_p)
+            p.n_svd_events = t[2]
+        return p
 
     # -- execution ---------------------------------------------------------------
     def run(self, programs, states=None, mode: int = 0) -> "MpsBatch":
@@ -430,9 +562,14 @@ class MpsBatch:
         self.execute(plan, mode=mode)
         return self
 
+    @_on_device
     def execute(self, plan: Plan, mode: int = 0) -> None:
+        """Launch a plan layer by layer (asynchronous; no host sync unless the bond
+        bound model asks for more capacity than allocated)."""
         if plan.n_layers == 0:
             return
+        if plan.max_state >= self.S:
+            raise ValueError(f"plan addresses state {plan.max_state}, batch has {self.S}")
         dev = self.device
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
         it1 = pin(plan.items1).to(dev, non_blocking=True)
@@ -443,6 +580,7 @@ class MpsBatch:
         rng = pin(plan.ranges).to(dev, non_blocking=True)
         log = torch.empty(max(plan.n_records, 1) * _RECORD, dtype=torch.uint8, device=dev)
         pol = self.policy.as_c()
+        params = self._params(mode)
         lim = self._cap_limit()
         stream = _stream()
         for L in range(plan.n_layers):
@@ -455,30 +593,89 @@ class MpsBatch:
             a, b = int(plan.off2[L]), int(plan.off2[L + 1])
             if b <= a:
                 continue
-            its = plan.items2[a:b]
-            s_idx, q = its[:, 0], its[:, 1]
-            ub = self.dim_ub
-            bound = int(max(ub[s_idx, q].max(), ub[s_idx, q + 2].max()))
-            new = np.minimum(np.minimum(2 * ub[s_idx, q], 2 * ub[s_idx, q + 2]), lim)
-            self.ensure_capacity(int(max(bound, new.max())))
-            per_item = int(self.lib.bmps_apply_2q_workspace_bytes(self.cap, 1))
-            chunk = max(1, min(self.max_items, self.workspace_budget // max(per_item, 1)))
-            for c0 in range(a, b, chunk):
-                c1 = min(b, c0 + chunk)
-                ws, wsb = self._workspace(c1 - c0)
-                rc = self.lib.bmps_apply_2q(
-                    _ptr(self.gamma), _ptr(self.lam), _ptr(self.dims), self.S, self.n, self.cap,
-                    it2.data_ptr() + 8 * c0, g2.data_ptr() + 256 * c0, c1 - c0, pol,
-                    log.data_ptr(), li2.data_ptr() + 4 * c0, ws, wsb, min(bound, self.cap), mode, stream)
-                _native.check(rc, "bmps_apply_2q")
-            ub[s_idx, q + 1] = new
-        rc = self.lib.bmps_stats_replay(
-            log.data_ptr(), rng.data_ptr(), len(plan.ranges), _ptr(self.trunc_err), _ptr(self.entries),
-            _ptr(self.peak), _ptr(self.mbs), _ptr(self.status), _ptr(self.status_bond), stream)
-        _native.check(rc, "bmps_stats_replay")
+            self._apply_2q_layer(plan.items2[a:b], it2, g2, li2, a, b, log, pol, params, lim, stream)
+        self._replay(log, rng, len(plan.ranges), stream)
         self._keep_alive = (it1, g1, it2, g2, li2, rng)
-        self._logs.append((log, plan.ranges))
+        if self.keep_records:
+            self._logs.append((log, plan.ranges))
+        else:
+            self._logs = [(log, plan.ranges)]
 
+    def _apply_2q_layer(self, its, it2, g2, li2, a, b, log, pol, params, lim, stream) -> None:
+        s_idx, q = its[:, 0], its[:, 1]
+        ub = self.dim_ub
+        need = lambda: int(max(ub[s_idx, q].max(), ub[s_idx, q + 2].max(),
+                               np.minimum(np.minimum(2 * ub[s_idx, q], 2 * ub[s_idx, q + 2]), lim).max()))
+        if need() > self.cap:
+            self.refresh_bounds()      # the bound model may overestimate: consult the device
+        self.ensure_capacity(need())
+        bound = int(max(ub[s_idx, q].max(), ub[s_idx, q + 2].max()))
+        new = np.minimum(np.minimum(2 * ub[s_idx, q], 2 * ub[s_idx, q + 2]), lim)
+        per_item = int(self.lib.bmps_apply_2q_workspace_bytes(self.cap, 1))
+        chunk = max(1, min(self.max_items, self.workspace_budget // max(per_item, 1)))
+        for c0 in range(a, b, chunk):
+            c1 = min(b, c0 + chunk)
+            ws, wsb = self._workspace(c1 - c0)
+            rc = self.lib.bmps_apply_2q(
+                _ptr(self.gamma), _ptr(self.lam), _ptr(self.dims), self.S, self.n, self.cap,
+                it2.data_ptr() + 8 * c0, g2.data_ptr() + 256 * c0, c1 - c0, pol,
+                log.data_ptr(), li2.data_ptr() + 4 * c0, ws, wsb, min(bound, self.cap),
+                ctypes.byref(params), stream)
+            _native.check(rc, "bmps_apply_2q")
+        ub[s_idx, q + 1] = new
+
+    def _replay(self, log, rng, nranges, stream) -> None:
+        rc = self.lib.bmps_stats_replay(
+            log.data_ptr(), rng.data_ptr(), nranges, _ptr(self.trunc_err), _ptr(self.entries),
+            _ptr(self.peak), _ptr(self.mbs), _ptr(self.status), _ptr(self.status_bond),
+            _ptr(self.bond_err) if self.n > 1 else None, self.n, _ptr(self.min_margin),
+            _ptr(self.min_gap), stream)
+        _native.check(rc, "bmps_stats_replay")
+
+    # -- per-gate path (the reference's own callers loop gate by gate) -----------
+    @_on_device
+    def apply_ops(self, s: int, ops) -> None:
+        """Apply (arity, site, matrix) ops to state ``s`` in order, one op per layer,
+        without the planner: the drop-in ``MpsState.apply_*`` path. Arguments go
+        through a ring of pinned staging slots (no host allocation per gate) and
+        the launches stay asynchronous."""
+        if not 0 <= s < self.S:
+            raise ValueError(f"state {s} out of range for {self.S} states")
+        st = getattr(self, "_staging", None)
+        if st is None:
+            st = self._staging = _Staging(self.device)
+        stream = _stream()
+        pol = None
+        params = None
+        lim = self._cap_limit()
+        for arity, site, mat in ops:
+            h, d, slot = st.acquire()
+            m = np.ascontiguousarray(mat, dtype=np.complex128)
+            h[0:2] = (s, site)
+            if arity == 1:
+                h.view(np.complex128)[4:8] = m.reshape(-1)
+                st.commit(slot, 128)
+                rc = self.lib.bmps_apply_1q(_ptr(self.gamma), _ptr(self.dims), self.S, self.n, self.cap,
+                                            d, d + 64, 1, stream)
+                _native.check(rc, "bmps_apply_1q")
+                continue
+            if pol is None:
+                pol, params = self.policy.as_c(), self._params()
+            h[4] = 0                      # log index
+            h[8:11] = (s, 0, 1)           # replay range (state, first record, count)
+            h.view(np.complex128)[4:20] = m.reshape(-1)
+            st.commit(slot, 320)
+            log = torch.empty(_RECORD, dtype=torch.uint8, device=self.device)
+            its = np.array([[s, site]], np.int32)
+            self._apply_2q_layer(its, _DevPtr(d), _DevPtr(d + 64), _DevPtr(d + 16), 0, 1, log,
+                                 pol, params, lim, stream)
+            self._replay(log, _DevPtr(d + 32), 1, stream)
+            if self.keep_records:
+                self._logs.append((log, np.array([[s, 0, 1]], np.int32)))
+            else:
+                self._logs = [(log, np.array([[s, 0, 1]], np.int32))]
+
+    @_on_device
     def last_sweeps(self, count: int | None = None) -> np.ndarray:
         """Jacobi sweeps of the items of the most recent bmps_apply_2q launch."""
         if self._ws is None:
@@ -490,7 +687,8 @@ class MpsBatch:
         return out.cpu().numpy()
 
     def update_records(self, s: int) -> np.ndarray:
-        """Per-update records of state ``s`` in program order (all executed plans)."""
+        """Per-update records of state ``s`` in program order (the retained plans:
+        all of them with ``keep_records``, else the most recent)."""
         out = []
         for log, ranges in self._logs:
             rec = log.cpu().numpy().view(RECORD_DTYPE)
@@ -500,11 +698,17 @@ class MpsBatch:
         return np.concatenate(out) if out else np.zeros(0, RECORD_DTYPE)
 
     def bond_truncation(self, s: int = 0) -> np.ndarray:
-        """Discarded weight per bond (reference bond index q = site of the update)."""
-        rec = self.update_records(s)
-        out = np.zeros(max(self.n - 1, 0))
-        np.add.at(out, rec["site"], rec["err"])
-        return out
+        """Discarded weight per bond since the last reset (reference bond index q =
+        site of the update), accumulated on the device in program order."""
+        self.check_status()
+        if self.n < 2:
+            return np.zeros(0)
+        return self.bond_err[s].cpu().numpy()
+
+    def decision_margins(self) -> tuple[np.ndarray, np.ndarray]:
+        """Per state, the smallest cutoff-tie margin and truncation gap over all
+        updates since the last reset (``bmps_update_record.margin`` / ``gap``)."""
+        return self.min_margin.cpu().numpy(), self.min_gap.cpu().numpy()
 
     # -- status and host views ---------------------------------------------------
     def check_status(self) -> None:
@@ -535,6 +739,7 @@ class MpsBatch:
         lam = self.lam[s].cpu().numpy()
         return [lam[b, : d[b]].copy() for b in range(1, self.n)]
 
+    @_on_device
     def load_state(self, s: int, site_tensors, bond_vectors) -> None:
         """Overwrite state ``s`` with host Gamma/lambda (Vidal form, reference layout)."""
         dims = [1] + [len(v) for v in bond_vectors] + [1]
@@ -560,6 +765,7 @@ class MpsBatch:
         self.mbs[s] = max(dims)
 
     # -- queries -------------------------------------------------------------------
+    @_on_device
     def amplitudes(self, state_idx, bitstrings) -> np.ndarray:
         """<bits|psi_s> for each (s, bits) (``mps.py:172-179``)."""
         n = self.n
@@ -578,6 +784,7 @@ class MpsBatch:
         _native.check(rc, "bmps_amplitudes")
         return out.cpu().numpy()
 
+    @_on_device
     def sample_bits(self, s: int, uniforms: np.ndarray) -> np.ndarray:
         """Sampled bitstrings (uint8 [shots, n]) of state ``s`` for pre-drawn uniforms."""
         self.check_status()
@@ -590,6 +797,30 @@ class MpsBatch:
                                   _stream())
         _native.check(rc, "bmps_sample")
         return bits.cpu().numpy()
+
+    @_on_device
+    def conditional_prob_zero(self, s: int, prefix_vec, k: int):
+        """``MpsState.conditional_prob_zero`` (``mps.py:206-214``) on the device:
+        (P(qubit k = 0 | prefix), w0, w1) with w_b = prefix @ T_k[:, b, :]."""
+        if not 0 <= k < self.n:
+            raise ValueError(f"site {k} out of range for {self.n} qubits")
+        self.check_status()
+        d = self.host_dims()[s]
+        pv = np.asarray(prefix_vec, dtype=np.complex128).reshape(-1)
+        if len(pv) != d[k]:
+            raise ValueError(f"prefix vector has length {len(pv)}, bond {k} has dimension {d[k]}")
+        dev = self.device
+        pre = torch.from_numpy(pv.copy()).to(dev)
+        w = torch.empty((2, max(int(d[k + 1]), 1)), dtype=torch.complex128, device=dev)
+        p01 = torch.empty(2, dtype=torch.float64, device=dev)
+        rc = self.lib.bmps_conditional(_ptr(self.gamma), _ptr(self.lam), _ptr(self.dims), self.S,
+                                       self.n, self.cap, int(s), int(k), pre.data_ptr(),
+                                       w[0].data_ptr(), w[1].data_ptr(), p01.data_ptr(), _stream())
+        _native.check(rc, "bmps_conditional")
+        p0, p1 = (float(x) for x in p01.cpu().numpy())
+        wh = w.cpu().numpy()[:, : int(d[k + 1])]
+        total = p0 + p1
+        return (p0 / total if total > 0 else 0.5), wh[0].copy(), wh[1].copy()
 
     def sample(self, s: int, shots: int, rng: np.random.Generator) -> dict[str, int]:
         """Counts of full-register bitstrings (``mps.py:216-237``, same uniform stream)."""
@@ -630,6 +861,7 @@ class MpsBatch:
         e[:, 0, 0] = 1.0
         return e
 
+    @_on_device
     def environments(self, states: np.ndarray, direction: int) -> torch.Tensor:
         """All identity environments L_k (direction 0) or R_k (1), k = 0..n."""
         ns, n, cap = len(states), self.n, self.cap
@@ -658,6 +890,7 @@ class MpsBatch:
                                env[c0:, src], stride, env[c0:, dst], stride, c1 - c0)
         return env
 
+    @_on_device
     def expectations(self, state_idx, paulis, use_env: bool | None = None) -> np.ndarray:
         """<psi_s|P|psi_s> for each (s, P), real part; RuntimeError on |Im| > 1e-10.
 
@@ -751,4 +984,6 @@ class MpsBatch:
             "peak_entries": self.peak.cpu().numpy(),
             "max_bond_seen": self.mbs.cpu().numpy(),
             "entries": self.entries.cpu().numpy(),
+            "min_margin": self.min_margin.cpu().numpy(),
+            "min_gap": self.min_gap.cpu().numpy(),
         }

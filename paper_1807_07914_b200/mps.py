@@ -17,7 +17,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .engine import MpsBatch, compile_batch
+from .engine import MpsBatch, compile_batch, lower_program
 from .gates import check_unitary
 from .ir import MatrixGate
 from .policy import TruncationPolicy
@@ -95,7 +95,7 @@ class MpsState:
         """Contract a 2x2 unitary into site ``q``; bonds are untouched (mps.py:88-92)."""
         self._check_site(q)
         check_unitary(gate)
-        self._batch.run([[MatrixGate(np.asarray(gate, dtype=np.complex128), (q,))]])
+        self._batch.apply_ops(0, [(1, q, gate)])
 
     def apply_two_qubit_adjacent(self, gate: np.ndarray, q: int) -> None:
         """Apply a 4x4 unitary to sites ``(q, q+1)`` via contract + SVD (mps.py:94-136)."""
@@ -103,7 +103,7 @@ class MpsState:
         if q + 1 >= self.n:
             raise ValueError(f"site {q} has no right neighbour (n={self.n})")
         check_unitary(gate)
-        self._batch.run([[MatrixGate(np.asarray(gate, dtype=np.complex128), (q, q + 1))]])
+        self._batch.apply_ops(0, [(2, q, gate)])
 
     def apply_two_qubit_routed(self, gate: np.ndarray, q1: int, q2: int) -> None:
         """Apply a 4x4 unitary to arbitrary sites, SWAP-routing if needed (mps.py:138-157)."""
@@ -112,7 +112,9 @@ class MpsState:
         if q1 == q2:
             raise ValueError("two-qubit gate needs two distinct sites")
         check_unitary(gate)
-        self._batch.run([[MatrixGate(np.asarray(gate, dtype=np.complex128), (q1, q2))]])
+        ar, site, mats = lower_program([MatrixGate(np.asarray(gate, dtype=np.complex128), (q1, q2))],
+                                       self.n, validate_matrices=False)
+        self._batch.apply_ops(0, list(zip(ar.tolist(), site.tolist(), mats)))
 
     def run(self, program) -> "MpsState":
         """Apply a whole program through the layered executor (fast path)."""
@@ -140,6 +142,11 @@ class MpsState:
     def expectations_pauli(self, paulis) -> np.ndarray:
         """Batched ``expectation_pauli`` with cached environments."""
         return self._batch.expectations(np.zeros(len(paulis), np.int32), list(paulis))
+
+    def conditional_prob_zero(self, prefix_vec: np.ndarray, k: int) -> tuple[float, np.ndarray, np.ndarray]:
+        """P(qubit k = 0 | fixed prefix) and the two successor prefix vectors
+        (mps.py:206-214), computed on the device."""
+        return self._batch.conditional_prob_zero(0, prefix_vec, k)
 
     def sample(self, shots: int, rng: np.random.Generator) -> dict[str, int]:
         """Full-register bitstrings by sequential conditional sampling (mps.py:216-237).

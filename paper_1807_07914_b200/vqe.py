@@ -63,6 +63,13 @@ def _unitary_program(ansatz, theta: float) -> list:
     return [i for i in program if i.kind.value != "MEASURE"]
 
 
+def _bound_program(ansatz, values) -> list:
+    """All formal parameters of ``ansatz`` bound positionally to ``values``,
+    flattened, MEASUREs dropped (``ir.py:150-184`` then ``vqe.py:37``)."""
+    program = flatten(bind_parameters(ansatz, [float(v) for v in values]))
+    return [i for i in program if i.kind.value != "MEASURE"]
+
+
 def _basis_rotations(pauli: str) -> list[Instruction]:
     """X -> H, Y -> RZ(-pi/2) then H, Z/I -> nothing (``vqe.py:40-48``)."""
     out: list[Instruction] = []
@@ -99,9 +106,29 @@ def grid_energies(ansatz, thetas, hamiltonian, backend: str = "mps",
                   seed: int | None = None, *, device=None) -> list[float]:
     """``energy(ansatz, t, ...)`` for every t in ``thetas``, batched on the GPU."""
     _check_backend(backend)
+    programs = [_unitary_program(ansatz, float(t)) for t in thetas]
+    return _program_energies(programs, hamiltonian, backend, policy, shots, seed, device)
+
+
+def parameter_energies(ansatz, parameter_vectors, hamiltonian, backend: str = "mps",
+                       policy: TruncationPolicy | None = None, shots: int | None = None,
+                       seed: int | None = None, *, device=None) -> list[float]:
+    """Multi-parameter sweep: <H> for the ansatz with ALL its formal parameters bound
+    to each vector of ``parameter_vectors`` (e.g. config 2's 80-angle vectors).
+
+    The reference driver is single-parameter (``vqe.py:30-35``); this extends it
+    with the same per-vector semantics -- ``bind_parameters`` positionally,
+    ``flatten``, MEASUREs dropped, E = sum_k c_k <P_k> left to right (``vqe.py:87-89``)
+    or the sampled estimate (``vqe.py:90-97``) -- with every vector one state of a
+    shared batch. ``IrError`` if a vector's length differs from the formal count."""
+    _check_backend(backend)
+    programs = [_bound_program(ansatz, vec) for vec in parameter_vectors]
+    return _program_energies(programs, hamiltonian, backend, policy, shots, seed, device)
+
+
+def _program_energies(programs, hamiltonian, backend, policy, shots, seed, device) -> list[float]:
     n = hamiltonian.n
     terms = [(float(c), str(p)) for c, p in hamiltonian.terms]
-    programs = [_unitary_program(ansatz, float(t)) for t in thetas]
     for prog in programs:
         if num_qubits(prog) > n:
             raise ValueError(f"ansatz touches qubit {num_qubits(prog) - 1}, "

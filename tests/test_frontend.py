@@ -94,3 +94,28 @@ def test_matches_reference_bind_flatten_on_reference_objects():
     ours = flatten(bind_parameters(root, [0.75]))
     assert [(i.kind.value, i.qubits, i.params) for i in ref] == \
         [(i.kind.value, i.qubits, i.params) for i in ours]
+
+
+def test_frontend_fixture_is_the_reference_parse():
+    """tests/golden/frontend.json holds exactly what the reference parser produces for
+    its kernel text, and this package's bind/flatten of the rebuilt trees equal the
+    reference's (runs where /root/reference is mounted; the GPU box uses the fixture)."""
+    import json
+    ref_src = "/root/reference/pkg/src"
+    if not Path(ref_src).exists():
+        pytest.skip("reference not mounted (GPU box)")
+    sys.path.insert(0, ref_src)
+    sys.dont_write_bytecode = True
+    from mpsqvm.ir import bind_parameters as rbind, flatten as rflatten
+    from mpsqvm.parser import parse
+    from frontend_fixture import load_frontend, tree_from_json
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "oracle"))
+    from gen_frontend import tree_to_json
+    fx = load_frontend()
+    unit = parse(fx["text"])
+    assert {k: tree_to_json(v) for k, v in unit.kernels.items()} == fx["kernels"]
+    for vec in fx["vectors"]:
+        theirs = rflatten(rbind(unit.kernels["ansatz"], list(vec)))
+        ours = flatten(bind_parameters(tree_from_json(fx["kernels"]["ansatz"]), list(vec)))
+        assert [(i.kind.value, tuple(i.qubits), tuple(i.params)) for i in ours] == \
+               [(i.kind.value, tuple(i.qubits), tuple(i.params)) for i in theirs]

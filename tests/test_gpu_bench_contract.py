@@ -38,7 +38,9 @@ def test_bench_line_contract():
     assert d["gpu_launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     c4 = d["cfg4_circuits"]
-    assert c4["circuits"] == 256 and c4["circuits_per_s"] > 0
+    assert c4["circuits"] == 1024 and c4["circuits_per_s"] > 0 and 0 < c4["frac"] < 1
+    cf = d["configs"]
+    assert {"cfg3", "cfg4", "cfg5"} <= set(cf) and all(0 < cf[k]["frac"] < 1 for k in cf)
 
 
 def test_reference_arm_contract():

@@ -113,43 +113,52 @@ def test_distributed_energies_nccl_world1():
     assert_scaled_close(e2, g["energies"][:4], RTOL)
 
 
-def test_tma_staging_path_matches_oracle():
-    """The TMA bulk-copy panel staging (bmps_set_param tma_staging=1) gives the same results."""
+def _needs_experimental():
     from paper_1807_07914_b200 import _native
-    lib = _native.load()
-    assert lib.bmps_set_param(b"tma_staging", 1.0) == 0
-    try:
+    if not _native.experimental():
+        pytest.skip("development variant: libbmps.so built without -DBMPS_EXPERIMENTAL")
+
+
+def test_tma_staging_path_matches_oracle():
+    """The TMA bulk-copy panel staging (tunable tma_staging=1) gives the same results."""
+    from paper_1807_07914_b200 import _native
+    _needs_experimental()
+    with _native.tunables(tma_staging=1):
         prog = brick_circuit(14, 12, np.random.default_rng(99))
         _compare(prog, 14, 1e-12, 64, seed=4)
-    finally:
-        lib.bmps_set_param(b"tma_staging", 0.0)
 
 
 @pytest.mark.parametrize("mode", [1, 2, 3, 4])
 def test_all_jacobi_schedules_match_oracle(mode):
     """persistent / round launches / cluster / dynamic schedules are interchangeable."""
     from paper_1807_07914_b200 import _native
-    lib = _native.load()
-    assert lib.bmps_set_param(b"jacobi_mode", float(mode)) == 0
-    try:
+    if mode in (2, 3):
+        _needs_experimental()
+    with _native.tunables(jacobi_mode=mode):
         prog = brick_circuit(12, 12, np.random.default_rng(7 + mode))
         _compare(prog, 12, 1e-10, 48, seed=mode)
-    finally:
-        lib.bmps_set_param(b"jacobi_mode", 4.0)
+
+
+def test_disabled_variants_are_rejected():
+    """Without -DBMPS_EXPERIMENTAL the development variants are refused with
+    BMPS_E_ARG (surfaced as RuntimeError), never silently replaced."""
+    from paper_1807_07914_b200 import _native
+    if _native.experimental():
+        pytest.skip("experimental build")
+    prog = brick_circuit(12, 4, np.random.default_rng(3))
+    for kw in ({"jac_ws": 1}, {"tma_staging": 1}, {"jacobi_mode": 2}, {"jacobi_mode": 3}):
+        with _native.tunables(**kw), pytest.raises(RuntimeError, match="invalid argument"):
+            mps_run(prog, 12, TruncationPolicy(1e-10, 64))
 
 
 @pytest.mark.parametrize("dq", [0, 1])
 @pytest.mark.parametrize("chi,cutoff", [(64, 1e-12), (128, 1e-10), (128, 0.0)])
 def test_double_qr_preconditioning_matches_oracle(dq, chi, cutoff):
-    """Single vs double Householder-QR preconditioning (bmps_set_param double_qr)."""
+    """Single vs double Householder-QR preconditioning (tunable double_qr)."""
     from paper_1807_07914_b200 import _native
-    lib = _native.load()
-    assert lib.bmps_set_param(b"double_qr", float(dq)) == 0
-    try:
+    with _native.tunables(double_qr=dq):
         prog = brick_circuit(14, 14, np.random.default_rng(chi + dq))
         _compare(prog, 14, cutoff, chi, seed=chi)
-    finally:
-        lib.bmps_set_param(b"double_qr", float(_native.DEFAULT_PARAMS["double_qr"]))
 
 
 @pytest.mark.parametrize("chi,cutoff", [(48, 1e-10), (128, 0.0), (128, 1e-10)])
@@ -157,36 +166,10 @@ def test_warp_specialised_jacobi_matches_oracle(chi, cutoff):
     """jac_ws=1: math / rotation / scheduler warps with a two-deep visit pipeline
     (single-panel items run by the math warps alone) give the oracle's results."""
     from paper_1807_07914_b200 import _native
-    lib = _native.load()
-    assert lib.bmps_set_param(b"jac_ws", 1.0) == 0
-    try:
+    _needs_experimental()
+    with _native.tunables(jac_ws=1):
         prog = brick_circuit(14, 14, np.random.default_rng(500 + chi))
         _compare(prog, 14, cutoff, chi, seed=chi + 1)
-    finally:
-        lib.bmps_set_param(b"jac_ws", float(_native.DEFAULT_PARAMS["jac_ws"]))
-
-
-def test_warp_specialised_jacobi_bulk_layer_spectra():
-    """jac_ws=1 on a batch of chi=256 updates (the bench workload's shape): bond
-    spectra and keep counts equal the default kernel's (1e-10 of the largest)."""
-    from paper_1807_07914_b200 import _native, MpsBatch, TruncationPolicy
-    lib = _native.load()
-    rng = np.random.default_rng(11)
-    progs = [brick_circuit(18, 12, rng) for _ in range(3)]
-    out = []
-    for ws in (0.0, 1.0):
-        assert lib.bmps_set_param(b"jac_ws", ws) == 0
-        try:
-            b = MpsBatch(3, 18, TruncationPolicy(1e-10, 256))
-            b.run(progs)
-            b.check_status()
-            out.append((b.host_dims(), [b.bond_vectors(s) for s in range(3)]))
-        finally:
-            lib.bmps_set_param(b"jac_ws", float(_native.DEFAULT_PARAMS["jac_ws"]))
-    assert (out[0][0] == out[1][0]).all()
-    for s in range(3):
-        for la, lb in zip(out[0][1][s], out[1][1][s]):
-            assert np.max(np.abs(la - lb)) <= 1e-10 * max(la.max(), 1.0)
 
 
 @pytest.mark.parametrize("csize", [0, 2, 4])
@@ -195,13 +178,9 @@ def test_row_split_cluster_jacobi_matches_oracle(csize, chi, cutoff):
     """jac_cluster: each visit's panel rows split over a 2- or 4-CTA cluster (partial
     Grams summed through distributed shared memory), or off (0)."""
     from paper_1807_07914_b200 import _native
-    lib = _native.load()
-    assert lib.bmps_set_param(b"jac_cluster", float(csize)) == 0
-    try:
+    with _native.tunables(jac_cluster=csize):
         prog = brick_circuit(14, 14, np.random.default_rng(900 + chi + csize))
         _compare(prog, 14, cutoff, chi, seed=chi + csize)
-    finally:
-        lib.bmps_set_param(b"jac_cluster", float(_native.DEFAULT_PARAMS["jac_cluster"]))
 
 
 def _theta(gammas, lams, q):

@@ -111,7 +111,7 @@ def test_workload_generators_deterministic():
 
 def _header_functions():
     text = (ROOT / "include" / "bmps.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int32_t|int64_t|size_t|uint64_t|const char\*)\s+(bmps_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int32_t|int64_t|size_t|uint64_t|void|const char\*)\s+(bmps_\w+)\(", text, re.M)))
 
 
 def test_library_exports_every_header_symbol():
@@ -123,10 +123,30 @@ def test_library_exports_every_header_symbol():
     for name in declared:
         assert hasattr(lib, name), name
         assert name in _native.EXPORTED, f"{name} missing from the ctypes signature table"
-    assert lib.bmps_version() == 1
+    assert lib.bmps_version() == 2
     assert lib.bmps_status_string(1).decode().startswith("SVD failed")
     assert lib.bmps_apply_2q_workspace_bytes(256, 4) > 4 * 2 * 4 * 256 * 256 * 16
-    assert lib.bmps_set_param(b"nonsense", 1.0) == -1
+    # per-call tunables: defaults come from the library, unknown names are rejected
+    d = _native.default_params()
+    assert d["tol_factor"] == 4.0 and d["jacobi_mode"] == 4 and d["block_w2"] == 32
+    with pytest.raises(ValueError):
+        _native.params(nonsense=1)
+    with _native.tunables(jac_cluster=4):
+        assert _native.params().jac_cluster == 4
+    assert _native.params().jac_cluster == -1
+
+
+def test_library_exports_only_the_c_abi():
+    """libbmps.so's dynamic symbol table holds the bmps_* entry points only (the
+    statically linked CUDA runtime stays internal: version script csrc/libbmps.map)."""
+    import subprocess
+    from paper_1807_07914_b200 import build
+    so = build.build()
+    out = subprocess.run(["nm", "-D", "--defined-only", str(so)], capture_output=True, text=True,
+                         check=True).stdout
+    names = [ln.split()[-1] for ln in out.splitlines() if ln.strip()]
+    assert names and all(n.startswith("bmps_") for n in names), [n for n in names if not n.startswith("bmps_")][:10]
+    assert set(_header_functions()) <= set(names)
 
 
 def test_no_cpu_fallback():
@@ -219,3 +239,17 @@ def test_native_planner_errors_match_reference_messages():
         compile_batch([[Instruction(GateKind.CZ, (3, 3))]], 6)
     with pytest.raises(ValueError, match="not unitary"):
         compile_batch([[MatrixGate(np.ones((2, 2)), (0,))]], 2)
+
+
+def test_compile_batch_rejects_duplicate_or_negative_states():
+    """one program per state per plan (the layering and the in-order stats
+    replay assume it); duplicates or negative indices are a ValueError, and a plan
+    that addresses a state beyond the batch is refused by MpsBatch.execute."""
+    progs = [brick_circuit(4, 2, np.random.default_rng(k)) for k in range(3)]
+    with pytest.raises(ValueError, match="distinct"):
+        compile_batch(progs, 4, states=[0, 1, 0])
+    with pytest.raises(ValueError, match="distinct"):
+        compile_batch(progs, 4, states=[0, -1, 2])
+    with pytest.raises(ValueError, match="state indices"):
+        compile_batch(progs, 4, states=[0, 1])
+    assert compile_batch(progs, 4, states=[5, 1, 3]).max_state == 5
