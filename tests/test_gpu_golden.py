@@ -140,8 +140,10 @@ def test_cfg4_all_circuits():
     assert_scaled_close(zz, g["zz"], RTOL, "cfg4 <Z0 Z31>")
     sidx = np.repeat(np.arange(cnt, dtype=np.int32), 16)
     amps = b.amplitudes(sidx, [bits for c in range(cnt) for bits in w.bitstrings[c]]).reshape(cnt, 16)
-    for c in range(cnt):   # scaled per circuit (each circuit is its own output set)
-        assert_scaled_close(amps[c], g["amps"][c], RTOL, f"cfg4 amplitudes circuit {c}")
+    # the scale is max|ref| over the config's output set (all 16 x 1024
+    # amplitudes; a single circuit's 16 amplitudes can all be ~2^-16, where 1e-10 of
+    # them is below the double-precision floor of a unit-norm state)
+    assert_scaled_close(amps, g["amps"], RTOL, "cfg4 amplitudes")
     np.testing.assert_array_equal(b.host_dims()[:, 1:w.n], g["dims"])
     st = b.stats()
     np.testing.assert_allclose(st["trunc_error_sq"], g["trunc_error_sq"], rtol=1e-10)
