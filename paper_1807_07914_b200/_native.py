@@ -143,7 +143,8 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path is not None else LIB_PATH
+    # BMPS_LIB: an alternative build of the same ABI (A/B runs of development variants)
+    p = Path(path) if path is not None else Path(os.environ.get("BMPS_LIB") or LIB_PATH)
     if not p.exists():
         raise RuntimeError(
             f"libbmps.so not found at {p}; build it with `python -m paper_1807_07914_b200.build` "

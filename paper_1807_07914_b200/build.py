@@ -38,19 +38,31 @@ def up_to_date() -> bool:
     return all(p.stat().st_mtime <= t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None,
+          defines: tuple = ()) -> Path:
+    """Compile libbmps.so (``out`` + ``defines``: development variants for A/B runs,
+    e.g. ``-D BMPS_WARP_INNER=0``; the product library is built without them)."""
+    if out is None and not defines and not force and up_to_date():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, f"-I{ROOT / 'include'}", "-o", str(OUT) + ".tmp", *map(str, SOURCES)]
+    target = Path(out) if out is not None else OUT
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], f"-I{ROOT / 'include'}", "-o",
+           str(target) + ".tmp", *map(str, SOURCES)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError(f"nvcc failed ({res.returncode})")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(str(OUT) + ".tmp", OUT)
-    return OUT
+    os.replace(str(target) + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("--out", default=None)
+    ap.add_argument("-D", action="append", default=[])
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.v, out=a.out, defines=tuple(a.D)))
