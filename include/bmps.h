@@ -131,6 +131,8 @@ typedef struct bmps_params {
   int32_t jac_ws;        /* warp-specialised Jacobi (BMPS_EXPERIMENTAL only) (0) */
   int32_t tma_staging;   /* TMA bulk panel staging (BMPS_EXPERIMENTAL only) (0) */
   int32_t cluster_size;  /* CTAs per item in mode 3 (8) */
+  int32_t qr_cluster;    /* QR panels taller than 384 rows on a row-split cluster when
+                            the batch is small (2 x items <= SMs) (1) */
   int32_t n_svd_events;  /* capacity of svd_events in event pairs (0: no timing) */
   void** svd_events;     /* host array of 2*n_svd_events cudaEvent_t: the call records
                             a pair bracketing its SVD stage (column sort, QR

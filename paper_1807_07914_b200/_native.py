@@ -36,7 +36,8 @@ class BmpsParams(ctypes.Structure):
                 ("gram_cache", ctypes.c_int32), ("pair_skip", ctypes.c_int32),
                 ("jac_cluster", ctypes.c_int32), ("jac_per_sm", ctypes.c_int32),
                 ("jac_ws", ctypes.c_int32), ("tma_staging", ctypes.c_int32),
-                ("cluster_size", ctypes.c_int32), ("n_svd_events", ctypes.c_int32),
+                ("cluster_size", ctypes.c_int32), ("qr_cluster", ctypes.c_int32),
+                ("n_svd_events", ctypes.c_int32),
                 ("svd_events", ctypes.c_void_p), ("svd_events_used", ctypes.c_void_p)]
 
 
@@ -90,7 +91,7 @@ _lib = None
 # mutable state: each call gets its own bmps_params)
 TUNABLES = ("tol_factor", "max_sweeps", "max_inner", "qr_min_cols", "jacobi_mode", "block_w2",
             "double_qr", "col_sort", "gram_cache", "pair_skip", "jac_cluster", "jac_per_sm",
-            "jac_ws", "tma_staging", "cluster_size")
+            "jac_ws", "tma_staging", "cluster_size", "qr_cluster")
 _overrides: dict = {}
 
 

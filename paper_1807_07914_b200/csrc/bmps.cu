@@ -761,6 +761,12 @@ const DevCache& device_cache() {
   cudaFuncSetAttribute(qr_panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(sizeof(double2) * kQrNb * kQrPanelSmemRows));
   cudaFuncSetAttribute(dq_apply_q1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQ1Smem);
+  cudaFuncSetAttribute(qr_panel_cluster_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(sizeof(double2) * kQrNb * kQrClusterRows));
+  cudaFuncSetAttribute(qr_panel_cluster_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(sizeof(double2) * kQrNb * kQrClusterRows));
+  cudaFuncSetAttribute(qr_panel_cluster_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(sizeof(double2) * kQrNb * kQrClusterRows));
   cudaFuncSetAttribute(jacobi_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)JacCfg<32>::kSmem);
   cudaFuncSetAttribute(jacobi_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -860,6 +866,7 @@ void bmps_default_params(bmps_params* p) {
   p->jac_ws = 0;
   p->tma_staging = 0;
   p->cluster_size = 8;
+  p->qr_cluster = 1;
   p->n_svd_events = 0;
   p->svd_events = nullptr;
   p->svd_events_used = nullptr;
@@ -1009,10 +1016,36 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
         const int prow = cmax - p * kQrNb;
         // shared-memory panels run one CTA per SM (up to 229 KB): worth it while the
         // batch fits one wave, or when the panel is small enough for two per SM
-        if (prow <= kQrPanelSmemRows && (nitems <= dc.sms || prow <= 150 * 32 / kQrNb))
+        if (prow > kQrPanelSmemRows && P.qr_cluster && 2 * nitems <= dc.sms) {
+          // tall panel, few items: row slices over a cluster, each resident in its CTA's
+          // shared memory (measured: cfg3 / cfg5 -1.5% time; with hundreds of items one
+          // CTA per item streaming from L2 keeps more SMs busy: bench 917 vs 909 updates/s)
+          const int cs = prow <= 2 * kQrClusterRows ? 2 : prow <= 4 * kQrClusterRows ? 4 : 8;
+          const int sl = (prow + cs - 1) / cs;
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3(nitems * cs, 1, 1);
+          cfg.blockDim = dim3(512, 1, 1);
+          cfg.dynamicSmemBytes = sizeof(double2) * kQrNb * sl;
+          cfg.stream = st;
+          cudaLaunchAttribute attr[1];
+          attr[0].id = cudaLaunchAttributeClusterDimension;
+          attr[0].val.clusterDim.x = cs;
+          attr[0].val.clusterDim.y = 1;
+          attr[0].val.clusterDim.z = 1;
+          cfg.attrs = attr;
+          cfg.numAttrs = 1;
+          const cudaError_t e = cs == 2 ? cudaLaunchKernelEx(&cfg, qr_panel_cluster_kernel<2>, qa)
+                              : cs == 4 ? cudaLaunchKernelEx(&cfg, qr_panel_cluster_kernel<4>, qa)
+                                        : cudaLaunchKernelEx(&cfg, qr_panel_cluster_kernel<8>, qa);
+          if (e != cudaSuccess) {
+            fprintf(stderr, "libbmps: cluster QR panel launch failed: %s\n", cudaGetErrorString(e));
+            return BMPS_E_LAUNCH;
+          }
+        } else if (prow <= kQrPanelSmemRows && (nitems <= dc.sms || prow <= 150 * 32 / kQrNb)) {
           qr_panel_kernel<true><<<nitems, 512, sizeof(double2) * kQrNb * prow, st>>>(qa);
-        else
+        } else {
           qr_panel_kernel<false><<<nitems, 512, 0, st>>>(qa);
+        }
         ++g_launches;
         const int trail = cmax - (p + 1) * kQrNb;
         if (trail > 0) {

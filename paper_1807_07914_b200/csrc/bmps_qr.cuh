@@ -16,6 +16,8 @@
 // P_k = I - conj(tau_k) v_k v_k^H with v_k[k] = 1 (LAPACK zlarfg convention:
 // H_k^H x = beta e_1, beta real).
 #pragma once
+#include <cooperative_groups.h>
+
 #include "bmps_common.cuh"
 
 namespace bmps {
@@ -102,6 +104,67 @@ BMPS_DEV double block_sum(double v, double* red) {
   return t;
 }
 
+// S = V^H V of a factored panel (Householder vectors below the diagonal of A's
+// columns j0..j1-1, rows [j0, r), global memory) and the T factor of its compact WY
+// form. 512 threads.
+BMPS_DEV void panel_build_t(const double2* A, int r, int j0, int j1, const double2* tau, double2* T) {
+  __shared__ double2 s_S[kQrNb][kQrNb];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // V^H V on DMMA (v_k[k] = 1, zero above k): 32-row chunks of V
+  // staged in shared memory, warp w accumulates 8x8 tile (w / 4, w % 4)
+  const int nbp = j1 - j0;
+  {
+    __shared__ double2 sVc[32][kQrNb + 1];
+    double sacc[4] = {0.0, 0.0, 0.0, 0.0};
+    const int kr = lane & 3, rc = lane >> 2;
+    const int ti = warp >> 2, tj = warp & 3;   // 512 threads: 16 warps cover 4 x 4 tiles
+    const bool own = ti < kQrNb / 8 && tj < kQrNb / 8;
+    // chunk loader: element i of the 32-row chunk at rb (each thread owns the same
+    // elements of every chunk: 32 x kQrNb <= 2 x 512); the next chunk is loaded into
+    // registers while the current one is multiplied
+    constexpr int kPer = (32 * kQrNb + 511) / 512;
+    auto vload = [&](int rb, int u) -> double2 {
+      const int i = tid + u * 512;
+      const int row = i % 32, p = i / 32;
+      const int gr = rb + row, k = j0 + p;
+      double2 v = make_double2(0.0, 0.0);
+      if (i < 32 * kQrNb && p < nbp && gr < r) {
+        if (gr == k) v = make_double2(1.0, 0.0);
+        else if (gr > k) v = A[(size_t)k * r + gr];
+      }
+      return v;
+    };
+    double2 vnext[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) vnext[u] = vload(j0, u);
+    for (int rb = j0; rb < r; rb += 32) {
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int i = tid + u * 512;
+        if (i < 32 * kQrNb) sVc[i % 32][i / 32] = vnext[u];
+      }
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) vnext[u] = rb + 32 < r ? vload(rb + 32, u) : make_double2(0.0, 0.0);
+      __syncthreads();
+      if (own) {
+#pragma unroll
+        for (int k4 = 0; k4 < 8; ++k4) {
+          const int k = k4 * 4 + kr;
+          zmma(sacc, cconj(sVc[k][ti * 8 + rc]), sVc[k][tj * 8 + rc]);
+        }
+      }
+      __syncthreads();
+    }
+    if (own) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        s_S[ti * 8 + rc][tj * 8 + kr * 2 + h] = make_double2(sacc[h], sacc[2 + h]);
+    }
+    __syncthreads();
+  }
+  if (warp == 0) build_t(T, &s_S[0][0], kQrNb, tau + j0, nbp);
+}
+
 // SMEM = true: the panel's rows [j0, r) are staged in shared memory for the
 // factorization (every column step then costs shared-memory instead of L2
 // round trips: ~4x faster for these latency-bound launches); the arithmetic and
@@ -116,7 +179,6 @@ constexpr int kQrPanelU = BMPS_QR_PANEL_U;
 template <bool SMEM>
 __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
   __shared__ double red[16];
-  __shared__ double2 s_S[kQrNb][kQrNb];
   extern __shared__ __align__(16) double2 spanel[];
   const int item = blockIdx.x;
   const ItemMeta* m = a.meta + item;
@@ -224,59 +286,123 @@ __global__ void __launch_bounds__(512) qr_panel_kernel(QrArgs a) {
     }
     __syncthreads();
   }
-  // S = V^H V for the panel on DMMA (v_k[k] = 1, zero above k): 32-row chunks of V
-  // staged in shared memory, warp w accumulates 8x8 tile (w / 4, w % 4)
-  const int nbp = j1 - j0;
-  {
-    __shared__ double2 sVc[32][kQrNb + 1];
-    double sacc[4] = {0.0, 0.0, 0.0, 0.0};
-    const int kr = lane & 3, rc = lane >> 2;
-    const int ti = warp >> 2, tj = warp & 3;   // 512 threads: 16 warps cover 4 x 4 tiles
-    const bool own = ti < kQrNb / 8 && tj < kQrNb / 8;
-    // chunk loader: element i of the 32-row chunk at rb (each thread owns the same
-    // elements of every chunk: 32 x kQrNb <= 2 x 512); the next chunk is loaded into
-    // registers while the current one is multiplied
-    constexpr int kPer = (32 * kQrNb + 511) / 512;
-    auto vload = [&](int rb, int u) -> double2 {
-      const int i = tid + u * 512;
-      const int row = i % 32, p = i / 32;
-      const int gr = rb + row, k = j0 + p;
-      double2 v = make_double2(0.0, 0.0);
-      if (i < 32 * kQrNb && p < nbp && gr < r) {
-        if (gr == k) v = make_double2(1.0, 0.0);
-        else if (gr > k) v = A[(size_t)k * r + gr];
-      }
-      return v;
-    };
-    double2 vnext[kPer];
+  panel_build_t(A, r, j0, j1, tau, T);
+}
+
+// Tall panels (rows [j0, r) beyond kQrPanelSmemRows): one thread-block cluster of CS
+// CTAs per item, CTA q staging the contiguous row slice q of the panel in its own
+// shared memory (<= kQrClusterRows rows, 128 KB), so no column step ever goes to L2
+// -- one CTA streaming a 2048-row panel from L2 reached ~75 GB/s and left 100 of
+// 148 SMs idle on config 5's ~50-item layers. Per column step k (2 cluster barriers):
+//   1. every CTA writes its partial ||x[k+1:]||^2 to shared memory; barrier; every
+//      CTA sums the CS partials in rank order (bit-identical in all CTAs) and reads
+//      alpha = x[k] from the owner of row k through DSMEM -> the same reflector
+//      (beta, tau, scale) everywhere;
+//   2. each CTA scales its rows, then writes its partial dots v^H x_j of the panel's
+//      remaining columns; barrier; rank-ordered sums -> f_j = conj(tau) w_j, and
+//      each CTA updates its own rows.
+// Same Householder algorithm as qr_panel_kernel (zlarfg convention); the
+// reductions run in a different, fixed order (deterministic). Rank 0 then forms
+// S = V^H V and T from the written-back panel.
+constexpr int kQrClusterRows = 256;
+template <int CS>
+__global__ void __launch_bounds__(512, 1) qr_panel_cluster_kernel(QrArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ double red[16];
+  __shared__ double2 part[kQrNb + 1];   // [0].x: norm partial; [1 + t]: dot partial of column k + 1 + t
+  extern __shared__ __align__(16) double2 spanel[];
+  const int rank = (int)cl.block_rank();
+  const int item = blockIdx.x / CS;
+  const ItemMeta* m = a.meta + item;
+  double2* A;
+  double2* tau;
+  int r;
+  const bool active = qr_pass(a, item, A, r, tau);
+  const int c = active ? m->c : 0;
+  const int j0 = a.panel * kQrNb;
+  // inactive items still take part in every cluster barrier (all CTAs of a cluster agree)
+  const bool work = active && j0 < c;
+  const int j1 = work ? min(j0 + kQrNb, c) : j0;
+  const int rows = work ? r - j0 : 0;
+  const int sl = (rows + CS - 1) / CS;            // rows per slice
+  const int lo = j0 + rank * sl, hi = min(j0 + (rank + 1) * sl, j0 + rows);   // my rows [lo, hi)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // staged column k holds my rows at spanel[(k - j0) * sl + (i - lo)]
+  for (int idx = tid; idx < (j1 - j0) * sl; idx += blockDim.x) {
+    const int kk = idx / sl, i = lo + idx % sl;
+    if (i < hi) spanel[idx] = A[(size_t)(j0 + kk) * r + i];
+  }
+  __syncthreads();
+  auto colp = [&](int k) -> double2* { return spanel + (size_t)(k - j0) * sl - lo; };
+  for (int k = j0; k < j1; ++k) {
+    double2* col = colp(k);
+    const int owner = (k - j0) / sl;
+    double s = 0.0;
+    for (int i = max(k + 1, lo) + tid; i < hi; i += blockDim.x) s += cabs2(col[i]);
+    s = block_sum(s, red);
+    if (tid == 0) part[0] = make_double2(s, 0.0);
+    cl.sync();
+    double xnorm2 = 0.0;
 #pragma unroll
-    for (int u = 0; u < kPer; ++u) vnext[u] = vload(j0, u);
-    for (int rb = j0; rb < r; rb += 32) {
+    for (int q = 0; q < CS; ++q) xnorm2 += cl.map_shared_rank(part, q)[0].x;
+    // x[k] in the owner's slice (its rows start at j0 + owner * sl)
+    const double2 alpha =
+        cl.map_shared_rank(spanel, owner)[(size_t)(k - j0) * sl + (k - (j0 + owner * sl))];
+    double2 t = make_double2(0.0, 0.0);
+    double2 scale = make_double2(0.0, 0.0);
+    double beta = alpha.x;
+    if (xnorm2 > 0.0 || alpha.y != 0.0) {
+      const double nrm = sqrt(cabs2(alpha) + xnorm2);
+      beta = alpha.x >= 0.0 ? -nrm : nrm;
+      t = make_double2((beta - alpha.x) / beta, -alpha.y / beta);
+      const double2 d = make_double2(alpha.x - beta, alpha.y);
+      const double inv = 1.0 / cabs2(d);
+      scale = make_double2(d.x * inv, -d.y * inv);
+    }
+    for (int i = max(k + 1, lo) + tid; i < hi; i += blockDim.x) col[i] = cmul(col[i], scale);
+    __syncthreads();   // every CTA has read the owner's alpha (cluster barrier below orders the write)
+    const bool rot = t.x != 0.0 || t.y != 0.0;
+    // partial dots of the reflector with columns k+1 .. j1-1 (one warp per column)
+    for (int jj = k + 1 + warp; jj < j1; jj += blockDim.x >> 5) {
+      const double2* cj = colp(jj);
+      double2 w = make_double2(0.0, 0.0);
+      if (rot) {
+        if (lane == 0 && owner == rank) w = cj[k];
+        for (int i = max(k + 1, lo) + lane; i < hi; i += 32) w = cfma(cconj(col[i]), cj[i], w);
 #pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int i = tid + u * 512;
-        if (i < 32 * kQrNb) sVc[i % 32][i / 32] = vnext[u];
-      }
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) vnext[u] = rb + 32 < r ? vload(rb + 32, u) : make_double2(0.0, 0.0);
-      __syncthreads();
-      if (own) {
-#pragma unroll
-        for (int k4 = 0; k4 < 8; ++k4) {
-          const int k = k4 * 4 + kr;
-          zmma(sacc, cconj(sVc[k][ti * 8 + rc]), sVc[k][tj * 8 + rc]);
+        for (int o = 16; o > 0; o >>= 1) {
+          w.x += __shfl_xor_sync(0xffffffffu, w.x, o);
+          w.y += __shfl_xor_sync(0xffffffffu, w.y, o);
         }
       }
-      __syncthreads();
+      if (lane == 0) part[1 + (jj - k - 1)] = w;
     }
-    if (own) {
+    cl.sync();   // partial dots visible; the owner's alpha read by everyone
+    if (owner == rank && tid == 0) {
+      col[k] = make_double2(beta, 0.0);
+      tau[k] = t;
+    }
+    for (int jj = k + 1 + warp; jj < j1 && rot; jj += blockDim.x >> 5) {
+      double2 w = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
-        s_S[ti * 8 + rc][tj * 8 + kr * 2 + h] = make_double2(sacc[h], sacc[2 + h]);
+      for (int q = 0; q < CS; ++q) w = cadd(w, cl.map_shared_rank(part, q)[1 + (jj - k - 1)]);
+      const double2 f = cmul(cconj(t), w);
+      double2* cj = colp(jj);
+      if (lane == 0 && owner == rank) cj[k] = csub(cj[k], f);
+      for (int i = max(k + 1, lo) + lane; i < hi; i += 32) cj[i] = csub(cj[i], cmul(col[i], f));
     }
+    // part[] is rewritten in the next step only after its first cluster barrier, which
+    // every CTA reaches after finishing these reads; local rows need a CTA barrier
     __syncthreads();
   }
-  if (warp == 0) build_t(T, &s_S[0][0], kQrNb, tau + j0, nbp);
+  for (int idx = tid; idx < (j1 - j0) * sl; idx += blockDim.x) {
+    const int kk = idx / sl, i = lo + idx % sl;
+    if (i < hi) A[(size_t)(j0 + kk) * r + i] = spanel[idx];
+  }
+  __threadfence();
+  cl.sync();   // the whole panel is back in global memory
+  if (rank == 0 && work) panel_build_t(A, r, j0, j1, tau, qr_tslot(a, tau));
 }
 
 // Compact-WY application to one 64-column chunk of A (rows [j0, r), ld r):

@@ -191,10 +191,19 @@ def _theta(gammas, lams, q):
     return np.einsum("l,lsm,m,mtr,r->lstr", lam_l, gammas[q], lams[q], gammas[q + 1], lam_r, optimize=True)
 
 
-def test_chi256_updates_on_cfg3_steady_state_match_oracle():
+@pytest.mark.parametrize("qr_cluster", [1, 0])
+def test_chi256_updates_on_cfg3_steady_state_match_oracle(qr_cluster):
     """The bench's unit of work at full size: chi = 256 CNOT updates (512 x 512 theta,
     keep 256 of 512) on a GPU-evolved cfg3 state (50 qubits, 25 layers), against the
-    oracle applied to the same tensors: new bond vector and the two-site tensor."""
+    oracle applied to the same tensors: new bond vector and the two-site tensor.
+    The 512-row QR panels run on 2-CTA row-split clusters (qr_cluster=1, default) or
+    one CTA streaming from L2 (0)."""
+    from paper_1807_07914_b200 import _native
+    with _native.tunables(qr_cluster=qr_cluster):
+        _chi256_steady_state_case()
+
+
+def _chi256_steady_state_case():
     import bench
     from paper_1807_07914_b200.ir import GateKind, Instruction
     st = mps_run(bench.prefix_program(1003, 25), bench.N_QUBITS, TruncationPolicy(bench.CUTOFF, bench.CHI))
