@@ -31,9 +31,6 @@ namespace bmps {
 #ifndef BMPS_CLAIM_SLEEP_NS
 #define BMPS_CLAIM_SLEEP_NS 2000   // dynamic Jacobi: back-off of a CTA that found no open visit
 #endif
-#ifndef BMPS_REGQ
-#define BMPS_REGQ 0   // register-resident Q in the cross rounds of the inner sweep (measured neutral, spills)
-#endif
 
 #ifdef BMPS_EXPERIMENTAL
 constexpr bool kTmaStaging = true;    // TMA bulk panel staging compiled in (measured slower)
@@ -122,11 +119,19 @@ struct JacArgs {
   int nbcap;
 };
 
+// Rotation parameters of one inner round (NP = w pairs).
+template <int NP>
+struct RotBuf {
+  double c[NP], s[NP];
+  double2 e[NP];
+  double2 se[NP], ce[NP];   // s e, c e
+  int i[NP], j[NP], act[NP];
+};
+// Two rounds' parameters: round rho's are read by the Q update while the rotation
+// warp writes round rho + 1's (jac_inner).
+template <int W2>
 struct RotShared {
-  double c[32], s[32];
-  double2 e[32];
-  double2 se[32], ce[32];   // s e, c e
-  int i[32], j[32], act[32];
+  RotBuf<W2 / 2> b[2];
 };
 
 // Thread groups a Jacobi phase runs on. CtaGrp: the whole CTA (classic kernels,
@@ -564,146 +569,120 @@ BMPS_DEV void inner_pair(bool full, int rho, int p, int& i, int& j) {
 
 // One (or more) cyclic Jacobi sweeps on the W2 x W2 Gram, accumulating Q.
 // Returns the number of rotations of the first sweep (block-uniform).
+//
+// Per round rho, two barriers:
+//   A. G <- J_rho^H G J_rho as independent 2x2 blocks (upper triangle computed,
+//      lower mirrored), all threads; barrier;
+//   B. the first warp of the group computes round rho + 1's rotations from the
+//      updated G into the other parameter buffer WHILE the remaining warps apply
+//      round rho's rotations to Q (Q <- Q J_rho); counting barrier.
+// The latency-bound rotation chain (square roots and divisions of the 2x2 Gram
+// entries) thus runs under the Q update instead of in front of a barrier the whole
+// CTA waits at (ncu: that wait was the largest stall of the kernel). Every element
+// of G and Q sees the same operations in the same order as a round-by-round sweep.
 template <int W2, class G = CtaGrp>
-BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared& rs, double tol, double noise2,
+BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared<W2>& rs, double tol, double noise2,
                        double fro, bool full, int max_inner) {
   using C = JacCfg<W2>;
   constexpr int w = W2 / 2;
+  static_assert(w <= 32, "one warp computes a round's rotations");
+  constexpr int kQThreads = G::kN - 32;   // threads of the Q update in phase B
   const int tid = G::tid();
-  // Cross sweeps keep Q in registers: thread (warp gw, lane) owns row `lane` of the
-  // I-block columns p = gw*PP .. gw*PP+PP-1 and of the J-block columns they are
-  // paired with (w + (p + rho) mod w). Between rounds the partners advance by one
-  // pair: a register move inside the thread, one shared exchange with the next
-  // warp (sQ is free until the end). After the w cross rounds the pairing is back
-  // to the identity and Q is written out.
-  constexpr int NW = G::kN / 32;
-  constexpr bool kRegQ = BMPS_REGQ && W2 == 32 && w % NW == 0;
-  constexpr int PP = kRegQ ? w / NW : 1;
-  const bool regq = kRegQ && !full;
-  const int lane = tid & 31, gw = tid >> 5;
-  double2 qi[PP], qj[PP];
-  if (regq) {
-#pragma unroll
-    for (int u = 0; u < PP; ++u) {
-      const int p = gw * PP + u;
-      qi[u] = make_double2(lane == p ? 1.0 : 0.0, 0.0);
-      qj[u] = make_double2(lane == w + p ? 1.0 : 0.0, 0.0);
-    }
-  } else {
-    for (int idx = tid; idx < W2 * W2; idx += G::n()) {
-      const int i = idx % W2, j = idx / W2;
-      sQ[i + j * C::LDG] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-    }
+  for (int idx = tid; idx < W2 * W2; idx += G::n()) {
+    const int i = idx % W2, j = idx / W2;
+    sQ[i + j * C::LDG] = make_double2(i == j ? 1.0 : 0.0, 0.0);
   }
+  // rotation of pair p (< w) in round rho into buffer rb; returns 1 if it rotates
+  auto rotate = [&](int rho, int p, RotBuf<w>& rb) -> int {
+    int i, j;
+    inner_pair<W2>(full, rho, p, i, j);
+    double c = 1.0, s = 0.0;
+    double2 e = make_double2(1.0, 0.0);
+    int act = jacobi_rotation(sG[i + i * C::LDGG].x, sG[j + j * C::LDGG].x, sG[i + j * C::LDGG], tol,
+                              noise2, fro, c, s, e);
+    if (!act) {
+      c = 1.0;
+      s = 0.0;
+      e = make_double2(1.0, 0.0);
+    }
+    rb.i[p] = i;
+    rb.j[p] = j;
+    rb.act[p] = act;
+    rb.c[p] = c;
+    rb.s[p] = s;
+    rb.e[p] = e;
+    rb.se[p] = cscale(e, s);
+    rb.ce[p] = cscale(e, c);
+    return act;
+  };
   int first = 0;
   const int rounds = full ? W2 - 1 : w;
   for (int it = 0; it < max_inner; ++it) {
     int any = 0;
+    int nact = G::count(tid < w ? rotate(0, tid, rs.b[0]) : 0);
     for (int rho = 0; rho < rounds; ++rho) {
-      if (threadIdx.x == 0) WS_TR(12, it * 1000 + rho);
       BMPS_TICK(tr0);
-      int act = 0;
-      if (tid < w) {
-        int i, j;
-        inner_pair<W2>(full, rho, tid, i, j);
-        double c = 1.0, s = 0.0;
-        double2 e = make_double2(1.0, 0.0);
-        act = jacobi_rotation(sG[i + i * C::LDGG].x, sG[j + j * C::LDGG].x, sG[i + j * C::LDGG], tol,
-                              noise2, fro, c, s, e);
-        if (!act) {
-          c = 1.0;
-          s = 0.0;
-          e = make_double2(1.0, 0.0);
-        }
-        rs.i[tid] = i;
-        rs.j[tid] = j;
-        rs.act[tid] = act;
-        rs.c[tid] = c;
-        rs.s[tid] = s;
-        rs.e[tid] = e;
-        rs.se[tid] = cscale(e, s);
-        rs.ce[tid] = cscale(e, c);
-      }
-      const int nact = G::count(act);
-      BMPS_TICK(tr1);
-      BMPS_ACC(4, tr0, tr1);
-      BMPS_ACC(6, 0, 1);
+      RotBuf<w>& cur = rs.b[rho & 1];
+      RotBuf<w>& nxt = rs.b[(rho + 1) & 1];
       any += nact;
-      if (nact == 0 && !regq) continue;
-      // G <- J^H G J as independent 2x2 blocks (p <= q computed, (q, p) mirrored);
-      // Q <- Q J
-      for (int idx = tid; idx < (nact ? w * (w + 1) / 2 : 0); idx += G::n()) {
-        const int q = (int)((sqrtf(8.0f * (float)idx + 1.0f) - 1.0f) * 0.5f);
-        const int p = idx - q * (q + 1) / 2;
-        if (!(rs.act[p] | rs.act[q])) continue;  // identity on both sides
-        const int ip = rs.i[p], jp = rs.j[p], iq = rs.i[q], jq = rs.j[q];
-        const double cp = rs.c[p], sp = rs.s[p], cq = rs.c[q], sq = rs.s[q];
-        const double2 sep = rs.se[p], cep = rs.ce[p], seq = rs.se[q], ceq = rs.ce[q];
-        const double2 g00 = sG[ip + iq * C::LDGG], g01 = sG[ip + jq * C::LDGG];
-        const double2 g10 = sG[jp + iq * C::LDGG], g11 = sG[jp + jq * C::LDGG];
-        // right: [x_iq, x_jq] <- [x_iq, x_jq] [[cq, sq], [-sq e_q*, cq e_q*]]
-        const double2 r00 = cmsc(g00, cq, seq, g01);
-        const double2 r01 = cmac(g00, sq, ceq, g01);
-        const double2 r10 = cmsc(g10, cq, seq, g11);
-        const double2 r11 = cmac(g10, sq, ceq, g11);
-        // left: rows ip, jp by J_p^H = [[cp, -sp e_p], [sp, cp e_p]]
-        const double2 n00 = cms(r00, cp, sep, r10);
-        const double2 n01 = cms(r01, cp, sep, r11);
-        const double2 n10 = cma(r00, sp, cep, r10);
-        const double2 n11 = cma(r01, sp, cep, r11);
-        sG[ip + iq * C::LDGG] = n00;
-        sG[ip + jq * C::LDGG] = n01;
-        sG[jp + iq * C::LDGG] = n10;
-        sG[jp + jq * C::LDGG] = n11;
-        if (p != q) {
-          sG[iq + ip * C::LDGG] = cconj(n00);
-          sG[jq + ip * C::LDGG] = cconj(n01);
-          sG[iq + jp * C::LDGG] = cconj(n10);
-          sG[jq + jp * C::LDGG] = cconj(n11);
-        }
-      }
-      if (regq) {
-#pragma unroll
-        for (int u = 0; u < PP; ++u) {
-          const int p = gw * PP + u;
-          if (rs.act[p]) {
-            const double2 ni = cmsc(qi[u], rs.c[p], rs.se[p], qj[u]);
-            const double2 nj = cmac(qi[u], rs.s[p], rs.ce[p], qj[u]);
-            qi[u] = ni;
-            qj[u] = nj;
+      if (nact) {
+        // A. G <- J^H G J as independent 2x2 blocks (p <= q computed, (q, p) mirrored)
+        for (int idx = tid; idx < w * (w + 1) / 2; idx += G::n()) {
+          const int q = (int)((sqrtf(8.0f * (float)idx + 1.0f) - 1.0f) * 0.5f);
+          const int p = idx - q * (q + 1) / 2;
+          if (!(cur.act[p] | cur.act[q])) continue;  // identity on both sides
+          const int ip = cur.i[p], jp = cur.j[p], iq = cur.i[q], jq = cur.j[q];
+          const double cp = cur.c[p], sp = cur.s[p], cq = cur.c[q], sq = cur.s[q];
+          const double2 sep = cur.se[p], cep = cur.ce[p], seq = cur.se[q], ceq = cur.ce[q];
+          const double2 g00 = sG[ip + iq * C::LDGG], g01 = sG[ip + jq * C::LDGG];
+          const double2 g10 = sG[jp + iq * C::LDGG], g11 = sG[jp + jq * C::LDGG];
+          // right: [x_iq, x_jq] <- [x_iq, x_jq] [[cq, sq], [-sq e_q*, cq e_q*]]
+          const double2 r00 = cmsc(g00, cq, seq, g01);
+          const double2 r01 = cmac(g00, sq, ceq, g01);
+          const double2 r10 = cmsc(g10, cq, seq, g11);
+          const double2 r11 = cmac(g10, sq, ceq, g11);
+          // left: rows ip, jp by J_p^H = [[cp, -sp e_p], [sp, cp e_p]]
+          const double2 n00 = cms(r00, cp, sep, r10);
+          const double2 n01 = cms(r01, cp, sep, r11);
+          const double2 n10 = cma(r00, sp, cep, r10);
+          const double2 n11 = cma(r01, sp, cep, r11);
+          sG[ip + iq * C::LDGG] = n00;
+          sG[ip + jq * C::LDGG] = n01;
+          sG[jp + iq * C::LDGG] = n10;
+          sG[jp + jq * C::LDGG] = n11;
+          if (p != q) {
+            sG[iq + ip * C::LDGG] = cconj(n00);
+            sG[jq + ip * C::LDGG] = cconj(n01);
+            sG[iq + jp * C::LDGG] = cconj(n10);
+            sG[jq + jp * C::LDGG] = cconj(n11);
           }
         }
-        sQ[gw * 32 + lane] = qj[0];
-#pragma unroll
-        for (int u = 0; u + 1 < PP; ++u) qj[u] = qj[u + 1];
         G::sync();
-        qj[PP - 1] = sQ[((gw + 1) % NW) * 32 + lane];
-        continue;
       }
-      for (int idx = tid; idx < W2 * w; idx += G::n()) {
-        const int k = idx % W2, q = idx / W2;
-        if (!rs.act[q]) continue;
-        const int iq = rs.i[q], jq = rs.j[q];
-        const double cq = rs.c[q], sq = rs.s[q];
-        const double2 qi = sQ[k + iq * C::LDG], qj = sQ[k + jq * C::LDG];
-        sQ[k + iq * C::LDG] = cmsc(qi, cq, rs.se[q], qj);
-        sQ[k + jq * C::LDG] = cmac(qi, sq, rs.ce[q], qj);
+      BMPS_TICK(tr1);
+      BMPS_ACC(5, tr0, tr1);
+      // B. next round's rotations (first warp) || Q <- Q J_rho (the other warps)
+      int act = 0;
+      if (tid < 32) {
+        if (rho + 1 < rounds && tid < w) act = rotate(rho + 1, tid, nxt);
+      } else if (nact) {
+        for (int idx = tid - 32; idx < W2 * w; idx += kQThreads) {
+          const int k = idx % W2, q = idx / W2;
+          if (!cur.act[q]) continue;
+          const int iq = cur.i[q], jq = cur.j[q];
+          const double cq = cur.c[q], sq = cur.s[q];
+          const double2 qi = sQ[k + iq * C::LDG], qj = sQ[k + jq * C::LDG];
+          sQ[k + iq * C::LDG] = cmsc(qi, cq, cur.se[q], qj);
+          sQ[k + jq * C::LDG] = cmac(qi, sq, cur.ce[q], qj);
+        }
       }
-      G::sync();
+      nact = G::count(act);
       BMPS_TICK(tr2);
-      BMPS_ACC(5, tr1, tr2);
+      BMPS_ACC(4, tr1, tr2);
+      BMPS_ACC(6, 0, 1);
     }
     if (it == 0) first = any;
     if (!any) break;
-  }
-  if (regq) {
-    G::sync();   // every thread has taken its last exchange value
-#pragma unroll
-    for (int u = 0; u < PP; ++u) {
-      const int p = gw * PP + u;
-      sQ[lane + p * C::LDG] = qi[u];
-      sQ[lane + (w + p) * C::LDG] = qj[u];
-    }
   }
   return first;
 }
@@ -725,7 +704,7 @@ BMPS_DEV double2* jac_ring3(double2* sP, double2* sQ, int k) {
 template <int W2, class G = CtaGrp>
 BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, double noise2,
                         double fro, bool full, int max_inner, bool resident, double2* sG,
-                        double2* sQ, double2* sP, RotShared& rs, JacStage& st, bool tma,
+                        double2* sQ, double2* sP, RotShared<W2>& rs, JacStage& st, bool tma,
                         double2* gcache = nullptr, bool inner_regs = false) {
   using C = JacCfg<W2>;
   BMPS_TICK(tv0);
@@ -905,7 +884,7 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_ke
   double2* sQ = jsm;
   double2* sP = sQ + W2 * C::LDG;
   double2* sG = C::G_IN_BUF ? sP + C::BUF : sP + C::NBUF * C::BUF;
-  __shared__ RotShared rs;
+  __shared__ RotShared<W2> rs;
   __shared__ unsigned long long jbar[2];
   const int item = blockIdx.y;
   ItemMeta* m = args.meta + item;
@@ -1035,7 +1014,7 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dy
   double2* sQ = jsm;
   double2* sP = sQ + W2 * C::LDG;
   double2* sG = C::G_IN_BUF ? sP + C::BUF : sP + C::NBUF * C::BUF;
-  __shared__ RotShared rs;
+  __shared__ RotShared<W2> rs;
   __shared__ int s_item, s_v;
   __shared__ unsigned s_round;
   __shared__ unsigned long long jbar[2];
@@ -1515,7 +1494,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) jacobi_ws_kernel(JacArgs args) 
   double2* sQ0 = jsm;                    // Q[0], Q[1]
   double2* sG0 = sQ0 + 2 * WC::QSZ;      // G[0], G[1]
   double2* sP = sG0 + 2 * WC::GSZ;       // two staging buffers
-  __shared__ RotShared rs_rot, rs_math;
+  __shared__ RotShared<W2> rs_rot, rs_math;
   __shared__ WsVisit wv[2];
   __shared__ WsClaim claims[kWsRing];
   __shared__ WsDone dones[kWsRing];
@@ -1841,7 +1820,7 @@ __global__ void __launch_bounds__(256, 3) jacobi_cluster_kernel(JacArgs args) {
   double2* sP = sQ + W2 * C::LDG;
   double2* sG = C::G_IN_BUF ? sP + C::BUF : nullptr;   // W2 = 32 only
   double2* sPart = sP + C::NBUF * C::BUF;
-  __shared__ RotShared rs;
+  __shared__ RotShared<W2> rs;
   __shared__ int c_item, c_v;
   __shared__ unsigned c_round;
   __shared__ unsigned long long jbar[2];
