@@ -100,14 +100,27 @@ def experimental() -> bool:
     return bool(load().bmps_build_flags() & 1)
 
 
+_param_cache: dict = {}
+
+
 def params(**extra) -> BmpsParams:
-    """A ``bmps_params`` of the library defaults, the active overrides and ``extra``."""
+    """A ``bmps_params`` of the library defaults, the active overrides and ``extra``
+    (a fresh struct; the default-plus-overrides part is memoised per override set)."""
+    key = tuple(sorted({**_overrides, **extra}.items()))
+    base = _param_cache.get(key)
+    if base is not None:
+        p = BmpsParams()
+        ctypes.pointer(p)[0] = base
+        return p
     p = BmpsParams()
     load().bmps_default_params(ctypes.byref(p))
     for k, v in {**_overrides, **extra}.items():
         if k not in TUNABLES:
             raise ValueError(f"unknown tunable {k!r}")
         setattr(p, k, type(getattr(p, k))(v))
+    saved = BmpsParams()
+    ctypes.pointer(saved)[0] = p
+    _param_cache[key] = saved
     return p
 
 
