@@ -204,13 +204,16 @@ int32_t bmps_sample(const double* gamma, const double* lam, const int32_t* dims,
  * the building block of MpsState.expectation_pauli / norm_sq
  * (mps.py:181-204): direction 0 (left, E_{k+1} from E_k, mps.py:200) or
  * 1 (right, R_k from R_{k+1}). Environments are cap x cap complex128
- * matrices (row stride cap); item i's input starts at env_in + i*in_stride
- * and its output at env_out + i*out_stride (strides in complex elements).
+ * matrices (row stride cap); item i's input starts at env_in + j*in_stride
+ * and its output at env_out + k*out_stride (strides in complex elements), with
+ * j = in_idx[i] and k = out_idx[i] when those device index arrays are given,
+ * else j = k = i (gather / scatter without copies).
  * pauli codes I=0 X=1 Y=2 Z=3. scratch: complex128 [2][count][2*cap*cap]. */
 int32_t bmps_env_transfer(const double* gamma, const double* lam, const int32_t* dims, int32_t S,
                           int32_t n, int32_t cap, const int32_t* state_idx, const int32_t* site,
                           const uint8_t* pauli, int32_t direction, const double* env_in,
-                          int64_t in_stride, double* env_out, int64_t out_stride, double* scratch,
+                          int64_t in_stride, const int32_t* in_idx, double* env_out,
+                          int64_t out_stride, const int32_t* out_idx, double* scratch,
                           int32_t count, void* stream);
 
 /* MpsState.expectation_pauli (mps.py:188-204) for a batch of (state, string)
@@ -237,11 +240,12 @@ int32_t bmps_env_sweep(const double* gamma, const double* lam, const int32_t* di
 
 /* <E_left, R_right> contraction: out[i] = sum_{r,q} L_i[r,q] * R_i[r,q] over
  * the dims[s][b_i] x dims[s][b_i] leading block (complex128 out); L_i at
- * env_l + i*l_stride, R_i at env_r + i*r_stride (complex elements). */
+ * env_l + l*l_stride, R_i at env_r + r*r_stride (complex elements) with
+ * l = l_idx[i], r = r_idx[i] when given (device int32), else l = r = i. */
 int32_t bmps_env_close(const int32_t* dims, int32_t n, int32_t cap, const int32_t* state_idx,
                        const int32_t* bond, const double* env_l, int64_t l_stride,
-                       const double* env_r, int64_t r_stride, int32_t count, double* out,
-                       void* stream);
+                       const int32_t* l_idx, const double* env_r, int64_t r_stride,
+                       const int32_t* r_idx, int32_t count, double* out, void* stream);
 
 /* ---- dense statevector backend (R:src/mpsqvm/dense.py) --------------------
  * amps: complex128 [S][2^n], flat index with qubit 0 as the HIGH bit

@@ -65,8 +65,8 @@ _SIGNATURES = {
     "bmps_apply_2q_sweeps": ([_P, _I, _P, _P], _I),
     "bmps_amplitudes": ([_P, _P, _P, _I, _I, _I, _P, _P, _I, _P, _P], _I),
     "bmps_sample": ([_P, _P, _P, _I, _I, _I, _P, _P, _I, _P, _P], _I),
-    "bmps_env_transfer": ([_P, _P, _P, _I, _I, _I, _P, _P, _P, _I, _P, _L, _P, _L, _P, _I, _P], _I),
-    "bmps_env_close": ([_P, _I, _I, _P, _P, _P, _L, _P, _L, _I, _P, _P], _I),
+    "bmps_env_transfer": ([_P, _P, _P, _I, _I, _I, _P, _P, _P, _I, _P, _L, _P, _P, _L, _P, _P, _I, _P], _I),
+    "bmps_env_close": ([_P, _I, _I, _P, _P, _P, _L, _P, _P, _L, _P, _I, _P, _P], _I),
     "bmps_env_sweep": ([_P, _P, _P, _I, _I, _I, _P, _I, _I, _P, _L, _P], _I),
     "bmps_pauli_sweep": ([_P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _L, _I, _P, _P], _I),
     "bmps_plan_expanded_count": ([_P, _P, _P, _L], _L),

@@ -364,11 +364,12 @@ struct EnvL1 : EnvOpBase {
   const double2* ot;
   double2* f;
   size_t env_stride, ot_stride;
+  const int* env_idx;   // optional: item i reads environment env_idx[i]
   const double2 *e_, *o_;
   double2* f_;
   BMPS_DEV bool begin(int item, int& M, int& N, int& K) {
     dims_of(item);
-    e_ = env + (size_t)item * env_stride;
+    e_ = env + (size_t)(env_idx ? env_idx[item] : item) * env_stride;
     o_ = ot + (size_t)item * ot_stride;
     f_ = f + (size_t)item * ot_stride;
     M = dl;
@@ -393,6 +394,7 @@ struct EnvL2 : EnvOpBase {
   const double2* f;
   double2* out;
   size_t ot_stride, env_stride;
+  const int* env_idx;   // optional: item i writes environment env_idx[i]
   const double2* g_;
   const double* lam_;
   const double2* f_;
@@ -403,7 +405,7 @@ struct EnvL2 : EnvOpBase {
     g_ = sv.site(s, k);
     lam_ = sv.bond(s, k + 1);
     f_ = f + (size_t)item * ot_stride;
-    o_ = out + (size_t)item * env_stride;
+    o_ = out + (size_t)(env_idx ? env_idx[item] : item) * env_stride;
     M = dr;
     N = dr;
     K = 2 * dl;
@@ -421,11 +423,12 @@ struct EnvR1 : EnvOpBase {
   const double2* ot;
   double2* f;
   size_t env_stride, ot_stride;
+  const int* env_idx;   // optional: item i reads environment env_idx[i]
   const double2 *e_, *o_;
   double2* f_;
   BMPS_DEV bool begin(int item, int& M, int& N, int& K) {
     dims_of(item);
-    e_ = env + (size_t)item * env_stride;
+    e_ = env + (size_t)(env_idx ? env_idx[item] : item) * env_stride;
     o_ = ot + (size_t)item * ot_stride;
     f_ = f + (size_t)item * ot_stride;
     M = 2 * dl;
@@ -444,6 +447,7 @@ struct EnvR2 : EnvOpBase {
   const double2* f;
   double2* out;
   size_t ot_stride, env_stride;
+  const int* env_idx;   // optional: item i writes environment env_idx[i]
   const double2* g_;
   const double* lam_;
   const double2* f_;
@@ -454,7 +458,7 @@ struct EnvR2 : EnvOpBase {
     g_ = sv.site(s, k);
     lam_ = sv.bond(s, k + 1);
     f_ = f + (size_t)item * ot_stride;
-    o_ = out + (size_t)item * env_stride;
+    o_ = out + (size_t)(env_idx ? env_idx[item] : item) * env_stride;
     M = dl;
     N = dl;
     K = 2 * dr;
@@ -474,12 +478,13 @@ struct EnvR2 : EnvOpBase {
 __global__ void __launch_bounds__(256) env_close_kernel(const int* dims, int n, int cap,
                                                         const int* state_idx, const int* bond,
                                                         const double2* el, size_t l_stride,
-                                                        const double2* er, size_t r_stride,
+                                                        const int* l_idx, const double2* er,
+                                                        size_t r_stride, const int* r_idx,
                                                         double2* out) {
   const int it = blockIdx.x;
   const int D = dims[(size_t)state_idx[it] * (n + 1) + bond[it]];
-  const double2* a = el + (size_t)it * l_stride;
-  const double2* b = er + (size_t)it * r_stride;
+  const double2* a = el + (size_t)(l_idx ? l_idx[it] : it) * l_stride;
+  const double2* b = er + (size_t)(r_idx ? r_idx[it] : it) * r_stride;
   double2 acc = make_double2(0.0, 0.0);
   for (int idx = threadIdx.x; idx < D * D; idx += blockDim.x) {
     const int i = idx / D, j = idx % D;
@@ -1338,7 +1343,8 @@ int32_t bmps_conditional(const double* gamma, const double* lam, const int32_t* 
 int32_t bmps_env_transfer(const double* gamma, const double* lam, const int32_t* dims, int32_t S,
                           int32_t n, int32_t cap, const int32_t* state_idx, const int32_t* site,
                           const uint8_t* pauli, int32_t direction, const double* env_in,
-                          int64_t in_stride, double* env_out, int64_t out_stride, double* scratch,
+                          int64_t in_stride, const int32_t* in_idx, double* env_out,
+                          int64_t out_stride, const int32_t* out_idx, double* scratch,
                           int32_t count, void* stream) {
   if (count == 0) return BMPS_OK;
   if (count < 0 || S < 1 || n < 1 || cap < 1 || (direction != 0 && direction != 1))
@@ -1358,26 +1364,28 @@ int32_t bmps_env_transfer(const double* gamma, const double* lam, const int32_t*
     EnvL1 g1;
     g1.sv = sv; g1.state_idx = state_idx; g1.site = site;
     g1.env = (const double2*)env_in; g1.ot = ot; g1.f = f;
-    g1.env_stride = (size_t)in_stride; g1.ot_stride = ot_stride;
+    g1.env_stride = (size_t)in_stride; g1.ot_stride = ot_stride; g1.env_idx = in_idx;
     gemm_kernel<EnvL1><<<dim3(t1, t2, count), 256, 0, st>>>(g1);
     ++g_launches;
     if ((rc = launch_status())) return rc;
     EnvL2 g2;
     g2.sv = sv; g2.state_idx = state_idx; g2.site = site;
     g2.f = f; g2.out = (double2*)env_out; g2.ot_stride = ot_stride; g2.env_stride = (size_t)out_stride;
+    g2.env_idx = out_idx;
     gemm_kernel<EnvL2><<<dim3(t1, t1, count), 256, 0, st>>>(g2);
     ++g_launches;
   } else {
     EnvR1 g1;
     g1.sv = sv; g1.state_idx = state_idx; g1.site = site;
     g1.env = (const double2*)env_in; g1.ot = ot; g1.f = f;
-    g1.env_stride = (size_t)in_stride; g1.ot_stride = ot_stride;
+    g1.env_stride = (size_t)in_stride; g1.ot_stride = ot_stride; g1.env_idx = in_idx;
     gemm_kernel<EnvR1><<<dim3(t2, t1, count), 256, 0, st>>>(g1);
     ++g_launches;
     if ((rc = launch_status())) return rc;
     EnvR2 g2;
     g2.sv = sv; g2.state_idx = state_idx; g2.site = site;
     g2.f = f; g2.out = (double2*)env_out; g2.ot_stride = ot_stride; g2.env_stride = (size_t)out_stride;
+    g2.env_idx = out_idx;
     gemm_kernel<EnvR2><<<dim3(t1, t1, count), 256, 0, st>>>(g2);
     ++g_launches;
   }
@@ -1420,13 +1428,13 @@ int32_t bmps_env_sweep(const double* gamma, const double* lam, const int32_t* di
 
 int32_t bmps_env_close(const int32_t* dims, int32_t n, int32_t cap, const int32_t* state_idx,
                        const int32_t* bond, const double* env_l, int64_t l_stride,
-                       const double* env_r, int64_t r_stride, int32_t count, double* out,
-                       void* stream) {
+                       const int32_t* l_idx, const double* env_r, int64_t r_stride,
+                       const int32_t* r_idx, int32_t count, double* out, void* stream) {
   if (count == 0) return BMPS_OK;
   if (count < 0 || n < 1 || cap < 1) return BMPS_E_ARG;
   env_close_kernel<<<count, 256, 0, (cudaStream_t)stream>>>(
-      dims, n, cap, state_idx, bond, (const double2*)env_l, (size_t)l_stride,
-      (const double2*)env_r, (size_t)r_stride, (double2*)out);
+      dims, n, cap, state_idx, bond, (const double2*)env_l, (size_t)l_stride, l_idx,
+      (const double2*)env_r, (size_t)r_stride, r_idx, (double2*)out);
   ++g_launches;
   return launch_status();
 }

@@ -836,12 +836,14 @@ class MpsBatch:
 
     def _transfer(self, sidx: torch.Tensor, site: torch.Tensor, codes: torch.Tensor, direction: int,
                   env_in: torch.Tensor, in_stride: int, env_out: torch.Tensor, out_stride: int,
-                  count: int) -> None:
+                  count: int, in_idx: torch.Tensor | None = None,
+                  out_idx: torch.Tensor | None = None) -> None:
         scratch = self._scratch(count)
         rc = self.lib.bmps_env_transfer(
             _ptr(self.gamma), _ptr(self.lam), _ptr(self.dims), self.S, self.n, self.cap,
             sidx.data_ptr(), site.data_ptr(), codes.data_ptr(), direction, env_in.data_ptr(), in_stride,
-            env_out.data_ptr(), out_stride, scratch.data_ptr(), count, _stream())
+            _ptr(in_idx), env_out.data_ptr(), out_stride, _ptr(out_idx), scratch.data_ptr(), count,
+            _stream())
         _native.check(rc, "bmps_env_transfer")
 
     def _scratch(self, count: int) -> torch.Tensor:
@@ -935,42 +937,61 @@ class MpsBatch:
             if bad.any():
                 raise RuntimeError(f"expectation has imaginary residue {out.imag[bad][0]:.3e}")
             return out.real.copy()
+        # cap > 32: each string is swept from its cached left environment L_lo over its
+        # support on the DMMA transfer GEMMs, one launch pair per site step for all
+        # strings still active, environments addressed through device index arrays
+        # (no gathers or scatters), and closed against the cached R_{hi+1}
+        E = n + 1
+        cc = cap * cap
+        to_dev = lambda a, dt=np.int32: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
+        if use_env:
+            Lflat = Lenv.view(len(uniq) * E, cap, cap)
+            Rflat = Renv.view(len(uniq) * E, cap, cap)
+        else:
+            Lflat = Rflat = self._identity_env(1)
         chunk = self._env_chunk()
         for c0 in range(0, npairs, chunk):
             c1 = min(npairs, c0 + chunk)
             cnt = c1 - c0
-            s_t = torch.as_tensor(state_idx[c0:c1]).to(dev)
             lo_c, hi_c = lo[c0:c1], hi[c0:c1]
-            if use_env:
-                u = torch.as_tensor(inv[c0:c1]).to(dev)
-                cur = Lenv[u, torch.as_tensor(np.maximum(lo_c, 0)).to(dev)].contiguous()
-                right = Renv[u, torch.as_tensor(np.where(hi_c >= 0, hi_c + 1, lo_c)).to(dev)].contiguous()
-            else:
-                cur = self._identity_env(cnt)
-                right = self._identity_env(cnt)
-            nxt = torch.empty_like(cur)
+            u_c = inv[c0:c1] if use_env else np.zeros(cnt, np.int64)
             span = np.where(hi_c >= lo_c, hi_c - lo_c + 1, 0)
-            codes_d = torch.from_numpy(codes[c0:c1]).to(dev)
+            codes_c = codes[c0:c1]
+            cur = torch.empty((2, cnt, cap, cap), dtype=torch.complex128, device=dev)
             for t in range(int(span.max()) if cnt else 0):
                 act = np.nonzero(span > t)[0]
                 if len(act) == 0:
                     break
-                a_t = torch.as_tensor(act).to(dev)
-                site = torch.as_tensor((lo_c[act] + t).astype(np.int32)).to(dev)
-                cd = codes_d[a_t, site.long()].contiguous()
-                sub_in = cur[a_t].contiguous()
-                sub_out = torch.empty_like(sub_in)
-                self._transfer(s_t[a_t].contiguous(), site, cd, 0, sub_in, cap * cap, sub_out,
-                               cap * cap, len(act))
-                cur[a_t] = sub_out
-            bond = torch.as_tensor(np.where(span > 0, hi_c + 1, lo_c).astype(np.int32)).to(dev)
-            res = torch.empty(cnt, dtype=torch.complex128, device=dev)
-            rc = self.lib.bmps_env_close(_ptr(self.dims), n, cap, s_t.data_ptr(), bond.data_ptr(),
-                                         cur.data_ptr(), cap * cap, right.data_ptr(), cap * cap, cnt,
-                                         res.data_ptr(), _stream())
-            _native.check(rc, "bmps_env_close")
-            out[c0:c1] = res.cpu().numpy()
-            del nxt
+                site_h = (lo_c[act] + t).astype(np.int32)
+                if t == 0:
+                    src = Lflat
+                    in_idx = u_c[act] * E + lo_c[act] if use_env else np.zeros(len(act))
+                else:
+                    src, in_idx = cur[(t - 1) & 1], act
+                self._transfer(to_dev(state_idx[c0:c1][act]), to_dev(site_h),
+                               to_dev(codes_c[act, site_h], np.uint8), 0, src, cc, cur[t & 1], cc,
+                               len(act), in_idx=to_dev(in_idx), out_idx=to_dev(act))
+            bond = np.where(span > 0, hi_c + 1, lo_c).astype(np.int32)
+            r_idx = u_c * E + bond if use_env else np.zeros(cnt)
+            # left environment: L_lo (no support), else the last ping-pong buffer
+            for grp, base, l_idx in (
+                    (span == 0, Lflat, u_c * E + lo_c if use_env else np.zeros(cnt)),
+                    ((span > 0) & (span % 2 == 1), cur[0], np.arange(cnt)),
+                    ((span > 0) & (span % 2 == 0), cur[1], np.arange(cnt))):
+                sel = np.nonzero(grp)[0]
+                if len(sel) == 0:
+                    continue
+                part = torch.empty(len(sel), dtype=torch.complex128, device=dev)
+                # keep every index tensor referenced until the launch is queued (a freed
+                # temporary's block could be refilled by the next copy before the kernel runs)
+                d_s, d_b = to_dev(state_idx[c0:c1][sel]), to_dev(bond[sel])
+                d_l, d_r = to_dev(l_idx[sel]), to_dev(r_idx[sel])
+                rc = self.lib.bmps_env_close(
+                    _ptr(self.dims), n, cap, d_s.data_ptr(), d_b.data_ptr(), base.data_ptr(), cc,
+                    d_l.data_ptr(), Rflat.data_ptr(), cc, d_r.data_ptr(), len(sel), part.data_ptr(),
+                    _stream())
+                _native.check(rc, "bmps_env_close")
+                out[c0 + sel] = part.cpu().numpy()
         bad = np.abs(out.imag) > 1e-10
         if bad.any():
             raise RuntimeError(f"expectation has imaginary residue {out.imag[bad][0]:.3e}")
