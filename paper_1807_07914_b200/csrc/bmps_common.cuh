@@ -2,6 +2,7 @@
 // (DMMA, mma.sync m8n8k4 f64) complex tile products, state indexing.
 #pragma once
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <math_constants.h>
 #include <stdint.h>
 
@@ -11,6 +12,20 @@
 #define BMPS_HOSTDEV __host__ __device__
 
 namespace bmps {
+
+// Device-side invariant checks of a -DBMPS_DEBUG_CHECKS build (bounds of the items
+// a launch touches, the Jacobi scheduling protocol); compiled out otherwise.
+#ifdef BMPS_DEBUG_CHECKS
+#define BMPS_CHECK(cond)                                                                   \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("BMPS_CHECK failed %s:%d block %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x, #cond); \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define BMPS_CHECK(cond) do { } while (0)
+#endif
 
 constexpr double kEps = 1.1102230246251565e-16;   // unit roundoff of float64
 constexpr double kPinvFloor = 1e-12;              // mps.py:21 _PINV_FLOOR

@@ -93,8 +93,36 @@ struct JacSched {
   unsigned long long ticket;  // (round << 32) | next visit index to claim
   int done;                   // visits of the current round completed
   int dirty;                  // any rotation in the current sweep
-  int pad[4];
+  int pad[4];                 // -DBMPS_DEBUG_CHECKS: [0..1] visit mask of the round, [2] round
 };
+
+// Invariant checks of the lock-free visit scheduling (-DBMPS_DEBUG_CHECKS; the
+// pool's compute-sanitizer is closed, so the claim / completion protocol checks
+// itself): every visit of a round completes exactly once, in the round its ticket
+// was claimed for, and a round is closed only when all its visits completed.
+BMPS_DEV void jac_debug_mark(JacSched* sc, int v, unsigned rnd, int nvis) {
+#ifdef BMPS_DEBUG_CHECKS
+  BMPS_CHECK(v >= 0 && v < nvis && nvis <= 64);
+  BMPS_CHECK((unsigned)atomicAdd(&sc->pad[2], 0) == rnd);
+  const unsigned long long old = atomicOr((unsigned long long*)sc->pad, 1ull << v);
+  BMPS_CHECK(!(old & (1ull << v)));
+#else
+  (void)sc; (void)v; (void)rnd; (void)nvis;
+#endif
+}
+// Called by the CTA that completed the last visit of round rnd, before it opens
+// round rnd + 1 (or retires the item).
+BMPS_DEV void jac_debug_close(JacSched* sc, unsigned rnd, int nvis) {
+#ifdef BMPS_DEBUG_CHECKS
+  unsigned long long* mask = (unsigned long long*)sc->pad;
+  const unsigned long long full = nvis >= 64 ? ~0ull : ((1ull << nvis) - 1);
+  BMPS_CHECK(atomicAdd(mask, 0ull) == full);
+  atomicExch(mask, 0ull);
+  atomicExch(&sc->pad[2], (int)(rnd + 1));
+#else
+  (void)sc; (void)rnd; (void)nvis;
+#endif
+}
 
 struct JacArgs {
   ItemMeta* meta;
@@ -1113,6 +1141,7 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dy
     const int v = s_v;
     const unsigned rnd = s_round;
     ItemMeta* m = args.meta + i;
+    BMPS_CHECK(i < nitems && !m->conv);
     const int r = m->jrows, c = m->c;
     double2* X = (m->dq ? args.Z : m->precond ? args.Y : args.X) + (size_t)i * args.mat_stride;
     int nb = (c + w - 1) / w;
@@ -1185,10 +1214,12 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dy
     __syncthreads();
     if (threadIdx.x == 0) {
       if (dirty) atomicOr(&sc->dirty, 1);
+      jac_debug_mark(sc, v, rnd, nb / 2);
       __threadfence();
       const int d = atomicAdd(&sc->done, 1);
       if (d == nb / 2 - 1) {
         // last visit of the round: open the next round (or finish the item)
+        jac_debug_close(sc, rnd, nb / 2);
         sc->done = 0;
         bool finished = false;
         if (rho == rounds - 1) {
@@ -1276,7 +1307,7 @@ struct WsVisit {
 // opening of the next round or the end of the item (as in jacobi_dynamic_kernel).
 template <int W2>
 BMPS_DEV void jac_complete(const JacArgs& args, int i, unsigned rnd, int I, int J, bool dirty,
-                           bool skipped) {
+                           bool skipped, int v) {
   constexpr int w = W2 / 2;
   ItemMeta* m = args.meta + i;
   int nb = (m->c + w - 1) / w;
@@ -1296,9 +1327,11 @@ BMPS_DEV void jac_complete(const JacArgs& args, int i, unsigned rnd, int I, int 
     }
   }
   if (dirty) atomicOr(&sc->dirty, 1);
+  if (v >= 0) jac_debug_mark(sc, v, rnd, nb / 2);
   __threadfence();
   const int d = atomicAdd(&sc->done, 1);
   if (d == nb / 2 - 1) {
+    if (v >= 0) jac_debug_close(sc, rnd, nb / 2);
     sc->done = 0;
     bool finished = false;
     if (rho == rounds - 1) {
@@ -1368,7 +1401,7 @@ BMPS_DEV int ws_claim(const JacArgs& args, int& cursor, int& v_out, unsigned& rn
         const int lc = *((volatile const int*)(last_rot + args.nbcap + I * args.nbcap + J));
         if (lc >= 0 && *((volatile const int*)(last_rot + I)) < lc &&
             *((volatile const int*)(last_rot + J)) < lc) {
-          jac_complete<W2>(args, got, rnd_out, I, J, false, true);
+          jac_complete<W2>(args, got, rnd_out, I, J, false, true, (int)v_out);
           continue;
         }
       }
@@ -1520,7 +1553,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) jacobi_ws_kernel(JacArgs args) 
       // finished visits first: they may open the rounds the next claim needs
       while (vd[ds].flag) {
         __threadfence_block();
-        jac_complete<W2>(args, vd[ds].item, vd[ds].rnd, vd[ds].I, vd[ds].J, vd[ds].dirty != 0, false);
+        jac_complete<W2>(args, vd[ds].item, vd[ds].rnd, vd[ds].I, vd[ds].J, vd[ds].dirty != 0, false, -1);
         vd[ds].flag = 0;
         ds = (ds + 1) % kWsRing;
       }
@@ -1943,7 +1976,7 @@ __global__ void __launch_bounds__(256, 3) jacobi_cluster_kernel(JacArgs args) {
     if (nrot > 0) cl_apply_rows<W2>(X, r, c, I, J, sQ, sP, row0, row1);
     __threadfence();
     cl.sync();         // every rank's panel rows (and rank 0's cache) are written
-    if (rank == 0 && tid == 0) jac_complete<W2>(args, i, rnd, I, J, nrot > 0, false);
+    if (rank == 0 && tid == 0) jac_complete<W2>(args, i, rnd, I, J, nrot > 0, false, v);
   }
 }
 

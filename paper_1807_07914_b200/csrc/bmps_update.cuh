@@ -75,6 +75,8 @@ __global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* ite
   int M, N, K;
   op.begin(item, M, N, K);
   const int dl = op.dl, dm = op.dm, dr = op.dr;
+  BMPS_CHECK(items[2 * item + 1] >= 0 && items[2 * item + 1] + 2 <= sv.n && dl >= 1 && dm >= 1 &&
+             dr >= 1 && dl <= sv.cap && dm <= sv.cap && dr <= sv.cap);
   const int orient = dl >= dr ? 0 : 1;
   const int R = orient == 0 ? 2 * dl : 2 * dr;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -314,6 +316,7 @@ __global__ void __launch_bounds__(512) finalize_kernel(StateView sv, const int* 
     for (int k = 0; k < keep; ++k) nrm2 += ssig[k] * ssig[k];
     const double nrm = sqrt(nrm2);
     if (nrm == 0.0 && !status) status = BMPS_S_ALL_TRUNCATED;
+    BMPS_CHECK(keep >= 1 && keep <= sv.cap && keep <= c);
     m->keep = keep;
     m->err = err;
     m->norm = nrm;
