@@ -378,13 +378,10 @@ struct EnvL1 : EnvOpBase {
     return true;
   }
   BMPS_DEV double2 a(int i, int k) const { return e_[(size_t)i * cap + k]; }
-  BMPS_DEV double2 b(int k, int j) const {
-    const int s = j / dr, q = j % dr;
-    return o_[(size_t)(2 * k + s) * cap + q];
-  }
+  // GEMM column j = 2q + s (interleaved, no integer division in the loaders)
+  BMPS_DEV double2 b(int k, int j) const { return o_[(size_t)(2 * k + (j & 1)) * cap + (j >> 1)]; }
   BMPS_DEV void store(int i, int j, double2 v) const {
-    const int s = j / dr, q = j % dr;
-    f_[(size_t)(2 * i + s) * cap + q] = v;
+    f_[(size_t)(2 * i + (j & 1)) * cap + (j >> 1)] = v;
   }
 };
 
@@ -464,12 +461,13 @@ struct EnvR2 : EnvOpBase {
     K = 2 * dr;
     return true;
   }
+  // GEMM depth k = 2r + s (interleaved, no integer division in the loaders)
   BMPS_DEV double2 a(int i, int k) const {
-    const int s = k / dr, r = k % dr;
+    const int s = k & 1, r = k >> 1;
     return cconj(cscale(g_[(size_t)(2 * i + s) * cap + r], lam_[r]));
   }
   BMPS_DEV double2 b(int k, int j) const {
-    const int s = k / dr, r = k % dr;
+    const int s = k & 1, r = k >> 1;
     return f_[(size_t)(2 * j + s) * cap + r];
   }
   BMPS_DEV void store(int i, int j, double2 v) const { o_[(size_t)i * cap + j] = v; }

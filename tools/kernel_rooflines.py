@@ -16,7 +16,7 @@ timed with CUDA events on the launching stream over repeated launches after warm
   16 dl dr (dl + dr). Timed with the host loop of launches
   inside the region (one launch pair per site), so gaps count against it.
 * K2 ``theta_kernel`` / K4 ``gemm_kernel<SplitOp>``: from the committed ncu launch
-  list of the bench step (``profiles/r01_step_launches_final5.csv``), per-launch
+  list of the bench step (``profiles/r02_step_launches.csv``), per-launch
   duration vs the nominal flops of its updates (one grid slice per chi=256 update).
 
 Prints one JSON object; ``profiles/r01_kernel_rooflines.json`` keeps a GPU run.
@@ -112,7 +112,7 @@ def main() -> None:
     from paper_1807_07914_b200.engine import _ptr, _stream
 
     peak_gbs, peak_src = hbm_peak()
-    fp64 = bench.FP64_PEAK_TFLOPS
+    fp64 = bench.fp64_peak()[0]
     R, n = args.replicas, bench.N_QUBITS
     batch = MpsBatch(R, n, TruncationPolicy(bench.CUTOFF, bench.CHI))
     batch.run([bench.prefix_program(1003 + r, bench.STEADY_LAYERS) for r in range(R)])
