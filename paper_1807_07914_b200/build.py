@@ -45,7 +45,8 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None,
     if out is None and not defines and not force and up_to_date():
         return OUT
     target = Path(out) if out is not None else OUT
-    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], f"-I{ROOT / 'include'}", "-o",
+    target.parent.mkdir(parents=True, exist_ok=True)
+    cmd =[nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], f"-I{ROOT / 'include'}", "-o",
            str(target) + ".tmp", *map(str, SOURCES)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
