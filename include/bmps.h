@@ -62,11 +62,6 @@ typedef struct bmps_policy {
   int32_t relative;  /* TruncationPolicy.relative (mps.py:35) */
 } bmps_policy;
 
-/* Development aid (no reference counterpart): point the warp-specialised Jacobi
- * kernel's per-CTA progress words at pinned host memory (16 int32 per CTA); only in
- * builds with -DBMPS_WS_TRACE, BMPS_E_ARG otherwise. */
-int32_t bmps_debug_set_trace(void* host_pinned);
-
 /* ABI version and a human-readable message for a return/status code. */
 int32_t bmps_version(void);
 const char* bmps_status_string(int32_t code);
@@ -84,6 +79,9 @@ int32_t bmps_build_flags(void);
  * -DBMPS_PHASE_TIMERS build; returns BMPS_E_ARG in normal builds. out4 is a host
  * array of 16 uint64. */
 int32_t bmps_phase_cycles(uint64_t* out4);
+/* Development aid (-DBMPS_PHASE_TIMERS builds; BMPS_E_ARG otherwise): per-warp clock
+ * trace of the Jacobi inner sweep's rotation / Q-update phase, 64 x 8 x 4 uint64. */
+int32_t bmps_inner_trace(uint64_t* out, int32_t n);
 
 /* MpsState.__init__ (mps.py:55-66): |0...0>, unit boundary bonds, stats reset. */
 int32_t bmps_init_product(double* gamma, double* lam, int32_t* dims, double* trunc_err,
@@ -128,7 +126,7 @@ typedef struct bmps_params {
   int32_t pair_skip;     /* skip cross visits of provably clean block pairs (1) */
   int32_t jac_cluster;   /* row-split cluster visits: -1 auto, 0 off, 2 / 4 CTAs (-1) */
   int32_t jac_per_sm;    /* dynamic Jacobi CTAs per SM, 0 = occupancy maximum (0) */
-  int32_t jac_ws;        /* warp-specialised Jacobi (BMPS_EXPERIMENTAL only) (0) */
+  int32_t jac_ws;        /* reserved (the warp-specialised Jacobi was removed); must be 0 */
   int32_t tma_staging;   /* TMA bulk panel staging (BMPS_EXPERIMENTAL only) (0) */
   int32_t cluster_size;  /* CTAs per item in mode 3 (8) */
   int32_t qr_cluster;    /* QR panels taller than 384 rows on a row-split cluster when

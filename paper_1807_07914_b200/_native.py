@@ -55,7 +55,7 @@ _SIGNATURES = {
     "bmps_build_flags": ([], _I),
     "bmps_default_params": ([_P], None),
     "bmps_phase_cycles": ([_P], _I),
-    "bmps_debug_set_trace": ([_P], _I),
+    "bmps_inner_trace": ([_P, _I], _I),
     "bmps_init_product": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P], _I),
     "bmps_apply_1q": ([_P, _P, _I, _I, _I, _P, _P, _I, _P], _I),
     "bmps_apply_2q_workspace_bytes": ([_I, _I], _SZ),

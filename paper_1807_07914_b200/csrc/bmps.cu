@@ -791,10 +791,6 @@ const DevCache& device_cache() {
   cudaFuncSetAttribute(env_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepCapSmem);
   cudaFuncSetAttribute(dense_run_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(sizeof(double2) << kDenseSmemQubits));
-#ifdef BMPS_EXPERIMENTAL
-  cudaFuncSetAttribute(jacobi_ws_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)WsCfg<32>::kSmem);
-#endif
   cudaDeviceGetAttribute(&dc.sms, cudaDevAttrMultiProcessorCount, dev);
   if (dc.sms <= 0) dc.sms = kNumSMs;
   int per_sm = 0;
@@ -804,10 +800,6 @@ const DevCache& device_cache() {
   dc.jac_slots[1] = std::max(1, per_sm) * dc.sms;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_dynamic_kernel<64>, 256, JacCfg<64>::kSmem);
   dc.jac_slots[2] = std::max(1, per_sm) * dc.sms;
-#ifdef BMPS_EXPERIMENTAL
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_ws_kernel<32>, kWsThreads, WsCfg<32>::kSmem);
-  dc.jac_slots[3] = std::max(1, per_sm) * dc.sms;
-#endif
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dc.cl_per_sm, jacobi_cluster_kernel<32, 4>, 256,
                                                 ClCfg<32>::kSmem);
   dc.cl_per_sm = std::max(dc.cl_per_sm, 1);
@@ -886,16 +878,15 @@ int32_t bmps_phase_cycles(uint64_t* out4) {
 #endif
 }
 
-// Development aid: per-CTA progress words of the warp-specialised Jacobi kernel
-// written to pinned host memory (builds with -DBMPS_WS_TRACE only).
-int32_t bmps_debug_set_trace(void* host_pinned) {
-#if defined(BMPS_WS_TRACE) && defined(BMPS_EXPERIMENTAL)
-  void* dptr = nullptr;
-  if (host_pinned && cudaHostGetDevicePointer(&dptr, host_pinned, 0) != cudaSuccess) return BMPS_E_ARG;
-  cudaMemcpyToSymbol(g_ws_trace, &dptr, sizeof(void*));
+// Development aid: per-warp phase-B trace of the inner sweep (-DBMPS_PHASE_TIMERS only):
+// out = 64 rounds x 8 warps x {start, own work done, barrier released, rotations}.
+int32_t bmps_inner_trace(uint64_t* out, int32_t n) {
+#ifdef BMPS_PHASE_TIMERS
+  if (!out || n < 64 * 8 * 4) return BMPS_E_ARG;
+  cudaMemcpyFromSymbol(out, g_inner_trace, sizeof(unsigned long long) * 64 * 8 * 4);
   return BMPS_OK;
 #else
-  (void)host_pinned;
+  (void)out; (void)n;
   return BMPS_E_ARG;
 #endif
 }
@@ -960,10 +951,10 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       P.jac_per_sm < 0 || P.jac_per_sm > 8 || P.cluster_size < 1 || P.cluster_size > 16 ||
       !(P.jacobi_mode == 0 || P.jacobi_mode == 1 || P.jacobi_mode == 4 || P.jacobi_mode == 2 ||
         P.jacobi_mode == 3) ||
-      (P.n_svd_events > 0 && (!P.svd_events || !P.svd_events_used)))
+      P.jac_ws != 0 || (P.n_svd_events > 0 && (!P.svd_events || !P.svd_events_used)))
     return BMPS_E_ARG;
 #ifndef BMPS_EXPERIMENTAL
-  if (P.jac_ws || P.tma_staging || P.jacobi_mode == 2 || P.jacobi_mode == 3) return BMPS_E_ARG;
+  if (P.tma_staging || P.jacobi_mode == 2 || P.jacobi_mode == 3) return BMPS_E_ARG;
 #endif
   const bool timed = P.n_svd_events > 0;
   if (timed && *P.svd_events_used >= P.n_svd_events) return BMPS_E_ARG;
@@ -1105,13 +1096,12 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       // mode (0: 16 when nitems x visits < CTA slots) is off by default
       int wi = P.block_w2 == 64 ? 2 : P.block_w2 == 16 ? 0 : 1;
       if (P.block_w2 == 0) wi = (long long)nitems * (nbmax / 2) < dc.jac_slots[1] ? 0 : 1;
-      const bool ws_mode = wi == 1 && P.jac_ws;
-      int slots = dc.jac_slots[ws_mode ? 3 : wi];
+      int slots = dc.jac_slots[wi];
       // small batches: one visit per cluster of CTAs (row split), see jacobi_cluster_kernel
       // (auto: when a round's visits fit the co-resident clusters; a visit on a cluster
       // of CS CTAs finishes sooner, but CS x fewer visits are in flight)
       int csize = 0;
-      if (wi == 1 && !P.tma_staging && P.jac_cluster != 0 && !ws_mode) {
+      if (wi == 1 && !P.tma_staging && P.jac_cluster != 0) {
         const long long vis_round = (long long)nitems * (nbmax / 2);
         if (P.jac_cluster > 0) csize = P.jac_cluster;
         else if (vis_round <= (long long)dc.cl_per_sm * dc.sms / 4) csize = 4;
@@ -1143,10 +1133,6 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
           return BMPS_E_LAUNCH;
         }
       }
-#ifdef BMPS_EXPERIMENTAL
-      else if (ws_mode)
-        jacobi_ws_kernel<32><<<grid, kWsThreads, WsCfg<32>::kSmem, st>>>(ja);
-#endif
       else if (wi == 2)
         jacobi_dynamic_kernel<64><<<grid, 256, JacCfg<64>::kSmem, st>>>(ja);
       else if (wi == 1)

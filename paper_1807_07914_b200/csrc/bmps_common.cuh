@@ -165,71 +165,36 @@ BMPS_DEV bool jacobi_needs(double a, double b, double2 g, double tol, double noi
   const double lo = fmin(a, b), hi = fmax(a, b);
   if (!(hi > noise2) || !(lo > kNegligible * hi)) return false;
   const double thr = tol * fro;
-  return cabs2(g) > thr * thr * lo;
+  const double g2 = cabs2(g);
+  return g2 > thr * thr * lo && g2 > 1e-290;
 }
 
-#ifndef BMPS_ROT32
-#define BMPS_ROT32 0   // FP32 rotation angles: parity-green, throughput-neutral (measured), off
-#endif
-BMPS_DEV bool jacobi_rotation(double a, double b, double2 g, double tol, double noise2, double fro,
-                              double& c, double& s, double2& e) {
+// Branch-free rotation of one pair: a, b = squared column norms, g = x_i^H x_j,
+// thr2 = (tol ||M||_F)^2. Returns 1 and (c, s, e) if the pair rotates (the test of
+// jacobi_needs, plus |g|^2 > 1e-290 so every reciprocal square root below sees a
+// normal number: a pair that fails only this last test has a column below 1e-131
+// ||M||_F, far under the noise floor), else 0 and the identity.
+// With delta = b - a and rho = sqrt(delta^2 + 4|g|^2):
+//   c = sqrt((1 + |delta| / rho) / 2),  s = sign(delta) |g| / (rho c),  e = g / |g|,
+// the same small-angle rotation as Rutishauser's tangent formula with c^2 + s^2 = 1 by
+// construction. No branches: 1/|g| and 1/rho are independent chains the scheduler
+// interleaves, and the call sits on the inner sweep's critical path.
+BMPS_DEV int jacobi_rotation(double a, double b, double2 g, double thr2, double noise2, double& c,
+                             double& s, double2& e) {
   const double lo = fmin(a, b), hi = fmax(a, b);
-  if (!(hi > noise2) || !(lo > kNegligible * hi)) return false;
   const double g2 = cabs2(g);
-  const double thr = tol * fro;
-  if (!(g2 > thr * thr * lo)) return false;            // |g| > tol * sqrt(lo) * fro
-  // Two dependent rsqrt stages (rho and c in parallel with 1/|g|): with
-  // delta = b - a and rho = sqrt(delta^2 + 4|g|^2),
-  //   c = sqrt((1 + |delta| / rho) / 2),  s = sign(delta) |g| / (rho c),
-  // the same small-angle rotation as Rutishauser's tangent formula
-  // (zeta = delta / 2|g|, t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2))), with
-  // c^2 + s^2 = 1 by construction; the rotation chain is ~40% shorter, which is
-  // what the inner sweep waits on (the FP64 pipe is shared with other CTAs' DMMA).
-#if BMPS_ROT32
-  // Angle in FP32 (the FP32 pipe is not shared with the DMMA of other CTAs), then an
-  // FP64 renormalisation so the transform stays unitary to FP64 rounding: c, s and e
-  // are scaled by 1/sqrt(c^2 + s^2) and 1/|e| with the series 1 - d/2 + 3d^2/8
-  // (|d| ~ 1e-7, remainder ~1e-21). The 2x2 Gram is first scaled by a power of two
-  // (exact) so hi is O(1); a pair whose scaled |g|^2 leaves the FP32 range takes the
-  // FP64 path below. (numpy model on harvested cfg3 theta: same sweep count, sigma
-  // error 9e-14 vs 3e-14 relative.)
-  {
-    const int eh = (int)((__double_as_longlong(hi) >> 52) & 0x7ff);
-    const double sc = __longlong_as_double((long long)(2046 - eh) << 52);   // 2^(1023 - eh)
-    // delta in FP64 first: nearly equal column norms cancel catastrophically in FP32
-    const float df = (float)((b - a) * sc);
-    const float gxf = (float)(g.x * sc), gyf = (float)(g.y * sc);
-    const float g2f = fmaf(gxf, gxf, gyf * gyf);
-    if (g2f > 1e-30f) {
-      const float rrf = rsqrtf(fmaf(df, df, 4.0f * g2f));
-      const float c2f = fmaf(0.5f * fabsf(df), rrf, 0.5f);
-      const float rcf = rsqrtf(c2f);
-      const float rgf = rsqrtf(g2f);
-      const double c0 = (double)(c2f * rcf);
-      const double s0 = (double)((g2f * rgf) * rrf * rcf);
-      const double ex = (double)(gxf * rgf), ey = (double)(gyf * rgf);
-      const double d = fma(c0, c0, s0 * s0) - 1.0;
-      const double n = fma(d, fma(d, 0.375, -0.5), 1.0);
-      const double de = fma(ex, ex, ey * ey) - 1.0;
-      const double ne = fma(de, fma(de, 0.375, -0.5), 1.0);
-      c = c0 * n;
-      s = df < 0.0f ? -(s0 * n) : s0 * n;
-      e = make_double2(ex * ne, ey * ne);
-      return true;
-    }
-  }
-#endif
-  const double rg = g2 > 1e-290 ? fast_rsqrt(g2) : rsqrt(g2);   // 1 / |g|, off the chain
-  const double delta = b - a;
-  const double rho2 = fma(delta, delta, 4.0 * g2);
-  const double rr = rho2 > 1e-290 ? fast_rsqrt(rho2) : rsqrt(rho2);
-  const double c2 = fma(0.5 * fabs(delta), rr, 0.5);       // in [1/2, 1]
-  const double rc = fast_rsqrt(c2);                         // 1 / c
-  c = c2 * rc;
-  const double sm = (g2 * rg) * rr * rc;                    // |g| / (rho c)
-  s = delta < 0 ? -sm : sm;
-  e = make_double2(g.x * rg, g.y * rg);
-  return true;
+  const bool act = (hi > noise2) && (lo > kNegligible * hi) && (g2 > thr2 * lo) && (g2 > 1e-290);
+  const double g2s = act ? g2 : 1.0;                      // keeps the arithmetic finite
+  const double delta = act ? b - a : 0.0;
+  const double rg = fast_rsqrt(g2s);                      // 1 / |g|
+  const double rr = fast_rsqrt(fma(delta, delta, 4.0 * g2s));
+  const double c2 = fma(0.5 * fabs(delta), rr, 0.5);      // in [1/2, 1]
+  const double rc = fast_rsqrt(c2);                       // 1 / c
+  const double sm = (g2s * rg) * rr * rc;                 // |g| / (rho c)
+  c = act ? c2 * rc : 1.0;
+  s = act ? (delta < 0 ? -sm : sm) : 0.0;
+  e = act ? make_double2(g.x * rg, g.y * rg) : make_double2(1.0, 0.0);
+  return act ? 1 : 0;
 }
 
 // cp.async 16-byte global -> shared copy, zero-filled when !valid.

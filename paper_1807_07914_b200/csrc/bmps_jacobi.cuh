@@ -38,6 +38,10 @@ constexpr bool kTmaStaging = true;    // TMA bulk panel staging compiled in (mea
 constexpr bool kTmaStaging = false;
 #endif
 
+#ifndef BMPS_GROUP_WARPS_HIGH
+#define BMPS_GROUP_WARPS_HIGH 1   // inner sweep: the per-group scalar phase runs on the CTA's last warps
+#endif
+
 #ifndef BMPS_JAC_MINB
 #define BMPS_JAC_MINB 4   // resident Jacobi CTAs per SM the register budget is sized for
 #endif
@@ -45,6 +49,10 @@ constexpr bool kTmaStaging = false;
 #ifdef BMPS_PHASE_TIMERS
 // cycles spent in [0] Gram pass, [1] inner sweep (incl. check), [2] apply pass, [3] visits
 __device__ unsigned long long g_phase_cycles[16];
+// per-warp arrival trace of the inner sweep's phase B (CTA 0, first 64 rounds): start of
+// the phase, end of the warp's own work, release from the counting barrier
+__device__ unsigned long long g_inner_trace[64 * 8 * 4];
+__device__ int g_inner_trace_n;
 #define BMPS_TICK(var) const long long var = clock64()
 #define BMPS_ACC(slot, t0, t1) \
   if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[slot], (unsigned long long)((t1) - (t0)))
@@ -54,16 +62,6 @@ __device__ unsigned long long g_phase_cycles[16];
 #define WS_ACC(lead, slot, t0, t1)
 #define BMPS_TICK(var)
 #define BMPS_ACC(slot, t0, t1)
-#endif
-
-#ifdef BMPS_WS_TRACE
-// development aid: per-CTA progress words in pinned host memory (readable while a
-// kernel hangs), set by bmps_debug_set_trace
-__device__ volatile int* g_ws_trace;
-#define WS_TR(slot, val) \
-  do { if (g_ws_trace) g_ws_trace[blockIdx.x * 16 + (slot)] = (int)(val); } while (0)
-#else
-#define WS_TR(slot, val) do { } while (0)
 #endif
 
 template <int W2>
@@ -147,19 +145,19 @@ struct JacArgs {
   int nbcap;
 };
 
-// Rotation parameters of one inner round (NP = w pairs).
-template <int NP>
-struct RotBuf {
-  double c[NP], s[NP];
-  double2 e[NP];
-  double2 se[NP], ce[NP];   // s e, c e
-  int i[NP], j[NP], act[NP];
-};
-// Two rounds' parameters: round rho's are read by the Q update while the rotation
-// warp writes round rho + 1's (jac_inner).
+// Shared state of the inner (Gram-space) sweep, see jac_inner: per column group the
+// four rotations of the current round -- cs = (c, s), colb[0] = s e, colb[1] = -c e, so
+// that both columns of a rotated pair are x_a c - conj(s e) x_b and x_a s - conj(-c e) x_b
+// (one code path indexed by the column half); ab = a | b << 4 | active << 8 (columns
+// local to the group) -- and the group's rotation count of the batch (double-buffered
+// by batch parity).
 template <int W2>
-struct RotShared {
-  RotBuf<W2 / 2> b[2];
+struct InnerShared {
+  static constexpr int NG = W2 / 8;
+  double2 cs[NG][4];
+  double2 colb[NG][2][4];
+  int ab[NG][4];
+  int cnt[2][NG];
 };
 
 // Thread groups a Jacobi phase runs on. CtaGrp: the whole CTA (classic kernels,
@@ -595,119 +593,311 @@ BMPS_DEV void inner_pair(bool full, int rho, int p, int& i, int& j) {
   }
 }
 
-// One (or more) cyclic Jacobi sweeps on the W2 x W2 Gram, accumulating Q.
+// One (or more) cyclic Jacobi sweeps on the W2 x W2 Gram G, accumulating Q.
 // Returns the number of rotations of the first sweep (block-uniform).
 //
-// Per round rho, two barriers:
-//   A. G <- J_rho^H G J_rho as independent 2x2 blocks (upper triangle computed,
-//      lower mirrored), all threads; barrier;
-//   B. the first warp of the group computes round rho + 1's rotations from the
-//      updated G into the other parameter buffer WHILE the remaining warps apply
-//      round rho's rotations to Q (Q <- Q J_rho); counting barrier.
-// The latency-bound rotation chain (square roots and divisions of the 2x2 Gram
-// entries) thus runs under the Q update instead of in front of a barrier the whole
-// CTA waits at (ncu: that wait was the largest stall of the kernel). Every element
-// of G and Q sees the same operations in the same order as a round-by-round sweep.
-template <int W2, class G = CtaGrp>
-BMPS_DEV int jac_inner(double2* sG, double2* sQ, RotShared<W2>& rs, double tol, double noise2,
-                       double fro, bool full, int max_inner) {
+// Pair ordering: round R pairs column i with i ^ R -- R = 1 .. W2-1 for a full sweep,
+// R = W2/2 .. W2-1 for the cross sweep between the two blocks of the panel (each pair
+// exactly once either way). Rounds are taken in batches of four, R = 4 mm + r: within a
+// batch every rotation stays inside a group of 8 columns (two aligned quads qa and
+// qb = qa ^ mm; for mm = 0 the pairs stay inside each quad), so the W2/8 groups evolve
+// independently for four rounds:
+//   S. one warp per group runs the batch's rounds on the group's 8 x 8 diagonal block of
+//      G (4 rotations per round on 4 lanes; the off-diagonal 2x2 pair blocks as lane
+//      pairs, the rotated diagonal blocks in closed form) and accumulates the group's
+//      8 x 8 unitary K_g = J_r0 .. J_r3 -- warp-synchronous, no CTA barrier inside;
+//   M. after one barrier all warps apply the batch on FP64 tensor cores: the
+//      off-diagonal group blocks G_pq <- K_p^H G_pq K_q (8 x 8 x 8 complex products,
+//      3-product DMMA, the mirror block written from the same accumulators) and
+//      Q[:, g] <- Q[:, g] K_g; second barrier.
+// Two CTA barriers per four rounds, and the 2 (W2/8 - 1) / (W2/8) of the Gram-space
+// work that lies outside the diagonal group blocks runs as dense 8 x 8 tiles on the
+// tensor pipe instead of scalar FP64 with shared-memory round trips per round (the
+// round-by-round sweep was bound by those and by two barriers per round). `work` holds
+// the K_g (W2/8 x 64 complex; the idle staging buffer 0).
+template <int W2>
+BMPS_DEV int batch_col(int qa, int qb, int a) { return 4 * (a < 4 ? qa : qb) + (a & 3); }
+
+BMPS_DEV double2 shfl_xor_z(double2 v, int mask) {
+  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, mask), __shfl_xor_sync(0xffffffffu, v.y, mask));
+}
+
+// Phase S of jac_inner for one column group (one warp): a run of rounds in which pair P
+// of round ri joins local columns A_P and B_{P ^ ri}, register-resident.
+//   MODE 0: A_P = P, B_P = 4 + P, rounds ri = 0..3 (quad qa against quad qb);
+//   MODE 1: A_P = 2P, B_P = 2P + 1, one round (pairs (0,1)(2,3) inside each quad);
+//   MODE 2: A_P = {0,1,4,5}, B_P = A_P + 2, rounds ri = 0, 1 ({0,1} x {2,3} per quad).
+// Lanes 0..15 = (t, u) hold the 2x2 pair block (rows of pair t, columns of pair u) of
+// the group's 8 x 8 diagonal Gram block -- both triangles, each lane rotating its own
+// copy -- and all 32 lanes = (row k, pair tk) hold the two columns of pair tk of K_g.
+// From one round to the next only the B partners change (P ^ ri), i.e. the B-side
+// entries move between lanes by XOR shuffles; the four rotations of a round are computed
+// by the diagonal lanes (t, t) from their own registers and reach the other lanes
+// through 192 bytes of shared memory -- the only memory round trip of a round. Returns
+// the number of rotations. `k_identity`: K_g starts as the identity (not loaded).
+template <int W2, int MODE>
+BMPS_DEV int jac_group_rounds(double2* sG, double2* Kg, InnerShared<W2>& is, int g, int qa, int qb,
+                              bool k_identity, double thr2, double noise2) {
   using C = JacCfg<W2>;
-  constexpr int w = W2 / 2;
-  static_assert(w <= 32, "one warp computes a round's rotations");
-  constexpr int kQThreads = G::kN - 32;   // threads of the Q update in phase B
-  const int tid = G::tid();
+  constexpr int NR = MODE == 0 ? 4 : MODE == 1 ? 1 : 2;
+  const int lane = threadIdx.x & 31;
+  const int t = (lane >> 2) & 3, u = lane & 3;
+  const int k = lane & 7, tk = lane >> 3;
+  const bool drole = lane < 16;
+  auto la = [](int P) { return MODE == 0 ? P : MODE == 1 ? 2 * P : (P & 1) + 4 * (P >> 1); };
+  auto lb = [](int P) { return MODE == 0 ? 4 + P : MODE == 1 ? 2 * P + 1 : (P & 1) + 4 * (P >> 1) + 2; };
+  const int cAt = batch_col<W2>(qa, qb, la(t)), cAu = batch_col<W2>(qa, qb, la(u));
+  double2 g00 = make_double2(0.0, 0.0), g01 = g00, g10 = g00, g11 = g00;
+  if (drole) {
+    const int cBt = batch_col<W2>(qa, qb, lb(t)), cBu = batch_col<W2>(qa, qb, lb(u));
+    g00 = sG[cAt + cAu * C::LDGG];
+    g01 = sG[cAt + cBu * C::LDGG];
+    g10 = sG[cBt + cAu * C::LDGG];
+    g11 = sG[cBt + cBu * C::LDGG];
+  }
+  double2 ka, kb;
+  if (k_identity) {
+    ka = make_double2(k == la(tk) ? 1.0 : 0.0, 0.0);
+    kb = make_double2(k == lb(tk) ? 1.0 : 0.0, 0.0);
+  } else {
+    ka = Kg[k + 8 * la(tk)];
+    kb = Kg[k + 8 * lb(tk)];
+  }
+  int cnt = 0;
+#pragma unroll
+  for (int ri = 0; ri < NR; ++ri) {
+#ifdef BMPS_INNER_TIMERS
+    const long long q0 = clock64();
+#endif
+    if (ri > 0) {
+      const int x = ri ^ (ri - 1);
+      g01 = shfl_xor_z(g01, x);
+      g10 = shfl_xor_z(g10, x << 2);
+      g11 = shfl_xor_z(g11, x | (x << 2));
+      kb = shfl_xor_z(kb, x << 3);
+    }
+    int act = 0;
+#ifdef BMPS_INNER_TIMERS
+    const long long q1 = clock64();
+#endif
+    if (drole && t == u) {
+      double c, s;
+      double2 e;
+      act = jacobi_rotation(g00.x, g11.x, g01, thr2, noise2, c, s, e);
+      is.cs[g][t] = make_double2(c, s);
+      is.colb[g][0][t] = cscale(e, s);
+      is.colb[g][1][t] = cscale(e, -c);
+    }
+#ifdef BMPS_INNER_TIMERS
+    const long long q2 = clock64();
+#endif
+    const unsigned am = __ballot_sync(0xffffffffu, act);
+    __syncwarp();
+#ifdef BMPS_INNER_TIMERS
+    const long long q3 = clock64();
+#endif
+    if (am) {
+      cnt += __popc(am);
+      if (drole) {
+        // columns by pair u (right rotation), then rows by pair t (left rotation)
+        const double2 csu = is.cs[g][u], seu = is.colb[g][0][u], mcu = is.colb[g][1][u];
+        const double2 r00 = cmsc(g00, csu.x, seu, g01), r01 = cmsc(g00, csu.y, mcu, g01);
+        const double2 r10 = cmsc(g10, csu.x, seu, g11), r11 = cmsc(g10, csu.y, mcu, g11);
+        const double2 cst = is.cs[g][t], set = is.colb[g][0][t], mct = is.colb[g][1][t];
+        g00 = cms(r00, cst.x, set, r10);
+        g01 = cms(r01, cst.x, set, r11);
+        g10 = cms(r00, cst.y, mct, r10);
+        g11 = cms(r01, cst.y, mct, r11);
+        if (act) {   // the rotated pair itself: diagonal by construction
+          g00.y = 0.0;
+          g11.y = 0.0;
+          g01 = make_double2(0.0, 0.0);
+          g10 = make_double2(0.0, 0.0);
+        }
+      }
+      {
+        const double2 csk = is.cs[g][tk];
+        const double2 na = cmsc(ka, csk.x, is.colb[g][0][tk], kb);
+        kb = cmsc(ka, csk.y, is.colb[g][1][tk], kb);
+        ka = na;
+      }
+    }
+    __syncwarp();   // the parameters are consumed before the next round rewrites them
+#ifdef BMPS_INNER_TIMERS
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+      const long long q4 = clock64();
+      atomicAdd(&g_phase_cycles[8], (unsigned long long)(q1 - q0));
+      atomicAdd(&g_phase_cycles[9], (unsigned long long)(q2 - q1));
+      atomicAdd(&g_phase_cycles[10], (unsigned long long)(q3 - q2));
+      atomicAdd(&g_phase_cycles[11], (unsigned long long)(q4 - q3));
+      atomicAdd(&g_phase_cycles[12], 1ull);
+    }
+#endif
+  }
+  constexpr int xl = NR - 1;   // B partners of the last round
+  if (drole) {
+    const int cBt = batch_col<W2>(qa, qb, lb(t ^ xl)), cBu = batch_col<W2>(qa, qb, lb(u ^ xl));
+    sG[cAt + cAu * C::LDGG] = g00;
+    sG[cAt + cBu * C::LDGG] = g01;
+    sG[cBt + cAu * C::LDGG] = g10;
+    sG[cBt + cBu * C::LDGG] = g11;
+  }
+  Kg[k + 8 * la(tk)] = ka;
+  Kg[k + 8 * lb(tk ^ xl)] = kb;
+  return cnt;
+}
+
+template <int W2, class G = CtaGrp>
+BMPS_DEV int jac_inner(double2* sG, double2* sQ, double2* work, InnerShared<W2>& is, double tol,
+                       double noise2, double fro, bool full, int max_inner) {
+  using C = JacCfg<W2>;
+  constexpr int NQ = W2 / 4, NG = W2 / 8, NW = G::kN / 32;
+  constexpr int NBo = NG * (NG - 1) / 2;   // off-diagonal group blocks (p < q)
+  constexpr int NT = NBo + NG * NG;        // + Q tiles (8 rows x one group)
+  static_assert(NW >= NG, "one warp per column group");
+  const int tid = G::tid(), lane = tid & 31, wrp = tid >> 5;
+  const int kr = lane & 3, rc = lane >> 2;
   for (int idx = tid; idx < W2 * W2; idx += G::n()) {
     const int i = idx % W2, j = idx / W2;
     sQ[i + j * C::LDG] = make_double2(i == j ? 1.0 : 0.0, 0.0);
   }
-  // rotation of pair p (< w) in round rho into buffer rb; returns 1 if it rotates
-  auto rotate = [&](int rho, int p, RotBuf<w>& rb) -> int {
-    int i, j;
-    inner_pair<W2>(full, rho, p, i, j);
-    double c = 1.0, s = 0.0;
-    double2 e = make_double2(1.0, 0.0);
-    int act = jacobi_rotation(sG[i + i * C::LDGG].x, sG[j + j * C::LDGG].x, sG[i + j * C::LDGG], tol,
-                              noise2, fro, c, s, e);
-    if (!act) {
-      c = 1.0;
-      s = 0.0;
-      e = make_double2(1.0, 0.0);
-    }
-    rb.i[p] = i;
-    rb.j[p] = j;
-    rb.act[p] = act;
-    rb.c[p] = c;
-    rb.s[p] = s;
-    rb.e[p] = e;
-    rb.se[p] = cscale(e, s);
-    rb.ce[p] = cscale(e, c);
-    return act;
-  };
   int first = 0;
-  const int rounds = full ? W2 - 1 : w;
+  const int nbatch = full ? NQ : NQ / 2;
+  const double thr2 = (tol * fro) * (tol * fro);
+  // Spare warps (W2 <= 32: half of the CTA) apply batch b's K_g to Q while the group
+  // warps already run batch b + 1's rounds: Q is not read by the sweep itself, so only the
+  // off-diagonal Gram blocks stay between the two barriers. K_g and the rotation counts
+  // are double-buffered by batch parity.
+  constexpr bool kDefer = NW >= 2 * NG;
+  constexpr int NSP = kDefer ? NW - NG : NW;   // warps of a deferred Q pass
+  // quads of group g in batch mm: the g-th qa with qa < qa ^ mm (bit hb clear); mm = 0
+  // pairs inside the quads 2g and 2g + 1
+  auto group_quads = [](int mm, int g, int& qa, int& qb) {
+    if (mm == 0) {
+      qa = 2 * g;
+      qb = 2 * g + 1;
+    } else {
+      const int hb = 31 - __clz(mm);
+      qa = ((g >> hb) << (hb + 1)) | (g & ((1 << hb) - 1));
+      qb = qa ^ mm;
+    }
+  };
+  // Q[8 t .. 8 t + 7, group g] <- (same) K_g for tile = g + NG t (one warp)
+  auto q_tile = [&](int tile, int mm, const double2* K, const int* cnt) {
+    const int g = tile % NG, t8 = (tile / NG) * 8;
+    if (!cnt[g]) return;
+    int qa, qb;
+    group_quads(mm, g, qa, qb);
+    const double2* Kg = K + g * 64;
+    double acc[kZ3];
+#pragma unroll
+    for (int z = 0; z < kZ3; ++z) acc[z] = 0.0;
+#pragma unroll
+    for (int sx = 0; sx < 2; ++sx)
+      zmma3(acc, sQ[(t8 + rc) + batch_col<W2>(qa, qb, 4 * sx + kr) * C::LDG], Kg[(4 * sx + kr) + rc * 8]);
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      sQ[(t8 + rc) + batch_col<W2>(qa, qb, 2 * kr + h) * C::LDG] = z3_get(acc, h);
+  };
+  const bool gwarp = BMPS_GROUP_WARPS_HIGH ? wrp >= NW - NG : wrp < NG;
+  const int gidx = BMPS_GROUP_WARPS_HIGH ? wrp - (NW - NG) : wrp;       // group of a group warp
+  const int sidx = BMPS_GROUP_WARPS_HIGH ? wrp : wrp - NG;              // index of a spare warp
   for (int it = 0; it < max_inner; ++it) {
-    int any = 0;
-    int nact = G::count(tid < w ? rotate(0, tid, rs.b[0]) : 0);
-    for (int rho = 0; rho < rounds; ++rho) {
+    int any = 0, prev_nact = 0, prev_mm = 0;
+    for (int bi = 0; bi < nbatch; ++bi) {
       BMPS_TICK(tr0);
-      RotBuf<w>& cur = rs.b[rho & 1];
-      RotBuf<w>& nxt = rs.b[(rho + 1) & 1];
+      const int mm = full ? bi : NQ / 2 + bi;
+      int* cnt = is.cnt[bi & 1];
+      double2* K = work + (kDefer ? (bi & 1) * NG * 64 : 0);
+      if (gwarp) {
+        // ---- S: the batch's rounds, one group per warp (the group warps sit on
+        // distinct SM sub-partitions: NG = 4 consecutive warp ids) ----
+        const int g = gidx;
+        int qa, qb;
+        group_quads(mm, g, qa, qb);
+        double2* Kg = K + g * 64;
+        int gcnt;
+        if (mm == 0) {
+          // pairs inside each quad: (0,1)(2,3), then the 2 x 2 cross rounds of {0,1} x {2,3}
+          gcnt = jac_group_rounds<W2, 1>(sG, Kg, is, g, qa, qb, true, thr2, noise2);
+          __syncwarp();
+          gcnt += jac_group_rounds<W2, 2>(sG, Kg, is, g, qa, qb, false, thr2, noise2);
+        } else {
+          gcnt = jac_group_rounds<W2, 0>(sG, Kg, is, g, qa, qb, true, thr2, noise2);
+        }
+        if (lane == 0) cnt[g] = gcnt;
+      } else if (kDefer && prev_nact) {
+        // the previous batch's Q update, under this batch's rounds
+        for (int tile = sidx; tile < NG * NG; tile += NSP)
+          q_tile(tile, prev_mm, work + ((bi - 1) & 1) * NG * 64, is.cnt[(bi - 1) & 1]);
+      }
+      G::sync();
+      BMPS_TICK(tr1);
+      BMPS_ACC(4, tr0, tr1);
+      int nact = 0;
+#pragma unroll
+      for (int g = 0; g < NG; ++g) nact += cnt[g];
       any += nact;
       if (nact) {
-        // A. G <- J^H G J as independent 2x2 blocks (p <= q computed, (q, p) mirrored)
-        for (int idx = tid; idx < w * (w + 1) / 2; idx += G::n()) {
-          const int q = (int)((sqrtf(8.0f * (float)idx + 1.0f) - 1.0f) * 0.5f);
-          const int p = idx - q * (q + 1) / 2;
-          if (!(cur.act[p] | cur.act[q])) continue;  // identity on both sides
-          const int ip = cur.i[p], jp = cur.j[p], iq = cur.i[q], jq = cur.j[q];
-          const double cp = cur.c[p], sp = cur.s[p], cq = cur.c[q], sq = cur.s[q];
-          const double2 sep = cur.se[p], cep = cur.ce[p], seq = cur.se[q], ceq = cur.ce[q];
-          const double2 g00 = sG[ip + iq * C::LDGG], g01 = sG[ip + jq * C::LDGG];
-          const double2 g10 = sG[jp + iq * C::LDGG], g11 = sG[jp + jq * C::LDGG];
-          // right: [x_iq, x_jq] <- [x_iq, x_jq] [[cq, sq], [-sq e_q*, cq e_q*]]
-          const double2 r00 = cmsc(g00, cq, seq, g01);
-          const double2 r01 = cmac(g00, sq, ceq, g01);
-          const double2 r10 = cmsc(g10, cq, seq, g11);
-          const double2 r11 = cmac(g10, sq, ceq, g11);
-          // left: rows ip, jp by J_p^H = [[cp, -sp e_p], [sp, cp e_p]]
-          const double2 n00 = cms(r00, cp, sep, r10);
-          const double2 n01 = cms(r01, cp, sep, r11);
-          const double2 n10 = cma(r00, sp, cep, r10);
-          const double2 n11 = cma(r01, sp, cep, r11);
-          sG[ip + iq * C::LDGG] = n00;
-          sG[ip + jq * C::LDGG] = n01;
-          sG[jp + iq * C::LDGG] = n10;
-          sG[jp + jq * C::LDGG] = n11;
-          if (p != q) {
-            sG[iq + ip * C::LDGG] = cconj(n00);
-            sG[jq + ip * C::LDGG] = cconj(n01);
-            sG[iq + jp * C::LDGG] = cconj(n10);
-            sG[jq + jp * C::LDGG] = cconj(n11);
+        // ---- M: the off-diagonal group blocks on the tensor cores ----
+        for (int task = wrp; task < (kDefer ? NBo : NT); task += NW) {
+          if (task < NBo) {
+            int q = 1;
+            while (q * (q + 1) / 2 <= task) ++q;
+            const int p = task - q * (q - 1) / 2;
+            if (!(cnt[p] | cnt[q])) continue;   // both K are the identity
+            int pa, pb, qa, qb;
+            group_quads(mm, p, pa, pb);
+            group_quads(mm, q, qa, qb);
+            const double2* Kp = K + p * 64;
+            const double2* Kq = K + q * 64;
+            const int row = batch_col<W2>(pa, pb, rc);
+            double acc[kZ3];
+#pragma unroll
+            for (int z = 0; z < kZ3; ++z) acc[z] = 0.0;
+            // T = G_pq K_q
+#pragma unroll
+            for (int sx = 0; sx < 2; ++sx)
+              zmma3(acc, sG[row + batch_col<W2>(qa, qb, 4 * sx + kr) * C::LDGG], Kq[(4 * sx + kr) + rc * 8]);
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              sG[row + batch_col<W2>(qa, qb, 2 * kr + h) * C::LDGG] = z3_get(acc, h);
+            __syncwarp();
+            // G_pq <- K_p^H T (and the mirror block)
+#pragma unroll
+            for (int z = 0; z < kZ3; ++z) acc[z] = 0.0;
+            const int cq = batch_col<W2>(qa, qb, rc);
+#pragma unroll
+            for (int sx = 0; sx < 2; ++sx)
+              zmma3(acc, cconj(Kp[(4 * sx + kr) + rc * 8]),
+                    sG[batch_col<W2>(pa, pb, 4 * sx + kr) + cq * C::LDGG]);
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int cc = batch_col<W2>(qa, qb, 2 * kr + h);
+              const double2 v = z3_get(acc, h);
+              sG[row + cc * C::LDGG] = v;
+              sG[cc + row * C::LDGG] = cconj(v);
+            }
+          } else {
+            q_tile(task - NBo, mm, K, cnt);
           }
         }
         G::sync();
       }
-      BMPS_TICK(tr1);
-      BMPS_ACC(5, tr0, tr1);
-      // B. next round's rotations (first warp) || Q <- Q J_rho (the other warps)
-      int act = 0;
-      if (tid < 32) {
-        if (rho + 1 < rounds && tid < w) act = rotate(rho + 1, tid, nxt);
-      } else if (nact) {
-        for (int idx = tid - 32; idx < W2 * w; idx += kQThreads) {
-          const int k = idx % W2, q = idx / W2;
-          if (!cur.act[q]) continue;
-          const int iq = cur.i[q], jq = cur.j[q];
-          const double cq = cur.c[q], sq = cur.s[q];
-          const double2 qi = sQ[k + iq * C::LDG], qj = sQ[k + jq * C::LDG];
-          sQ[k + iq * C::LDG] = cmsc(qi, cq, cur.se[q], qj);
-          sQ[k + jq * C::LDG] = cmac(qi, sq, cur.ce[q], qj);
-        }
-      }
-      nact = G::count(act);
+      prev_nact = nact;
+      prev_mm = mm;
       BMPS_TICK(tr2);
-      BMPS_ACC(4, tr1, tr2);
+      BMPS_ACC(5, tr1, tr2);
       BMPS_ACC(6, 0, 1);
+    }
+    if (kDefer) {
+      if (prev_nact)
+        for (int tile = wrp; tile < NG * NG; tile += NW)
+          q_tile(tile, prev_mm, work + ((nbatch - 1) & 1) * NG * 64, is.cnt[(nbatch - 1) & 1]);
+      G::sync();
     }
     if (it == 0) first = any;
     if (!any) break;
@@ -732,8 +922,8 @@ BMPS_DEV double2* jac_ring3(double2* sP, double2* sQ, int k) {
 template <int W2, class G = CtaGrp>
 BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, double noise2,
                         double fro, bool full, int max_inner, bool resident, double2* sG,
-                        double2* sQ, double2* sP, RotShared<W2>& rs, JacStage& st, bool tma,
-                        double2* gcache = nullptr, bool inner_regs = false) {
+                        double2* sQ, double2* sP, InnerShared<W2>& rs, JacStage& st, bool tma,
+                        double2* gcache = nullptr) {
   using C = JacCfg<W2>;
   BMPS_TICK(tv0);
   const int nch = (r + C::RC - 1) / C::RC;
@@ -804,12 +994,9 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
   if (cross_gram) jac_gram_store_cross<W2, G>(gacc, sG, scratch, cI, cJ);
   else jac_gram_store<W2, G>(gacc, sG, scratch);
   G::sync();
-  const bool staged = nch == 1;  // single chunk still in buffer 0 from the Gram pass
-  // prefetch the first apply chunk so its load overlaps the inner sweep
-  if (!resident && !staged) {
-    if (bulk) jac_issue_bulk<W2>(sP, st, 0, X, r, c, 0, I, J);
-    else jac_issue_chunk<W2>(sP, X, r, c, 0, I, J);
-  }
+  // staging buffer 0 is the inner sweep's workspace (the K_g), so the panel is
+  // re-streamed for the apply even when it is a single chunk
+  constexpr bool staged = false;
   // fast path: one parallel test of every pair the inner sweep would visit
   int need = 0;
   {
@@ -829,21 +1016,19 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
                           noise2, fro);
     }
   }
-  const int nrot = (G::count(need) != 0) ? jac_inner<W2, G>(sG, sQ, rs, tol, noise2, fro, full, max_inner)
-                                          : 0;
+  const int needed = G::count(need);
+  const int nrot = needed ? jac_inner<W2, G>(sG, sQ, sP, rs, tol, noise2, fro, full, max_inner) : 0;
   BMPS_TICK(tv2);
   BMPS_ACC(1, tv1, tv2);
   BMPS_ACC(3, 0, 1);
   if (gcache != nullptr && !resident && (full || nrot > 0)) jac_cache_store<W2, G>(sG, cI, cJ);
   if (C::G_IN_BUF) G::sync();  // sG (buffer 1) is read before the apply refills it
-  if (nrot == 0) {
-    if (!resident && !staged) {
-      if (bulk) jac_wait_bulk(st, 0);
-      else cp_async_wait<0>();
-    }
-    return false;
-  }
+  if (nrot == 0) return false;
   double aacc[C::AT][kZ3];
+  if (!resident) {
+    if (bulk) jac_issue_bulk<W2>(sP, st, 0, X, r, c, 0, I, J);
+    else jac_issue_chunk<W2>(sP, X, r, c, 0, I, J);
+  }
   if (resident) {
     jac_apply_mma<W2>(aacc, sP, sQ);
     G::sync();
@@ -912,7 +1097,7 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_ke
   double2* sQ = jsm;
   double2* sP = sQ + W2 * C::LDG;
   double2* sG = C::G_IN_BUF ? sP + C::BUF : sP + C::NBUF * C::BUF;
-  __shared__ RotShared<W2> rs;
+  __shared__ InnerShared<W2> rs;
   __shared__ unsigned long long jbar[2];
   const int item = blockIdx.y;
   ItemMeta* m = args.meta + item;
@@ -931,7 +1116,7 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_ke
   if (nb == 2) {
     // single panel: the whole matrix is one visit, iterated to convergence
     if (blockIdx.x != 0) return;
-    const bool resident = r <= C::RC;
+    const bool resident = false;   // (the inner sweep needs staging buffer 0)
     if (resident) jac_load_resident<W2>(sP, X, r, c);
     int sweep = 0;
     bool clean = false;
@@ -1042,7 +1227,7 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dy
   double2* sQ = jsm;
   double2* sP = sQ + W2 * C::LDG;
   double2* sG = C::G_IN_BUF ? sP + C::BUF : sP + C::NBUF * C::BUF;
-  __shared__ RotShared<W2> rs;
+  __shared__ InnerShared<W2> rs;
   __shared__ int s_item, s_v;
   __shared__ unsigned s_round;
   __shared__ unsigned long long jbar[2];
@@ -1152,7 +1337,7 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dy
     JacSched* sc = args.sched + i;
     if (nb == 2) {
       // single panel: the one claimer iterates the whole item to convergence
-      const bool resident = r <= C::RC;
+      const bool resident = false;   // (the inner sweep needs staging buffer 0)
       if (resident) jac_load_resident<W2>(sP, X, r, c);
       int sweep = 0;
       bool clean = false;
@@ -1249,58 +1434,7 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dy
 }
 
 // ---------------------------------------------------------------------------
-// Warp-specialised dynamic kernel (default for W2 = 32).
-//
-// A visit is Gram -> inner (Gram-space) sweep -> apply. The inner sweep is a
-// chain of latency-bound rounds that leaves the tensor pipe idle, so the CTA
-// is split into 8 math warps (Gram / apply on DMMA, cp.async staging) and 4
-// rotation warps (inner sweep). Visits are software-pipelined two deep: while
-// the rotation warps sweep the Gram of visit k, the math warps form the Gram of
-// visit k+1 and then apply visit k's rotations, so the inner sweep runs under
-// the tensor work. Two Gram buffers and two Q buffers hand visits back and
-// forth through named barriers (GF[b]: Gram b full, math arrives / rotation
-// waits; QF[b]: Q b full, rotation arrives / math waits; the alternation makes
-// the "empty" signals implicit). Claiming, exact visit skipping and round
-// bookkeeping are those of jacobi_dynamic_kernel.
-constexpr int kWsMath = 256, kWsRot = 128, kWsPair = kWsMath + kWsRot, kWsSched = kWsPair;
-constexpr int kWsThreads = kWsPair + 32;   // + one scheduler warp
-using WsMath = NamedGrp<0, kWsMath, 1>;
-using WsRot = NamedGrp<kWsMath, kWsRot, 2>;
-// GF / QF hand-offs between the math and rotation warps (384 threads; the
-// scheduler warp does not take part). The waiting side uses the convergent
-// intrinsic; the arriving side calls it right after a barrier of its own group
-// (converged, straight-line).
-BMPS_DEV void ws_arrive(int id) {
-  if (id == 3) asm volatile("bar.arrive 3, %0;\n" ::"n"(kWsPair) : "memory");
-  else if (id == 4) asm volatile("bar.arrive 4, %0;\n" ::"n"(kWsPair) : "memory");
-  else if (id == 5) asm volatile("bar.arrive 5, %0;\n" ::"n"(kWsPair) : "memory");
-  else asm volatile("bar.arrive 6, %0;\n" ::"n"(kWsPair) : "memory");
-}
-BMPS_DEV void ws_wait(int id) {
-  if (id == 3) __barrier_sync_count(3, kWsPair);
-  else if (id == 4) __barrier_sync_count(4, kWsPair);
-  else if (id == 5) __barrier_sync_count(5, kWsPair);
-  else __barrier_sync_count(6, kWsPair);
-}
-constexpr int kWsGf = 3, kWsQf = 5;   // named barrier ids GF[0..1], QF[0..1]
-
-
-
-template <int W2>
-struct WsCfg {
-  using C = JacCfg<W2>;
-  static constexpr int QSZ = W2 * C::LDG;    // one Q buffer (complex elements)
-  static constexpr int GSZ = W2 * C::LDGG;   // one Gram buffer
-  static constexpr size_t kSmem = (size_t)(2 * QSZ + 2 * GSZ + 2 * C::BUF) * sizeof(double2);
-};
-
-// Visit handed from the math warps to the rotation warps (and nrot back).
-struct WsVisit {
-  double tol, noise2, fro;
-  double2* cI;
-  double2* cJ;
-  int full, stop, nrot, pad;
-};
+// Visit claiming and round bookkeeping shared by the cluster kernel.
 
 // Round bookkeeping of a finished visit (one thread): the pair log for exact
 // skipping, the item's dirty flag, and -- for the last visit of a round -- the
@@ -1410,366 +1544,6 @@ BMPS_DEV int ws_claim(const JacArgs& args, int& cursor, int& v_out, unsigned& rn
   }
 }
 
-#ifdef BMPS_EXPERIMENTAL  // the warp-specialised pipeline (measured slower)
-
-BMPS_DEV void cp_async_wait_n(int n) {
-  if (n <= 0) cp_async_wait<0>();
-  else if (n == 1) cp_async_wait<1>();
-  else if (n == 2) cp_async_wait<2>();
-  else cp_async_wait<3>();
-}
-
-// Staging ring of the warp-specialised visit phases: slots 0, 1 are the staging
-// buffers, slots 2, 3 borrow whichever Q / Gram buffers are idle in that phase
-// (all hold >= one RCP x W2 chunk).
-struct WsRing {
-  double2* s0;
-  double2* s2;
-  double2* s3;
-  int depth;
-  template <int W2>
-  BMPS_DEV double2* slot(int k) const {
-    return k < 2 ? s0 + k * JacCfg<W2>::BUF : (k == 2 ? s2 : s3);
-  }
-};
-
-// Gram of the panel (I, J) into sG (math warps), chunks streamed through a
-// depth-deep cp.async ring (depth - 1 chunks in flight). Cross visits form only
-// G_IJ and take the rotated intra-block Grams from the cache.
-template <int W2>
-BMPS_DEV void ws_gram(const double2* X, int r, int c, int I, int J, bool cross, double2* sG,
-                      const WsRing& ring, double2* scratch, const double2* cI, const double2* cJ) {
-  using C = JacCfg<W2>;
-  const int nch = (r + C::RC - 1) / C::RC;
-  const int D = ring.depth;
-  double gacc[C::GT + 1][kZ3];
-#pragma unroll
-  for (int u = 0; u < C::GT + 1; ++u)
-#pragma unroll
-    for (int q = 0; q < kZ3; ++q) gacc[u][q] = 0.0;
-  for (int k = 0; k < D - 1 && k < nch; ++k)
-    jac_issue_chunk<W2>(ring.slot<W2>(k), X, r, c, k * C::RC, I, J);
-  for (int k = 0; k < nch; ++k) {
-    const double2* cur = ring.slot<W2>(k % D);
-    const int nxt = k + D - 1;
-    if (nxt < nch) jac_issue_chunk<W2>(ring.slot<W2>(nxt % D), X, r, c, nxt * C::RC, I, J);
-    cp_async_wait_n(min(nch - 1, nxt) - k);
-    WsMath::sync();
-    if (cross) jac_gram_chunk_cross<W2>(gacc, cur, min(C::RC, r - k * C::RC));
-    else jac_gram_chunk<W2>(gacc, cur, min(C::RC, r - k * C::RC));
-    WsMath::sync();
-  }
-  if (cross) jac_gram_store_cross<W2, WsMath>(gacc, sG, scratch, cI, cJ);
-  else jac_gram_store<W2, WsMath>(gacc, sG, scratch);
-}
-
-// Wait for the rotation warps' verdict on a visit and apply its Q (math warps).
-// The first chunks are requested before the wait so their loads overlap the tail
-// of the inner sweep. Returns the rotation count.
-template <int W2>
-BMPS_DEV int ws_finish(double2* X, int r, int c, int I, int J, const double2* sQ, const WsRing& ring,
-                       int pb, const WsVisit* wv) {
-  using C = JacCfg<W2>;
-  const int nch = (r + C::RC - 1) / C::RC;
-  const int D = ring.depth;
-  for (int k = 0; k < D - 1 && k < nch; ++k)
-    jac_issue_chunk<W2>(ring.slot<W2>(k), X, r, c, k * C::RC, I, J);
-  BMPS_TICK(fw0);
-  ws_wait(kWsQf + pb);
-  BMPS_TICK(fw1);
-  WS_ACC(0, 1, fw0, fw1);
-  const int nrot = ((volatile const WsVisit*)wv)[pb].nrot;
-  if (nrot == 0) {
-    cp_async_wait<0>();
-    return 0;
-  }
-  double aacc[C::AT][kZ3];
-  for (int k = 0; k < nch; ++k) {
-    const double2* cur = ring.slot<W2>(k % D);
-    const int nxt = k + D - 1;
-    if (nxt < nch) jac_issue_chunk<W2>(ring.slot<W2>(nxt % D), X, r, c, nxt * C::RC, I, J);
-    cp_async_wait_n(min(nch - 1, nxt) - k);
-    WsMath::sync();
-    jac_apply_mma<W2>(aacc, cur, sQ);
-    jac_apply_store_global<W2>(aacc, X, r, c, k * C::RC, I, J);
-    WsMath::sync();
-  }
-  BMPS_TICK(fw2);
-  WS_ACC(0, 2, fw1, fw2);
-  return nrot;
-}
-
-// Claim ring (scheduler -> math) and completion ring (math -> scheduler) in
-// shared memory, single producer / single consumer, polled with volatile flags.
-struct WsClaim {
-  int item, v, flag, pad;
-  unsigned rnd, pad2;
-};
-struct WsDone {
-  int item, I, J, dirty, flag, pad;
-  unsigned rnd, pad2;
-};
-constexpr int kWsRing = 2;
-#ifndef BMPS_WS_GRAM_DEPTH
-#define BMPS_WS_GRAM_DEPTH 4
-#endif
-#ifndef BMPS_WS_APPLY_DEPTH
-#define BMPS_WS_APPLY_DEPTH 2
-#endif
-constexpr int kWsGramDepth = BMPS_WS_GRAM_DEPTH, kWsApplyDepth = BMPS_WS_APPLY_DEPTH;
-
-template <int W2>
-__global__ void __launch_bounds__(kWsThreads, 2) jacobi_ws_kernel(JacArgs args) {
-  using C = JacCfg<W2>;
-  using WC = WsCfg<W2>;
-  constexpr int w = W2 / 2;
-  extern __shared__ __align__(16) double2 jsm[];
-  double2* sQ0 = jsm;                    // Q[0], Q[1]
-  double2* sG0 = sQ0 + 2 * WC::QSZ;      // G[0], G[1]
-  double2* sP = sG0 + 2 * WC::GSZ;       // two staging buffers
-  __shared__ RotShared<W2> rs_rot, rs_math;
-  __shared__ WsVisit wv[2];
-  __shared__ WsClaim claims[kWsRing];
-  __shared__ WsDone dones[kWsRing];
-  __shared__ int s_item, s_v;
-  __shared__ unsigned s_round;
-  __shared__ unsigned long long jbar[2];
-  if (threadIdx.x < kWsRing) {
-    claims[threadIdx.x].flag = 0;
-    dones[threadIdx.x].flag = 0;
-  }
-  if (threadIdx.x == 0) wv[0].stop = wv[1].stop = 0;
-  __syncthreads();
-
-  if (threadIdx.x >= kWsSched) {
-    // ---- scheduler warp (lane 0): claims visits ahead of the math warps, completes
-    // skippable visits, and does the round bookkeeping of finished visits ----
-    if (threadIdx.x != kWsSched) return;
-    volatile WsClaim* vc = claims;
-    volatile WsDone* vd = dones;
-    int cursor = blockIdx.x % args.nitems;
-    int cs = 0, ds = 0;
-    for (;;) {
-      // finished visits first: they may open the rounds the next claim needs
-      while (vd[ds].flag) {
-        __threadfence_block();
-        jac_complete<W2>(args, vd[ds].item, vd[ds].rnd, vd[ds].I, vd[ds].J, vd[ds].dirty != 0, false, -1);
-        vd[ds].flag = 0;
-        ds = (ds + 1) % kWsRing;
-      }
-      if (vc[cs].flag) {       // ring full: the math warps are busy
-        __nanosleep(256);
-        continue;
-      }
-      int v = 0;
-      unsigned rnd = 0;
-      const int it = ws_claim<W2>(args, cursor, v, rnd);
-      if (it == -1) {
-        // nothing claimable: tell the math warps once (they finish their pending
-        // visit, whose completion may open a round), then back off
-        vc[cs].item = -1;
-        __threadfence_block();
-        vc[cs].flag = 1;
-        cs = (cs + 1) % kWsRing;
-        __nanosleep(1000);
-        cursor = (cursor + 1) % args.nitems;
-        continue;
-      }
-      vc[cs].item = it;
-      vc[cs].v = v;
-      vc[cs].rnd = rnd;
-      __threadfence_block();
-      vc[cs].flag = 1;
-      cs = (cs + 1) % kWsRing;
-      if (it == -2) return;
-    }
-  }
-
-  if (threadIdx.x >= kWsMath) {
-    // ---- rotation warps: inner sweeps, in visit order ----
-    for (int b = 0;; b ^= 1) {
-      BMPS_TICK(rw0);
-      ws_wait(kWsGf + b);
-      BMPS_TICK(rw1);
-      WS_ACC(kWsMath, 4, rw0, rw1);
-      const volatile WsVisit& v = wv[b];
-      if (v.stop) break;
-      double2* sG = sG0 + b * WC::GSZ;
-      double2* sQ = sQ0 + b * WC::QSZ;
-      const bool full = v.full;
-      const double tol = v.tol, noise2 = v.noise2, fro = v.fro;
-      double2* cI = v.cI;
-      double2* cJ = v.cJ;
-      int need = 0;
-      const int npairs = full ? W2 * W2 : w * w;
-      for (int idx = WsRot::tid(); idx < npairs && !need; idx += kWsRot) {
-        int i, j;
-        if (full) {
-          i = idx % W2;
-          j = idx / W2;
-          if (i >= j) continue;
-        } else {
-          i = idx % w;
-          j = w + idx / w;
-        }
-        need = jacobi_needs(sG[i + i * C::LDGG].x, sG[j + j * C::LDGG].x, sG[i + j * C::LDGG], tol,
-                            noise2, fro);
-      }
-      const int nrot = WsRot::count(need) != 0
-                           ? jac_inner<W2, WsRot>(sG, sQ, rs_rot, tol, noise2, fro, full, args.max_inner)
-                           : 0;
-      if (cI != nullptr && (full || nrot > 0)) jac_cache_store<W2, WsRot>(sG, cI, cJ);
-      if (WsRot::tid() == 0) wv[b].nrot = nrot;
-      WsRot::sync();
-      BMPS_TICK(rw2);
-      WS_ACC(kWsMath, 5, rw1, rw2);
-      WS_ACC(kWsMath, 6, 0, 1);
-      ws_arrive(kWsQf + b);
-    }
-    return;
-  }
-
-  // ---- math warps: Gram, apply ----
-  JacStage st{jbar, 0u};   // unused (no TMA staging here)
-  const int mt = threadIdx.x;
-  int b = 0;               // buffer pair of the next new visit
-  int cs = 0, ds = 0;      // claim / completion ring slots
-  bool pend = false;       // a visit is with the rotation warps (buffer b ^ 1)
-  int p_item = 0, p_I = 0, p_J = 0, p_r = 0, p_c = 0;
-  unsigned p_rnd = 0;
-  double2* p_X = nullptr;
-  // finish the pending visit and hand its completion to the scheduler warp
-  auto finish_pending = [&]() {
-    // apply ring: staging buffers + the pending visit's Gram buffer (the rotation
-    // warps are done with it once QF is passed; loads issued before that only
-    // target the staging buffers, depth 3 -> slots 0, 1 first)
-    const WsRing aring{sP, sG0 + (b ^ 1) * WC::GSZ, nullptr, kWsApplyDepth};
-    ws_finish<W2>(p_X, p_r, p_c, p_I, p_J, sQ0 + (b ^ 1) * WC::QSZ, aring, b ^ 1, wv);
-    if (mt == 0) {
-      volatile WsDone* vd = dones;
-      while (vd[ds].flag) __nanosleep(64);
-      vd[ds].item = p_item;
-      vd[ds].I = p_I;
-      vd[ds].J = p_J;
-      vd[ds].rnd = p_rnd;
-      vd[ds].dirty = wv[b ^ 1].nrot > 0;
-      __threadfence();     // the visit's panel (all math threads, ordered by the apply's
-                           // last barrier) and Gram-cache stores before the completion
-      vd[ds].flag = 1;
-    }
-    ds = (ds + 1) % kWsRing;
-  };
-  for (;;) {
-    BMPS_TICK(cw0);
-    if (mt == 0) {
-      volatile WsClaim* vc = claims;
-      while (!vc[cs].flag) { }
-      __threadfence_block();
-      s_item = vc[cs].item;
-      s_v = vc[cs].v;
-      s_round = vc[cs].rnd;
-      __threadfence_block();
-      vc[cs].flag = 0;
-    }
-    cs = (cs + 1) % kWsRing;
-    WsMath::sync();
-    const int i = s_item, v = s_v;
-    const unsigned rnd = s_round;
-    WsMath::sync();
-    BMPS_TICK(cw1);
-    if (i >= 0) { WS_ACC(0, 7, cw0, cw1); } else { WS_ACC(0, 8, cw0, cw1); WS_ACC(0, 9, 0, 1); }
-    if (i < 0) {
-      if (pend) {
-        finish_pending();
-        pend = false;
-      }
-      if (i == -2) break;
-      continue;
-    }
-    ItemMeta* m = args.meta + i;
-    const int r = m->jrows, c = m->c;
-    double2* X = (m->dq ? args.Z : m->precond ? args.Y : args.X) + (size_t)i * args.mat_stride;
-    int nb = (c + w - 1) / w;
-    nb += nb & 1;
-    const double tol = args.tol_factor * sqrt((double)r) * kEps;
-    const double noise2 = kNoiseRel * kNoiseRel * m->fro2;
-    const double fro = sqrt(m->fro2);
-    double2* sG = sG0 + b * WC::GSZ;
-    double2* sQ = sQ0 + b * WC::QSZ;
-    if (nb == 2) {
-      // single panel: the math warps iterate the whole item (buffer pair b is free)
-      const bool resident = r <= C::RC;
-      if (resident) jac_load_resident<W2, WsMath>(sP, X, r, c);
-      int sweep = 0;
-      bool clean = false;
-      for (; sweep < args.max_sweeps; ++sweep) {
-        if (!jac_visit<W2, WsMath>(X, r, c, 0, 1, tol, noise2, fro, true, 64, resident, sG, sQ, sP, rs_math,
-                                   st, false)) {
-          clean = true;
-          break;
-        }
-      }
-      if (resident) {
-        WsMath::sync();
-        jac_store_chunk<W2>(sP, X, r, c, 0, 0, 1);
-      }
-      WsMath::sync();
-      if (mt == 0) {
-        __threadfence();
-        m->sweeps = sweep;
-        if (!clean) m->status = BMPS_S_SVD_FAILED;
-        __threadfence();
-        m->conv = 1;
-        atomicSub(args.active, 1);
-      }
-      WsMath::sync();
-      continue;
-    }
-    const int rounds = nb - 1;
-    const int rho = (int)(rnd % (unsigned)rounds);
-    int I, J;
-    tourney_pair(nb, rho, v, I, J);
-    double2* gc = args.gcache ? args.gcache + (size_t)i * args.gcache_stride : nullptr;
-    double2* cI = gc ? gc + (size_t)I * w * w : nullptr;
-    double2* cJ = gc ? gc + (size_t)J * w * w : nullptr;
-    const bool full = rho == 0;
-    if (mt == 0) {
-      wv[b].tol = tol;
-      wv[b].noise2 = noise2;
-      wv[b].fro = fro;
-      wv[b].cI = cI;
-      wv[b].cJ = cJ;
-      wv[b].full = full;
-      wv[b].stop = 0;
-    }
-    // Q[b] is free (its last apply finished before this point): scratch for the
-    // k-split Gram partials
-    BMPS_TICK(gw0);
-    const WsRing gring{sP, sQ, sG, kWsGramDepth};
-    ws_gram<W2>(X, r, c, I, J, gc != nullptr && !full, sG, gring, sQ, cI, cJ);
-    WsMath::sync();
-    BMPS_TICK(gw1);
-    WS_ACC(0, 0, gw0, gw1);
-    WS_ACC(0, 3, 0, 1);
-    ws_arrive(kWsGf + b);
-    if (pend) finish_pending();
-    pend = true;
-    p_item = i;
-    p_I = I;
-    p_J = J;
-    p_r = r;
-    p_c = c;
-    p_rnd = rnd;
-    p_X = X;
-    b ^= 1;
-  }
-  if (mt == 0) wv[b].stop = 1;
-  WsMath::sync();
-  ws_arrive(kWsGf + b);
-}
-
-#endif  // BMPS_EXPERIMENTAL
-
 // ---------------------------------------------------------------------------
 // Row-split cluster kernel (small batches: one circuit's brick layer).
 //
@@ -1853,7 +1627,7 @@ __global__ void __launch_bounds__(256, 3) jacobi_cluster_kernel(JacArgs args) {
   double2* sP = sQ + W2 * C::LDG;
   double2* sG = C::G_IN_BUF ? sP + C::BUF : nullptr;   // W2 = 32 only
   double2* sPart = sP + C::NBUF * C::BUF;
-  __shared__ RotShared<W2> rs;
+  __shared__ InnerShared<W2> rs;
   __shared__ int c_item, c_v;
   __shared__ unsigned c_round;
   __shared__ unsigned long long jbar[2];
@@ -1895,7 +1669,7 @@ __global__ void __launch_bounds__(256, 3) jacobi_cluster_kernel(JacArgs args) {
     if (nb == 2) {
       // single panel: rank 0 iterates the item alone (small; the others move on)
       if (rank == 0) {
-        const bool resident = r <= C::RC;
+        const bool resident = false;   // (the inner sweep needs staging buffer 0)
         if (resident) jac_load_resident<W2>(sP, X, r, c);
         int sweep = 0;
         bool clean = false;
@@ -1969,7 +1743,7 @@ __global__ void __launch_bounds__(256, 3) jacobi_cluster_kernel(JacArgs args) {
                             noise2, fro);
       }
     }
-    const int nrot = __syncthreads_or(need) ? jac_inner<W2>(sG, sQ, rs, tol, noise2, fro, full, args.max_inner)
+    const int nrot = __syncthreads_or(need) ? jac_inner<W2>(sG, sQ, sP, rs, tol, noise2, fro, full, args.max_inner)
                                             : 0;
     if (rank == 0 && gc != nullptr && (full || nrot > 0)) jac_cache_store<W2>(sG, cI, cJ);
     __syncthreads();   // sG (staging buffer 1) is read before the apply refills it

@@ -175,13 +175,11 @@ def test_cfg5():
     _check_margins(b, 0, g)
 
 
-@pytest.mark.parametrize("param,value", [("jac_cluster", 4), ("jac_cluster", 2), ("jac_ws", 1)])
+@pytest.mark.parametrize("param,value", [("jac_cluster", 4), ("jac_cluster", 2)])
 @pytest.mark.parametrize("cfg", ["cfg3", "cfg5"])
 def test_golden_under_jacobi_variants(cfg, param, value):
     """The config-scale goldens (cfg3: chi 256, cfg5: chi 1024) through the row-split
-    cluster kernel forced on every layer and through the warp-specialised kernel."""
+    cluster kernel forced on every layer."""
     from paper_1807_07914_b200 import _native
-    if param == "jac_ws" and not _native.experimental():
-        pytest.skip("development variant: libbmps.so built without -DBMPS_EXPERIMENTAL")
     with _native.tunables(**{param: value}):
         (test_cfg3 if cfg == "cfg3" else test_cfg5)()

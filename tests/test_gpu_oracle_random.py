@@ -141,12 +141,15 @@ def test_all_jacobi_schedules_match_oracle(mode):
 
 def test_disabled_variants_are_rejected():
     """Without -DBMPS_EXPERIMENTAL the development variants are refused with
-    BMPS_E_ARG (surfaced as RuntimeError), never silently replaced."""
+    BMPS_E_ARG (surfaced as RuntimeError), never silently replaced; the reserved
+    jac_ws field (the removed warp-specialised kernel) is refused in every build."""
     from paper_1807_07914_b200 import _native
+    prog = brick_circuit(12, 4, np.random.default_rng(3))
+    with _native.tunables(jac_ws=1), pytest.raises(RuntimeError, match="invalid argument"):
+        mps_run(prog, 12, TruncationPolicy(1e-10, 64))
     if _native.experimental():
         pytest.skip("experimental build")
-    prog = brick_circuit(12, 4, np.random.default_rng(3))
-    for kw in ({"jac_ws": 1}, {"tma_staging": 1}, {"jacobi_mode": 2}, {"jacobi_mode": 3}):
+    for kw in ({"tma_staging": 1}, {"jacobi_mode": 2}, {"jacobi_mode": 3}):
         with _native.tunables(**kw), pytest.raises(RuntimeError, match="invalid argument"):
             mps_run(prog, 12, TruncationPolicy(1e-10, 64))
 
@@ -159,17 +162,6 @@ def test_double_qr_preconditioning_matches_oracle(dq, chi, cutoff):
     with _native.tunables(double_qr=dq):
         prog = brick_circuit(14, 14, np.random.default_rng(chi + dq))
         _compare(prog, 14, cutoff, chi, seed=chi)
-
-
-@pytest.mark.parametrize("chi,cutoff", [(48, 1e-10), (128, 0.0), (128, 1e-10)])
-def test_warp_specialised_jacobi_matches_oracle(chi, cutoff):
-    """jac_ws=1: math / rotation / scheduler warps with a two-deep visit pipeline
-    (single-panel items run by the math warps alone) give the oracle's results."""
-    from paper_1807_07914_b200 import _native
-    _needs_experimental()
-    with _native.tunables(jac_ws=1):
-        prog = brick_circuit(14, 14, np.random.default_rng(500 + chi))
-        _compare(prog, 14, cutoff, chi, seed=chi + 1)
 
 
 @pytest.mark.parametrize("csize", [0, 2, 4])

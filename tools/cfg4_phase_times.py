@@ -19,6 +19,7 @@ d = [out1[i] - out0[i] for i in range(16)]
 v = max(d[3], 1); claims = max(d[11], 1); rounds = max(d[6], 1)
 print(f"cfg4 {n_c} circuits evolve {dt:.3f} s; visits {d[3]} claims {d[11]} skips {d[13]}")
 print(f"per visit: gram {d[0]/v:.0f} inner {d[1]/v:.0f} apply {d[2]/v:.0f}; per claim {d[10]/claims:.0f}; idle {d[12]/v:.0f} per visit")
+print(f"rotation chain {d[7]/rounds:.0f}, Q update {d[8]/rounds:.0f} cycles per round (one thread each)")
 print(f"inner rounds {d[6]} ({d[6]/v:.1f} per visit): rotation+count {d[4]/rounds:.0f}, update+sync {d[5]/rounds:.0f} cycles per round")
 import numpy as np
 rec = b.update_records(0)

@@ -22,4 +22,5 @@ print(f"step {e0.elapsed_time(e1):.1f} ms; visits {d[3]} claims {d[11]} skips {d
 print(f"per visit: gram {d[0]/v:.0f} inner {d[1]/v:.0f} apply {d[2]/v:.0f}; per claim: claim {d[10]/claims:.0f}; idle total {d[12]/v:.0f} per visit")
 print(f"probes per claim attempt (incl. idle re-probes): {d[14] / max(d[11] + d[9], 1):.2f}; probes total {d[14]}")
 rounds = max(d[6], 1)
+print(f"rotation chain {d[7]/rounds:.0f}, Q update {d[8]/rounds:.0f} cycles per round (one thread each)")
 print(f"inner rounds {d[6]} ({d[6]/v:.1f} per visit): rotation+count {d[4]/rounds:.0f}, update+sync {d[5]/rounds:.0f} cycles per round")

@@ -1,8 +1,8 @@
-// Microbenchmark of the Jacobi inner (Gram-space) sweep alone: one CTA per
-// launch, a 32x32 Hermitian Gram from a random 512x32 panel, cross rounds
-// (as on a cross visit) -- cycles per round without the rest of the pipeline.
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I include -I paper_1807_07914_b200/csrc \
-//   -o tools/inner_bench tools/inner_bench.cu
+// Microbenchmark of the Jacobi inner (Gram-space) sweep alone: NCTA co-resident CTAs per
+// SM each sweeping a 32x32 Hermitian Gram of a random 512x32 panel (cross sweep, as on
+// a cross visit) -- cycles per sweep without the rest of the visit pipeline.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
+//   -I paper_1807_07914_b200/csrc -o tools/inner_bench tools/inner_bench.cu
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -11,11 +11,14 @@
 using namespace bmps;
 
 template <int W2>
-__global__ void inner_kernel(const double2* G0, int reps, long long* cyc, int* nrot, double2* Gout, double2* Qout) {
+__global__ void __launch_bounds__(256, 4)
+inner_kernel(const double2* G0, int reps, int full, long long* cyc, int* nrot, double2* Gout, double2* Qout) {
   using C = JacCfg<W2>;
-  __shared__ double2 sG[W2 * C::LDGG];
-  __shared__ double2 sQ[W2 * C::LDG];
-  __shared__ RotShared rs;
+  extern __shared__ __align__(16) double2 sm[];
+  double2* sG = sm;
+  double2* sQ = sG + W2 * C::LDGG;
+  double2* work = sQ + W2 * C::LDG;
+  __shared__ InnerShared<W2> is;
   long long tot = 0;
   int nr = 0;
   for (int rep = 0; rep < reps; ++rep) {
@@ -23,116 +26,22 @@ __global__ void inner_kernel(const double2* G0, int reps, long long* cyc, int* n
       sG[(i % W2) + (i / W2) * C::LDGG] = G0[i];
     __syncthreads();
     const long long t0 = clock64();
-    nr += jac_inner<W2>(sG, sQ, rs, 4.0 * sqrt(512.0) * kEps, 1e-28, 1.0, false, 1);
+    nr += jac_inner<W2>(sG, sQ, work, is, 4.0 * sqrt(512.0) * kEps, 1e-28, 1.0, full != 0, 1);
     __syncthreads();
     tot += clock64() - t0;
   }
-  if (threadIdx.x == 0) { *cyc = tot; *nrot = nr; }
-  for (int i = threadIdx.x; i < W2 * W2; i += blockDim.x) {
-    Gout[i] = sG[(i % W2) + (i / W2) * C::LDGG];
-    Qout[i] = sQ[(i % W2) + (i / W2) * C::LDG];
-  }
+  if (threadIdx.x == 0 && blockIdx.x == 0) { *cyc = tot; *nrot = nr; }
+  if (blockIdx.x == 0)
+    for (int i = threadIdx.x; i < W2 * W2; i += blockDim.x) {
+      Gout[i] = sG[(i % W2) + (i / W2) * C::LDGG];
+      Qout[i] = sQ[(i % W2) + (i / W2) * C::LDG];
+    }
 }
 
-
-// Configurable copy of jac_inner's cross path: MODE bit0 = G update, bit1 = Q update
-template <int W2, int MODE>
-__device__ int inner_var(double2* sG, double2* sQ, RotShared& rs, double tol, double noise2, double fro) {
-  using C = JacCfg<W2>;
-  constexpr int w = W2 / 2;
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < W2 * W2; idx += blockDim.x) {
-    const int i = idx % W2, j = idx / W2;
-    sQ[i + j * C::LDG] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-  }
-  int any = 0;
-  int pq_q = (int)((sqrtf(8.0f * (float)tid + 1.0f) - 1.0f) * 0.5f);
-  const int pq_p = tid - pq_q * (pq_q + 1) / 2;
-  for (int rho = 0; rho < w; ++rho) {
-    int act = 0;
-    if (tid < w) {
-      const int i = tid, j = w + (tid + rho) % w;
-      double c = 1.0, s = 0.0;
-      double2 e = make_double2(1.0, 0.0);
-      act = jacobi_rotation(sG[i + i * C::LDGG].x, sG[j + j * C::LDGG].x, sG[i + j * C::LDGG], tol, noise2, fro, c, s, e);
-      if (!act) { c = 1.0; s = 0.0; e = make_double2(1.0, 0.0); }
-      rs.i[tid] = i; rs.j[tid] = j; rs.act[tid] = act; rs.c[tid] = c; rs.s[tid] = s; rs.e[tid] = e;
-      rs.se[tid] = cscale(e, s); rs.ce[tid] = cscale(e, c);
-    }
-    const int nact = __syncthreads_count(act);
-    any += nact;
-    if (nact == 0) continue;
-    if (MODE & 1) {
-      for (int idx = tid; idx < w * (w + 1) / 2; idx += blockDim.x) {
-        const int q = (MODE & 256) ? pq_q : (int)((sqrtf(8.0f * (float)idx + 1.0f) - 1.0f) * 0.5f);
-        const int p = (MODE & 256) ? pq_p : idx - q * (q + 1) / 2;
-        if (!(MODE & 16) && !(rs.act[p] | rs.act[q])) continue;
-        const int ip = (MODE & 32) ? p : rs.i[p], jp = (MODE & 32) ? w + (p + rho) % w : rs.j[p];
-        const int iq = (MODE & 32) ? q : rs.i[q], jq = (MODE & 32) ? w + (q + rho) % w : rs.j[q];
-        const double cp = rs.c[p], sp = rs.s[p], cq = rs.c[q], sq = rs.s[q];
-        const double2 sep = rs.se[p], cep = rs.ce[p], seq = rs.se[q], ceq = rs.ce[q];
-        double2 g00, g01, g10, g11;
-        if (MODE & 64) {
-          g00 = make_double2(ip, iq); g01 = make_double2(ip, jq); g10 = make_double2(jp, iq); g11 = make_double2(jp, jq);
-        } else {
-          g00 = sG[ip + iq * C::LDGG]; g01 = sG[ip + jq * C::LDGG];
-          g10 = sG[jp + iq * C::LDGG]; g11 = sG[jp + jq * C::LDGG];
-        }
-        const double2 r00 = cmsc(g00, cq, seq, g01), r01 = cmac(g00, sq, ceq, g01);
-        const double2 r10 = cmsc(g10, cq, seq, g11), r11 = cmac(g10, sq, ceq, g11);
-        double2 n00 = cms(r00, cp, sep, r10), n01 = cms(r01, cp, sep, r11);
-        double2 n10 = cma(r00, sp, cep, r10), n11 = cma(r01, sp, cep, r11);
-        if (MODE & 8) { n00 = g00; n01 = g01; n10 = g10; n11 = g11; }
-        if (MODE & 128) {
-          if (n00.x == 12345.0 && n01.y == 1.0 && n10.x == 3.0 && n11.y == 2.0) sG[0] = n00;
-          continue;
-        }
-        sG[ip + iq * C::LDGG] = n00; sG[ip + jq * C::LDGG] = n01;
-        sG[jp + iq * C::LDGG] = n10; sG[jp + jq * C::LDGG] = n11;
-        if (!(MODE & 4) && p != q) {
-          sG[iq + ip * C::LDGG] = cconj(n00); sG[jq + ip * C::LDGG] = cconj(n01);
-          sG[iq + jp * C::LDGG] = cconj(n10); sG[jq + jp * C::LDGG] = cconj(n11);
-        }
-      }
-    }
-    if (MODE & 2) {
-      for (int idx = tid; idx < W2 * w; idx += blockDim.x) {
-        const int k = idx % W2, q = idx / W2;
-        if (!rs.act[q]) continue;
-        const int iq = rs.i[q], jq = rs.j[q];
-        const double cq = rs.c[q], sq = rs.s[q];
-        const double2 qi = sQ[k + iq * C::LDG], qj = sQ[k + jq * C::LDG];
-        sQ[k + iq * C::LDG] = cmsc(qi, cq, rs.se[q], qj);
-        sQ[k + jq * C::LDG] = cmac(qi, sq, rs.ce[q], qj);
-      }
-    }
-    __syncthreads();
-  }
-  return any;
-}
-
-template <int W2, int MODE>
-__global__ void var_kernel(const double2* G0, int reps, long long* cyc, int* nrot) {
-  using C = JacCfg<W2>;
-  __shared__ double2 sG[W2 * C::LDGG];
-  __shared__ double2 sQ[W2 * C::LDG];
-  __shared__ RotShared rs;
-  long long tot = 0;
-  int nr = 0;
-  for (int rep = 0; rep < reps; ++rep) {
-    for (int i = threadIdx.x; i < W2 * W2; i += blockDim.x) sG[(i % W2) + (i / W2) * C::LDGG] = G0[i];
-    __syncthreads();
-    const long long t0 = clock64();
-    nr += inner_var<W2, MODE>(sG, sQ, rs, 4.0 * sqrt(512.0) * kEps, 1e-28, 1.0);
-    __syncthreads();
-    tot += clock64() - t0;
-  }
-  if (threadIdx.x == 0) { *cyc = tot; *nrot = nr; }
-}
-
-int main() {
+int main(int argc, char** argv) {
   const int W2 = 32, R = 512;
-  std::vector<double2> P(R * W2), G(W2 * W2);
+  using C = JacCfg<W2>;
+  std::vector<double2> P(R * W2), G(W2 * W2), Go(W2 * W2), Q(W2 * W2);
   srand(1);
   for (auto& x : P) x = make_double2(rand() / (double)RAND_MAX - 0.5, rand() / (double)RAND_MAX - 0.5);
   for (int i = 0; i < W2; ++i)
@@ -145,37 +54,63 @@ int main() {
       }
       G[i + j * W2] = make_double2(re * 1e-3, im * 1e-3);
     }
-  double2 *dG, *dO, *dQ, *dO2, *dQ2; long long* dc; int* dn;
+  double2 *dG, *dO, *dQ; long long* dc; int* dn;
   cudaMalloc(&dG, sizeof(double2) * W2 * W2); cudaMalloc(&dO, sizeof(double2) * W2 * W2);
-  cudaMalloc(&dQ, sizeof(double2) * W2 * W2); cudaMalloc(&dO2, sizeof(double2) * W2 * W2);
-  cudaMalloc(&dQ2, sizeof(double2) * W2 * W2);
+  cudaMalloc(&dQ, sizeof(double2) * W2 * W2);
   cudaMalloc(&dc, 8); cudaMalloc(&dn, 4);
   cudaMemcpy(dG, G.data(), sizeof(double2) * W2 * W2, cudaMemcpyHostToDevice);
+  const size_t smem = sizeof(double2) * (W2 * C::LDGG + W2 * C::LDG + 8 * 64);
+  cudaFuncSetAttribute(inner_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int reps = 200;
-  inner_kernel<32><<<1, 256>>>(dG, 2, dc, dn, dO, dQ);
-  inner_kernel<32><<<1, 256>>>(dG, reps, dc, dn, dO, dQ);
-  long long c; int n;
-  cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost); cudaMemcpy(&n, dn, 4, cudaMemcpyDeviceToHost);
-  printf("cross inner sweep: %.0f cycles per sweep, %.0f per round (16 rounds), rotations/sweep %d\n",
-         (double)c / reps, (double)c / reps / 16, n / reps);
-  const char* names[13] = {"rotations only", "+G", "+Q", "+G+Q", "G nomirror", "G nomath", "G noact", "G arith idx", "G all three",
-                           "G noloads", "G nostores", "G pq hoisted", "G nold nost"};
-  for (int mode = 0; mode < 13; ++mode) {
-    if (mode == 0) var_kernel<32, 0><<<1, 256>>>(dG, reps, dc, dn);
-    if (mode == 1) var_kernel<32, 1><<<1, 256>>>(dG, reps, dc, dn);
-    if (mode == 2) var_kernel<32, 2><<<1, 256>>>(dG, reps, dc, dn);
-    if (mode == 3) var_kernel<32, 3><<<1, 256>>>(dG, reps, dc, dn);
-    if (mode == 4) var_kernel<32, 1 | 4><<<1, 256>>>(dG, reps, dc, dn);
-    if (mode == 5) var_kernel<32, 1 | 8><<<1, 256>>>(dG, reps, dc, dn);
-    if (mode == 6) var_kernel<32, 1 | 16><<<1, 256>>>(dG, reps, dc, dn);
-    if (mode == 7) var_kernel<32, 1 | 32><<<1, 256>>>(dG, reps, dc, dn);
-    if (mode == 8) var_kernel<32, 1 | 4 | 16 | 32><<<1, 256>>>(dG, reps, dc, dn);
-    if (mode == 9) var_kernel<32, 1 | 64><<<1, 256>>>(dG, reps, dc, dn);
-    if (mode == 10) var_kernel<32, 1 | 128><<<1, 256>>>(dG, reps, dc, dn);
-    if (mode == 11) var_kernel<32, 1 | 256><<<1, 256>>>(dG, reps, dc, dn);
-    if (mode == 12) var_kernel<32, 1 | 64 | 128><<<1, 256>>>(dG, reps, dc, dn);
-    cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost); cudaMemcpy(&n, dn, 4, cudaMemcpyDeviceToHost);
-    printf("variant %-15s: %.0f cycles per round (rot/sweep %d)\n", names[mode], (double)c / reps / 16, n / reps);
-  }
+  for (int full = 0; full < 2; ++full)
+    for (int ncta : {1, 2, 4}) {
+      inner_kernel<32><<<148 * ncta, 256, smem>>>(dG, 2, full, dc, dn, dO, dQ);
+      inner_kernel<32><<<148 * ncta, 256, smem>>>(dG, reps, full, dc, dn, dO, dQ);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+      long long c; int n;
+      cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost); cudaMemcpy(&n, dn, 4, cudaMemcpyDeviceToHost);
+#ifdef BMPS_PHASE_TIMERS
+      {
+        unsigned long long pc[16];
+        cudaMemcpyFromSymbol(pc, g_phase_cycles, sizeof(pc));
+        static unsigned long long prev[16];
+        const double nb = (double)(pc[6] - prev[6]);
+        printf("   batches %.0f: phase S %.0f, phase M %.0f cycles per batch (CTA 0.. all CTAs' thread 0)\n", nb,
+               (pc[4] - prev[4]) / nb, (pc[5] - prev[5]) / nb);
+        const double nr_ = (double)(pc[12] - prev[12]);
+        if (nr_ > 0)
+          printf("   per round (CTA 0, lane 0): shuffles %.0f, rotation %.0f, ballot+sync %.0f, updates+sync %.0f\n",
+                 (pc[8] - prev[8]) / nr_, (pc[9] - prev[9]) / nr_, (pc[10] - prev[10]) / nr_, (pc[11] - prev[11]) / nr_);
+        for (int i = 0; i < 16; ++i) prev[i] = pc[i];
+      }
+#endif
+      const int rounds = full ? 31 : 16;
+      printf("%s sweep, %d CTA/SM: %.0f cycles per sweep, %.0f per round (%d rounds), rotations/sweep %d\n",
+             full ? "full " : "cross", ncta, (double)c / reps, (double)c / reps / rounds, rounds, n / reps);
+    }
+  // consistency: Q^H G0 Q == G_out, Q unitary
+  cudaMemcpy(Go.data(), dO, sizeof(double2) * W2 * W2, cudaMemcpyDeviceToHost);
+  cudaMemcpy(Q.data(), dQ, sizeof(double2) * W2 * W2, cudaMemcpyDeviceToHost);
+  double err = 0, uerr = 0, gmax = 0;
+  for (int i = 0; i < W2; ++i)
+    for (int j = 0; j < W2; ++j) {
+      double re = 0, im = 0, ur = 0, ui = 0;
+      for (int k = 0; k < W2; ++k) {
+        double tr = 0, ti = 0;
+        for (int l = 0; l < W2; ++l) {
+          const double2 g = G[k + l * W2], q = Q[l + j * W2];
+          tr += g.x * q.x - g.y * q.y; ti += g.x * q.y + g.y * q.x;
+        }
+        const double2 qi = Q[k + i * W2];
+        re += qi.x * tr + qi.y * ti; im += qi.x * ti - qi.y * tr;
+        const double2 qj = Q[k + j * W2];
+        ur += qi.x * qj.x + qi.y * qj.y; ui += qi.x * qj.y - qi.y * qj.x;
+      }
+      err = fmax(err, hypot(re - Go[i + j * W2].x, im - Go[i + j * W2].y));
+      uerr = fmax(uerr, hypot(ur - (i == j), ui));
+      gmax = fmax(gmax, hypot(G[i + j * W2].x, G[i + j * W2].y));
+    }
+  printf("max |Q^H G0 Q - G_out| / max|G0| = %.2e, max |Q^H Q - I| = %.2e\n", err / gmax, uerr);
   return 0;
 }

@@ -76,6 +76,15 @@ def precond(M, double=True):
     R2 = np.linalg.qr(Y, mode='r')
     return R2.conj().T
 
+def precond_n(M, n, pivot=True):
+    """n alternating QRs (R^H of the previous factor), first with static column pivoting."""
+    if pivot:
+        M = M[:, np.argsort(-np.linalg.norm(M, axis=0))]
+    Y = M
+    for _ in range(n):
+        Y = np.linalg.qr(Y, mode='r').conj().T
+    return Y
+
 if __name__ == "__main__":
     qs = [int(x) for x in sys.argv[1].split(',')]
     variant = sys.argv[2]
@@ -90,6 +99,8 @@ if __name__ == "__main__":
         if variant == 'w8': kw['w'] = 8
         if variant == 'single': dbl = False
         Z = precond(M, dbl)
+        if variant.startswith('qr'):
+            Z = precond_n(M, int(variant[2:]))
         if variant == 'sort':
             Z = Z[:, np.argsort(-np.linalg.norm(Z, axis=0))]
         t = time.time()
