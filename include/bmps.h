@@ -77,7 +77,7 @@ int32_t bmps_build_flags(void);
 /* Development aid: cumulative cycles of the Jacobi phases (Gram pass, inner
  * sweep, apply pass, visit counts, warp-specialised waits) in a
  * -DBMPS_PHASE_TIMERS build; returns BMPS_E_ARG in normal builds. out4 is a host
- * array of 16 uint64. */
+ * array of 24 uint64. */
 int32_t bmps_phase_cycles(uint64_t* out4);
 /* Development aid (-DBMPS_PHASE_TIMERS builds; BMPS_E_ARG otherwise): per-warp clock
  * trace of the Jacobi inner sweep's rotation / Q-update phase, 64 x 8 x 4 uint64. */

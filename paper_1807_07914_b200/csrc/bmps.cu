@@ -870,7 +870,7 @@ void bmps_default_params(bmps_params* p) {
 // Development aid: cumulative Jacobi phase cycles (builds with -DBMPS_PHASE_TIMERS only).
 int32_t bmps_phase_cycles(uint64_t* out4) {
 #ifdef BMPS_PHASE_TIMERS
-  cudaMemcpyFromSymbol(out4, g_phase_cycles, 16 * sizeof(unsigned long long));
+  cudaMemcpyFromSymbol(out4, g_phase_cycles, 24 * sizeof(unsigned long long));
   return BMPS_OK;
 #else
   (void)out4;

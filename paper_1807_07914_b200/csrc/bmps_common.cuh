@@ -170,30 +170,28 @@ BMPS_DEV bool jacobi_needs(double a, double b, double2 g, double tol, double noi
 }
 
 // Branch-free rotation of one pair: a, b = squared column norms, g = x_i^H x_j,
-// thr2 = (tol ||M||_F)^2. Returns 1 and (c, s, e) if the pair rotates (the test of
-// jacobi_needs, plus |g|^2 > 1e-290 so every reciprocal square root below sees a
-// normal number: a pair that fails only this last test has a column below 1e-131
-// ||M||_F, far under the noise floor), else 0 and the identity.
-// With delta = b - a and rho = sqrt(delta^2 + 4|g|^2):
-//   c = sqrt((1 + |delta| / rho) / 2),  s = sign(delta) |g| / (rho c),  e = g / |g|,
-// the same small-angle rotation as Rutishauser's tangent formula with c^2 + s^2 = 1 by
-// construction. No branches: 1/|g| and 1/rho are independent chains the scheduler
-// interleaves, and the call sits on the inner sweep's critical path.
+// thr2 = (tol ||M||_F)^2. Returns 1 and (c, sigma) if the pair rotates (the test of
+// jacobi_needs, which includes |g|^2 > 1e-290 so every reciprocal square root below sees
+// a normal number), else 0 and the identity. The column transform is
+//   [x_i, x_j] <- [x_i, x_j] [[c, sigma], [-conj(sigma), c]],   c^2 + |sigma|^2 = 1:
+// with delta = b - a and rho = sqrt(delta^2 + 4|g|^2),
+//   c = sqrt((1 + |delta| / rho) / 2),   sigma = sign(delta) g / (rho c),
+// the same small-angle rotation as Rutishauser's tangent formula (the phase of g rides
+// on sigma, so no 1/|g| is needed). No branches: the call sits on the inner sweep's
+// critical path.
 BMPS_DEV int jacobi_rotation(double a, double b, double2 g, double thr2, double noise2, double& c,
-                             double& s, double2& e) {
+                             double2& sigma) {
   const double lo = fmin(a, b), hi = fmax(a, b);
   const double g2 = cabs2(g);
   const bool act = (hi > noise2) && (lo > kNegligible * hi) && (g2 > thr2 * lo) && (g2 > 1e-290);
   const double g2s = act ? g2 : 1.0;                      // keeps the arithmetic finite
   const double delta = act ? b - a : 0.0;
-  const double rg = fast_rsqrt(g2s);                      // 1 / |g|
   const double rr = fast_rsqrt(fma(delta, delta, 4.0 * g2s));
   const double c2 = fma(0.5 * fabs(delta), rr, 0.5);      // in [1/2, 1]
   const double rc = fast_rsqrt(c2);                       // 1 / c
-  const double sm = (g2s * rg) * rr * rc;                 // |g| / (rho c)
+  const double kap = delta < 0 ? -(rr * rc) : rr * rc;    // sign(delta) / (rho c)
   c = act ? c2 * rc : 1.0;
-  s = act ? (delta < 0 ? -sm : sm) : 0.0;
-  e = act ? make_double2(g.x * rg, g.y * rg) : make_double2(1.0, 0.0);
+  sigma = act ? make_double2(g.x * kap, g.y * kap) : make_double2(0.0, 0.0);
   return act ? 1 : 0;
 }
 

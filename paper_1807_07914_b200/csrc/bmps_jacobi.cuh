@@ -48,7 +48,7 @@ constexpr bool kTmaStaging = false;
 
 #ifdef BMPS_PHASE_TIMERS
 // cycles spent in [0] Gram pass, [1] inner sweep (incl. check), [2] apply pass, [3] visits
-__device__ unsigned long long g_phase_cycles[16];
+__device__ unsigned long long g_phase_cycles[24];   // [16..20]: per-round segments of phase S
 // per-warp arrival trace of the inner sweep's phase B (CTA 0, first 64 rounds): start of
 // the phase, end of the warp's own work, release from the counting barrier
 __device__ unsigned long long g_inner_trace[64 * 8 * 4];
@@ -146,17 +146,13 @@ struct JacArgs {
 };
 
 // Shared state of the inner (Gram-space) sweep, see jac_inner: per column group the
-// four rotations of the current round -- cs = (c, s), colb[0] = s e, colb[1] = -c e, so
-// that both columns of a rotated pair are x_a c - conj(s e) x_b and x_a s - conj(-c e) x_b
-// (one code path indexed by the column half); ab = a | b << 4 | active << 8 (columns
-// local to the group) -- and the group's rotation count of the batch (double-buffered
-// by batch parity).
+// four rotations (c, sigma) of the current round and the group's rotation count of the
+// batch (double-buffered by batch parity).
 template <int W2>
 struct InnerShared {
   static constexpr int NG = W2 / 8;
-  double2 cs[NG][4];
-  double2 colb[NG][2][4];
-  int ab[NG][4];
+  double2 sg[NG][4];
+  double c[NG][4];
   int cnt[2][NG];
 };
 
@@ -633,7 +629,7 @@ BMPS_DEV double2 shfl_xor_z(double2 v, int mask) {
 // From one round to the next only the B partners change (P ^ ri), i.e. the B-side
 // entries move between lanes by XOR shuffles; the four rotations of a round are computed
 // by the diagonal lanes (t, t) from their own registers and reach the other lanes
-// through 192 bytes of shared memory -- the only memory round trip of a round. Returns
+// through 96 bytes of shared memory -- the only memory round trip of a round. Returns
 // the number of rotations. `k_identity`: K_g starts as the identity (not loaded).
 template <int W2, int MODE>
 BMPS_DEV int jac_group_rounds(double2* sG, double2* Kg, InnerShared<W2>& is, int g, int qa, int qb,
@@ -681,12 +677,15 @@ BMPS_DEV int jac_group_rounds(double2* sG, double2* Kg, InnerShared<W2>& is, int
     const long long q1 = clock64();
 #endif
     if (drole && t == u) {
-      double c, s;
-      double2 e;
-      act = jacobi_rotation(g00.x, g11.x, g01, thr2, noise2, c, s, e);
-      is.cs[g][t] = make_double2(c, s);
-      is.colb[g][0][t] = cscale(e, s);
-      is.colb[g][1][t] = cscale(e, -c);
+      double c;
+      double2 sg;
+#ifdef BMPS_X_SKIP_ROT
+      c = 0.8; sg = make_double2(g01.x > 0 ? 0.6 : -0.6, 0.0); act = 1;
+#else
+      act = jacobi_rotation(g00.x, g11.x, g01, thr2, noise2, c, sg);
+#endif
+      is.c[g][t] = c;
+      is.sg[g][t] = sg;
     }
 #ifdef BMPS_INNER_TIMERS
     const long long q2 = clock64();
@@ -698,16 +697,17 @@ BMPS_DEV int jac_group_rounds(double2* sG, double2* Kg, InnerShared<W2>& is, int
 #endif
     if (am) {
       cnt += __popc(am);
+#ifndef BMPS_X_SKIP_D
       if (drole) {
-        // columns by pair u (right rotation), then rows by pair t (left rotation)
-        const double2 csu = is.cs[g][u], seu = is.colb[g][0][u], mcu = is.colb[g][1][u];
-        const double2 r00 = cmsc(g00, csu.x, seu, g01), r01 = cmsc(g00, csu.y, mcu, g01);
-        const double2 r10 = cmsc(g10, csu.x, seu, g11), r11 = cmsc(g10, csu.y, mcu, g11);
-        const double2 cst = is.cs[g][t], set = is.colb[g][0][t], mct = is.colb[g][1][t];
-        g00 = cms(r00, cst.x, set, r10);
-        g01 = cms(r01, cst.x, set, r11);
-        g10 = cms(r00, cst.y, mct, r10);
-        g11 = cms(r01, cst.y, mct, r11);
+        // columns by pair u (right: J_u), then rows by pair t (left: J_t^H)
+        const double cu = is.c[g][u], ct = is.c[g][t];
+        const double2 su = is.sg[g][u], st = is.sg[g][t];
+        const double2 r00 = cmsc(g00, cu, su, g01), r01 = cma(g01, cu, su, g00);
+        const double2 r10 = cmsc(g10, cu, su, g11), r11 = cma(g11, cu, su, g10);
+        g00 = cms(r00, ct, st, r10);
+        g01 = cms(r01, ct, st, r11);
+        g10 = cmac(r10, ct, st, r00);
+        g11 = cmac(r11, ct, st, r01);
         if (act) {   // the rotated pair itself: diagonal by construction
           g00.y = 0.0;
           g11.y = 0.0;
@@ -715,22 +715,26 @@ BMPS_DEV int jac_group_rounds(double2* sG, double2* Kg, InnerShared<W2>& is, int
           g10 = make_double2(0.0, 0.0);
         }
       }
+#endif
+#ifndef BMPS_X_SKIP_K
       {
-        const double2 csk = is.cs[g][tk];
-        const double2 na = cmsc(ka, csk.x, is.colb[g][0][tk], kb);
-        kb = cmsc(ka, csk.y, is.colb[g][1][tk], kb);
+        const double ck = is.c[g][tk];
+        const double2 sk = is.sg[g][tk];
+        const double2 na = cmsc(ka, ck, sk, kb);
+        kb = cma(kb, ck, sk, ka);
         ka = na;
       }
+#endif
     }
     __syncwarp();   // the parameters are consumed before the next round rewrites them
 #ifdef BMPS_INNER_TIMERS
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
+    if (lane == 0 && g == 0) {
       const long long q4 = clock64();
-      atomicAdd(&g_phase_cycles[8], (unsigned long long)(q1 - q0));
-      atomicAdd(&g_phase_cycles[9], (unsigned long long)(q2 - q1));
-      atomicAdd(&g_phase_cycles[10], (unsigned long long)(q3 - q2));
-      atomicAdd(&g_phase_cycles[11], (unsigned long long)(q4 - q3));
-      atomicAdd(&g_phase_cycles[12], 1ull);
+      atomicAdd(&g_phase_cycles[16], (unsigned long long)(q1 - q0));
+      atomicAdd(&g_phase_cycles[17], (unsigned long long)(q2 - q1));
+      atomicAdd(&g_phase_cycles[18], (unsigned long long)(q3 - q2));
+      atomicAdd(&g_phase_cycles[19], (unsigned long long)(q4 - q3));
+      atomicAdd(&g_phase_cycles[20], 1ull);
     }
 #endif
   }

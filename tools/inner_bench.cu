@@ -72,17 +72,17 @@ int main(int argc, char** argv) {
       cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost); cudaMemcpy(&n, dn, 4, cudaMemcpyDeviceToHost);
 #ifdef BMPS_PHASE_TIMERS
       {
-        unsigned long long pc[16];
+        unsigned long long pc[24];
         cudaMemcpyFromSymbol(pc, g_phase_cycles, sizeof(pc));
-        static unsigned long long prev[16];
+        static unsigned long long prev[24];
         const double nb = (double)(pc[6] - prev[6]);
         printf("   batches %.0f: phase S %.0f, phase M %.0f cycles per batch (CTA 0.. all CTAs' thread 0)\n", nb,
                (pc[4] - prev[4]) / nb, (pc[5] - prev[5]) / nb);
-        const double nr_ = (double)(pc[12] - prev[12]);
+        const double nr_ = (double)(pc[20] - prev[20]);
         if (nr_ > 0)
           printf("   per round (CTA 0, lane 0): shuffles %.0f, rotation %.0f, ballot+sync %.0f, updates+sync %.0f\n",
-                 (pc[8] - prev[8]) / nr_, (pc[9] - prev[9]) / nr_, (pc[10] - prev[10]) / nr_, (pc[11] - prev[11]) / nr_);
-        for (int i = 0; i < 16; ++i) prev[i] = pc[i];
+                 (pc[16] - prev[16]) / nr_, (pc[17] - prev[17]) / nr_, (pc[18] - prev[18]) / nr_, (pc[19] - prev[19]) / nr_);
+        for (int i = 0; i < 24; ++i) prev[i] = pc[i];
       }
 #endif
       const int rounds = full ? 31 : 16;

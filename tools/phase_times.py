@@ -12,10 +12,10 @@ b.run([bench.prefix_program(1003 + r, 25) for r in range(R)])
 dims = b.host_dims()
 full = [{q for q in range(8, 41) if (dims[r, q:q + 3] == 256).all()} for r in range(R)]
 plan = compile_batch([bench.bulk_layer(0, r, full[r]) for r in range(R)], 50)
-out0 = (ctypes.c_uint64 * 16)()
+out0 = (ctypes.c_uint64 * 24)()
 torch.cuda.synchronize(); lib.bmps_phase_cycles(out0)
 b.execute(plan); torch.cuda.synchronize()
-out1 = (ctypes.c_uint64 * 16)(); lib.bmps_phase_cycles(out1)
+out1 = (ctypes.c_uint64 * 24)(); lib.bmps_phase_cycles(out1)
 d = [out1[i] - out0[i] for i in range(8)]
 tot = d[0] + d[1] + d[2]
 print("visits", d[3], "cycles/visit gram %.0f inner %.0f apply %.0f" % (d[0]/d[3], d[1]/d[3], d[2]/d[3]),
