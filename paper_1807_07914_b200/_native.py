@@ -152,6 +152,9 @@ class tunables:
         return False
 
 
+_DEV_AIDS = ("bmps_phase_cycles", "bmps_inner_trace")   # timer-build diagnostics, not the product ABI
+
+
 def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     """Load libbmps.so and declare every exported signature (no device needed)."""
     global _lib
@@ -166,6 +169,8 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         )
     lib = ctypes.CDLL(str(p))
     for name, (args, res) in _SIGNATURES.items():
+        if name in _DEV_AIDS and os.environ.get("BMPS_LIB") and not hasattr(lib, name):
+            continue   # an older development variant under A/B (BMPS_LIB) may lack a dev aid
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res

@@ -25,9 +25,6 @@
 
 namespace bmps {
 
-#ifndef BMPS_WARP_CLAIM
-#define BMPS_WARP_CLAIM 1   // warp-cooperative visit claims in the dynamic kernel
-#endif
 #ifndef BMPS_CLAIM_SLEEP_NS
 #define BMPS_CLAIM_SLEEP_NS 2000   // dynamic Jacobi: back-off of a CTA that found no open visit
 #endif
@@ -38,6 +35,9 @@ constexpr bool kTmaStaging = true;    // TMA bulk panel staging compiled in (mea
 constexpr bool kTmaStaging = false;
 #endif
 
+#ifndef BMPS_INNER_DEFER
+#define BMPS_INNER_DEFER 1   // inner sweep: Q update of a batch under the next batch's rounds
+#endif
 #ifndef BMPS_GROUP_WARPS_HIGH
 #define BMPS_GROUP_WARPS_HIGH 1   // inner sweep: the per-group scalar phase runs on the CTA's last warps
 #endif
@@ -772,7 +772,7 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, double2* work, InnerShared<W2>&
   // warps already run batch b + 1's rounds: Q is not read by the sweep itself, so only the
   // off-diagonal Gram blocks stay between the two barriers. K_g and the rotation counts
   // are double-buffered by batch parity.
-  constexpr bool kDefer = NW >= 2 * NG;
+  constexpr bool kDefer = BMPS_INNER_DEFER && NW >= 2 * NG;
   constexpr int NSP = kDefer ? NW - NG : NW;   // warps of a deferred Q pass
   // quads of group g in batch mm: the g-th qa with qa < qa ^ mm (bit hb clear); mm = 0
   // pairs inside the quads 2g and 2g + 1
@@ -1241,9 +1241,13 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dy
   const int nitems = args.nitems;
   int cursor = blockIdx.x % nitems;
   volatile int* active = args.active;
-  while (*active > 0) {
+  // The exit test is taken by one thread and broadcast with the claim (s_item = -2): a
+  // per-thread `while (*active > 0)` let the warps of a CTA disagree when the last item
+  // retired between their reads -- the warps that stayed re-ran the previous claim from
+  // the stale shared words while warp 0 had left (found by the -DBMPS_DEBUG_CHECKS build:
+  // "claimed item already retired", tools/debug_stress.py).
+  for (;;) {
     BMPS_TICK(dc0);
-#if BMPS_WARP_CLAIM
     // warp 0 probes 32 items per round trip (lane l: item cursor + base + l), ballots
     // the ones with unclaimed visits and tries them in probe order; a claim used to
     // scan ~10 exhausted items one dependent load at a time (~7k cycles per visit)
@@ -1285,40 +1289,15 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dy
       }
       if (got >= 0) cursor = got;
       if (lane == 0) {
-        s_item = got;
+        s_item = (got < 0 && *active <= 0) ? -2 : got;
         s_v = gv;
         s_round = grnd;
         __threadfence();
       }
     }
-#else
-    if (threadIdx.x == 0) {
-      s_item = -1;
-      for (int probe = 0; probe < nitems; ++probe) {
-        const int i = (cursor + probe) % nitems;
-        JacSched* sc = args.sched + i;
-        WS_ACC(0, 14, 0, 1);   // probes (timer builds)
-        if (args.meta[i].conv) continue;
-        const int c = args.meta[i].c;
-        int nb = (c + w - 1) / w;
-        nb += nb & 1;
-        const unsigned nbv = (unsigned)(nb / 2);
-        const unsigned long long peek = *((volatile unsigned long long*)&sc->ticket);
-        if ((unsigned)(peek & 0xffffffffull) >= nbv) continue;
-        const unsigned long long old = atomicAdd(&sc->ticket, 1ull);
-        const unsigned v = (unsigned)(old & 0xffffffffull);
-        if (v >= nbv) continue;
-        s_item = i;
-        s_v = (int)v;
-        s_round = (unsigned)(old >> 32);
-        cursor = i;
-        break;
-      }
-      __threadfence();
-    }
-#endif
     __syncthreads();
     const int i = s_item;
+    if (i == -2) break;   // every item has converged (block-uniform)
     BMPS_TICK(dc1);
     if (i >= 0) { WS_ACC(0, 10, dc0, dc1); WS_ACC(0, 11, 0, 1); } else { WS_ACC(0, 12, dc0, dc1); }
     if (i < 0) {
@@ -1330,6 +1309,13 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dy
     const int v = s_v;
     const unsigned rnd = s_round;
     ItemMeta* m = args.meta + i;
+#ifdef BMPS_DEBUG_CHECKS
+    if (!(i < nitems && !m->conv) && (threadIdx.x & 31) == 0)
+      printf("claim check: block %d warp %d i %d nitems %d conv %d v %d rnd %u ticket %llx done %d c %d\n",
+             (int)blockIdx.x, (int)(threadIdx.x >> 5), i, nitems, i < nitems ? m->conv : -1, v, rnd,
+             i < nitems ? args.sched[i].ticket : 0ull, i < nitems ? args.sched[i].done : -1,
+             i < nitems ? m->c : -1);
+#endif
     BMPS_CHECK(i < nitems && !m->conv);
     const int r = m->jrows, c = m->c;
     double2* X = (m->dq ? args.Z : m->precond ? args.Y : args.X) + (size_t)i * args.mat_stride;

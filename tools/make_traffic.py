@@ -49,8 +49,8 @@ out = {
     "kernels": {n: {k: v for k, v in m.items()} for n, m in per.items()},
     "note": ("svd_* covers the K3 kernels (dq_colsort, qr_panel/qr_update/qr_form_y, "
              "jacobi_dynamic, dq_sort, dq_apply_q1). sm__ops_path_tensor_src_fp64 counts flops "
-             "(2 per DMMA multiply-add: 3.63e9 DMMA.8x8x4 x 256 x 2 = 1.86e12 on the Jacobi "
-             "launch of profiles/r01_jacobi_full2)."),
+             "(2 per DMMA multiply-add; 1.94e12 on the Jacobi launch of "
+             "profiles/r02_jacobi_full.txt = 3.79e9 DMMA.8x8x4 x 256 x 2)."),
 }
 json.dump(out, open(sys.argv[3], 'w'), indent=1)
 print(json.dumps({k: v for k, v in out.items() if k != 'kernels'}, indent=1))
