@@ -83,6 +83,17 @@ int32_t bmps_phase_cycles(uint64_t* out4);
  * trace of the Jacobi inner sweep's rotation / Q-update phase, 64 x 8 x 4 uint64. */
 int32_t bmps_inner_trace(uint64_t* out, int32_t n);
 
+/* Test hook (no reference counterpart; tests/test_gpu_inner_sweep.py): one inner
+ * Gram-space Jacobi sweep of a 32-column block-pair visit (jac_inner, the scalar part of
+ * mps.py:116's SVD replacement) on a caller-supplied 32 x 32 Hermitian Gram (complex128,
+ * column-major, device). full = 1: all 496 pairs, 0: the 256 pairs between columns 0..15
+ * and 16..31. tol, noise2, fro as in the rotation test |g| > tol * min(|x_i|, |x_j|) * fro.
+ * Writes the rotated Gram, the accumulated unitary Q (G_out = Q^H G_in Q) and the number
+ * of rotations of the first sweep. */
+int32_t bmps_debug_inner_sweep(const double* gram_in, double* gram_out, double* q_out,
+                               int32_t full, double tol, double noise2, double fro,
+                               int32_t max_inner, int32_t* nrot, void* stream);
+
 /* MpsState.__init__ (mps.py:55-66): |0...0>, unit boundary bonds, stats reset. */
 int32_t bmps_init_product(double* gamma, double* lam, int32_t* dims, double* trunc_err,
                           int64_t* entries, int64_t* peak, int32_t* max_bond_seen,

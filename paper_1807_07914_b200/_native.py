@@ -56,6 +56,7 @@ _SIGNATURES = {
     "bmps_default_params": ([_P], None),
     "bmps_phase_cycles": ([_P], _I),
     "bmps_inner_trace": ([_P, _I], _I),
+    "bmps_debug_inner_sweep": ([_P, _P, _P, _I, ctypes.c_double, ctypes.c_double, ctypes.c_double, _I, _P, _P], _I),
     "bmps_init_product": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P], _I),
     "bmps_apply_1q": ([_P, _P, _I, _I, _I, _P, _P, _I, _P], _I),
     "bmps_apply_2q_workspace_bytes": ([_I, _I], _SZ),
@@ -152,7 +153,7 @@ class tunables:
         return False
 
 
-_DEV_AIDS = ("bmps_phase_cycles", "bmps_inner_trace")   # timer-build diagnostics, not the product ABI
+_DEV_AIDS = ("bmps_phase_cycles", "bmps_inner_trace", "bmps_debug_inner_sweep")   # timer-build diagnostics, not the product ABI
 
 
 def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:

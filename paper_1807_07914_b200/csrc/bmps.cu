@@ -827,6 +827,29 @@ StateView make_view(double* gamma, double* lam, int32_t* dims, int n, int cap) {
   return sv;
 }
 
+// Test hook kernel of bmps_debug_inner_sweep: jac_inner on one 32 x 32 Gram.
+__global__ void __launch_bounds__(256) inner_sweep_test_kernel(const double2* gin, double2* gout,
+                                                              double2* qout, int full, double tol,
+                                                              double noise2, double fro, int max_inner,
+                                                              int* nrot) {
+  constexpr int W2 = 32;
+  using C = JacCfg<W2>;
+  extern __shared__ __align__(16) double2 tsm[];
+  double2* sG = tsm;
+  double2* sQ = sG + W2 * C::LDGG;
+  double2* work = sQ + W2 * C::LDG;
+  __shared__ InnerShared<W2> is;
+  for (int i = threadIdx.x; i < W2 * W2; i += blockDim.x) sG[(i % W2) + (i / W2) * C::LDGG] = gin[i];
+  __syncthreads();
+  const int n = jac_inner<W2>(sG, sQ, work, is, tol, noise2, fro, full != 0, max_inner);
+  __syncthreads();
+  for (int i = threadIdx.x; i < W2 * W2; i += blockDim.x) {
+    gout[i] = sG[(i % W2) + (i / W2) * C::LDGG];
+    qout[i] = sQ[(i % W2) + (i / W2) * C::LDG];
+  }
+  if (threadIdx.x == 0) *nrot = n;
+}
+
 }  // namespace
 
 extern "C" {
@@ -889,6 +912,25 @@ int32_t bmps_inner_trace(uint64_t* out, int32_t n) {
   (void)out; (void)n;
   return BMPS_E_ARG;
 #endif
+}
+
+// Test hook: one inner (Gram-space) sweep of the W2 = 32 visit on a caller-supplied Gram.
+int32_t bmps_debug_inner_sweep(const double* gram_in, double* gram_out, double* q_out,
+                               int32_t full, double tol, double noise2, double fro,
+                               int32_t max_inner, int32_t* nrot, void* stream) {
+  if (!gram_in || !gram_out || !q_out || !nrot || max_inner < 1) return BMPS_E_ARG;
+  constexpr int W2 = 32;
+  using C = JacCfg<W2>;
+  const size_t smem = sizeof(double2) * (size_t)(W2 * C::LDGG + W2 * C::LDG + 12 * 64);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(inner_sweep_test_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  inner_sweep_test_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(
+      (const double2*)gram_in, (double2*)gram_out, (double2*)q_out, full, tol, noise2, fro, max_inner, nrot);
+  ++g_launches;
+  return launch_status();
 }
 
 const char* bmps_status_string(int32_t code) {
