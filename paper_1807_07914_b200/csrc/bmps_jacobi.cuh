@@ -38,9 +38,6 @@ constexpr bool kTmaStaging = false;
 #ifndef BMPS_INNER_DEFER
 #define BMPS_INNER_DEFER 1   // inner sweep: Q update of a batch under the next batch's rounds
 #endif
-#ifndef BMPS_GROUP_WARPS_HIGH
-#define BMPS_GROUP_WARPS_HIGH 1   // inner sweep: the per-group scalar phase runs on the CTA's last warps
-#endif
 
 #ifndef BMPS_JAC_MINB
 #define BMPS_JAC_MINB 4   // resident Jacobi CTAs per SM the register budget is sized for
@@ -618,87 +615,84 @@ BMPS_DEV double2 shfl_xor_z(double2 v, int mask) {
   return make_double2(__shfl_xor_sync(0xffffffffu, v.x, mask), __shfl_xor_sync(0xffffffffu, v.y, mask));
 }
 
-// Phase S of jac_inner for one column group (one warp): a run of rounds in which pair P
-// of round ri joins local columns A_P and B_{P ^ ri}, register-resident.
+// Phase S of jac_inner for TWO column groups per warp (lanes 0..15: group ga, lanes
+// 16..31: group gb): a run of rounds in which pair P of round ri joins local columns A_P
+// and B_{P ^ ri}, register-resident.
 //   MODE 0: A_P = P, B_P = 4 + P, rounds ri = 0..3 (quad qa against quad qb);
 //   MODE 1: A_P = 2P, B_P = 2P + 1, one round (pairs (0,1)(2,3) inside each quad);
 //   MODE 2: A_P = {0,1,4,5}, B_P = A_P + 2, rounds ri = 0, 1 ({0,1} x {2,3} per quad).
-// Lanes 0..15 = (t, u) hold the 2x2 pair block (rows of pair t, columns of pair u) of
-// the group's 8 x 8 diagonal Gram block -- both triangles, each lane rotating its own
-// copy -- and all 32 lanes = (row k, pair tk) hold the two columns of pair tk of K_g.
-// From one round to the next only the B partners change (P ^ ri), i.e. the B-side
-// entries move between lanes by XOR shuffles; the four rotations of a round are computed
-// by the diagonal lanes (t, t) from their own registers and reach the other lanes
-// through 96 bytes of shared memory -- the only memory round trip of a round. Returns
-// the number of rotations. `k_identity`: K_g starts as the identity (not loaded).
+// Each half warp = lanes (t, u) holds the 2x2 pair blocks (rows of pair t, columns of pair
+// u) of its group's 8 x 8 diagonal Gram block -- both triangles, each lane rotating its own
+// copy -- and all 32 lanes = (row k, pair tk) hold the two columns of pair tk of both
+// groups' K. From one round to the next only the B partners change (P ^ ri), i.e. the
+// B-side entries move between lanes by XOR shuffles (inside a half warp); the rotations of a
+// round are computed by the diagonal lanes (t, t) from their own registers and reach the
+// other lanes through 96 bytes of shared memory per group -- the only memory round trip
+// of a round. Two groups per warp because the scalar FP64 instructions cost the shared
+// FP64 pipe two cycles per warp instruction however many lanes are active: with one
+// group per warp, four CTAs' phase-S warps kept the pipe of their sub-partition ~85% busy
+// in the cfg4 regime and every round waited for it. Returns the rotation counts
+// (group ga | group gb << 16). `k_identity`: K starts as the identity (not loaded).
 template <int W2, int MODE>
-BMPS_DEV int jac_group_rounds(double2* sG, double2* Kg, InnerShared<W2>& is, int g, int qa, int qb,
-                              bool k_identity, double thr2, double noise2) {
+BMPS_DEV int jac_group_rounds(double2* sG, double2* Kga, double2* Kgb, InnerShared<W2>& is, int ga,
+                              int qaa, int qba, int qab, int qbb, bool k_identity, double thr2,
+                              double noise2) {
   using C = JacCfg<W2>;
   constexpr int NR = MODE == 0 ? 4 : MODE == 1 ? 1 : 2;
   const int lane = threadIdx.x & 31;
+  const int hf = lane >> 4;                       // which of the warp's two groups (D role)
   const int t = (lane >> 2) & 3, u = lane & 3;
   const int k = lane & 7, tk = lane >> 3;
-  const bool drole = lane < 16;
+  const int g = ga + hf;
+  const int qa = hf ? qab : qaa, qb = hf ? qbb : qba;
   auto la = [](int P) { return MODE == 0 ? P : MODE == 1 ? 2 * P : (P & 1) + 4 * (P >> 1); };
   auto lb = [](int P) { return MODE == 0 ? 4 + P : MODE == 1 ? 2 * P + 1 : (P & 1) + 4 * (P >> 1) + 2; };
   const int cAt = batch_col<W2>(qa, qb, la(t)), cAu = batch_col<W2>(qa, qb, la(u));
-  double2 g00 = make_double2(0.0, 0.0), g01 = g00, g10 = g00, g11 = g00;
-  if (drole) {
+  double2 g00, g01, g10, g11;
+  {
     const int cBt = batch_col<W2>(qa, qb, lb(t)), cBu = batch_col<W2>(qa, qb, lb(u));
     g00 = sG[cAt + cAu * C::LDGG];
     g01 = sG[cAt + cBu * C::LDGG];
     g10 = sG[cBt + cAu * C::LDGG];
     g11 = sG[cBt + cBu * C::LDGG];
   }
-  double2 ka, kb;
+  double2 ka[2], kb[2];
   if (k_identity) {
-    ka = make_double2(k == la(tk) ? 1.0 : 0.0, 0.0);
-    kb = make_double2(k == lb(tk) ? 1.0 : 0.0, 0.0);
+#pragma unroll
+    for (int z = 0; z < 2; ++z) {
+      ka[z] = make_double2(k == la(tk) ? 1.0 : 0.0, 0.0);
+      kb[z] = make_double2(k == lb(tk) ? 1.0 : 0.0, 0.0);
+    }
   } else {
-    ka = Kg[k + 8 * la(tk)];
-    kb = Kg[k + 8 * lb(tk)];
+    ka[0] = Kga[k + 8 * la(tk)];
+    kb[0] = Kga[k + 8 * lb(tk)];
+    ka[1] = Kgb[k + 8 * la(tk)];
+    kb[1] = Kgb[k + 8 * lb(tk)];
   }
   int cnt = 0;
 #pragma unroll
   for (int ri = 0; ri < NR; ++ri) {
-#ifdef BMPS_INNER_TIMERS
-    const long long q0 = clock64();
-#endif
     if (ri > 0) {
       const int x = ri ^ (ri - 1);
       g01 = shfl_xor_z(g01, x);
       g10 = shfl_xor_z(g10, x << 2);
       g11 = shfl_xor_z(g11, x | (x << 2));
-      kb = shfl_xor_z(kb, x << 3);
+      kb[0] = shfl_xor_z(kb[0], x << 3);
+      kb[1] = shfl_xor_z(kb[1], x << 3);
     }
     int act = 0;
-#ifdef BMPS_INNER_TIMERS
-    const long long q1 = clock64();
-#endif
-    if (drole && t == u) {
+    if (t == u) {
       double c;
       double2 sg;
-#ifdef BMPS_X_SKIP_ROT
-      c = 0.8; sg = make_double2(g01.x > 0 ? 0.6 : -0.6, 0.0); act = 1;
-#else
       act = jacobi_rotation(g00.x, g11.x, g01, thr2, noise2, c, sg);
-#endif
       is.c[g][t] = c;
       is.sg[g][t] = sg;
     }
-#ifdef BMPS_INNER_TIMERS
-    const long long q2 = clock64();
-#endif
     const unsigned am = __ballot_sync(0xffffffffu, act);
     __syncwarp();
-#ifdef BMPS_INNER_TIMERS
-    const long long q3 = clock64();
-#endif
     if (am) {
-      cnt += __popc(am);
-#ifndef BMPS_X_SKIP_D
-      if (drole) {
+      cnt += __popc(am & 0xffffu) | (__popc(am >> 16) << 16);
+      {
         // columns by pair u (right: J_u), then rows by pair t (left: J_t^H)
         const double cu = is.c[g][u], ct = is.c[g][t];
         const double2 su = is.sg[g][u], st = is.sg[g][t];
@@ -715,39 +709,29 @@ BMPS_DEV int jac_group_rounds(double2* sG, double2* Kg, InnerShared<W2>& is, int
           g10 = make_double2(0.0, 0.0);
         }
       }
-#endif
-#ifndef BMPS_X_SKIP_K
-      {
-        const double ck = is.c[g][tk];
-        const double2 sk = is.sg[g][tk];
-        const double2 na = cmsc(ka, ck, sk, kb);
-        kb = cma(kb, ck, sk, ka);
-        ka = na;
+#pragma unroll
+      for (int z = 0; z < 2; ++z) {
+        const double ck = is.c[ga + z][tk];
+        const double2 sk = is.sg[ga + z][tk];
+        const double2 na = cmsc(ka[z], ck, sk, kb[z]);
+        kb[z] = cma(kb[z], ck, sk, ka[z]);
+        ka[z] = na;
       }
-#endif
     }
     __syncwarp();   // the parameters are consumed before the next round rewrites them
-#ifdef BMPS_INNER_TIMERS
-    if (lane == 0 && g == 0) {
-      const long long q4 = clock64();
-      atomicAdd(&g_phase_cycles[16], (unsigned long long)(q1 - q0));
-      atomicAdd(&g_phase_cycles[17], (unsigned long long)(q2 - q1));
-      atomicAdd(&g_phase_cycles[18], (unsigned long long)(q3 - q2));
-      atomicAdd(&g_phase_cycles[19], (unsigned long long)(q4 - q3));
-      atomicAdd(&g_phase_cycles[20], 1ull);
-    }
-#endif
   }
   constexpr int xl = NR - 1;   // B partners of the last round
-  if (drole) {
+  {
     const int cBt = batch_col<W2>(qa, qb, lb(t ^ xl)), cBu = batch_col<W2>(qa, qb, lb(u ^ xl));
     sG[cAt + cAu * C::LDGG] = g00;
     sG[cAt + cBu * C::LDGG] = g01;
     sG[cBt + cAu * C::LDGG] = g10;
     sG[cBt + cBu * C::LDGG] = g11;
   }
-  Kg[k + 8 * la(tk)] = ka;
-  Kg[k + 8 * lb(tk ^ xl)] = kb;
+  Kga[k + 8 * la(tk)] = ka[0];
+  Kga[k + 8 * lb(tk ^ xl)] = kb[0];
+  Kgb[k + 8 * la(tk)] = ka[1];
+  Kgb[k + 8 * lb(tk ^ xl)] = kb[1];
   return cnt;
 }
 
@@ -758,7 +742,7 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, double2* work, InnerShared<W2>&
   constexpr int NQ = W2 / 4, NG = W2 / 8, NW = G::kN / 32;
   constexpr int NBo = NG * (NG - 1) / 2;   // off-diagonal group blocks (p < q)
   constexpr int NT = NBo + NG * NG;        // + Q tiles (8 rows x one group)
-  static_assert(NW >= NG, "one warp per column group");
+  static_assert(2 * NW >= W2 / 8, "one warp per two column groups");
   const int tid = G::tid(), lane = tid & 31, wrp = tid >> 5;
   const int kr = lane & 3, rc = lane >> 2;
   for (int idx = tid; idx < W2 * W2; idx += G::n()) {
@@ -772,8 +756,10 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, double2* work, InnerShared<W2>&
   // warps already run batch b + 1's rounds: Q is not read by the sweep itself, so only the
   // off-diagonal Gram blocks stay between the two barriers. K_g and the rotation counts
   // are double-buffered by batch parity.
-  constexpr bool kDefer = BMPS_INNER_DEFER && NW >= 2 * NG;
-  constexpr int NSP = kDefer ? NW - NG : NW;   // warps of a deferred Q pass
+  static_assert(NG % 2 == 0 || NG == 1, "two groups per phase-S warp");
+  constexpr int NGW = (NG + 1) / 2;            // phase-S warps (two groups each)
+  constexpr bool kDefer = BMPS_INNER_DEFER && NW >= 2 * NGW;
+  constexpr int NSP = NW - NGW;                // warps of a deferred Q pass
   // quads of group g in batch mm: the g-th qa with qa < qa ^ mm (bit hb clear); mm = 0
   // pairs inside the quads 2g and 2g + 1
   auto group_quads = [](int mm, int g, int& qa, int& qb) {
@@ -804,9 +790,6 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, double2* work, InnerShared<W2>&
     for (int h = 0; h < 2; ++h)
       sQ[(t8 + rc) + batch_col<W2>(qa, qb, 2 * kr + h) * C::LDG] = z3_get(acc, h);
   };
-  const bool gwarp = BMPS_GROUP_WARPS_HIGH ? wrp >= NW - NG : wrp < NG;
-  const int gidx = BMPS_GROUP_WARPS_HIGH ? wrp - (NW - NG) : wrp;       // group of a group warp
-  const int sidx = BMPS_GROUP_WARPS_HIGH ? wrp : wrp - NG;              // index of a spare warp
   for (int it = 0; it < max_inner; ++it) {
     int any = 0, prev_nact = 0, prev_mm = 0;
     for (int bi = 0; bi < nbatch; ++bi) {
@@ -814,25 +797,35 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, double2* work, InnerShared<W2>&
       const int mm = full ? bi : NQ / 2 + bi;
       int* cnt = is.cnt[bi & 1];
       double2* K = work + (kDefer ? (bi & 1) * NG * 64 : 0);
+      // the phase-S warps alternate between the CTA's last NGW warps and the NGW before
+      // them from batch to batch, so every SM sub-partition gets its share of the scalar
+      // work whatever the co-resident CTAs are doing
+      const int gbase = (kDefer && (bi & 1)) ? NW - 2 * NGW : NW - NGW;
+      const bool gwarp = wrp >= gbase && wrp < gbase + NGW;
       if (gwarp) {
-        // ---- S: the batch's rounds, one group per warp (the group warps sit on
-        // distinct SM sub-partitions: NG = 4 consecutive warp ids) ----
-        const int g = gidx;
-        int qa, qb;
-        group_quads(mm, g, qa, qb);
-        double2* Kg = K + g * 64;
+        // ---- S: the batch's rounds, two groups per warp ----
+        const int ga = 2 * (wrp - gbase), gb = NG > 1 ? ga + 1 : ga;
+        int qaa, qba, qab, qbb;
+        group_quads(mm, ga, qaa, qba);
+        group_quads(mm, gb, qab, qbb);
+        double2* Kga = K + ga * 64;
+        double2* Kgb = K + gb * 64;
         int gcnt;
         if (mm == 0) {
           // pairs inside each quad: (0,1)(2,3), then the 2 x 2 cross rounds of {0,1} x {2,3}
-          gcnt = jac_group_rounds<W2, 1>(sG, Kg, is, g, qa, qb, true, thr2, noise2);
+          gcnt = jac_group_rounds<W2, 1>(sG, Kga, Kgb, is, ga, qaa, qba, qab, qbb, true, thr2, noise2);
           __syncwarp();
-          gcnt += jac_group_rounds<W2, 2>(sG, Kg, is, g, qa, qb, false, thr2, noise2);
+          gcnt += jac_group_rounds<W2, 2>(sG, Kga, Kgb, is, ga, qaa, qba, qab, qbb, false, thr2, noise2);
         } else {
-          gcnt = jac_group_rounds<W2, 0>(sG, Kg, is, g, qa, qb, true, thr2, noise2);
+          gcnt = jac_group_rounds<W2, 0>(sG, Kga, Kgb, is, ga, qaa, qba, qab, qbb, true, thr2, noise2);
         }
-        if (lane == 0) cnt[g] = gcnt;
+        if (lane == 0) {
+          cnt[ga] = gcnt & 0xffff;
+          if (NG > 1) cnt[gb] = gcnt >> 16;
+        }
       } else if (kDefer && prev_nact) {
         // the previous batch's Q update, under this batch's rounds
+        const int sidx = wrp < gbase ? wrp : wrp - NGW;
         for (int tile = sidx; tile < NG * NG; tile += NSP)
           q_tile(tile, prev_mm, work + ((bi - 1) & 1) * NG * 64, is.cnt[(bi - 1) & 1]);
       }
