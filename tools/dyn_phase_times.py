@@ -2,7 +2,7 @@
 import ctypes, sys, os, pathlib, torch
 sys.path.insert(0, '.')
 from paper_1807_07914_b200 import _native
-os.environ['BMPS_LIB'] = os.environ.get('TIMERS_LIB', 'tools/libbmps_timers.so')
+os.environ['BMPS_LIB'] = os.environ.get('TIMERS_LIB', 'tools/variants/timers.so')
 lib = _native.load()
 import bench
 from paper_1807_07914_b200 import MpsBatch, TruncationPolicy, compile_batch
