@@ -161,7 +161,12 @@ struct CtaGrp {
   BMPS_DEV static int tid() { return (int)threadIdx.x; }
   BMPS_DEV static int n() { return (int)blockDim.x; }
   BMPS_DEV static void sync() { __syncthreads(); }
-  BMPS_DEV static int count(int p) { return __syncthreads_count(p); }
+  // BAR counts arrivals in units of warps: a warp must arrive converged (the compiler
+  // does not always reconverge ahead of BAR.RED as it does ahead of BAR.SYNC)
+  BMPS_DEV static int count(int p) {
+    __syncwarp();
+    return __syncthreads_count(p);
+  }
 };
 template <int BASE, int N, int ID>
 struct NamedGrp {
@@ -791,7 +796,7 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, double2* work, InnerShared<W2>&
       sQ[(t8 + rc) + batch_col<W2>(qa, qb, 2 * kr + h) * C::LDG] = z3_get(acc, h);
   };
   for (int it = 0; it < max_inner; ++it) {
-    int any = 0, prev_nact = 0, prev_mm = 0;
+    int any = 0, nrot = 0, prev_nact = 0, prev_mm = 0;
     for (int bi = 0; bi < nbatch; ++bi) {
       BMPS_TICK(tr0);
       const int mm = full ? bi : NQ / 2 + bi;
@@ -802,6 +807,7 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, double2* work, InnerShared<W2>&
       // work whatever the co-resident CTAs are doing
       const int gbase = (kDefer && (bi & 1)) ? NW - 2 * NGW : NW - NGW;
       const bool gwarp = wrp >= gbase && wrp < gbase + NGW;
+      int my_act = 0;   // this warp's groups rotated in this batch (warp-uniform)
       if (gwarp) {
         // ---- S: the batch's rounds, two groups per warp ----
         const int ga = 2 * (wrp - gbase), gb = NG > 1 ? ga + 1 : ga;
@@ -823,19 +829,24 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, double2* work, InnerShared<W2>&
           cnt[ga] = gcnt & 0xffff;
           if (NG > 1) cnt[gb] = gcnt >> 16;
         }
+        my_act = gcnt != 0;
       } else if (kDefer && prev_nact) {
         // the previous batch's Q update, under this batch's rounds
         const int sidx = wrp < gbase ? wrp : wrp - NGW;
         for (int tile = sidx; tile < NG * NG; tile += NSP)
           q_tile(tile, prev_mm, work + ((bi - 1) & 1) * NG * 64, is.cnt[(bi - 1) & 1]);
       }
-      G::sync();
+      // one counting barrier closes phase S and tells every thread -- from the barrier
+      // itself, not from shared memory -- whether any group rotated: the number of CTA
+      // barriers a thread executes must never depend on a value it reads after one
+      const int nact = G::count(my_act);
       BMPS_TICK(tr1);
       BMPS_ACC(4, tr0, tr1);
-      int nact = 0;
+      any |= nact;
+      if (nact) {
 #pragma unroll
-      for (int g = 0; g < NG; ++g) nact += cnt[g];
-      any += nact;
+        for (int g = 0; g < NG; ++g) nrot += cnt[g];   // reported only, never branched on
+      }
       if (nact) {
         // ---- M: the off-diagonal group blocks on the tensor cores ----
         for (int task = wrp; task < (kDefer ? NBo : NT); task += NW) {
@@ -896,7 +907,7 @@ BMPS_DEV int jac_inner(double2* sG, double2* sQ, double2* work, InnerShared<W2>&
           q_tile(tile, prev_mm, work + ((nbatch - 1) & 1) * NG * 64, is.cnt[(nbatch - 1) & 1]);
       G::sync();
     }
-    if (it == 0) first = any;
+    if (it == 0) first = any ? max(nrot, 1) : 0;
     if (!any) break;
   }
   return first;
@@ -999,21 +1010,26 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
   {
     constexpr int w = W2 / 2;
     const int npairs = full ? W2 * W2 : w * w;
-    for (int idx = G::tid(); idx < npairs && !need; idx += G::n()) {
+    // no early exit: a warp must reach the counting barrier converged -- BAR counts
+    // arrivals in units of warps, so a warp arriving in two fragments releases it early
+    // (seen on the 64-column kernel: "Warp Illegal Instruction", cuda-gdb found one lane of
+    // a warp a whole phase ahead of the other 31)
+    for (int idx = G::tid(); idx < npairs; idx += G::n()) {
       int i, j;
       if (full) {
         i = idx % W2;
         j = idx / W2;
-        if (i >= j) continue;
       } else {
         i = idx % w;
         j = w + idx / w;
       }
-      need = jacobi_needs(sG[i + i * C::LDGG].x, sG[j + j * C::LDGG].x, sG[i + j * C::LDGG], tol,
-                          noise2, fro);
+      need |= (i < j) && jacobi_needs(sG[i + i * C::LDGG].x, sG[j + j * C::LDGG].x, sG[i + j * C::LDGG],
+                                      tol, noise2, fro);
     }
+    __syncwarp();
   }
   const int needed = G::count(need);
+
   const int nrot = needed ? jac_inner<W2, G>(sG, sQ, sP, rs, tol, noise2, fro, full, max_inner) : 0;
   BMPS_TICK(tv2);
   BMPS_ACC(1, tv1, tv2);
@@ -1712,19 +1728,19 @@ __global__ void __launch_bounds__(256, 3) jacobi_cluster_kernel(JacArgs args) {
     int need = 0;
     {
       const int npairs = full ? W2 * W2 : w * w;
-      for (int idx = tid; idx < npairs && !need; idx += blockDim.x) {
+      for (int idx = tid; idx < npairs; idx += blockDim.x) {   // no early exit, see jac_visit
         int a, b2;
         if (full) {
           a = idx % W2;
           b2 = idx / W2;
-          if (a >= b2) continue;
         } else {
           a = idx % w;
           b2 = w + idx / w;
         }
-        need = jacobi_needs(sG[a + a * C::LDGG].x, sG[b2 + b2 * C::LDGG].x, sG[a + b2 * C::LDGG], tol,
-                            noise2, fro);
+        need |= (a < b2) && jacobi_needs(sG[a + a * C::LDGG].x, sG[b2 + b2 * C::LDGG].x,
+                                         sG[a + b2 * C::LDGG], tol, noise2, fro);
       }
+      __syncwarp();
     }
     const int nrot = __syncthreads_or(need) ? jac_inner<W2>(sG, sQ, sP, rs, tol, noise2, fro, full, args.max_inner)
                                             : 0;

@@ -154,6 +154,17 @@ def test_disabled_variants_are_rejected():
             mps_run(prog, 12, TruncationPolicy(1e-10, 64))
 
 
+@pytest.mark.parametrize("w2", [16, 64])
+@pytest.mark.parametrize("chi,cutoff", [(64, 1e-10), (128, 0.0)])
+def test_other_panel_widths_match_oracle(w2, chi, cutoff):
+    """block_w2 = 16 / 64: visits of 16- and 64-column panels (2 and 8 column groups in
+    the batched inner sweep, deferred Q update on 7 / 4 spare warps) instead of 32."""
+    from paper_1807_07914_b200 import _native
+    with _native.tunables(block_w2=w2):
+        prog = brick_circuit(14, 14, np.random.default_rng(700 + chi + w2))
+        _compare(prog, 14, cutoff, chi, seed=chi + w2)
+
+
 @pytest.mark.parametrize("dq", [0, 1])
 @pytest.mark.parametrize("chi,cutoff", [(64, 1e-12), (128, 1e-10), (128, 0.0)])
 def test_double_qr_preconditioning_matches_oracle(dq, chi, cutoff):
