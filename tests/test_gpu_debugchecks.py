@@ -28,3 +28,16 @@ def test_debug_checks_are_live(mode):
         assert out.returncode == 0 and "DEBUGCHECK ok" in text, text[-2000:]
     else:
         assert "BMPS_CHECK failed" in text, text[-2000:]
+
+
+@pytest.mark.skipif(not LIB.exists(), reason="debug-checks build absent")
+def test_visit_scheduling_invariants_hold_under_stress():
+    """tools/debug_stress.py under the invariant-check build: cfg4 slices (thousands of
+    small items per launch, where a CTA once re-ran a stale claim after the launch's last
+    item retired) and chi = 256 bench steps; any violated invariant traps."""
+    env = {**os.environ, "BMPS_LIB": str(LIB)}
+    out = subprocess.run([sys.executable, "tools/debug_stress.py", "8"], cwd=ROOT, env=env,
+                         capture_output=True, text=True, timeout=600)
+    text = out.stdout + out.stderr
+    assert out.returncode == 0 and "BMPS_CHECK" not in text, text[-2000:]
+    assert "cfg4 x 8 ok" in text and "chi256 steps x 8 ok" in text
