@@ -922,11 +922,8 @@ int32_t bmps_debug_inner_sweep(const double* gram_in, double* gram_out, double* 
   constexpr int W2 = 32;
   using C = JacCfg<W2>;
   const size_t smem = sizeof(double2) * (size_t)(W2 * C::LDGG + W2 * C::LDG + 12 * 64);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(inner_sweep_test_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  // per call: the attribute is per device and this is a test hook, not a hot path
+  cudaFuncSetAttribute(inner_sweep_test_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   inner_sweep_test_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(
       (const double2*)gram_in, (double2*)gram_out, (double2*)q_out, full, tol, noise2, fro, max_inner, nrot);
   ++g_launches;
