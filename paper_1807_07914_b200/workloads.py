@@ -52,6 +52,31 @@ def brick_circuit(n: int, depth: int, rng: np.random.Generator, haar_prob: float
     return program
 
 
+ROUND_POOL = ("X", "Y", "Z", "RX", "RY", "RZ")
+
+
+def round_circuit(n: int, rounds: int, seed: int, pool: tuple = ROUND_POOL) -> list:
+    """The reference's memory-scaling workload (``R:src/mpsqvm/bench.py:45-60``,
+    ``generate_round_circuit``): a Hadamard layer, then per round one gate of ``pool`` on
+    every qubit (angles U[0, 2 pi), drawn in the reference's order from
+    ``default_rng(seed)``, so a seed names the same circuit in both code bases) and a
+    CNOT brick layer starting at qubit 0 on odd rounds, at qubit 1 on even ones. Its
+    acceptance laws: chi = 4 after two rounds, chi = 2^(n/2) at saturation."""
+    if n < 2:
+        raise ValueError("need at least 2 qubits")
+    if rounds < 1:
+        raise ValueError("need at least 1 round")
+    rng = np.random.default_rng(seed)
+    program: list = [Instruction(GateKind.H, (q,)) for q in range(n)]
+    for r in range(1, rounds + 1):
+        for q in range(n):
+            kind = GateKind(pool[int(rng.integers(len(pool)))])
+            params = (float(rng.uniform(0.0, 2.0 * np.pi)),) if kind.num_params else ()
+            program.append(Instruction(kind, (q,), params))
+        program += [Instruction(GateKind.CNOT, (a, a + 1)) for a in range((r + 1) % 2, n - 1, 2)]
+    return program
+
+
 def random_bitstrings(n: int, count: int, rng: np.random.Generator) -> list[str]:
     bits = rng.integers(0, 2, size=(count, n))
     return ["".join("1" if b else "0" for b in row) for row in bits]
