@@ -148,6 +148,15 @@ typedef struct bmps_params {
                             preconditioner, Jacobi, double-QR epilogue) at index
                             *svd_events_used, then increments it */
   int32_t* svd_events_used;
+  /* threshold schedule of the dynamic Jacobi (jacobi_mode 4): in sweeps < thr_a_sweeps a
+   * block-pair visit whose largest relative coupling |x_i^H x_j| / (|x_i| |x_j|) is below
+   * thr_a only forms its Gram (no rotations, no panel update) and keeps the item's sweep
+   * open; thr_b until thr_b_sweeps; afterwards every visit rotates down to tol_factor, so
+   * the converged state is the same. 0 sweeps = off. */
+  double thr_a;          /* (3e-2) */
+  double thr_b;          /* (3e-3) */
+  int32_t thr_a_sweeps;  /* (2) */
+  int32_t thr_b_sweeps;  /* (5) */
 } bmps_params;
 
 void bmps_default_params(bmps_params* p);

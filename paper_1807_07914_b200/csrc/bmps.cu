@@ -888,6 +888,10 @@ void bmps_default_params(bmps_params* p) {
   p->n_svd_events = 0;
   p->svd_events = nullptr;
   p->svd_events_used = nullptr;
+  p->thr_a = 3e-2;
+  p->thr_b = 3e-3;
+  p->thr_a_sweeps = 2;
+  p->thr_b_sweeps = 5;
 }
 
 // Development aid: cumulative Jacobi phase cycles (builds with -DBMPS_PHASE_TIMERS only).
@@ -990,7 +994,8 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       P.jac_per_sm < 0 || P.jac_per_sm > 8 || P.cluster_size < 1 || P.cluster_size > 16 ||
       !(P.jacobi_mode == 0 || P.jacobi_mode == 1 || P.jacobi_mode == 4 || P.jacobi_mode == 2 ||
         P.jacobi_mode == 3) ||
-      P.jac_ws != 0 || (P.n_svd_events > 0 && (!P.svd_events || !P.svd_events_used)))
+      P.jac_ws != 0 || !(P.thr_a >= 0) || !(P.thr_b >= 0) || P.thr_a_sweeps < 0 ||
+      P.thr_b_sweeps < 0 || P.thr_b_sweeps >= P.max_sweeps || (P.n_svd_events > 0 && (!P.svd_events || !P.svd_events_used)))
     return BMPS_E_ARG;
 #ifndef BMPS_EXPERIMENTAL
   if (P.tma_staging || P.jacobi_mode == 2 || P.jacobi_mode == 3) return BMPS_E_ARG;
@@ -1112,6 +1117,10 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
   ja.gcache_stride = ws.gcache_stride;
   ja.pairlog = P.pair_skip ? ws.pairlog : nullptr;
   ja.nbcap = ws.nbcap;
+  ja.thr_a = P.thr_a;
+  ja.thr_b = P.thr_b;
+  ja.thr_a_sweeps = P.thr_a_sweeps;
+  ja.thr_b_sweeps = P.thr_b_sweeps;
   if (cmax <= 64) {
     ja.persistent = 1;
     if (cmax <= 32)

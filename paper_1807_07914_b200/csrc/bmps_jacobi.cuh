@@ -140,6 +140,8 @@ struct JacArgs {
                      // [nbcap x nbcap] round of the last clean check of each block pair
                      // (-1: none / rotated since); nullptr: no skipping
   int nbcap;
+  double thr_a, thr_b;        // dynamic mode: relative-coupling thresholds of the first
+  int thr_a_sweeps, thr_b_sweeps;   // sweeps (< a_sweeps: thr_a, < b_sweeps: thr_b, then 0)
 };
 
 // Shared state of the inner (Gram-space) sweep, see jac_inner: per column group the
@@ -927,11 +929,16 @@ BMPS_DEV double2* jac_ring3(double2* sP, double2* sQ, int k) {
 // `resident`, the whole panel (r <= RC) already sits in buffer 0 and is
 // neither loaded nor stored here. W2 = 32 streams the panel with TMA bulk
 // copies (double buffered, mbarrier completion); W2 = 64 with cp.async.
+// Returns 0: the pair is clean (no pair of columns fails the rotation test), 1: rotated,
+// 2: deferred -- `thr2` > 0 and no pair's relative coupling |g|^2 / (a b) reaches it: the
+// visit costs its Gram pass only and the caller keeps the sweep open (threshold Jacobi:
+// early sweeps spend their inner sweeps and applies on the large couplings; the last
+// sweeps run with thr2 = 0, so the final state is the same fixed point).
 template <int W2, class G = CtaGrp>
-BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, double noise2,
-                        double fro, bool full, int max_inner, bool resident, double2* sG,
-                        double2* sQ, double2* sP, InnerShared<W2>& rs, JacStage& st, bool tma,
-                        double2* gcache = nullptr) {
+BMPS_DEV int jac_visit(double2* X, int r, int c, int I, int J, double tol, double noise2,
+                       double fro, bool full, int max_inner, bool resident, double2* sG,
+                       double2* sQ, double2* sP, InnerShared<W2>& rs, JacStage& st, bool tma,
+                       double2* gcache = nullptr, double thr2 = 0.0) {
   using C = JacCfg<W2>;
   BMPS_TICK(tv0);
   const int nch = (r + C::RC - 1) / C::RC;
@@ -1023,12 +1030,20 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
         i = idx % w;
         j = w + idx / w;
       }
-      need |= (i < j) && jacobi_needs(sG[i + i * C::LDGG].x, sG[j + j * C::LDGG].x, sG[i + j * C::LDGG],
-                                      tol, noise2, fro);
+      if (i < j) {
+        const double a = sG[i + i * C::LDGG].x, b = sG[j + j * C::LDGG].x;
+        const double2 g = sG[i + j * C::LDGG];
+        if (jacobi_needs(a, b, g, tol, noise2, fro)) need |= 1 | (cabs2(g) > thr2 * a * b ? 2 : 0);
+      }
     }
     __syncwarp();
   }
-  const int needed = G::count(need);
+  int needed = G::count(need & 1);
+  bool deferred = false;
+  if (needed && thr2 > 0.0) {          // block-uniform
+    deferred = G::count(need & 2) == 0;
+    if (deferred) needed = 0;
+  }
 
   const int nrot = needed ? jac_inner<W2, G>(sG, sQ, sP, rs, tol, noise2, fro, full, max_inner) : 0;
   BMPS_TICK(tv2);
@@ -1036,7 +1051,7 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
   BMPS_ACC(3, 0, 1);
   if (gcache != nullptr && !resident && (full || nrot > 0)) jac_cache_store<W2, G>(sG, cI, cJ);
   if (C::G_IN_BUF) G::sync();  // sG (buffer 1) is read before the apply refills it
-  if (nrot == 0) return false;
+  if (nrot == 0) return deferred ? 2 : 0;
   double aacc[C::AT][kZ3];
   if (!resident) {
     if (bulk) jac_issue_bulk<W2>(sP, st, 0, X, r, c, 0, I, J);
@@ -1047,7 +1062,7 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
     G::sync();
     jac_apply_writeback<W2>(aacc, sP);
     G::sync();
-    return true;
+    return 1;
   }
   if (bulk) {
     for (int k = 0; k < nch; ++k) {
@@ -1071,7 +1086,7 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
       jac_store_bulk<W2>(cur, X, r, c, k * C::RC, I, J);
     }
     jac_flush_bulk();
-    return true;
+    return 1;
   }
 
   // cp.async re-stream: load chunk k+1 while chunk k is multiplied and stored
@@ -1093,7 +1108,7 @@ BMPS_DEV bool jac_visit(double2* X, int r, int c, int I, int J, double tol, doub
   }
   BMPS_TICK(tv3);
   BMPS_ACC(2, tv2, tv3);
-  return true;
+  return 1;
 }
 
 template <int W2, class G = CtaGrp>
@@ -1380,13 +1395,17 @@ __global__ void __launch_bounds__(256, (W2 <= 32) ? BMPS_JAC_MINB : 1) jacobi_dy
       skip = lc >= 0 && *((volatile int*)(last_rot + I)) < lc && *((volatile int*)(last_rot + J)) < lc;
     }
     if (skip) { WS_ACC(0, 13, 0, 1); }
-    const bool dirty = skip ? false
-                            : jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, rho == 0,
-                                            args.max_inner, false, sG, sQ, sP, rs, st, args.tma, gc);
+    const double thr = sweep < args.thr_a_sweeps ? args.thr_a : sweep < args.thr_b_sweeps ? args.thr_b : 0.0;
+    const int ret = skip ? 0
+                         : jac_visit<W2>(X, r, c, I, J, tol, noise2, fro, rho == 0, args.max_inner,
+                                         false, sG, sQ, sP, rs, st, args.tma, gc, thr * thr);
+    const bool dirty = ret != 0;   // rotated, or deferred by the sweep's threshold: not converged
     if (last_rot && !skip && threadIdx.x == 0) {
-      if (dirty) {
+      if (ret == 1) {
         last_rot[I] = (int)rnd;
         last_rot[J] = (int)rnd;
+        *last_chk = -1;
+      } else if (ret == 2) {
         *last_chk = -1;
       } else {
         *last_chk = (int)rnd;

@@ -154,6 +154,19 @@ def test_disabled_variants_are_rejected():
             mps_run(prog, 12, TruncationPolicy(1e-10, 64))
 
 
+@pytest.mark.parametrize("sched", [(0.0, 0, 0.0, 0), (3e-2, 2, 3e-3, 5), (1e-1, 3, 1e-2, 6)])
+@pytest.mark.parametrize("chi,cutoff", [(64, 1e-10), (128, 0.0)])
+def test_threshold_schedules_match_oracle(sched, chi, cutoff):
+    """Threshold Jacobi (thr_a / thr_b: early sweeps defer block pairs whose largest
+    relative coupling is under the sweep's threshold): off, the default schedule and a
+    coarser one all converge to the oracle's results."""
+    from paper_1807_07914_b200 import _native
+    ta, sa, tb, sb = sched
+    with _native.tunables(thr_a=ta, thr_a_sweeps=sa, thr_b=tb, thr_b_sweeps=sb):
+        prog = brick_circuit(14, 14, np.random.default_rng(800 + chi))
+        _compare(prog, 14, cutoff, chi, seed=chi + sa)
+
+
 @pytest.mark.parametrize("w2", [16, 64])
 @pytest.mark.parametrize("chi,cutoff", [(64, 1e-10), (128, 0.0)])
 def test_other_panel_widths_match_oracle(w2, chi, cutoff):

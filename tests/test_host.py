@@ -129,6 +129,7 @@ def test_library_exports_every_header_symbol():
     # per-call tunables: defaults come from the library, unknown names are rejected
     d = _native.default_params()
     assert d["tol_factor"] == 4.0 and d["jacobi_mode"] == 4 and d["block_w2"] == 32
+    assert (d["thr_a"], d["thr_a_sweeps"], d["thr_b"], d["thr_b_sweeps"]) == (3e-2, 2, 3e-3, 5)
     with pytest.raises(ValueError):
         _native.params(nonsense=1)
     with _native.tunables(jac_cluster=4):
