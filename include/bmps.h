@@ -157,6 +157,8 @@ typedef struct bmps_params {
   double thr_b;          /* (3e-3) */
   int32_t thr_a_sweeps;  /* (2) */
   int32_t thr_b_sweeps;  /* (5) */
+  int32_t thr_auto;      /* 1: no thresholds when a round's visits do not fill the resident
+                            CTAs (latency-bound launch: the sweep count is what matters) (1) */
 } bmps_params;
 
 void bmps_default_params(bmps_params* p);

@@ -892,6 +892,7 @@ void bmps_default_params(bmps_params* p) {
   p->thr_b = 3e-3;
   p->thr_a_sweeps = 2;
   p->thr_b_sweeps = 5;
+  p->thr_auto = 1;
 }
 
 // Development aid: cumulative Jacobi phase cycles (builds with -DBMPS_PHASE_TIMERS only).
@@ -1160,6 +1161,10 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
                     : wi == 1 ? nbmax / 2
                               : (cmax + 15) / 16;
       const int grid = std::min(slots, nitems * vis);
+      // threshold sweeps trade a fraction of a sweep for fewer applies: a gain when the
+      // launch is throughput-bound, a loss when a round's visits do not even fill the
+      // resident CTAs and the item's sweep count is what the layer waits for
+      if (P.thr_auto && (long long)nitems * vis < slots) ja.thr_a_sweeps = ja.thr_b_sweeps = 0;
       if (csize > 0) {
         const int nclusters = std::max(1, std::min(nitems * (nbmax / 2), dc.cl_per_sm * dc.sms / csize));
         cudaLaunchConfig_t cfg = {};

@@ -162,7 +162,7 @@ def test_threshold_schedules_match_oracle(sched, chi, cutoff):
     coarser one all converge to the oracle's results."""
     from paper_1807_07914_b200 import _native
     ta, sa, tb, sb = sched
-    with _native.tunables(thr_a=ta, thr_a_sweeps=sa, thr_b=tb, thr_b_sweeps=sb):
+    with _native.tunables(thr_a=ta, thr_a_sweeps=sa, thr_b=tb, thr_b_sweeps=sb, thr_auto=0):
         prog = brick_circuit(14, 14, np.random.default_rng(800 + chi))
         _compare(prog, 14, cutoff, chi, seed=chi + sa)
 
