@@ -159,6 +159,8 @@ typedef struct bmps_params {
   int32_t thr_b_sweeps;  /* (5) */
   int32_t thr_auto;      /* 1: no thresholds when a round's visits do not fill the resident
                             CTAs (latency-bound launch: the sweep count is what matters) (1) */
+  int32_t qr_small;      /* QR panels of <= 128 rows on the 128-thread short-panel kernel: -1 when
+                            the batch exceeds the SM count, 0 never, 1 always (-1) */
 } bmps_params;
 
 void bmps_default_params(bmps_params* p);

@@ -763,6 +763,8 @@ const DevCache& device_cache() {
   cudaFuncSetAttribute(qr_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQrUpdateSmem);
   cudaFuncSetAttribute(qr_panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(sizeof(double2) * kQrNb * kQrPanelSmemRows));
+  cudaFuncSetAttribute(qr_panel_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(sizeof(double2) * kQrNb * qr_small_ld(kQrSmallRows)));
   cudaFuncSetAttribute(dq_apply_q1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQ1Smem);
   cudaFuncSetAttribute(qr_panel_cluster_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(sizeof(double2) * kQrNb * kQrClusterRows));
@@ -893,6 +895,7 @@ void bmps_default_params(bmps_params* p) {
   p->thr_a_sweeps = 2;
   p->thr_b_sweeps = 5;
   p->thr_auto = 1;
+  p->qr_small = -1;
 }
 
 // Development aid: cumulative Jacobi phase cycles (builds with -DBMPS_PHASE_TIMERS only).
@@ -996,7 +999,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       !(P.jacobi_mode == 0 || P.jacobi_mode == 1 || P.jacobi_mode == 4 || P.jacobi_mode == 2 ||
         P.jacobi_mode == 3) ||
       P.jac_ws != 0 || !(P.thr_a >= 0) || !(P.thr_b >= 0) || P.thr_a_sweeps < 0 ||
-      P.thr_b_sweeps < 0 || P.thr_b_sweeps >= P.max_sweeps || (P.n_svd_events > 0 && (!P.svd_events || !P.svd_events_used)))
+      P.thr_b_sweeps < 0 || P.thr_b_sweeps >= P.max_sweeps || P.qr_small < -1 || P.qr_small > 1 || (P.n_svd_events > 0 && (!P.svd_events || !P.svd_events_used)))
     return BMPS_E_ARG;
 #ifndef BMPS_EXPERIMENTAL
   if (P.tma_staging || P.jacobi_mode == 2 || P.jacobi_mode == 3) return BMPS_E_ARG;
@@ -1080,6 +1083,10 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
             fprintf(stderr, "libbmps: cluster QR panel launch failed: %s\n", cudaGetErrorString(e));
             return BMPS_E_LAUNCH;
           }
+        } else if (kQrNb == 32 && prow <= kQrSmallRows &&
+                   (P.qr_small > 0 || (P.qr_small < 0 && nitems > dc.sms))) {
+          // short panel: 128 threads, two barriers per column step, three CTAs per SM
+          qr_panel_small_kernel<<<nitems, 128, sizeof(double2) * kQrNb * qr_small_ld(std::max(prow, 32)), st>>>(qa);
         } else if (prow <= kQrPanelSmemRows && (nitems <= dc.sms || prow <= 150 * 32 / kQrNb)) {
           qr_panel_kernel<true><<<nitems, 512, sizeof(double2) * kQrNb * prow, st>>>(qa);
         } else {

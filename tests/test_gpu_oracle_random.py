@@ -188,6 +188,18 @@ def test_double_qr_preconditioning_matches_oracle(dq, chi, cutoff):
         _compare(prog, 14, cutoff, chi, seed=chi)
 
 
+@pytest.mark.parametrize("small", [1, 0])
+@pytest.mark.parametrize("chi,cutoff,n", [(64, 1e-10, 14), (128, 0.0, 14), (40, 1e-12, 13)])
+def test_short_qr_panel_kernel_matches_oracle(small, chi, cutoff, n):
+    """qr_small: QR panels of <= 128 rows on the 128-thread short-panel kernel (forced on
+    for these small batches; auto only takes it when the batch exceeds the SM count) or
+    on the 512-thread kernel (0). chi = 40 gives ragged panels (80 columns: 32 + 32 + 16)."""
+    from paper_1807_07914_b200 import _native
+    with _native.tunables(qr_small=small):
+        prog = brick_circuit(n, 14, np.random.default_rng(600 + chi))
+        _compare(prog, n, cutoff, chi, seed=chi + 1)
+
+
 @pytest.mark.parametrize("csize", [0, 2, 4])
 @pytest.mark.parametrize("chi,cutoff", [(64, 1e-10), (128, 0.0)])
 def test_row_split_cluster_jacobi_matches_oracle(csize, chi, cutoff):
