@@ -49,21 +49,45 @@ def simulate_batch(programs, n: int, policy: TruncationPolicy | None = None, *, 
                    mode: int = 0, chunk: int | None = None, keep_records: bool = False) -> MpsBatch:
     """Run ``programs[i]`` on state i of a fresh ``MpsBatch`` (one device).
 
-    Batches of 256 or more circuits are planned and launched in ``chunk``-circuit
-    slices (default: a quarter of the batch, at least 128): launches are asynchronous,
-    so the host plans slice k+1 -- the one per-op host cost -- while the GPU runs
-    slice k. Each state's program lies in one slice, so results are those of one plan
-    (bit-identical). cfg4 (measured, B200): 256 circuits 262 -> 303 circuits/s,
-    1024 circuits 280 -> 334 circuits/s (``tools/cfg4_chunks.py``).
+    Batches of 256 or more circuits are planned and launched in slices: launches are
+    asynchronous, so the host plans slice k+1 -- the one per-op host cost -- while the
+    GPU runs slice k. Only the first slice's planning is exposed, so the default
+    schedule starts small and doubles (S/16, S/8, then quarters of the batch; at least
+    64 circuits); ``chunk`` forces equal slices. Each state's program lies in one
+    slice, so results are those of one plan (bit-identical). cfg4 (measured, B200):
+    1024 circuits 280 (one plan) -> 334 (quarters) circuits/s (``tools/cfg4_chunks.py``).
     """
     S = len(programs)
     batch = MpsBatch(S, n, policy, device=device, keep_records=keep_records)
-    if chunk is None:
-        chunk = S if S < 256 else max(128, -(-S // 4))
-    for c0 in range(0, S, max(1, chunk)):
-        c1 = min(S, c0 + chunk)
+    for c0, c1 in slice_schedule(S, chunk):
         batch.execute(compile_batch(programs[c0:c1], n, states=range(c0, c1)), mode=mode)
     return batch
+
+
+def slice_schedule(S: int, chunk: int | None = None) -> list[tuple[int, int]]:
+    """[c0, c1) circuit slices of ``simulate_batch``: equal ``chunk``-sized ones, or by
+    default one slice below 256 circuits, else S/16, S/8, then quarters (>= 64 each; a
+    remainder under half a slice joins the last one)."""
+    if chunk is not None:
+        chunk = max(1, chunk)
+        return [(c0, min(S, c0 + chunk)) for c0 in range(0, S, chunk)]
+    if S < 256:
+        return [(0, S)] if S else []
+    sizes, left, step = [], S, max(64, S // 16)
+    cap = max(64, -(-S // 4))
+    while left > 0:
+        take = min(step, left)
+        sizes.append(take)
+        left -= take
+        step = min(cap, step * 2)
+    if len(sizes) > 1 and sizes[-1] < cap // 2:
+        last = sizes.pop()
+        sizes[-1] += last
+    out, c0 = [], 0
+    for z in sizes:
+        out.append((c0, c0 + z))
+        c0 += z
+    return out
 
 
 @dataclass

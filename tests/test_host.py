@@ -254,3 +254,18 @@ def test_compile_batch_rejects_duplicate_or_negative_states():
     with pytest.raises(ValueError, match="state indices"):
         compile_batch(progs, 4, states=[0, 1])
     assert compile_batch(progs, 4, states=[5, 1, 3]).max_state == 5
+
+
+def test_simulate_batch_slice_schedule_covers_every_circuit_once():
+    """simulate_batch's default slices (small first slice, doubling, quarters) and the
+    fixed-size ones tile [0, S) exactly."""
+    from paper_1807_07914_b200.backends import slice_schedule
+    for S in (0, 1, 255, 256, 300, 512, 1000, 1024, 4096):
+        for chunk in (None, 1, 100, 5000):
+            sl = slice_schedule(S, chunk)
+            assert sum(b - a for a, b in sl) == S
+            assert all(a < b for a, b in sl)
+            assert all(sl[i][1] == sl[i + 1][0] for i in range(len(sl) - 1))
+            assert not sl or (sl[0][0] == 0 and sl[-1][1] == S)
+    assert slice_schedule(1024) == [(0, 64), (64, 192), (192, 448), (448, 704), (704, 1024)]
+    assert slice_schedule(200) == [(0, 200)]

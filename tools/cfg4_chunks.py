@@ -4,7 +4,7 @@ sys.path.insert(0, '.')
 from paper_1807_07914_b200 import workloads as W, simulate_batch, TruncationPolicy
 for S in (256, 1024):
     w4 = W.config4(circuits=S)
-    for chunk in (S, S // 2, S // 4, S // 8):
+    for chunk in (S, S // 4, S // 8, None):
         for rep in range(2):
             torch.cuda.synchronize(); t = time.perf_counter()
             b = simulate_batch(w4.programs, w4.n, TruncationPolicy(w4.cutoff, w4.max_bond), chunk=chunk)
