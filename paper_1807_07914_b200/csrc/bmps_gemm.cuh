@@ -28,39 +28,46 @@ constexpr int kKC = 16;
 #define BMPS_GEMM_PAD 1
 #endif
 constexpr int kLds = kTile + BMPS_GEMM_PAD;
+#ifndef BMPS_GEMM_MINB
+#define BMPS_GEMM_MINB 2
+#endif
+
+// Chunk k0 of both operands, global -> registers (4 + 4 elements per thread), and
+// registers -> the k-major staging tiles. Split so that the main loop can have chunk
+// k + 1's global loads in flight while chunk k is multiplied (gemm_mainloop).
+template <class Op>
+BMPS_DEV void gemm_fetch_chunk(const Op& op, double2 (&ra)[4], double2 (&rb)[4], int M, int N, int K,
+                               int m0, int n0, int k0, int tid) {
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int kk = Op::kAKMajor ? (tid & 15) : (tid >> 6) + 4 * it;
+    const int i = Op::kAKMajor ? (tid >> 4) + 16 * it : (tid & 63);
+    const int gi = m0 + i, gk = k0 + kk;
+    ra[it] = (gi < M && gk < K) ? op.a(gi, gk) : make_double2(0.0, 0.0);
+  }
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int kk = Op::kBKMajor ? (tid & 15) : (tid >> 6) + 4 * it;
+    const int j = Op::kBKMajor ? (tid >> 4) + 16 * it : (tid & 63);
+    const int gj = n0 + j, gk = k0 + kk;
+    rb[it] = (gj < N && gk < K) ? op.b(gk, gj) : make_double2(0.0, 0.0);
+  }
+}
 
 template <class Op>
-BMPS_DEV void gemm_load_chunk(const Op& op, double2 (*sA)[kLds], double2 (*sB)[kLds], int M,
-                              int N, int K, int m0, int n0, int k0, int tid) {
-  if (Op::kAKMajor) {
+BMPS_DEV void gemm_stage_chunk(double2 (*sA)[kLds], double2 (*sB)[kLds], const double2 (&ra)[4],
+                               const double2 (&rb)[4], int tid) {
 #pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const int kk = tid & 15, i = (tid >> 4) + 16 * it;
-      const int gi = m0 + i, gk = k0 + kk;
-      sA[kk][i] = (gi < M && gk < K) ? op.a(gi, gk) : make_double2(0.0, 0.0);
-    }
-  } else {
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const int i = tid & 63, kk = (tid >> 6) + 4 * it;
-      const int gi = m0 + i, gk = k0 + kk;
-      sA[kk][i] = (gi < M && gk < K) ? op.a(gi, gk) : make_double2(0.0, 0.0);
-    }
+  for (int it = 0; it < 4; ++it) {
+    const int kk = Op::kAKMajor ? (tid & 15) : (tid >> 6) + 4 * it;
+    const int i = Op::kAKMajor ? (tid >> 4) + 16 * it : (tid & 63);
+    sA[kk][i] = ra[it];
   }
-  if (Op::kBKMajor) {
 #pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const int kk = tid & 15, j = (tid >> 4) + 16 * it;
-      const int gj = n0 + j, gk = k0 + kk;
-      sB[kk][j] = (gj < N && gk < K) ? op.b(gk, gj) : make_double2(0.0, 0.0);
-    }
-  } else {
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const int j = tid & 63, kk = (tid >> 6) + 4 * it;
-      const int gj = n0 + j, gk = k0 + kk;
-      sB[kk][j] = (gj < N && gk < K) ? op.b(gk, gj) : make_double2(0.0, 0.0);
-    }
+  for (int it = 0; it < 4; ++it) {
+    const int kk = Op::kBKMajor ? (tid & 15) : (tid >> 6) + 4 * it;
+    const int j = Op::kBKMajor ? (tid >> 4) + 16 * it : (tid & 63);
+    sB[kk][j] = rb[it];
   }
 }
 
@@ -83,8 +90,27 @@ BMPS_DEV void gemm_mma_chunk(double (&acc)[4][2][4], const double2 (*sA)[kLds],
   }
 }
 
+// acc += A[m0.., :] B[:, n0..] over all of K: the next chunk's operands travel from global
+// memory to registers while the staged chunk is on the tensor pipe (the loop used to expose
+// one global round trip per 16-deep chunk); same arithmetic in the same order.
 template <class Op>
-__global__ void __launch_bounds__(256) gemm_kernel(Op op) {
+BMPS_DEV void gemm_mainloop(const Op& op, double (&acc)[4][2][4], double2 (*sA)[kLds],
+                            double2 (*sB)[kLds], int M, int N, int K, int m0, int n0, int tid) {
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;
+  double2 ra[4], rb[4];
+  gemm_fetch_chunk(op, ra, rb, M, N, K, m0, n0, 0, tid);
+  for (int k0 = 0; k0 < K; k0 += kKC) {
+    gemm_stage_chunk<Op>(sA, sB, ra, rb, tid);
+    __syncthreads();
+    if (k0 + kKC < K) gemm_fetch_chunk(op, ra, rb, M, N, K, m0, n0, k0 + kKC, tid);
+    gemm_mma_chunk(acc, sA, sB, wm, wn, lane);
+    __syncthreads();
+  }
+}
+
+template <class Op>
+__global__ void __launch_bounds__(256, BMPS_GEMM_MINB) gemm_kernel(Op op) {
   __shared__ __align__(16) double2 sA[kKC][kLds];
   __shared__ __align__(16) double2 sB[kKC][kLds];
   int M, N, K;
@@ -100,12 +126,7 @@ __global__ void __launch_bounds__(256) gemm_kernel(Op op) {
     for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[mi][ni][q] = 0.0;
-  for (int k0 = 0; k0 < K; k0 += kKC) {
-    gemm_load_chunk(op, sA, sB, M, N, K, m0, n0, k0, tid);
-    __syncthreads();
-    gemm_mma_chunk(acc, sA, sB, wm, wn, lane);
-    __syncthreads();
-  }
+  gemm_mainloop(op, acc, sA, sB, M, N, K, m0, n0, tid);
   const int rr = lane >> 2, cc = (lane & 3) * 2;
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)

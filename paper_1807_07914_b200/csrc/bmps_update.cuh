@@ -58,7 +58,7 @@ struct ThetaOp {
 constexpr int kThetaLdc = 65;
 constexpr size_t kThetaSmem = (size_t)kTile * kThetaLdc * sizeof(double2);
 
-__global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* items,
+__global__ void __launch_bounds__(256, BMPS_GEMM_MINB) theta_kernel(StateView sv, const int* items,
                                                     const double2* gates, ItemMeta* meta,
                                                     double2* M0, double2* X, size_t mat_stride,
                                                     int tiles_per_dim, int qr_min_cols,
@@ -108,12 +108,7 @@ __global__ void __launch_bounds__(256) theta_kernel(StateView sv, const int* ite
     for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[mi][ni][q] = 0.0;
-  for (int k0 = 0; k0 < K; k0 += kKC) {
-    gemm_load_chunk(op, sA, sB, M, N, K, m0, n0, k0, tid);
-    __syncthreads();
-    gemm_mma_chunk(acc, sA, sB, wm, wn, lane);
-    __syncthreads();
-  }
+  gemm_mainloop(op, acc, sA, sB, M, N, K, m0, n0, tid);
   {
     const int rr = lane >> 2, cc = (lane & 3) * 2;
 #pragma unroll
