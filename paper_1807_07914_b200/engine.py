@@ -186,11 +186,54 @@ def _kind_info(kind):
     return info
 
 
+_UNIFORM_FAST = True
+
+
+def _extract_uniform(programs):
+    """``_extract`` for a batch whose programs all have the first one's structure (same
+    gate kinds on the same qubits, op for op -- a VQE ansatz bound to many parameter
+    vectors, config 2): the structure is extracted once and tiled, only the rotation
+    angles are read per program. None if the batch is not uniform (or has matrix gates)."""
+    ref = programs[0]
+    try:
+        sig = [(op.kind, op.qubits) for op in ref]
+        for prog in programs[1:]:
+            if len(prog) != len(ref) or [(op.kind, op.qubits) for op in prog] != sig:
+                return None
+    except AttributeError:          # MatrixGate ops carry no kind
+        return None
+    # source positions of the kept ops (MEASUREs dropped) and of the rotations among them
+    infos = [_kind_info(k) for k, _ in sig]
+    kept = [i for i, info in enumerate(infos) if info is not None]
+    rot = [j for j, i in enumerate(kept) if infos[i][1]]
+    rot_src = [kept[j] for j in rot]
+    ar0, q10, q20, code0, _, _, _ = _extract_slow([ref])
+    S, m = len(programs), len(kept)
+    th = np.zeros((S, m), np.float64)
+    if rot:
+        th[:, rot] = [[float(prog[i].params[0]) for i in rot_src] for prog in programs]
+    return (np.tile(ar0, S), np.tile(q10, S), np.tile(q20, S), np.tile(code0, S),
+            th.reshape(-1).tolist(), {}, np.arange(S + 1, dtype=np.int64) * m)
+
+
+def _extract_slow(programs):
+    global _UNIFORM_FAST
+    saved, _UNIFORM_FAST = _UNIFORM_FAST, False
+    try:
+        return _extract(programs)
+    finally:
+        _UNIFORM_FAST = saved
+
+
 def _extract(programs):
     """Flat per-op arrays of a batch of programs (MEASUREs dropped): arity, q1,
     q2, gate code, rotation angle, custom matrices by op index, program offsets.
     This loop is the one per-op Python cost of planning (kind lookups cached by
     object identity; enum hashing is slow)."""
+    if _UNIFORM_FAST and len(programs) >= 4:
+        fast = _extract_uniform(programs)
+        if fast is not None:
+            return fast
     ar, q1, q2, code, theta = [], [], [], [], []
     ar_a, q1_a, q2_a, code_a, th_a = ar.append, q1.append, q2.append, code.append, theta.append
     custom = {}
@@ -438,6 +481,87 @@ class _Staging:
         self.events[slot] = ev
 
 
+class GraphedPlan:
+    """A plan run from |0...0> as ONE CUDA-graph launch: ``batch.reset()`` followed by
+    every layer of ``plan`` (the per-gate loop of
+    ``backends.py:52-59`` captured instead of re-issued).
+
+    For launch-bound work that repeats the same circuit STRUCTURE with new gate
+    matrices -- a VQE optimiser re-evaluating an ansatz at new angles (config 2: 76
+    sequential CNOT-ladder layers of tiny kernels, ~800 launches per evaluation) --
+    ``replay(gates1, gates2)`` copies the new matrices into the captured buffers and
+    launches the graph: no per-layer Python, ctypes or launch overhead. The first
+    construction runs the plan once eagerly (that sizes the bond capacity and the
+    workspace, which a graph cannot do), then records the second run. Results are
+    those of ``reset(); execute(plan)`` bit for bit (same kernels, same order).
+
+    The graph holds raw device pointers: it keeps its workspace alive itself, and
+    ``replay`` refuses to run if the batch has re-allocated its state tensors since
+    (a later plan that grew the bond capacity) -- capture again in that case.
+    """
+
+    def __init__(self, batch: "MpsBatch", plan: Plan, mode: int = 0):
+        if plan.n_layers == 0:
+            raise ValueError("empty plan")
+        if plan.max_state >= batch.S:
+            raise ValueError(f"plan addresses state {plan.max_state}, batch has {batch.S}")
+        self.batch, self.plan, self.mode = batch, plan, mode
+        with torch.cuda.device(batch.device):
+            # capacity by the host's bound model, not the warm run's true bonds: replays
+            # with other matrices may need more than this run did, and the recorded run
+            # must not ask the device (a sync) -- so no refresh_bounds here
+            batch._by_model = True
+            try:
+                self._record(batch, plan, mode)
+            finally:
+                batch._by_model = False
+        if batch._ws is not self._ws or batch.gamma is not self._state[0]:
+            raise RuntimeError("capacity or workspace changed during capture")
+
+    def _record(self, batch, plan, mode) -> None:
+        batch.reset()
+        batch.execute(plan, mode)            # sizes capacity + workspace, first-use setup
+        torch.cuda.synchronize()
+        batch.check_status()
+        self._bufs = batch._upload(plan)
+        self._log = torch.empty(max(plan.n_records, 1) * _RECORD, dtype=torch.uint8,
+                                device=batch.device)
+        torch.cuda.synchronize()
+        self._state = (batch.gamma, batch.lam, batch.dims)
+        self._ws = batch._ws                 # stays alive with the graph
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            batch.reset()
+            batch._launch(plan, self._bufs, self._log, mode)
+        self._dim_ub = batch.dim_ub.copy()
+
+    def replay(self, gates1=None, gates2=None) -> "MpsBatch":
+        """Run the captured plan again from |0...0> (asynchronous). ``gates1`` [n1, 2, 2]
+        / ``gates2`` [n2, 4, 4] complex128 replace the plan's matrices in plan order
+        (``Plan.gates1`` / ``Plan.gates2`` of a plan compiled from the re-bound programs)."""
+        b = self.batch
+        if b.gamma is not self._state[0] or b.lam is not self._state[1] or b.dims is not self._state[2]:
+            raise RuntimeError("the batch re-allocated its state since capture; capture the plan again")
+        with torch.cuda.device(b.device):
+            hosts = self._bufs[6]
+            for new, dev_t, host_t in ((gates1, self._bufs[1], hosts[1]), (gates2, self._bufs[3], hosts[3])):
+                if new is None:
+                    continue
+                a = np.ascontiguousarray(new, dtype=np.complex128).view(np.float64).reshape(-1)
+                if a.size != host_t.numel():
+                    raise ValueError(f"the captured plan holds {host_t.numel()} doubles of gate "
+                                     f"matrices here, got {a.size}")
+                # the previous replay's copy out of this pinned buffer must be done
+                torch.cuda.current_stream().synchronize()
+                host_t.view(-1).numpy()[:] = a
+                dev_t.view(-1).copy_(host_t.view(-1), non_blocking=True)
+            self.graph.replay()
+        b.dim_ub[:] = self._dim_ub
+        entry = (self._log, self.plan.ranges)
+        b._logs = b._logs + [entry] if b.keep_records else [entry]
+        return b
+
+
 class MpsBatch:
     """S independent n-qubit MPS states resident in HBM, initially |0...0>.
 
@@ -469,6 +593,7 @@ class MpsBatch:
         self._ws_bytes = 0
         self._logs: list = []
         self.svd_timer = None       # bench hook: (events array, used counter, capacity)
+        self._by_model = False      # size capacity by the host bound model only (graph capture)
         with torch.cuda.device(self.device):
             self._alloc(int(cap) if cap else 1)
             self.reset()
@@ -570,15 +695,24 @@ class MpsBatch:
             return
         if plan.max_state >= self.S:
             raise ValueError(f"plan addresses state {plan.max_state}, batch has {self.S}")
+        bufs = self._upload(plan)
+        log = torch.empty(max(plan.n_records, 1) * _RECORD, dtype=torch.uint8, device=self.device)
+        self._launch(plan, bufs, log, mode)
+        self._keep_alive = bufs
+
+    def _upload(self, plan: Plan) -> tuple:
+        """The plan's item / gate / log-index / range arrays on the device (pinned
+        staging, asynchronous copies): (it1, g1, it2, g2, li2, rng, pinned hosts)."""
         dev = self.device
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
-        it1 = pin(plan.items1).to(dev, non_blocking=True)
-        g1 = pin(plan.gates1.view(np.float64)).to(dev, non_blocking=True)
-        it2 = pin(plan.items2).to(dev, non_blocking=True)
-        g2 = pin(plan.gates2.view(np.float64)).to(dev, non_blocking=True)
-        li2 = pin(plan.logidx2).to(dev, non_blocking=True)
-        rng = pin(plan.ranges).to(dev, non_blocking=True)
-        log = torch.empty(max(plan.n_records, 1) * _RECORD, dtype=torch.uint8, device=dev)
+        hosts = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+                 for a in (plan.items1, plan.gates1.view(np.float64), plan.items2,
+                           plan.gates2.view(np.float64), plan.logidx2, plan.ranges)]
+        return tuple(h.to(dev, non_blocking=True) for h in hosts) + (hosts,)
+
+    def _launch(self, plan: Plan, bufs: tuple, log: torch.Tensor, mode: int = 0) -> None:
+        """Every layer's launches on the current stream (stream-ordered work only once
+        the capacity and workspace are sized: what ``capture`` records into a graph)."""
+        it1, g1, it2, g2, li2, rng = bufs[:6]
         pol = self.policy.as_c()
         params = self._params(mode)
         lim = self._cap_limit()
@@ -595,18 +729,22 @@ class MpsBatch:
                 continue
             self._apply_2q_layer(plan.items2[a:b], it2, g2, li2, a, b, log, pol, params, lim, stream)
         self._replay(log, rng, len(plan.ranges), stream)
-        self._keep_alive = (it1, g1, it2, g2, li2, rng)
         if self.keep_records:
             self._logs.append((log, plan.ranges))
         else:
             self._logs = [(log, plan.ranges)]
+
+    def capture(self, plan: Plan, mode: int = 0) -> "GraphedPlan":
+        """``reset()`` + ``execute(plan)`` recorded once into a CUDA graph that can be
+        replayed with new gate matrices (see ``GraphedPlan``)."""
+        return GraphedPlan(self, plan, mode)
 
     def _apply_2q_layer(self, its, it2, g2, li2, a, b, log, pol, params, lim, stream) -> None:
         s_idx, q = its[:, 0], its[:, 1]
         ub = self.dim_ub
         need = lambda: int(max(ub[s_idx, q].max(), ub[s_idx, q + 2].max(),
                                np.minimum(np.minimum(2 * ub[s_idx, q], 2 * ub[s_idx, q + 2]), lim).max()))
-        if need() > self.cap:
+        if need() > self.cap and not self._by_model:
             self.refresh_bounds()      # the bound model may overestimate: consult the device
         self.ensure_capacity(need())
         bound = int(max(ub[s_idx, q].max(), ub[s_idx, q + 2].max()))

@@ -269,3 +269,44 @@ def test_simulate_batch_slice_schedule_covers_every_circuit_once():
             assert not sl or (sl[0][0] == 0 and sl[-1][1] == S)
     assert slice_schedule(1024) == [(0, 64), (64, 192), (192, 448), (448, 704), (704, 1024)]
     assert slice_schedule(200) == [(0, 200)]
+
+
+def test_uniform_batch_extraction_equals_per_op_extraction():
+    """The planner's fast path for batches of one circuit structure (a bound VQE ansatz,
+    config 2) yields exactly the arrays of the per-op loop; mixed batches, MEASUREs and
+    matrix gates are handled (or declined) the same way."""
+    import numpy as np
+    from paper_1807_07914_b200 import engine, workloads as W
+    from paper_1807_07914_b200.ir import GateKind, Instruction, MatrixGate
+
+    def same(a, b):
+        for x, y in zip(a, b):
+            if isinstance(x, np.ndarray):
+                assert x.dtype == y.dtype and np.array_equal(x, y)
+            else:
+                assert x == y
+
+    progs = W.config2(batch=6).programs
+    fast = engine._extract_uniform(progs)
+    assert fast is not None
+    same(fast, engine._extract_slow(progs))
+    with_measure = [list(p) + [Instruction(GateKind.MEASURE, (0,))] for p in progs]
+    fast = engine._extract_uniform(with_measure)
+    assert fast is not None
+    same(fast, engine._extract_slow(with_measure))
+    mixed = list(progs[:5]) + [list(progs[5])[:-1]]
+    assert engine._extract_uniform(mixed) is None
+    swapped = list(progs[:5]) + [list(progs[5])[:-1] + [Instruction(GateKind.CZ, (0, 1))]]
+    assert engine._extract_uniform(swapped) is None
+    same(engine._extract(swapped), engine._extract_slow(swapped))
+    custom = [list(p) + [MatrixGate(np.eye(2, dtype=complex), (0,))] for p in progs]
+    assert engine._extract_uniform(custom) is None
+    # whole plans agree too
+    p_fast = engine.compile_batch(progs, 20)
+    engine._UNIFORM_FAST = False
+    try:
+        p_slow = engine.compile_batch(progs, 20)
+    finally:
+        engine._UNIFORM_FAST = True
+    for name in ("items1", "items2", "off1", "off2", "logidx2", "ranges", "gates1", "gates2"):
+        assert np.array_equal(getattr(p_fast, name), getattr(p_slow, name))
