@@ -40,7 +40,9 @@ def test_bench_line_contract():
     c4 = d["cfg4_circuits"]
     assert c4["circuits"] == 1024 and c4["circuits_per_s"] > 0 and 0 < c4["frac"] < 1
     cf = d["configs"]
-    assert {"cfg3", "cfg4", "cfg5"} <= set(cf) and all(0 < cf[k]["frac"] < 1 for k in cf)
+    assert {"cfg1", "cfg2", "cfg3", "cfg4", "cfg5"} <= set(cf)
+    assert all(0 < cf[k]["frac"] < 1 for k in ("cfg3", "cfg4", "cfg5"))
+    assert cf["cfg1"]["s"] > 0 and cf["cfg2"]["energies_per_s"] > 0 and cf["cfg2"]["vectors"] == 64
 
 
 def test_reference_arm_contract():
