@@ -1160,13 +1160,16 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       if (wi == 1 && !P.tma_staging && P.jac_cluster != 0) {
         const long long vis_round = (long long)nitems * (nbmax / 2);
         const long long cl_slots = (long long)dc.cl_per_sm * dc.sms;
+        // Auto rule, from per-layer A/B timings of config 3 (tools/cfg3_layer_times.py,
+        // profiles/r02_cluster_rule_ab.log): row-split visits pay off on tall panels only --
+        // layers of <= 256-column items ran 10-20% slower on clusters of either size -- and
+        // pairs while the round's visit bound stays within twice the co-resident pairs: config
+        // 3's 24-25-item layers (bound 384-400 visits, ~16 of the items at full width) gain
+        // 13%, a layer of 32 full-width items (512 visits) loses 12%, 16 items are neutral.
+        const bool tall = cmax >= 384;
         if (P.jac_cluster > 0) csize = P.jac_cluster;
-        else if (vis_round <= cl_slots / 4) csize = 4;
-        // pairs up to three times the co-resident cluster pairs: measured on config 3 (16-33
-        // items per layer, 256-528 visits per round against 222 pairs) 0.877 -> 0.757 s with
-        // the limit at 450, 600, 900 or 1500 visits, no gain at 300; config 5 (thousands of
-        // visits per round) is slower on clusters (forced: 3.94 -> 5.45 s) and stays off them
-        else if (2 * vis_round <= 3 * cl_slots) csize = 2;
+        else if (tall && vis_round <= cl_slots / 4) csize = 4;
+        else if (tall && vis_round <= cl_slots) csize = 2;
       }
       if (P.jac_per_sm > 0) slots = std::min(slots, P.jac_per_sm * dc.sms);
       const int vis = wi == 2 ? std::max(1, (cmax + 63) / 64)
