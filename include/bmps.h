@@ -161,6 +161,10 @@ typedef struct bmps_params {
                             CTAs (latency-bound launch: the sweep count is what matters) (1) */
   int32_t qr_small;      /* QR panels of <= 128 rows on the 128-thread short-panel kernel: -1 when
                             the batch exceeds the SM count, 0 never, 1 always (-1) */
+  int32_t visits_hint;   /* the caller's estimate of the block-pair visits one Jacobi round of this
+                            call has (sum over items of ceil(columns / 16) / 2, from its own bond
+                            bounds); 0 = unknown: items x the widest item's count. Picks the CTAs
+                            per SM of latency-bound launches. (0) */
 } bmps_params;
 
 void bmps_default_params(bmps_params* p);

@@ -41,7 +41,8 @@ class BmpsParams(ctypes.Structure):
                 ("svd_events", ctypes.c_void_p), ("svd_events_used", ctypes.c_void_p),
                 ("thr_a", ctypes.c_double), ("thr_b", ctypes.c_double),
                 ("thr_a_sweeps", ctypes.c_int32), ("thr_b_sweeps", ctypes.c_int32),
-                ("thr_auto", ctypes.c_int32), ("qr_small", ctypes.c_int32)]
+                ("thr_auto", ctypes.c_int32), ("qr_small", ctypes.c_int32),
+                ("visits_hint", ctypes.c_int32)]
 
 
 RECORD_BYTES = 48  # sizeof(bmps_update_record)
@@ -96,7 +97,7 @@ _lib = None
 TUNABLES = ("tol_factor", "max_sweeps", "max_inner", "qr_min_cols", "jacobi_mode", "block_w2",
             "double_qr", "col_sort", "gram_cache", "pair_skip", "jac_cluster", "jac_per_sm",
             "jac_ws", "tma_staging", "cluster_size", "qr_cluster", "thr_a", "thr_b", "thr_a_sweeps",
-            "thr_b_sweeps", "thr_auto", "qr_small")
+            "thr_b_sweeps", "thr_auto", "qr_small", "visits_hint")
 _overrides: dict = {}
 
 

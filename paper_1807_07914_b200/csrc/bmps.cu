@@ -896,6 +896,7 @@ void bmps_default_params(bmps_params* p) {
   p->thr_b_sweeps = 5;
   p->thr_auto = 1;
   p->qr_small = -1;
+  p->visits_hint = 0;
 }
 
 // Development aid: cumulative Jacobi phase cycles (builds with -DBMPS_PHASE_TIMERS only).
@@ -999,7 +1000,7 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       !(P.jacobi_mode == 0 || P.jacobi_mode == 1 || P.jacobi_mode == 4 || P.jacobi_mode == 2 ||
         P.jacobi_mode == 3) ||
       P.jac_ws != 0 || !(P.thr_a >= 0) || !(P.thr_b >= 0) || P.thr_a_sweeps < 0 ||
-      P.thr_b_sweeps < 0 || P.thr_b_sweeps >= P.max_sweeps || P.qr_small < -1 || P.qr_small > 1 || (P.n_svd_events > 0 && (!P.svd_events || !P.svd_events_used)))
+      P.thr_b_sweeps < 0 || P.thr_b_sweeps >= P.max_sweeps || P.qr_small < -1 || P.qr_small > 1 || P.visits_hint < 0 || (P.n_svd_events > 0 && (!P.svd_events || !P.svd_events_used)))
     return BMPS_E_ARG;
 #ifndef BMPS_EXPERIMENTAL
   if (P.tma_staging || P.jacobi_mode == 2 || P.jacobi_mode == 3) return BMPS_E_ARG;
@@ -1157,21 +1158,31 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       // (auto: when a round's visits fit the co-resident clusters; a visit on a cluster
       // of CS CTAs finishes sooner, but CS x fewer visits are in flight)
       int csize = 0;
+      // Auto rules, from per-layer A/B timings of config 3 (tools/cfg3_layer_times.py,
+      // profiles/r02_cluster_rule_ab.log). vis_est = the caller's estimate of the visits one
+      // round really has (bmps_params.visits_hint, from per-item bond bounds), else the
+      // bound items x blocks / 2. Tiny rounds of tall panels: one visit per 4-CTA cluster.
+      const long long vis_est = P.visits_hint > 0 ? P.visits_hint : (long long)nitems * (nbmax / 2);
       if (wi == 1 && !P.tma_staging && P.jac_cluster != 0) {
-        const long long vis_round = (long long)nitems * (nbmax / 2);
         const long long cl_slots = (long long)dc.cl_per_sm * dc.sms;
-        // Auto rule, from per-layer A/B timings of config 3 (tools/cfg3_layer_times.py,
-        // profiles/r02_cluster_rule_ab.log): row-split visits pay off on tall panels only --
-        // layers of <= 256-column items ran 10-20% slower on clusters of either size -- and
-        // pairs while the round's visit bound stays within twice the co-resident pairs: config
-        // 3's 24-25-item layers (bound 384-400 visits, ~16 of the items at full width) gain
-        // 13%, a layer of 32 full-width items (512 visits) loses 12%, 16 items are neutral.
         const bool tall = cmax >= 384;
         if (P.jac_cluster > 0) csize = P.jac_cluster;
-        else if (tall && vis_round <= cl_slots / 4) csize = 4;
-        else if (tall && vis_round <= cl_slots) csize = 2;
+        else if (tall && vis_est <= cl_slots / 4) csize = 4;
       }
-      if (P.jac_per_sm > 0) slots = std::min(slots, P.jac_per_sm * dc.sms);
+      // CTAs per SM by the visits a round has: visits sharing an SM time-slice its FP64 pipe
+      // (two co-resident visits each take about twice as long as one alone), so below the
+      // throughput regime fewer, faster CTAs win -- a round is as slow as its slowest visit.
+      // Measured (chi = 256 steady-state layers, ms per layer at 1 / 2 / 3 / 4 CTAs per SM;
+      // profiles/r02_per_sm_ab.log, r02_cfg3_layer_times.log): ~290 visits per round (config
+      // 3) 31-33 / 32-35 / - / 37-41; 528 visits: 52.5 / 41.9 / 44.2 / 47.1; 780: 72.5 / 55.5
+      // / 51.5 / 53.1; 1040: 92.7 / 70.2 / 63.5 / 62.2. The best count is ceil(visits / 2.2
+      // SMs): one CTA slot per ~2.2 visits of the round, the occupancy maximum from ~1000.
+      if (P.jac_per_sm > 0) {
+        slots = std::min(slots, P.jac_per_sm * dc.sms);
+      } else if (csize == 0 && wi == 1) {
+        const long long k = (10LL * vis_est + 22LL * dc.sms - 1) / (22LL * dc.sms);
+        if (k * dc.sms < slots) slots = (int)std::max(1LL, k) * dc.sms;
+      }
       const int vis = wi == 2 ? std::max(1, (cmax + 63) / 64)
                     : wi == 1 ? nbmax / 2
                               : (cmax + 15) / 16;

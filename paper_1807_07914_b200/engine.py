@@ -751,9 +751,14 @@ class MpsBatch:
         new = np.minimum(np.minimum(2 * ub[s_idx, q], 2 * ub[s_idx, q + 2]), lim)
         per_item = int(self.lib.bmps_apply_2q_workspace_bytes(self.cap, 1))
         chunk = max(1, min(self.max_items, self.workspace_budget // max(per_item, 1)))
+        # visits of one Jacobi round, from the per-item bounds: columns = 2 min(dl, dr),
+        # blocks of 16 paired up (bmps_params.visits_hint)
+        blocks = (2 * np.minimum(ub[s_idx, q], ub[s_idx, q + 2]) + 15) // 16
+        visits = np.maximum(1, (blocks + (blocks & 1)) // 2)
         for c0 in range(a, b, chunk):
             c1 = min(b, c0 + chunk)
             ws, wsb = self._workspace(c1 - c0)
+            params.visits_hint = int(min(visits[c0 - a:c1 - a].sum(), 2 ** 31 - 1))
             rc = self.lib.bmps_apply_2q(
                 _ptr(self.gamma), _ptr(self.lam), _ptr(self.dims), self.S, self.n, self.cap,
                 it2.data_ptr() + 8 * c0, g2.data_ptr() + 256 * c0, c1 - c0, pol,
