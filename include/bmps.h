@@ -135,7 +135,8 @@ typedef struct bmps_params {
   int32_t col_sort;      /* descending-norm column order ahead of the first QR (1) */
   int32_t gram_cache;    /* cross visits reuse rotated intra-block Grams (1) */
   int32_t pair_skip;     /* skip cross visits of provably clean block pairs (1) */
-  int32_t jac_cluster;   /* row-split cluster visits: -1 auto, 0 off, 2 / 4 CTAs (-1) */
+  int32_t jac_cluster;   /* row-split cluster visits: 2 / 4 CTAs per visit when forced; -1 (auto)
+                            and 0 use single-CTA visits (-1) */
   int32_t jac_per_sm;    /* dynamic Jacobi CTAs per SM, 0 = occupancy maximum (0) */
   int32_t jac_ws;        /* reserved (the warp-specialised Jacobi was removed); must be 0 */
   int32_t tma_staging;   /* TMA bulk panel staging (BMPS_EXPERIMENTAL only) (0) */

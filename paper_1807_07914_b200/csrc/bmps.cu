@@ -1158,17 +1158,15 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       // (auto: when a round's visits fit the co-resident clusters; a visit on a cluster
       // of CS CTAs finishes sooner, but CS x fewer visits are in flight)
       int csize = 0;
-      // Auto rules, from per-layer A/B timings of config 3 (tools/cfg3_layer_times.py,
-      // profiles/r02_cluster_rule_ab.log). vis_est = the caller's estimate of the visits one
-      // round really has (bmps_params.visits_hint, from per-item bond bounds), else the
-      // bound items x blocks / 2. Tiny rounds of tall panels: one visit per 4-CTA cluster.
+      // vis_est = the caller's estimate of the visits one round really has
+      // (bmps_params.visits_hint, from per-item bond bounds), else the bound items x blocks / 2
       const long long vis_est = P.visits_hint > 0 ? P.visits_hint : (long long)nitems * (nbmax / 2);
-      if (wi == 1 && !P.tma_staging && P.jac_cluster != 0) {
-        const long long cl_slots = (long long)dc.cl_per_sm * dc.sms;
-        const bool tall = cmax >= 384;
-        if (P.jac_cluster > 0) csize = P.jac_cluster;
-        else if (tall && vis_est <= cl_slots / 4) csize = 4;
-      }
+      // Row-split cluster visits (jacobi_cluster_kernel) only when forced (jac_cluster 2 / 4):
+      // per-layer A/B timings (tools/cfg3_layer_times.py, profiles/r02_cluster_rule_ab.log)
+      // showed that what they bought was fewer visits per SM, which the grid rule below gives
+      // the single-CTA visits directly -- config 3's layers 32-35 ms on pairs vs 31-33 ms at
+      // one CTA per SM, config 1's 8-item layers 2.56 ms on 4-CTA clusters vs 2.45 ms
+      if (wi == 1 && !P.tma_staging && P.jac_cluster > 0) csize = P.jac_cluster;
       // CTAs per SM by the visits a round has: visits sharing an SM time-slice its FP64 pipe
       // (two co-resident visits each take about twice as long as one alone), so below the
       // throughput regime fewer, faster CTAs win -- a round is as slow as its slowest visit.

@@ -6,7 +6,8 @@ from paper_1807_07914_b200 import MpsBatch, TruncationPolicy, compile_batch, _na
 from paper_1807_07914_b200.engine import SvdTimer
 from paper_1807_07914_b200 import workloads as W
 
-w = W.config3()
+import os
+w = W.CONFIGS[os.environ.get("CFG", "cfg3")]()
 plan = compile_batch(w.programs, w.n)
 specs = sys.argv[1:3] or ["jac_cluster=0", "jac_cluster=2"]
 res, meta = [], []
