@@ -1167,9 +1167,10 @@ int32_t bmps_apply_2q(double* gamma, double* lam, int32_t* dims, int32_t S, int3
       // the single-CTA visits directly -- config 3's layers 32-35 ms on pairs vs 31-33 ms at
       // one CTA per SM, config 1's 8-item layers 2.56 ms on 4-CTA clusters vs 2.45 ms
       if (wi == 1 && !P.tma_staging && P.jac_cluster > 0) csize = P.jac_cluster;
-      // CTAs per SM by the visits a round has: visits sharing an SM time-slice its FP64 pipe
-      // (two co-resident visits each take about twice as long as one alone), so below the
-      // throughput regime fewer, faster CTAs win -- a round is as slow as its slowest visit.
+      // CTAs per SM by the visits a round has: by the layer times below, two visits sharing an
+      // SM each take about twice as long as one alone (cause not isolated: L2 hit rate and
+      // DRAM reads are the same, profiles/r02_per_sm_mechanism.log), so below the throughput
+      // regime fewer, faster CTAs win -- a round is as slow as its slowest visit.
       // Measured (chi = 256 steady-state layers, ms per layer at 1 / 2 / 3 / 4 CTAs per SM;
       // profiles/r02_per_sm_ab.log, r02_cfg3_layer_times.log): ~290 visits per round (config
       // 3) 31-33 / 32-35 / - / 37-41; 528 visits: 52.5 / 41.9 / 44.2 / 47.1; 780: 72.5 / 55.5
